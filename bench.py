@@ -1,0 +1,308 @@
+"""Benchmark of the HI operator (one GMRES matvec's hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--mode fp64|fp32c]
+    python bench.py --impl reference ...        # the reference's CPU path (oracle port)
+
+A "step" is one application of the fiber HI operator to one batch of force
+densities: the fused Stokeslet + (eps L)^2/2 doublet all-pairs sum over every
+fiber node (complementary_velocities, system.py:623-709), the near-field
+corrections and the local self terms M f + K_delta f (fiber.py:244-258).
+Default workload: BASELINE config 5 (16,384 fibers x 64 nodes = 1,048,576
+points, the largest single-GPU configuration), synthetic seeded inputs.
+Multi-GPU: target-block sharding, NCCL all-gather of the force densities
+once per step, fixed total work ("strong" scaling).
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_PAIR = 35          # fused Stokeslet + doublet, minimal formula
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--mode", default="fp64", choices=["fp64", "fp32c"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks ----
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 7
+                          for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------- reference (CPU) ----
+def cpu_pair_rate(X, forces, eps, sample_rows, seed=0):
+    """Reference algorithm on the host cores (oracle C port of the numba
+    kernels, OpenMP over all threads): the Stokeslet pass plus the doublet
+    pass of complementary_velocities (system.py:656-671) for a row sample of
+    targets against all sources.  Returns (pairs/s, seconds, pairs, threads)."""
+    from oracle import ops, pairs
+    nf, n, _ = X.shape
+    src = X.reshape(-1, 3)
+    grp = np.repeat(np.arange(nf, dtype=np.int64), n)
+    geos = [ops.geometry(X[m]) for m in range(nf)]
+    w = np.concatenate([g["weights"] for g in geos])
+    strengths = w[:, None] * forces.reshape(-1, 3)              # system.py:657-658
+    c = np.repeat([(eps * g["L"]) ** 2 / 2.0 for g in geos], n)  # system.py:542
+    dbl = c[:, None] * strengths
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(src.shape[0], size=sample_rows, replace=False))
+    pref = 1.0 / (8.0 * np.pi)
+    t0 = time.perf_counter()
+    u1, _ = pairs.stokeslet_sum(src[rows], grp[rows], src, grp, strengths, pref)
+    u2, _ = pairs.doublet_sum(src[rows], grp[rows], src, grp, dbl, pref)
+    dt = time.perf_counter() - t0
+    npairs = sample_rows * (src.shape[0] - n)
+    return npairs / dt, dt, npairs, pairs.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_1602_05650_b200 import configs
+    cloud = configs.make(args.config, seed=args.seed)
+    f = configs.forces(cloud, seed=args.seed + 1)
+    N = cloud.n_points
+    rows = max(64, int(round(4e9 / N / 2)))  # ~4e9 pair evaluations (2 passes) per step
+    rows = min(rows, N)
+    for _ in range(args.warmup):
+        cpu_pair_rate(cloud.X, f, cloud.eps, min(rows, 256), seed=1)
+    rates, times = [], []
+    for k in range(args.steps):
+        r, dt, npairs, threads = cpu_pair_rate(cloud.X, f, cloud.eps, rows, seed=100 + k)
+        rates.append(r)
+        times.append(dt)
+    value = statistics.median(rates)
+    full_pairs = N * N - cloud.n_fibers * cloud.n_nodes ** 2
+    line = {
+        "impl": "reference", "metric": "stokes_pair_interactions_per_s", "value": value,
+        "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * full_pairs / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded rejection-sampled fiber cloud, N(0,1) forces)",
+        "config": {"workload": f"{args.config}: HI operator matvec, {cloud.n_fibers} fibers x "
+                               f"{cloud.n_nodes} nodes", "points": N, "pairs_per_step": full_pairs},
+        "cpu_baseline": {"value": value, "unit": "pair-interactions/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{rows} target rows x {N} sources, Stokeslet + doublet passes "
+                                   f"(oracle/oracle_pairs.c, OpenMP); ms_per_step extrapolated "
+                                   f"linearly in rows to the full {N}-row matvec"},
+        "e2e": {"value": value, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours (GPU) ----
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_05650_b200 import _native, configs, kernels
+    from paper_1602_05650_b200.dist import ShardedHIOperator
+    from paper_1602_05650_b200.operator import FiberHIOperator
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    _native.load(require_device=True)
+    mode = _native.SF_MODE_FP64 if args.mode == "fp64" else _native.SF_MODE_FP32C
+    cloud = configs.make(args.config, seed=args.seed)
+    f_all = configs.forces(cloud, seed=args.seed + 1)
+    op = FiberHIOperator(cloud.X, cloud.eps, device=dev, mode=mode, shard=(rank, world))
+    sop = ShardedHIOperator(op)
+    f_local = torch.as_tensor(f_all[op.f0:op.f0 + op.nown], device=dev).contiguous()
+    u_nl = torch.empty((op.Nown, 3), dtype=torch.float64, device=dev)
+    u_self = torch.empty((op.Nown, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        sop.apply(f_local, out_nl=u_nl, out_self=u_self)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    op.check_bad()
+    barrier()
+    # ---- timed region: exactly K steps, L2 flushed between steps (outside events)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            starts[k].record()
+            step()
+            ends[k].record()
+        barrier()
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_step = sum(ms) / len(ms)
+    t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    total_pairs = cloud.n_points ** 2 - cloud.n_fibers * cloud.n_nodes ** 2
+    value = total_pairs / (ms_step * 1e-3)
+
+    # ---- e2e: host (pinned) forces in, host velocities out, through the public API
+    f_host = torch.as_tensor(f_all[op.f0:op.f0 + op.nown]).pin_memory()
+    out_host = torch.empty((2, op.Nown, 3), dtype=torch.float64).pin_memory()
+    e_s = torch.cuda.Event(enable_timing=True)
+    e_e = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e_s.record()
+    for _ in range(args.steps):
+        fd = f_host.to(dev, non_blocking=True)
+        a, b = sop.apply(fd)
+        out_host[0].copy_(a, non_blocking=True)
+        out_host[1].copy_(b, non_blocking=True)
+    e_e.record()
+    barrier()
+    e2e_ms = torch.tensor([e_s.elapsed_time(e_e) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    # ---- roofline of the dominant kernel (pack + pair + ordered reduce), this GPU
+    reps = max(2, min(args.steps, 3))
+    fs = sop.gather_sources(f_local)
+    r_s = torch.cuda.Event(enable_timing=True)
+    r_e = torch.cuda.Event(enable_timing=True)
+    op.apply(fs, out_nl=u_nl, self_terms=False)
+    torch.cuda.synchronize()
+    r_s.record()
+    for _ in range(reps):
+        op.apply(fs, out_nl=u_nl, self_terms=False)
+    r_e.record()
+    torch.cuda.synchronize()
+    pair_ms = r_s.elapsed_time(r_e) / reps
+    peak_flops, _ = kernels.dfma_peak(1 << 15)
+    achieved = op.pairs_per_apply * FLOPS_PER_PAIR / (pair_ms * 1e-3)
+
+    lines = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rows = max(64, int(round(3e9 / cloud.n_points / 2)))
+            rate, dt, npairs, threads = cpu_pair_rate(cloud.X, f_all, cloud.eps, rows)
+            cpu = {"value": rate, "unit": "pair-interactions/s", "cores": threads, "kind": "port",
+                   "sample": f"{rows} target rows x {cloud.n_points} sources, Stokeslet + doublet "
+                             f"passes of the oracle C port (OpenMP), {dt:.1f} s"}
+        clocks = clk.summary()
+        lines = {
+            "metric": "stokes_pair_interactions_per_s", "value": value,
+            "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.mode == "fp64" else "f32-compute/f64-accumulate",
+            "data": "synthetic (seeded rejection-sampled perturbed fiber cloud, N(0,1) forces)",
+            "config": {"workload": f"{args.config}: HI operator matvec (Stokeslet+doublet all-pairs "
+                                   f"+ near + M+K_delta self terms), {cloud.n_fibers} fibers x "
+                                   f"{cloud.n_nodes} nodes", "points": cloud.n_points,
+                       "pairs_per_step": total_pairs, "parallelism": f"target-shard{world}",
+                       "l2": "flushed between timed steps (256 MB write); K_delta 4.8 GB > L2",
+                       "steps_per_s": 1e3 / ms_step},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
+                         "peak": peak_flops / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / peak_flops, "traffic": None,
+                         "kernel": "pack + pair_kernel<SbtP<true>> + reduce_partials",
+                         "flops_per_pair": FLOPS_PER_PAIR,
+                         "peak_source": "measured DFMA microbenchmark (sf_dfma_peak) on this GPU; "
+                                        f"nominal {NOMINAL_FP64_TFLOPS:.1f} TFLOP/s at 1965 MHz",
+                         "kernel_ms": pair_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": total_pairs / (e2e_ms * 1e-3), "unit": "pair-interactions/s",
+                    "h2d_bytes_per_step": int(cloud.n_points * 3 * 8),
+                    "d2h_bytes_per_step": int(2 * cloud.n_points * 3 * 8)},
+            "gpu_launches": args.steps * op.launches_per_apply,
+            "clocks": clocks,
+        }
+        print(json.dumps(lines), flush=True)
+    barrier()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

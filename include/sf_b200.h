@@ -1,0 +1,206 @@
+/*
+ * sf_b200.h — C ABI of the B200-native hydrodynamic-interaction (HI) operator
+ * for the slender-fiber method of arXiv 1602.05650 (reference package
+ * `slenderflow`, /root/reference/pkg/src/slenderflow).
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes; no torch or C++ types;
+ *   - arrays are C-contiguous: points/vectors (N,3) float64 AoS, group ids
+ *     int64 (-1 = no exclusion, kernels.py:337-339), matrices row-major;
+ *   - `sf_*` entry points take DEVICE pointers and a cudaStream_t passed as
+ *     `void *stream` (NULL = legacy default stream); they allocate nothing,
+ *     never synchronise, and return SF_OK (0) or an error code;
+ *   - `sf_host_*` entry points take HOST pointers, exactly the arrays the
+ *     reference passes to its numba kernels, copy in, run, copy out and
+ *     synchronise (the drop-in a ctypes/cffi binding of kernels.py calls);
+ *   - `bad` outputs count target/source pairs closer than MIN_SEPARATION
+ *     that were skipped (kernels.py:99-101); like the reference the kernels
+ *     never raise — callers raise SingularEvaluationError when bad > 0;
+ *   - every per-target sum runs over sources in one fixed order, so results
+ *     are bitwise reproducible run to run and independent of grid size.
+ */
+#ifndef SF_B200_H
+#define SF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SF_OK = 0,
+    SF_EINVAL = 1,  /* bad argument (negative size, NULL pointer with n > 0) */
+    SF_ECUDA = 2,   /* CUDA runtime error; see sf_last_error() */
+    SF_ENOMEM = 3,  /* device allocation failed (host entry points only) */
+    SF_ENODEV = 4   /* no CUDA device */
+};
+
+/* Arithmetic mode of the pair kernels. */
+enum {
+    SF_MODE_FP64 = 0,  /* FP64 compute, FP64 accumulate */
+    SF_MODE_FP32C = 1  /* FP32 pair arithmetic, FP64 accumulation per tile */
+};
+
+int sf_abi_version(void);
+const char *sf_last_error(void);
+int sf_device_sm_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Pair sums.  Device pointers.  `bad` is a device int64 that the call
+ * OVERWRITES with the skipped-pair count (pass NULL to ignore).
+ * ------------------------------------------------------------------------- */
+
+/* Replaces kernels.stokeslet_sum (kernels.py:72-111), reached through
+ * DirectSummation.stokeslet (system.py:93-105):
+ *   out_i = pref * sum_{j: g_j != g_i, r2 >= 1e-24} [f_j/r + (r.f_j) r/r^3]. */
+int sf_stokeslet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                     const double *src, const int64_t *sgrp, int64_t ns,
+                     const double *f, double pref, double *out, int64_t *bad,
+                     void *stream);
+
+/* Replaces kernels.doublet_sum (kernels.py:114-145):
+ *   out_i = pref * sum [f_j/r^3 - 3 (r.f_j) r/r^5]. */
+int sf_doublet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                   const double *src, const int64_t *sgrp, int64_t ns,
+                   const double *f, double pref, double *out, int64_t *bad,
+                   void *stream);
+
+/* Fused slender-body pair sum: the Stokeslet sum plus the source-doublet sum
+ * in ONE pass (system.py:656-671 issue two passes over the same pairs):
+ *   out_i = pref * sum_j [ f_j/r + (r.f_j) r/r^3
+ *                        + c_j (f_j/r^3 - 3 (r.f_j) r/r^5) ]
+ * f_j are the quadrature-weighted strengths (system.py:657-658) and
+ * c_j = (eps_l L_l)^2/2 of the source's fiber (system.py:542, 662-664);
+ * dcoef == NULL means c_j = 0 (Stokeslet only).  mode: SF_MODE_*. */
+int sf_sbt_pair(const double *trg, const int64_t *tgrp, int64_t nt,
+                const double *src, const int64_t *sgrp, int64_t ns,
+                const double *f, const double *dcoef, double pref, int mode,
+                double *out, int64_t *bad, void *stream);
+
+/* Replaces kernels.stresslet_sum (kernels.py:177-213), pref = -3/(4 pi mu),
+ * qw = density times quadrature weight (system.py:673-687, body.py:237-251). */
+int sf_stresslet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                     const double *src, const int64_t *sgrp, int64_t ns,
+                     const double *nrm, const double *qw, double pref,
+                     double *out, int64_t *bad, void *stream);
+
+/* Replaces kernels.stresslet_sum_subtracted (kernels.py:216-249), reached
+ * through body.double_layer_onsurface (body.py:254-262). */
+int sf_stresslet_sum_subtracted(const double *nodes, const double *nrm,
+                                const double *w, const double *q, int64_t n,
+                                double pref, double *out, void *stream);
+
+/* Replaces kernels.stresslet_rowsum (kernels.py:252-281); out is (n,3,3). */
+int sf_stresslet_rowsum(const double *nodes, const double *nrm, const double *w,
+                        int64_t n, double pref, double *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Fiber self terms (batched over nf fibers of n nodes; fiber-major arrays).
+ * ------------------------------------------------------------------------- */
+
+/* Replaces kernels.kdelta_matrix (kernels.py:284-334) called once per fiber
+ * by Fiber.kdelta_matrix (fiber.py:213-222).  X,tang (nf,n,3); s,s_alpha
+ * (nf,n); w (n) Clenshaw-Curtis weights shared by all fibers; delta (nf);
+ * K (nf,3n,3n) fully overwritten. */
+int sf_kdelta_build_batched(const double *X, const double *s,
+                            const double *s_alpha, const double *tang,
+                            const double *w, int64_t nf, int64_t n,
+                            const double *delta, double pref, double *K,
+                            void *stream);
+
+/* u = M f + K f (+ u if accumulate): local_mobility_apply (fiber.py:244-250)
+ * plus nonlocal_Kdelta_apply (fiber.py:253-258) for every fiber.
+ * c_log (nf) = -ln(eps^2 e)/(8 pi mu), c_two = 2/(8 pi mu). */
+int sf_self_apply_batched(const double *K, const double *tang,
+                          const double *c_log, double c_two, const double *f,
+                          int64_t nf, int64_t n, int accumulate, double *u,
+                          void *stream);
+
+/* Per-fiber geometry (spectral.arclength_map, spectral.py:139-154, and
+ * Fiber.refresh_geometry, fiber.py:133-147): from centrelines X (nf,n,3),
+ * the Chebyshev differentiation matrix D (n,n), the arclength integration
+ * matrix S (n,n) and Clenshaw-Curtis weights wcc (n), writes s, s_alpha,
+ * node weights wcc*s_alpha (fiber.py:172-174) (nf,n), tangents (nf,n,3),
+ * L (nf) and, when delta_ratio > 0, delta = delta_ratio * L (fiber.py:144).
+ * *degenerate (device int, nullable) counts nodes with s_alpha <= 1e-12. */
+int sf_fiber_geometry_batched(const double *X, int64_t nf, int64_t n, const double *D,
+                              const double *S, const double *wcc, double delta_ratio,
+                              double *s, double *s_alpha, double *tang, double *wnode,
+                              double *L, double *delta, int *degenerate, void *stream);
+
+/* The fiber part of the HI operator in one call (system.py:656-671 + 702-707,
+ * fiber.py:244-258), for the target fibers [t_fiber0, t_fiber0 + t_nfibers)
+ * against ALL nf fibers as sources (the target-block shard of a multi-GPU
+ * run; t_fiber0 = 0, t_nfibers = nf on one GPU).  With f (nf*n,3) force
+ * densities of every fiber:
+ *   out_nl   (t_nfibers*n,3) = Stokeslet + doublet sum over other fibers'
+ *              nodes of the strengths wnode_j f_j, plus the near corrections
+ *              of the CSR map (rows are shard-local target indices; its x
+ *              vector is the global f);
+ *   out_self (t_nfibers*n,3) = M f + K f of the target fibers (skipped when
+ *              out_self == NULL); K holds the target fibers' matrices.
+ * dcoef (nf*n) or NULL; near_nrows == 0 disables the near map. */
+int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf, int64_t n,
+                      int64_t t_fiber0, int64_t t_nfibers, const double *wnode,
+                      const double *dcoef, double pref, int mode, const double *K,
+                      const double *tang, const double *c_log, double c_two,
+                      const int64_t *near_row_ptr, const int64_t *near_rows,
+                      int64_t near_nrows, const int64_t *near_w_off,
+                      const int64_t *near_x_off, const int64_t *near_x_len,
+                      const double *near_W, const double *f, double *out_nl,
+                      double *out_self, int64_t *bad, void *stream);
+
+/* Source-split factor the pair kernels use for nt targets x ns sources (a
+ * pure function of the sizes; each target's sum is split into this many
+ * ordered chunks).  Used to count kernel launches. */
+int sf_pair_split(int64_t nt, int64_t ns);
+
+/* Near-field correction apply (system.py:702-707): for every entry e,
+ * u[t_e] += W_e (3 x 3 m_e) . x[off_e : off_e + 3 m_e].  Entries must be
+ * grouped by target (row_ptr CSR over `nrows` distinct targets rows[]);
+ * within a target they are applied in list order.  W is packed per entry at
+ * w_off[e] (doubles). */
+int sf_near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows,
+                  const int64_t *w_off, const int64_t *x_off, const int64_t *x_len,
+                  const double *W, const double *x, double *u, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer drop-ins (copy in, compute, copy out, synchronise).
+ * ------------------------------------------------------------------------- */
+int sf_host_stokeslet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                          const double *src, const int64_t *sgrp, int64_t ns,
+                          const double *f, double pref, double *out, int64_t *bad);
+int sf_host_doublet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                        const double *src, const int64_t *sgrp, int64_t ns,
+                        const double *f, double pref, double *out, int64_t *bad);
+int sf_host_sbt_pair(const double *trg, const int64_t *tgrp, int64_t nt,
+                     const double *src, const int64_t *sgrp, int64_t ns,
+                     const double *f, const double *dcoef, double pref, int mode,
+                     double *out, int64_t *bad);
+int sf_host_stresslet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
+                          const double *src, const int64_t *sgrp, int64_t ns,
+                          const double *nrm, const double *qw, double pref,
+                          double *out, int64_t *bad);
+int sf_host_stresslet_sum_subtracted(const double *nodes, const double *nrm,
+                                     const double *w, const double *q, int64_t n,
+                                     double pref, double *out);
+int sf_host_stresslet_rowsum(const double *nodes, const double *nrm,
+                             const double *w, int64_t n, double pref, double *out);
+int sf_host_kdelta_matrix(const double *X, const double *s, const double *s_alpha,
+                          const double *tang, const double *w, int64_t n,
+                          double delta, double pref, double *K);
+
+/* ---------------------------------------------------------------------------
+ * Measurement helpers.
+ * ------------------------------------------------------------------------- */
+
+/* FP64 DFMA throughput microbenchmark: runs `iters` dependent-chain DFMA
+ * iterations on every resident thread; writes achieved DFMA FLOP/s (2 per
+ * DFMA) into *flops.  Used as the roofline denominator. */
+int sf_dfma_peak(int64_t iters, double *flops, double *ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SF_B200_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of libsf_b200.so (the C ABI declared in include/sf_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every device entry point raises NativeUnavailable.
+"""
+
+import ctypes
+import os
+
+from .build import LIB
+
+SF_OK = 0
+SF_MODE_FP64 = 0
+SF_MODE_FP32C = 1
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library could not be loaded (not built, or no GPU)."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+    def __init__(self, fn, code, msg):
+        super().__init__(f"{fn} failed with status {code}: {msg}")
+        self.code = code
+
+
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_P = ctypes.c_void_p
+
+# name -> argtypes (all return int status)
+_SIGNATURES = {
+    "sf_abi_version": [],
+    "sf_device_sm_count": [],
+    "sf_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P, _P],
+    "sf_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P, _P],
+    "sf_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P, _P],
+    "sf_stresslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _P, _P, _P],
+    "sf_stresslet_sum_subtracted": [_P, _P, _P, _P, _I64, _D, _P, _P],
+    "sf_stresslet_rowsum": [_P, _P, _P, _I64, _D, _P, _P],
+    "sf_kdelta_build_batched": [_P, _P, _P, _P, _P, _I64, _I64, _P, _D, _P, _P],
+    "sf_self_apply_batched": [_P, _P, _P, _D, _P, _I64, _I64, _I, _P, _P],
+    "sf_near_apply": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P],
+    "sf_fiber_geometry_batched": [_P, _I64, _I64, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P, _P,
+                                  _P],
+    "sf_fiber_hi_apply": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _D, _I, _P, _P, _P, _D, _P,
+                          _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sf_pair_split": [_I64, _I64],
+    "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
+    "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
+    "sf_host_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P],
+    "sf_host_stresslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _P, _P],
+    "sf_host_stresslet_sum_subtracted": [_P, _P, _P, _P, _I64, _D, _P],
+    "sf_host_stresslet_rowsum": [_P, _P, _P, _I64, _D, _P],
+    "sf_host_kdelta_matrix": [_P, _P, _P, _P, _P, _I64, _D, _D, _P],
+    "sf_dfma_peak": [_I64, _P, _P],
+}
+
+_lib = None
+
+
+def exported_symbols():
+    return sorted(_SIGNATURES) + ["sf_last_error"]
+
+
+def load(require_device=False):
+    """Load the library (cached).  require_device also checks for a GPU."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise NativeUnavailable(
+                f"{LIB} is not built; run `python -m paper_1602_05650_b200.build`")
+        lib = ctypes.CDLL(LIB)
+        for name, argtypes in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _I
+        lib.sf_last_error.argtypes = []
+        lib.sf_last_error.restype = ctypes.c_char_p
+        _lib = lib
+    if require_device and _lib.sf_device_sm_count() <= 0:
+        raise NativeUnavailable("no CUDA device visible to libsf_b200")
+    return _lib
+
+
+def call(name, *args):
+    lib = load(require_device=True)
+    rc = getattr(lib, name)(*args)
+    if rc != SF_OK:
+        raise NativeError(name, rc, lib.sf_last_error().decode(errors="replace"))
+    return rc

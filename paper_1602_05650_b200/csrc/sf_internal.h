@@ -1,0 +1,62 @@
+// sf_internal.h — library-internal declarations shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/sf_b200.h"
+
+namespace sf {
+
+// Records a CUDA error (if any) from the last launch; returns SF_OK/SF_ECUDA.
+int check_launch(const char *what);
+int set_error(int code, const char *fmt, ...);
+
+// Grow-only, stream-ordered device scratch.  One instance per stream; slots
+// are independent buffers.  Steady-state calls allocate nothing.
+class Workspace {
+   public:
+    static constexpr int kSlots = 8;
+    void *get(int slot, size_t bytes, cudaStream_t st);
+    ~Workspace();
+
+   private:
+    void *ptr_[kSlots] = {};
+    size_t cap_[kSlots] = {};
+};
+Workspace &workspace_for(cudaStream_t st);
+
+int pairs_sbt(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
+              const int64_t *sgrp, int64_t ns, const double *f, const double *dcoef, double pref,
+              int mode, double *out, int64_t *bad, cudaStream_t st, Workspace &ws);
+int pairs_doublet_only(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
+                       const int64_t *sgrp, int64_t ns, const double *f, double pref, double *out,
+                       int64_t *bad, cudaStream_t st, Workspace &ws);
+int pairs_stresslet(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
+                    const int64_t *sgrp, int64_t ns, const double *nrm, const double *qw,
+                    double pref, double *out, int64_t *bad, cudaStream_t st, Workspace &ws);
+int pairs_dl_subtracted(const double *nodes, const double *nrm, const double *w, const double *q,
+                        int64_t n, double pref, double *out, cudaStream_t st, Workspace &ws);
+int pairs_rowsum(const double *nodes, const double *nrm, const double *w, int64_t n, double pref,
+                 double *out, cudaStream_t st, Workspace &ws);
+
+int fiber_kdelta_build(const double *X, const double *s, const double *s_alpha,
+                       const double *tang, const double *w, int64_t nf, int64_t n,
+                       const double *delta, double pref, double *K, cudaStream_t st);
+int fiber_self_apply(const double *K, const double *tang, const double *c_log, double c_two,
+                     const double *f, int64_t nf, int64_t n, int accumulate, double *u,
+                     cudaStream_t st);
+int fiber_geometry(const double *X, int64_t nf, int64_t n, const double *D, const double *S,
+                   const double *wcc, double delta_ratio, double *s, double *s_alpha,
+                   double *tang, double *wnode, double *L, double *delta, int *degenerate,
+                   cudaStream_t st);
+int pairs_sbt_weighted(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
+                       const int64_t *sgrp, int64_t ns, const double *f, const double *wsrc,
+                       const double *dcoef, double pref, int mode, double *out, int64_t *bad,
+                       cudaStream_t st, Workspace &ws);
+int pair_split(int64_t nt, int64_t ns);
+int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
+               const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,
+               double *u, cudaStream_t st);
+
+}  // namespace sf

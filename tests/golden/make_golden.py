@@ -1,0 +1,151 @@
+"""Generate golden vectors by running the REFERENCE itself (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden.py
+
+Imports `slenderflow` read-only from /root/reference/pkg/src and stores its
+outputs on seeded inputs as small .npz fixtures next to this script.  The
+fixtures travel with the repo; nothing at test time reads /root/reference.
+Inputs (fiber centrelines) come from paper_1602_05650_b200.configs so the
+device path, the oracle and the reference see bit-identical arrays.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import numba  # noqa: E402
+import scipy  # noqa: E402
+from slenderflow import body, fiber, kernels, system  # noqa: E402
+
+from paper_1602_05650_b200 import configs  # noqa: E402
+
+
+def versions():
+    return dict(numpy=np.__version__, scipy=scipy.__version__, numba=numba.__version__)
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def pairs_small():
+    """Pair kernels on random inputs, with group exclusion and coincidences."""
+    rng = np.random.default_rng(2024)
+    ns, nt = 300, 200
+    src = rng.standard_normal((ns, 3)) * 1.5
+    sgrp = np.repeat(np.arange(10, dtype=np.int64), 30)
+    f = rng.standard_normal((ns, 3))
+    trg = rng.standard_normal((nt, 3)) * 1.5
+    tgrp = rng.integers(-1, 10, nt).astype(np.int64)
+    # coincidences: target 0 on source 5 (same group -> excluded, not bad);
+    # target 1 on source 40 in a different group -> bad
+    trg[0] = src[5]
+    tgrp[0] = sgrp[5]
+    trg[1] = src[40]
+    tgrp[1] = 7
+    pref = 1.0 / (8.0 * np.pi * 0.9)
+    st, st_bad = kernels.stokeslet_sum(trg, tgrp, src, sgrp, f, pref)
+    db, db_bad = kernels.doublet_sum(trg, tgrp, src, sgrp, f, pref)
+    nrm = rng.standard_normal((ns, 3))
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    qw = rng.standard_normal((ns, 3))
+    sp = -3.0 / (4.0 * np.pi * 1.1)
+    ss, ss_bad = kernels.stresslet_sum(trg, tgrp, src, sgrp, nrm, qw, sp)
+    # surface self terms on a sphere mesh
+    mesh = body.make_surface(body.sphere_shape(1.3), (4, 6))
+    q = rng.standard_normal((mesh.n_nodes, 3))
+    sub = kernels.stresslet_sum_subtracted(mesh.nodes, mesh.normals, mesh.weights, q, sp)
+    rsum = kernels.stresslet_rowsum(mesh.nodes, mesh.normals, mesh.weights, sp)
+    const = np.tile([0.4, -1.0, 2.0], (mesh.n_nodes, 1))
+    sub_const = kernels.stresslet_sum_subtracted(mesh.nodes, mesh.normals, mesh.weights, const, sp)
+    # K_delta of a bent fiber
+    p = 24
+    g = fiber.shared_grid(p)
+    th = (g.nodes + 1.0) * 0.4
+    X = np.stack([np.cos(th), np.sin(th), 0.1 * th], axis=1)
+    fib = fiber.Fiber(X, eps=0.01, E=1.0)
+    K = fib.kdelta_matrix(0.7)
+    save("pairs_small.npz", src=src, sgrp=sgrp, f=f, trg=trg, tgrp=tgrp, pref=pref,
+         stokeslet=st, stokeslet_bad=st_bad, doublet=db, doublet_bad=db_bad,
+         nrm=nrm, qw=qw, spref=sp, stresslet=ss, stresslet_bad=ss_bad,
+         mesh_nodes=mesh.nodes, mesh_normals=mesh.normals, mesh_weights=mesh.weights,
+         q=q, subtracted=sub, rowsum=rsum, subtracted_const=sub_const,
+         kd_X=X, kd_s=fib.s, kd_sa=fib.s_alpha, kd_t=fib.tangents, kd_w=g.weights,
+         kd_delta=fib.delta, kd_pref=1.0 / (8.0 * np.pi * 0.7), kd_K=K, **versions())
+
+
+def operator_fixture(name, cloud, seed_f=1, mu=1.0, keep_k=2):
+    """C1-form HI operator: complementary_velocities + local self terms."""
+    f = configs.forces(cloud, seed=seed_f)
+    fibs = [fiber.Fiber(X, eps=cloud.eps, E=cloud.E) for X in cloud.X]
+    st = system.SystemState(fibs, mu=mu)
+    cache = system.InteractionCache(st)
+    res = system.complementary_velocities(st, fiber_forces=list(f), cache=cache)
+    u_nl = np.vstack(res.fibers)
+    u_self = np.vstack([fiber.local_mobility_apply(fb, fm, mu) + fiber.nonlocal_Kdelta_apply(fb, fm, mu)
+                        for fb, fm in zip(fibs, f)])
+    near_t = np.array([t for t, _, _ in cache.near_fiber], dtype=np.int64)
+    near_l = np.array([l for _, l, _ in cache.near_fiber], dtype=np.int64)
+    near_W = (np.stack([W for _, _, W in cache.near_fiber]) if cache.near_fiber
+              else np.zeros((0, 3, 3 * cloud.n_nodes)))
+    geo = dict(s=np.stack([fb.s for fb in fibs]), s_alpha=np.stack([fb.s_alpha for fb in fibs]),
+               tangents=np.stack([fb.tangents for fb in fibs]), L=np.array([fb.L for fb in fibs]),
+               delta=np.array([fb.delta for fb in fibs]),
+               weights=np.stack([fb.node_weights() for fb in fibs]))
+    Ks = np.stack([fibs[m].kdelta_matrix(mu) for m in range(keep_k)])
+    save(name, X=cloud.X, forces=f, eps=cloud.eps, E=cloud.E, mu=mu, p=cloud.p,
+         u_nl=u_nl, u_self=u_self, near_t=near_t, near_l=near_l, near_W=near_W, K=Ks,
+         **geo, **versions())
+    print(f"  {name}: {len(cache.near_fiber)} near pairs")
+
+
+def surfaces_fixture():
+    """Fibers + rigid particle + periphery: every surface term of the operator."""
+    per = body.Periphery(body.make_surface(body.sphere_shape(6.0), (8, 8)))
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(1.0), (6, 6)))
+    part.F_ext = np.array([0.3, -0.1, 2.0])
+    part.L_ext = np.array([0.05, 0.2, -0.1])
+    fibs = [fiber.straight_fiber(15, (2.5, 0.0, -1.0), (0, 0, 1.0), 2.0),
+            fiber.straight_fiber(15, (-2.4, 0.5, -0.5), (0.6, 0.8, 0.0), 1.5),
+            fiber.straight_fiber(15, (0.3, 2.6, 0.2), (0.0, 0.6, 0.8), 1.8)]
+    st = system.SystemState(fibs, [part], per)
+    rng = np.random.default_rng(99)
+    q0 = rng.standard_normal((per.mesh.n_nodes, 3)) * 0.1
+    q1 = rng.standard_normal((part.mesh.n_nodes, 3)) * 0.1
+    f = [rng.standard_normal((16, 3)) for _ in fibs]
+    wrench = (part.F_ext, part.L_ext)
+    cache = system.InteractionCache(st)
+    res = system.complementary_velocities(st, periphery_density=q0, particle_densities=[q1],
+                                          fiber_forces=f, particle_wrenches=[wrench], cache=cache)
+    mu = st.mu
+    save("surfaces.npz",
+         per_nodes=per.mesh.nodes, per_normals=per.mesh.normals, per_weights=per.mesh.weights,
+         part_nodes=part.mesh.nodes, part_normals=part.mesh.normals,
+         part_weights=part.mesh.weights, part_center=part.center,
+         F_ext=part.F_ext, L_ext=part.L_ext,
+         X=np.stack([fb.X for fb in fibs]), eps=0.01, L=np.array([fb.L for fb in fibs]),
+         weights=np.stack([fb.node_weights() for fb in fibs]), forces=np.stack(f),
+         q0=q0, q1=q1, u_per=res.periphery, u_part=res.particles[0],
+         u_fib=np.vstack(res.fibers), n_near_fiber=len(cache.near_fiber),
+         n_near_surface=len(cache.near_surface),
+         dl_on_per=body.double_layer_onsurface(per.mesh, q0, mu),
+         dl_on_part=body.double_layer_onsurface(part.mesh, q1, mu),
+         rowsum_part=kernels.stresslet_rowsum(part.mesh.nodes, part.mesh.normals,
+                                              part.mesh.weights, -3.0 / (4.0 * np.pi * mu)),
+         **versions())
+    print(f"  surfaces: near fiber {len(cache.near_fiber)}, near surface {len(cache.near_surface)}")
+
+
+if __name__ == "__main__":
+    pairs_small()
+    operator_fixture("c1_near.npz", configs.make("c1", seed=0))
+    operator_fixture("c1_clean.npz", configs.make("c1_clean", seed=0))
+    surfaces_fixture()
