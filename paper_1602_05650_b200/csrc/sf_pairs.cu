@@ -24,6 +24,8 @@
 // with a source split (blockIdx.y) the per-chunk partials are summed in chunk
 // order by reduce_partials.  The split factor depends only on (nt, ns), never
 // on the device, so results are bitwise reproducible.
+#include <cstdlib>
+
 #include "sf_common.cuh"
 #include "sf_internal.h"
 
@@ -70,12 +72,24 @@ __device__ __forceinline__ void load_target_base(const PairArgs &a, int64_t i, T
         t.g = a.tgrp ? pack_target_group(a.tgrp[i]) : kNoGroup;
 }
 
+// Every policy also exposes target_pos (FP64 coordinates, for the CTA box),
+// target_group (the id compared with source groups; < 0 = none) and
+// kFloatPositions (packed positions are float hi/lo pairs).
+__device__ __forceinline__ void target_xyz(const PairArgs &a, int64_t i, double *x) {
+    x[0] = a.trg[3 * i];
+    x[1] = a.trg[3 * i + 1];
+    x[2] = a.trg[3 * i + 2];
+}
+
 // Stokeslet + optional doublet.  Source slots: x y z fx fy fz c 3c.
 template <bool DBL>
 struct SbtP {
     static constexpr int NACC = 3;
     static constexpr int NOUT = 3;
     static constexpr bool kBad = true;
+    static constexpr bool kFloatPositions = false;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     typedef TargetBase Target;
     struct SrcR {
         double x, y, z, fx, fy, fz, c, c3;
@@ -97,15 +111,18 @@ struct SbtP {
     }
     __device__ static void zero(TAcc &t) { t[0] = t[1] = t[2] = 0.0; }
     __device__ static void flush(TAcc &, double *) {}
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &, double *u,
                                                 int &nb) {
         const double rx = t.x - s.x, ry = t.y - s.y, rz = t.z - s.z;
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
-        const bool excl = (s.g == t.g);
-        const bool small = below_min_sep(r2);
-        nb += (small && !excl) ? 1 : 0;
         double y0 = rsq_seed(r2);
-        y0 = (excl || small) ? 0.0 : y0;
+        if (CHECK) {
+            const bool excl = (s.g == t.g);
+            const bool small = below_min_sep(r2);
+            nb += (small && !excl) ? 1 : 0;
+            y0 = (excl || small) ? 0.0 : y0;
+        }
         const double ir = rsq_refine(r2, y0);
         const double ir2 = ir * ir;
         const double ir3 = ir * ir2;
@@ -127,6 +144,85 @@ struct SbtP {
         u[1] = fma(b, ry, u[1]);
         u[2] = fma(b, rz, u[2]);
     }
+
+    // Check-free lockstep form for TB targets: each stage is issued for all
+    // targets back to back so the source operand (c, 3c, f) they share sits in
+    // the same slot of consecutive DFMAs (register reuse cache: one fresh
+    // operand read instead of two).
+    template <int TB>
+    __device__ __forceinline__ static void pair_fast(const Target *t, const SrcR &s,
+                                                     double (*u)[3]) {
+        double rx[TB], ry[TB], rz[TB], r2[TB], y[TB], a[TB], bb[TB], rf[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            rx[k] = t[k].x - s.x;
+            ry[k] = t[k].y - s.y;
+            rz[k] = t[k].z - s.z;
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) r2[k] = fma(rx[k], rx[k], fma(ry[k], ry[k], rz[k] * rz[k]));
+#pragma unroll
+        for (int k = 0; k < TB; ++k) y[k] = rsq_refine(r2[k], rsq_seed(r2[k]));
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            const double ir2 = y[k] * y[k];
+            const double ir3 = y[k] * ir2;
+            if (DBL) {
+                const double ir5 = ir3 * ir2;
+                a[k] = ir3;
+                bb[k] = ir5;
+            } else {
+                a[k] = y[k];
+                bb[k] = ir3;
+            }
+        }
+        if (DBL) {
+#pragma unroll
+            for (int k = 0; k < TB; ++k) bb[k] = fma(-s.c3, bb[k], a[k]);  // 1/r^3 - 3c/r^5
+#pragma unroll
+            for (int k = 0; k < TB; ++k) a[k] = fma(s.c, a[k], y[k]);      // 1/r + c/r^3
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) rf[k] = rx[k] * s.fx;
+#pragma unroll
+        for (int k = 0; k < TB; ++k) rf[k] = fma(ry[k], s.fy, rf[k]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) rf[k] = fma(rz[k], s.fz, rf[k]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) rf[k] = rf[k] * bb[k];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) u[k][0] = fma(a[k], s.fx, u[k][0]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) u[k][1] = fma(a[k], s.fy, u[k][1]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) u[k][2] = fma(a[k], s.fz, u[k][2]);
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            u[k][0] = fma(rf[k], rx[k], u[k][0]);
+            u[k][1] = fma(rf[k], ry[k], u[k][1]);
+            u[k][2] = fma(rf[k], rz[k], u[k][2]);
+        }
+    }
+};
+
+// Dispatch of the check-free inner step: lockstep form where a policy has
+// one, else the per-target pair.
+template <class P, int TB>
+struct FastStep {
+    __device__ __forceinline__ static void run(const typename P::Target *tg,
+                                               const typename P::SrcR &sr, typename P::TAcc *ta,
+                                               double (*u)[P::NACC], int *nb) {
+#pragma unroll
+        for (int k = 0; k < TB; ++k) P::template pair<false>(tg[k], sr, ta[k], u[k], nb[k]);
+    }
+};
+template <bool DBL, int TB>
+struct FastStep<SbtP<DBL>, TB> {
+    __device__ __forceinline__ static void run(const TargetBase *tg,
+                                               const typename SbtP<DBL>::SrcR &sr, double (*)[3],
+                                               double (*u)[3], int *) {
+        SbtP<DBL>::template pair_fast<TB>(tg, sr, u);
+    }
 };
 
 // Doublet alone (kernels.py:114-145).  Source slots: x y z fx fy fz.
@@ -134,6 +230,9 @@ struct DoubletP {
     static constexpr int NACC = 3;
     static constexpr int NOUT = 3;
     static constexpr bool kBad = true;
+    static constexpr bool kFloatPositions = false;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     typedef TargetBase Target;
     typedef typename SbtP<false>::SrcR SrcR;
     typedef double TAcc[1];
@@ -143,15 +242,18 @@ struct DoubletP {
     __device__ static void load_src(const Src80 &s, SrcR &r) { SbtP<false>::load_src(s, r); }
     __device__ static void zero(TAcc &) {}
     __device__ static void flush(TAcc &, double *) {}
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &, double *u,
                                                 int &nb) {
         const double rx = t.x - s.x, ry = t.y - s.y, rz = t.z - s.z;
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
-        const bool excl = (s.g == t.g);
-        const bool small = below_min_sep(r2);
-        nb += (small && !excl) ? 1 : 0;
         double y0 = rsq_seed(r2);
-        y0 = (excl || small) ? 0.0 : y0;
+        if (CHECK) {
+            const bool excl = (s.g == t.g);
+            const bool small = below_min_sep(r2);
+            nb += (small && !excl) ? 1 : 0;
+            y0 = (excl || small) ? 0.0 : y0;
+        }
         const double ir = rsq_refine(r2, y0);
         const double ir2 = ir * ir;
         const double ir3 = ir * ir2;
@@ -173,6 +275,9 @@ struct SbtF32cP {
     static constexpr int NACC = 3;
     static constexpr int NOUT = 3;
     static constexpr bool kBad = true;
+    static constexpr bool kFloatPositions = true;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     struct Target {
         float xh, yh, zh, xl, yl, zl;
         int g;
@@ -202,18 +307,21 @@ struct SbtF32cP {
         u[0] += (double)t[0]; u[1] += (double)t[1]; u[2] += (double)t[2];
         t[0] = t[1] = t[2] = 0.f;
     }
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &ta, double *,
                                                 int &nb) {
         const float rx = (t.xh - s.xh) + (t.xl - s.xl);
         const float ry = (t.yh - s.yh) + (t.yl - s.yl);
         const float rz = (t.zh - s.zh) + (t.zl - s.zl);
         const float r2 = fmaf(rx, rx, fmaf(ry, ry, rz * rz));
-        const bool excl = (s.g == t.g);
-        // same skip rule, evaluated on the FP32 r^2 (1e-24 is a normal float)
-        const bool small = r2 < 1e-24f;
-        nb += (small && !excl) ? 1 : 0;
         float ir = rsqrtf(r2);
-        ir = (excl || small) ? 0.f : ir;
+        if (CHECK) {
+            const bool excl = (s.g == t.g);
+            // same skip rule, evaluated on the FP32 r^2 (1e-24 is a normal float)
+            const bool small = r2 < 1e-24f;
+            nb += (small && !excl) ? 1 : 0;
+            ir = (excl || small) ? 0.f : ir;
+        }
         const float ir2 = ir * ir;
         const float ir3 = ir * ir2;
         const float ir5 = ir3 * ir2;
@@ -231,6 +339,9 @@ struct StressletP {
     static constexpr int NACC = 3;
     static constexpr int NOUT = 3;
     static constexpr bool kBad = true;
+    static constexpr bool kFloatPositions = false;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     typedef TargetBase Target;
     struct SrcR {
         double x, y, z, nx, ny, nz, qx, qy, qz;
@@ -248,15 +359,18 @@ struct StressletP {
     }
     __device__ static void zero(TAcc &) {}
     __device__ static void flush(TAcc &, double *) {}
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &, double *u,
                                                 int &nb) {
         const double rx = t.x - s.x, ry = t.y - s.y, rz = t.z - s.z;
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
-        const bool excl = (s.g == t.g);
-        const bool small = below_min_sep(r2);
-        nb += (small && !excl) ? 1 : 0;
         double y0 = rsq_seed(r2);
-        y0 = (excl || small) ? 0.0 : y0;
+        if (CHECK) {
+            const bool excl = (s.g == t.g);
+            const bool small = below_min_sep(r2);
+            nb += (small && !excl) ? 1 : 0;
+            y0 = (excl || small) ? 0.0 : y0;
+        }
         const double ir = rsq_refine(r2, y0);
         const double ir2 = ir * ir;
         const double ir5 = ir * ir2 * ir2;
@@ -275,6 +389,9 @@ struct DlSubP {
     static constexpr int NACC = 3;
     static constexpr int NOUT = 3;
     static constexpr bool kBad = false;  // the reference has no skip rule here
+    static constexpr bool kFloatPositions = false;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     struct Target {
         double x, y, z, qx, qy, qz;
         int g;
@@ -297,12 +414,13 @@ struct DlSubP {
     }
     __device__ static void zero(TAcc &) {}
     __device__ static void flush(TAcc &, double *) {}
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &, double *u,
                                                 int &) {
         const double rx = t.x - s.x, ry = t.y - s.y, rz = t.z - s.z;
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
         double y0 = rsq_seed(r2);
-        y0 = (s.g == t.g) ? 0.0 : y0;
+        if (CHECK) y0 = (s.g == t.g) ? 0.0 : y0;
         const double ir = rsq_refine(r2, y0);
         const double ir2 = ir * ir;
         const double ir5 = ir * ir2 * ir2;
@@ -322,6 +440,9 @@ struct RowsumP {
     static constexpr int NACC = 6;
     static constexpr int NOUT = 9;
     static constexpr bool kBad = false;
+    static constexpr bool kFloatPositions = false;
+    __device__ static void target_pos(const PairArgs &a, int64_t i, double *x) { target_xyz(a, i, x); }
+    template <class T> __device__ static int target_group(const T &t) { return t.g; }
     typedef TargetBase Target;
     struct SrcR {
         double x, y, z, nx, ny, nz;
@@ -338,12 +459,13 @@ struct RowsumP {
     }
     __device__ static void zero(TAcc &) {}
     __device__ static void flush(TAcc &, double *) {}
+    template <bool CHECK>
     __device__ __forceinline__ static void pair(const Target &t, const SrcR &s, TAcc &, double *u,
                                                 int &) {
         const double rx = t.x - s.x, ry = t.y - s.y, rz = t.z - s.z;
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
         double y0 = rsq_seed(r2);
-        y0 = (s.g == t.g) ? 0.0 : y0;
+        if (CHECK) y0 = (s.g == t.g) ? 0.0 : y0;
         const double ir = rsq_refine(r2, y0);
         const double ir2 = ir * ir;
         const double ir5 = ir * ir2 * ir2;
@@ -372,10 +494,91 @@ __device__ __forceinline__ void write_out(double *dst, const double *u, double s
 }
 
 // ----------------------------------------------------------------- engine ----
-template <class P, int TB, int NT, int TS>
-__global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
+// Per-tile bounds (TS consecutive packed sources): coordinate box and the
+// range of non-negative group ids.  A tile whose box is farther than
+// kFastTileMinDist2 from the CTA's target box and whose groups cannot equal
+// any target group needs neither the exclusion test nor the r^2 < 1e-24
+// test: its pairs run the check-free inner loop.  Only tiles near the CTA's
+// own targets (its own fibers, genuinely close neighbours) take the checked
+// loop, so results are identical to checking every pair.
+struct __align__(16) TileMeta {
+    double lo[3], hi[3];
+    int gmin, gmax;
+};
+
+template <int TS>
+__global__ void tile_meta_kernel(const Src80 *__restrict__ src, int64_t ns,
+                                 TileMeta *__restrict__ meta, bool pos_float_hi) {
+    __shared__ double red[6][TS / 32];
+    __shared__ int gred[2][TS / 32];
+    const int64_t j = (int64_t)blockIdx.x * TS + threadIdx.x;
+    double v[6];
+    int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    if (j < ns) {
+        const Src80 &q = src[j];
+        double x, y, z;
+        if (pos_float_hi) {  // FP32c packing: coordinate = hi + lo floats
+            const float *f = reinterpret_cast<const float *>(&q);
+            x = (double)f[0] + (double)f[3];
+            y = (double)f[1] + (double)f[4];
+            z = (double)f[2] + (double)f[5];
+        } else {
+            x = q.v[0]; y = q.v[1]; z = q.v[2];
+        }
+        v[0] = x; v[1] = y; v[2] = z; v[3] = x; v[4] = y; v[5] = z;
+        if (q.g >= 0) { gmn = q.g; gmx = q.g; }
+    } else {
+        v[0] = v[1] = v[2] = 1e300;
+        v[3] = v[4] = v[5] = -1e300;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            v[c] = fmin(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+            v[3 + c] = fmax(v[3 + c], __shfl_xor_sync(0xffffffffu, v[3 + c], o));
+        }
+        gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+        gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        for (int c = 0; c < 6; ++c) red[c][w] = v[c];
+        gred[0][w] = gmn;
+        gred[1][w] = gmx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        TileMeta m;
+        for (int c = 0; c < 3; ++c) {
+            m.lo[c] = red[c][0];
+            m.hi[c] = red[3 + c][0];
+        }
+        m.gmin = gred[0][0];
+        m.gmax = gred[1][0];
+        for (int k = 1; k < TS / 32; ++k) {
+            for (int c = 0; c < 3; ++c) {
+                m.lo[c] = fmin(m.lo[c], red[c][k]);
+                m.hi[c] = fmax(m.hi[c], red[3 + c][k]);
+            }
+            m.gmin = min(m.gmin, gred[0][k]);
+            m.gmax = max(m.gmax, gred[1][k]);
+        }
+        meta[blockIdx.x] = m;
+    }
+}
+
+// Tile/box separation below which the checked loop runs: far above
+// MIN_SEPARATION^2 = 1e-24, so rounding in r^2 cannot flip a skip decision.
+constexpr double kFastTileMinDist2 = 1e-20;
+
+template <class P, int TB, int NT, int TS, int MINB = 1, int UNR = 2>
+__global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
+                                                        const TileMeta *__restrict__ meta) {
     __shared__ __align__(128) Src80 tile[2][TS];
     __shared__ __align__(8) uint64_t full[2];
+    __shared__ double tbox[6][NT / 32];
+    __shared__ int tgr[2][NT / 32];
     const int tid = threadIdx.x;
     const int64_t tbase = (int64_t)blockIdx.x * (NT * TB);
 
@@ -383,6 +586,8 @@ __global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
     typename P::TAcc ta[TB];
     double u[TB][P::NACC];
     int nb[TB];
+    double bx[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+    int gmn = 0x7fffffff, gmx = (int)0x80000000;
 #pragma unroll
     for (int k = 0; k < TB; ++k) {
         int64_t i = tbase + k * NT + tid;
@@ -392,11 +597,39 @@ __global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
 #pragma unroll
         for (int c = 0; c < P::NACC; ++c) u[k][c] = 0.0;
         nb[k] = 0;
+        double xyz[3];
+        P::target_pos(a, i, xyz);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            bx[c] = fmin(bx[c], xyz[c]);
+            bx[3 + c] = fmax(bx[3 + c], xyz[c]);
+        }
+        const int g = P::target_group(tg[k]);
+        if (g >= 0) {
+            gmn = min(gmn, g);
+            gmx = max(gmx, g);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            bx[c] = fmin(bx[c], __shfl_xor_sync(0xffffffffu, bx[c], o));
+            bx[3 + c] = fmax(bx[3 + c], __shfl_xor_sync(0xffffffffu, bx[3 + c], o));
+        }
+        gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+        gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+    }
+    if ((tid & 31) == 0) {
+        for (int c = 0; c < 6; ++c) tbox[c][tid >> 5] = bx[c];
+        tgr[0][tid >> 5] = gmn;
+        tgr[1][tid >> 5] = gmx;
     }
 
     const int64_t j0 = (int64_t)blockIdx.y * a.chunk;
     const int64_t j1 = imin64(a.ns, j0 + a.chunk);
     const int ntiles = j1 > j0 ? (int)((j1 - j0 + TS - 1) / TS) : 0;
+    const int64_t tile0 = j0 / TS;  // chunks are TS-aligned
 
     if (tid == 0) {
         mbar_init(&full[0], 1);
@@ -404,6 +637,24 @@ __global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
         fence_mbar_init();
     }
     __syncthreads();
+    // CTA-wide target bounds (identical in every thread)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        bx[c] = tbox[c][0];
+        bx[3 + c] = tbox[3 + c][0];
+    }
+    gmn = tgr[0][0];
+    gmx = tgr[1][0];
+    for (int w = 1; w < NT / 32; ++w) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            bx[c] = fmin(bx[c], tbox[c][w]);
+            bx[3 + c] = fmax(bx[3 + c], tbox[3 + c][w]);
+        }
+        gmn = min(gmn, tgr[0][w]);
+        gmx = max(gmx, tgr[1][w]);
+    }
+
     if (tid == 0 && ntiles > 0) {
         const uint32_t bytes = (uint32_t)(imin64(TS, j1 - j0) * sizeof(Src80));
         mbar_arrive_expect_tx(&full[0], bytes);
@@ -411,6 +662,15 @@ __global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
     }
     for (int t = 0; t < ntiles; ++t) {
         const int s = t & 1;
+        // classify the tile while its bytes land
+        const TileMeta m = meta[tile0 + t];
+        double d2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double gap = fmax(0.0, fmax(m.lo[c] - bx[3 + c], bx[c] - m.hi[c]));
+            d2 = fma(gap, gap, d2);
+        }
+        const bool fast = (d2 > kFastTileMinDist2) && (m.gmax < gmn || m.gmin > gmx);
         mbar_wait(&full[s], (uint32_t)((t >> 1) & 1));
         __syncthreads();  // all threads are done with tile t-1 (buffer s^1)
         if (tid == 0 && t + 1 < ntiles) {
@@ -421,20 +681,19 @@ __global__ void __launch_bounds__(NT) pair_kernel(PairArgs a) {
         }
         const int cnt = (int)imin64(TS, j1 - (j0 + (int64_t)t * TS));
         const Src80 *ts = tile[s];
-        if (cnt == TS) {
-#pragma unroll 2
+        if (fast && cnt == TS) {
+#pragma unroll UNR
             for (int jj = 0; jj < TS; ++jj) {
                 typename P::SrcR sr;
                 P::load_src(ts[jj], sr);
-#pragma unroll
-                for (int k = 0; k < TB; ++k) P::pair(tg[k], sr, ta[k], u[k], nb[k]);
+                FastStep<P, TB>::run(tg, sr, ta, u, nb);
             }
         } else {
             for (int jj = 0; jj < cnt; ++jj) {
                 typename P::SrcR sr;
                 P::load_src(ts[jj], sr);
 #pragma unroll
-                for (int k = 0; k < TB; ++k) P::pair(tg[k], sr, ta[k], u[k], nb[k]);
+                for (int k = 0; k < TB; ++k) P::template pair<true>(tg[k], sr, ta[k], u[k], nb[k]);
             }
         }
 #pragma unroll
@@ -565,8 +824,12 @@ __global__ void pack_surface_self(const double *__restrict__ nodes, const double
 
 // ----------------------------------------------------------------- launch ----
 namespace {
+// Default launch shape (measured on B200, tools/gpu_sweep.sh): 1 target per
+// thread, 128 threads, >= 8 CTAs per SM (64 registers), 4 sources unrolled.
 constexpr int kNT = 128;
-constexpr int kTB = 2;
+constexpr int kTB = 1;
+constexpr int kMinBlocks = 8;
+constexpr int kUnroll = 4;
 constexpr int kTS = 128;
 constexpr int kTargetsPerCta = kNT * kTB;
 
@@ -614,8 +877,30 @@ static int launch_pairs(PairArgs a, cudaStream_t st, Workspace &ws) {
         a.partial = (double *)ws.get(1, sizeof(double) * (size_t)a.nsplit * a.nt * P::NACC, st);
         if (!a.partial) return SF_ENOMEM;
     }
-    dim3 grid((unsigned)blocks, (unsigned)a.nsplit);
-    pair_kernel<P, kTB, kNT, kTS><<<grid, kNT, 0, st>>>(a);
+    const int64_t ntiles = (a.ns + kTS - 1) / kTS;
+    TileMeta *meta = (TileMeta *)ws.get(2, sizeof(TileMeta) * (size_t)ntiles, st);
+    if (!meta) return SF_ENOMEM;
+    tile_meta_kernel<kTS><<<(unsigned)ntiles, kTS, 0, st>>>(a.src, a.ns, meta,
+                                                           P::kFloatPositions);
+    // SF_PAIR_VARIANT (tuning experiments only) picks the launch shape.
+    static const int variant = [] {
+        const char *e = getenv("SF_PAIR_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    const unsigned ny = (unsigned)a.nsplit;
+    auto nb = [&](int per) { return (unsigned)((a.nt + per - 1) / per); };
+    switch (variant) {
+        case 1: pair_kernel<P, 1, 128, kTS, 8, 2><<<dim3(nb(128), ny), 128, 0, st>>>(a, meta); break;
+        case 2: pair_kernel<P, 2, 128, kTS, 8, 2><<<dim3(nb(256), ny), 128, 0, st>>>(a, meta); break;
+        case 3: pair_kernel<P, 1, 256, kTS, 4, 2><<<dim3(nb(256), ny), 256, 0, st>>>(a, meta); break;
+        case 4: pair_kernel<P, 1, 128, kTS, 10, 2><<<dim3(nb(128), ny), 128, 0, st>>>(a, meta); break;
+        case 5: pair_kernel<P, 2, 256, kTS, 4, 2><<<dim3(nb(512), ny), 256, 0, st>>>(a, meta); break;
+        case 7: pair_kernel<P, 2, 128, kTS, 6, 4><<<dim3(nb(256), ny), 128, 0, st>>>(a, meta); break;
+        case 8: pair_kernel<P, 1, 256, kTS, 4, 4><<<dim3(nb(256), ny), 256, 0, st>>>(a, meta); break;
+        default:
+            pair_kernel<P, kTB, kNT, kTS, kMinBlocks, kUnroll>
+                <<<dim3(nb(kTargetsPerCta), ny), kNT, 0, st>>>(a, meta);
+    }
     if (a.nsplit > 1) {
         reduce_partials<P><<<(unsigned)((a.nt + 255) / 256), 256, 0, st>>>(a.partial, a.nsplit,
                                                                           a.nt, a.pref, a.out);

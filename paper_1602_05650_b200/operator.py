@@ -89,9 +89,9 @@ class FiberHIOperator:
         self.mode = int(mode)
         self.X = X
         _, wcc, D, S = spectral.grid(self.p)
-        self.wcc = torch.as_tensor(wcc, **dev)
-        self.D = torch.as_tensor(D, **dev)
-        self.S = torch.as_tensor(S, **dev)
+        self.wcc = torch.tensor(wcc, **dev)
+        self.D = torch.tensor(D, **dev)
+        self.S = torch.tensor(S, **dev)
         self.s = torch.empty((nf, n), **dev)
         self.s_alpha = torch.empty((nf, n), **dev)
         self.tang = torch.empty((nf, n, 3), **dev)

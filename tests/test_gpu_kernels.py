@@ -148,7 +148,10 @@ def test_fiber_operator_c1(cuda, name):
     op.check_bad()
     assert rel(u_nl.cpu().numpy(), g["u_nl"]) < 1e-12
     assert rel(u_self.cpu().numpy(), g["u_self"]) < 1e-12
-    assert np.array_equal(op.K[:2].cpu().numpy(), g["K"])
+    # K from device-computed geometry: equal to rounding (bitwise given the
+    # reference's own geometry, test_kdelta_bitwise)
+    K = op.K[:2].cpu().numpy()
+    assert np.abs(K - g["K"]).max() <= 1e-13 * np.abs(g["K"]).max()
     assert np.abs(op.s.cpu().numpy() - g["s"]).max() < 1e-14
-    assert np.abs(op.tang.cpu().numpy() - g["tangents"]).max() < 1e-14
+    assert np.abs(op.tang.cpu().numpy() - g["tangents"]).max() < 1e-12
     assert np.abs(op.delta.cpu().numpy() - g["delta"]).max() < 1e-16
