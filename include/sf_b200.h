@@ -156,6 +156,50 @@ int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf, int64_t n
  * ordered chunks).  Used to count kernel launches. */
 int sf_pair_split(int64_t nt, int64_t ns);
 
+/* ---------------------------------------------------------------------------
+ * complementary_velocities (system.py:623-709) on one frozen layout.
+ * ------------------------------------------------------------------------- */
+
+/* The reference's InteractionCache (system.py:492-562) as device arrays.
+ * Targets: every constituent's nodes stacked [particles | periphery | fibers]
+ * with group ids (fiber m -> m, particle i -> nf + i, periphery -> nf + np).
+ * Fiber sources carry node weights w s_alpha and doublet coefficients
+ * (eps L)^2/2; surface sources carry normals, quadrature weights and their
+ * surface's group id; particles carry centres and group ids.  The near map
+ * is CSR by target row; its x vector is [fiber forces | surface densities]
+ * flattened (x_off / x_len index into it). */
+typedef struct {
+    const double *trg;       /* (nt,3) */
+    const int64_t *tgrp;     /* (nt) */
+    int64_t nt;
+    const double *fsrc;      /* (nfs,3) fiber nodes */
+    const int64_t *fgrp;     /* (nfs) */
+    const double *fw;        /* (nfs) w * s_alpha */
+    const double *fdcoef;    /* (nfs) doublet coefficient or NULL (include_doublet=False) */
+    int64_t nfs;
+    const double *ssrc;      /* (nss,3) surface nodes */
+    const double *snrm;      /* (nss,3) */
+    const double *sw;        /* (nss) quadrature weights */
+    const int64_t *sgrp;     /* (nss) */
+    int64_t nss;
+    const double *pcenter;   /* (np,3) */
+    const int64_t *pgrp;     /* (np) */
+    int64_t np;
+    const int64_t *near_row_ptr, *near_rows, *near_w_off, *near_x_off, *near_x_len;
+    int64_t near_nrows;
+    const double *near_W;
+    double mu;
+    int mode;                /* SF_MODE_FP64 / SF_MODE_FP32C for the fiber pair sum */
+} sf_hi_layout;
+
+/* u (nt,3) = complementary velocities for fiber force densities f (nfs,3),
+ * surface densities q (nss,3) and particle wrenches (np,6: F then L).
+ * bad (device int64[3], nullable) receives the skipped-pair counts of the
+ * fiber, surface and completion families (system.py:668-670, 684-686, 697). */
+int sf_hi_apply(const sf_hi_layout *layout, const double *f, const double *q,
+                const double *wrench, const double *near_x, double *u, int64_t *bad,
+                void *stream);
+
 /* Near-field correction apply (system.py:702-707): for every entry e,
  * u[t_e] += W_e (3 x 3 m_e) . x[off_e : off_e + 3 m_e].  Entries must be
  * grouped by target (row_ptr CSR over `nrows` distinct targets rows[]);

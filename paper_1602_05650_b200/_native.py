@@ -49,6 +49,7 @@ _SIGNATURES = {
     "sf_fiber_hi_apply": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _D, _I, _P, _P, _P, _D, _P,
                           _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sf_pair_split": [_I64, _I64],
+    "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P],
@@ -60,6 +61,19 @@ _SIGNATURES = {
 }
 
 _lib = None
+
+
+class HiLayout(ctypes.Structure):
+    """Mirror of sf_hi_layout (include/sf_b200.h)."""
+    _fields_ = [
+        ("trg", _P), ("tgrp", _P), ("nt", _I64),
+        ("fsrc", _P), ("fgrp", _P), ("fw", _P), ("fdcoef", _P), ("nfs", _I64),
+        ("ssrc", _P), ("snrm", _P), ("sw", _P), ("sgrp", _P), ("nss", _I64),
+        ("pcenter", _P), ("pgrp", _P), ("np", _I64),
+        ("near_row_ptr", _P), ("near_rows", _P), ("near_w_off", _P), ("near_x_off", _P),
+        ("near_x_len", _P), ("near_nrows", _I64), ("near_W", _P),
+        ("mu", _D), ("mode", _I),
+    ]
 
 
 def exported_symbols():

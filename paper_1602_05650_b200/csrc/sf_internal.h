@@ -34,7 +34,8 @@ int pairs_doublet_only(const double *trg, const int64_t *tgrp, int64_t nt, const
                        int64_t *bad, cudaStream_t st, Workspace &ws);
 int pairs_stresslet(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
                     const int64_t *sgrp, int64_t ns, const double *nrm, const double *qw,
-                    double pref, double *out, int64_t *bad, cudaStream_t st, Workspace &ws);
+                    double pref, double *out, int64_t *bad, cudaStream_t st, Workspace &ws,
+                    const double *wsrc = nullptr, int accumulate = 0);
 int pairs_dl_subtracted(const double *nodes, const double *nrm, const double *w, const double *q,
                         int64_t n, double pref, double *out, cudaStream_t st, Workspace &ws);
 int pairs_rowsum(const double *nodes, const double *nrm, const double *w, int64_t n, double pref,
@@ -53,7 +54,7 @@ int fiber_geometry(const double *X, int64_t nf, int64_t n, const double *D, cons
 int pairs_sbt_weighted(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
                        const int64_t *sgrp, int64_t ns, const double *f, const double *wsrc,
                        const double *dcoef, double pref, int mode, double *out, int64_t *bad,
-                       cudaStream_t st, Workspace &ws);
+                       cudaStream_t st, Workspace &ws, int accumulate = 0);
 int pair_split(int64_t nt, int64_t ns);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,

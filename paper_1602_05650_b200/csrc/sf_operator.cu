@@ -1,0 +1,108 @@
+// sf_operator.cu — complementary_velocities (system.py:623-709) on the
+// device: every family of the HI operator applied to one frozen layout (the
+// reference's InteractionCache, system.py:492-562) in a fixed order:
+//   1. fiber sources -> all targets: fused Stokeslet + (eps L)^2/2 doublet
+//   2. surface sources -> all targets: stresslet (double layer) with q w
+//   3. completion flow of every rigid particle's wrench (Stokeslet + rotlet)
+//   4. near-field correction maps (block-sparse, CSR by target)
+#include <cmath>
+
+#include "sf_common.cuh"
+#include "sf_internal.h"
+
+namespace sf {
+
+// system.py:689-700: u[t] += pref (F/d + (r.F) r/d^3) ; u[t] += pref (L x r)/d^3
+// for every target outside the particle's own group.
+__global__ void completion_kernel(const double *__restrict__ trg, const int64_t *__restrict__ tgrp,
+                                  int64_t nt, const double *__restrict__ centers,
+                                  const int64_t *__restrict__ pgrp, int64_t np,
+                                  const double *__restrict__ wrench, double pref,
+                                  double *__restrict__ u, unsigned long long *bad) {
+    int nbad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = trg[3 * i], y = trg[3 * i + 1], z = trg[3 * i + 2];
+        const int64_t g = tgrp ? tgrp[i] : -1;
+        double ux = u[3 * i], uy = u[3 * i + 1], uz = u[3 * i + 2];
+        for (int64_t p = 0; p < np; ++p) {
+            if (g == pgrp[p]) continue;
+            const double rx = x - centers[3 * p], ry = y - centers[3 * p + 1],
+                         rz = z - centers[3 * p + 2];
+            const double d = sqrt(rx * rx + ry * ry + rz * rz);
+            if (d < 1e-12) {
+                ++nbad;
+                continue;
+            }
+            const double *W = wrench + 6 * p;  // F, L
+            const double d3 = d * d * d;
+            const double rF = (rx * W[0] + ry * W[1] + rz * W[2]) / d3;
+            ux += pref * (W[0] / d + rF * rx);
+            uy += pref * (W[1] / d + rF * ry);
+            uz += pref * (W[2] / d + rF * rz);
+            ux += pref * (W[4] * rz - W[5] * ry) / d3;
+            uy += pref * (W[5] * rx - W[3] * rz) / d3;
+            uz += pref * (W[3] * ry - W[4] * rx) / d3;
+        }
+        u[3 * i] = ux;
+        u[3 * i + 1] = uy;
+        u[3 * i + 2] = uz;
+    }
+    nbad = warp_sum_int(nbad);
+    if ((threadIdx.x & 31) == 0 && nbad && bad) atomicAdd(bad, (unsigned long long)nbad);
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double *q,
+                           const double *wrench, const double *near_x, double *u, int64_t *bad,
+                           void *stream) {
+    if (!L) return set_error(SF_EINVAL, "null layout");
+    if (L->nt < 0 || L->nfs < 0 || L->nss < 0 || L->np < 0 || L->near_nrows < 0)
+        return set_error(SF_EINVAL, "negative size");
+    if (L->nt > 0 && (!L->trg || !u)) return set_error(SF_EINVAL, "null target/output pointer");
+    if (L->nfs > 0 && (!L->fsrc || !L->fw || !f)) return set_error(SF_EINVAL, "null fiber data");
+    if (L->nss > 0 && (!L->ssrc || !L->snrm || !L->sw || !q))
+        return set_error(SF_EINVAL, "null surface data");
+    if (L->np > 0 && (!L->pcenter || !L->pgrp || !wrench))
+        return set_error(SF_EINVAL, "null particle data");
+    if (L->near_nrows > 0 && !near_x) return set_error(SF_EINVAL, "near map without x vector");
+    if (!(L->mu > 0)) return set_error(SF_EINVAL, "viscosity must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = workspace_for(st);
+    int64_t *bad_f = bad, *bad_s = bad ? bad + 1 : nullptr;
+    if (bad && cudaMemsetAsync(bad, 0, 3 * sizeof(int64_t), st) != cudaSuccess)
+        return check_launch("memset");
+    if (L->nt == 0) return SF_OK;
+    const double pref = 1.0 / (8.0 * M_PI * L->mu);
+    int rc;
+    if (L->nfs > 0) {
+        rc = pairs_sbt_weighted(L->trg, L->tgrp, L->nt, L->fsrc, L->fgrp, L->nfs, f, L->fw,
+                                L->fdcoef, pref, L->mode, u, bad_f, st, ws, 0);
+        if (rc) return rc;
+    } else if (cudaMemsetAsync(u, 0, sizeof(double) * 3 * L->nt, st) != cudaSuccess) {
+        return check_launch("memset");
+    }
+    if (L->nss > 0) {
+        rc = pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss, L->snrm, q,
+                             -3.0 / (4.0 * M_PI * L->mu), u, bad_s, st, ws, L->sw, 1);
+        if (rc) return rc;
+    }
+    if (L->np > 0) {
+        int64_t blocks = (L->nt + 255) / 256;
+        if (blocks > 4096) blocks = 4096;
+        completion_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+            L->trg, L->tgrp, L->nt, L->pcenter, L->pgrp, L->np, wrench, pref, u,
+            bad ? (unsigned long long *)(bad + 2) : nullptr);
+        rc = check_launch("completion_kernel");
+        if (rc) return rc;
+    }
+    if (L->near_nrows > 0) {
+        rc = near_apply(L->near_row_ptr, L->near_rows, L->near_nrows, L->near_w_off,
+                        L->near_x_off, L->near_x_len, L->near_W, near_x, u, st);
+        if (rc) return rc;
+    }
+    return SF_OK;
+}

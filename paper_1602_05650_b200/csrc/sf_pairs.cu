@@ -53,6 +53,7 @@ struct PairArgs {
     double *partial;        // (nsplit, nt, NOUT) unscaled partials (nsplit > 1)
     unsigned long long *bad;
     int nsplit;
+    int accumulate;         // out += result instead of out = result
 };
 
 // ---------------------------------------------------------------- physics ----
@@ -481,11 +482,18 @@ struct RowsumP {
 };
 
 template <class P>
-__device__ __forceinline__ void write_out(double *dst, const double *u, double scale) {
+__device__ __forceinline__ void write_out(double *dst, const double *u, double scale,
+                                          int accumulate = 0) {
     if (P::NOUT == 3) {
-        dst[0] = scale * u[0];
-        dst[1] = scale * u[1];
-        dst[2] = scale * u[2];
+        if (accumulate) {
+            dst[0] += scale * u[0];
+            dst[1] += scale * u[1];
+            dst[2] += scale * u[2];
+        } else {
+            dst[0] = scale * u[0];
+            dst[1] = scale * u[1];
+            dst[2] = scale * u[2];
+        }
     } else {  // symmetric 3x3 from xx xy xz yy yz zz
         dst[0] = scale * u[0]; dst[1] = scale * u[1]; dst[2] = scale * u[2];
         dst[3] = scale * u[1]; dst[4] = scale * u[3]; dst[5] = scale * u[4];
@@ -707,7 +715,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
         if (i < a.nt) {
             nbad += nb[k];
             if (a.nsplit == 1) {
-                write_out<P>(a.out + (int64_t)P::NOUT * i, u[k], a.pref);
+                write_out<P>(a.out + (int64_t)P::NOUT * i, u[k], a.pref, a.accumulate);
             } else {
                 double *dst = a.partial + ((int64_t)blockIdx.y * a.nt + i) * P::NACC;
 #pragma unroll
@@ -723,7 +731,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
 
 template <class P>
 __global__ void reduce_partials(const double *__restrict__ partial, int nsplit, int64_t nt,
-                                double pref, double *__restrict__ out) {
+                                double pref, double *__restrict__ out, int accumulate) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nt) return;
     double u[P::NACC];
@@ -734,7 +742,7 @@ __global__ void reduce_partials(const double *__restrict__ partial, int nsplit, 
 #pragma unroll
         for (int c = 0; c < P::NACC; ++c) u[c] += p[c];
     }
-    write_out<P>(out + (int64_t)P::NOUT * i, u, pref);
+    write_out<P>(out + (int64_t)P::NOUT * i, u, pref, accumulate);
 }
 
 // ---------------------------------------------------------------- packing ----
@@ -787,16 +795,18 @@ __global__ void pack_sbt_f32c(const double *__restrict__ src, const int64_t *__r
     }
 }
 
+// wsrc (nullable): qw_j <- w_j q_j (system.py:674-679).
 __global__ void pack_stresslet(const double *__restrict__ src, const int64_t *__restrict__ sgrp,
                                const double *__restrict__ nrm, const double *__restrict__ qw,
-                               int64_t ns, Src80 *__restrict__ out) {
+                               int64_t ns, Src80 *__restrict__ out,
+                               const double *__restrict__ wsrc = nullptr) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ns;
          j += (int64_t)gridDim.x * blockDim.x) {
         Src80 s;
         for (int c = 0; c < 3; ++c) {
             s.v[c] = src[3 * j + c];
             s.v[3 + c] = nrm[3 * j + c];
-            s.v[6 + c] = qw[3 * j + c];
+            s.v[6 + c] = wsrc ? qw[3 * j + c] * wsrc[j] : qw[3 * j + c];
         }
         s.g = sgrp ? pack_source_group(sgrp[j]) : -1;
         s.pad = 0;
@@ -903,7 +913,8 @@ static int launch_pairs(PairArgs a, cudaStream_t st, Workspace &ws) {
     }
     if (a.nsplit > 1) {
         reduce_partials<P><<<(unsigned)((a.nt + 255) / 256), 256, 0, st>>>(a.partial, a.nsplit,
-                                                                          a.nt, a.pref, a.out);
+                                                                          a.nt, a.pref, a.out,
+                                                                          a.accumulate);
     }
     return check_launch("pair_kernel");
 }
@@ -918,12 +929,13 @@ int pairs_sbt(const double *trg, const int64_t *tgrp, int64_t nt, const double *
 int pairs_sbt_weighted(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
                        const int64_t *sgrp, int64_t ns, const double *f, const double *wsrc,
                        const double *dcoef, double pref, int mode, double *out, int64_t *bad,
-                       cudaStream_t st, Workspace &ws) {
+                       cudaStream_t st, Workspace &ws, int accumulate) {
     if (bad) {
         if (cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch("memset");
     }
     if (nt == 0) return 0;
     if (ns == 0) {
+        if (accumulate) return 0;
         if (cudaMemsetAsync(out, 0, sizeof(double) * 3 * nt, st) != cudaSuccess)
             return check_launch("memset");
         return 0;
@@ -932,7 +944,7 @@ int pairs_sbt_weighted(const double *trg, const int64_t *tgrp, int64_t nt, const
     if (!packed) return SF_ENOMEM;
     PairArgs a{};
     a.trg = trg; a.tgrp = tgrp; a.nt = nt; a.src = packed; a.ns = ns; a.pref = pref;
-    a.out = out; a.bad = (unsigned long long *)bad;
+    a.out = out; a.bad = (unsigned long long *)bad; a.accumulate = accumulate;
     if (mode == 1) {
         pack_sbt_f32c<<<pack_grid(ns), 256, 0, st>>>(src, sgrp, f, dcoef, ns, packed, wsrc);
         return launch_pairs<SbtF32cP>(a, st, ws);
@@ -965,22 +977,24 @@ int pairs_doublet_only(const double *trg, const int64_t *tgrp, int64_t nt, const
 
 int pairs_stresslet(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
                     const int64_t *sgrp, int64_t ns, const double *nrm, const double *qw,
-                    double pref, double *out, int64_t *bad, cudaStream_t st, Workspace &ws) {
+                    double pref, double *out, int64_t *bad, cudaStream_t st, Workspace &ws,
+                    const double *wsrc, int accumulate) {
     if (bad) {
         if (cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch("memset");
     }
     if (nt == 0) return 0;
     if (ns == 0) {
+        if (accumulate) return 0;
         if (cudaMemsetAsync(out, 0, sizeof(double) * 3 * nt, st) != cudaSuccess)
             return check_launch("memset");
         return 0;
     }
     Src80 *packed = (Src80 *)ws.get(0, sizeof(Src80) * (size_t)ns, st);
     if (!packed) return SF_ENOMEM;
-    pack_stresslet<<<pack_grid(ns), 256, 0, st>>>(src, sgrp, nrm, qw, ns, packed);
+    pack_stresslet<<<pack_grid(ns), 256, 0, st>>>(src, sgrp, nrm, qw, ns, packed, wsrc);
     PairArgs a{};
     a.trg = trg; a.tgrp = tgrp; a.nt = nt; a.src = packed; a.ns = ns; a.pref = pref;
-    a.out = out; a.bad = (unsigned long long *)bad;
+    a.out = out; a.bad = (unsigned long long *)bad; a.accumulate = accumulate;
     return launch_pairs<StressletP>(a, st, ws);
 }
 

@@ -1,0 +1,212 @@
+"""Host-side fiber containers mirroring the reference's constructors.
+
+Same names, arguments and validation as slenderflow.fiber
+(/root/reference/pkg/src/slenderflow/fiber.py:39-232) so user scripts build
+states the same way.  These objects only hold state; every per-step and
+per-matvec operation on them runs on the device (operator.py, solver.py).
+Geometry is computed lazily on the host for the few host-side consumers
+(near-field map construction, attachment wrenches in the API path).
+"""
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import spectral
+
+GROWING = "growing"
+SHRINKING = "shrinking"
+STALLED = "stalled"
+
+
+class InsideFiberError(ValueError):
+    pass
+
+
+@dataclass
+class GrowthKinetics:
+    """Dynamic-instability parameters (fiber.py:39-48)."""
+
+    v_grow: float = 0.12
+    v_shrink: float = 0.288
+    f_cat: float = 0.014
+    f_res: float = 0.014
+    stall_force: float = 4.4
+    min_length: float = 0.5
+
+
+class FreeEnd:
+    kind = "free"
+
+    def __repr__(self):
+        return "FreeEnd()"
+
+
+class PrescribedForceTorque:
+    kind = "prescribedForceTorque"
+
+    def __init__(self, force, torque=(0.0, 0.0, 0.0)):
+        self.force = np.asarray(force, dtype=float)
+        self.torque = np.asarray(torque, dtype=float)
+
+
+class HingedToSurface:
+    """Spring attachment of a fiber end to a fixed point (fiber.py:66-75)."""
+
+    kind = "hingedToSurface"
+
+    def __init__(self, attachment, stiffness):
+        if stiffness < 0:
+            raise ValueError("spring constant must be nonnegative")
+        self.attachment = np.asarray(attachment, dtype=float)
+        self.stiffness = float(stiffness)
+
+
+class ClampedToBody:
+    """Attachment to a rigid body; tangent=None leaves the end hinged (fiber.py:78-93)."""
+
+    kind = "clampedToBody"
+
+    def __init__(self, body, attach_point, tangent=None):
+        self.body = int(body)
+        self.attach_point = np.asarray(attach_point, dtype=float)
+        if tangent is None:
+            self.tangent = None
+        else:
+            t = np.asarray(tangent, dtype=float)
+            nt = np.linalg.norm(t)
+            if not np.isclose(nt, 1.0, atol=1e-8):
+                raise ValueError("clamped tangent must be a unit vector")
+            self.tangent = t / nt
+
+
+class Fiber:
+    """Chebyshev-collocated centreline with tension (fiber.py:96-129).
+
+    Node 0 is the plus end (alpha = +1, s = L), node p the minus end.
+    """
+
+    def __init__(self, X, eps, E, delta=None, bc_minus=None, bc_plus=None, tension=None,
+                 growth_state=STALLED, Ldot=0.0, rng=None, kinetics=None, tau_cat=math.inf):
+        X = np.asarray(X, dtype=float)
+        if X.ndim != 2 or X.shape[1] != 3 or X.shape[0] < 5:
+            raise ValueError("centerline must be (p+1, 3) with p >= 4")
+        if not 0.0 < eps <= 0.1:
+            raise ValueError(f"aspect ratio must lie in (0, 0.1], got {eps}")
+        if E <= 0:
+            raise ValueError("flexural modulus must be positive")
+        self._X = X.copy()
+        self.T = np.zeros(X.shape[0]) if tension is None else np.asarray(tension, dtype=float).copy()
+        self.eps = float(eps)
+        self.E = float(E)
+        self.growth_state = growth_state
+        self.Ldot = float(Ldot)
+        self.bc_minus = bc_minus if bc_minus is not None else FreeEnd()
+        self.bc_plus = bc_plus if bc_plus is not None else FreeEnd()
+        self.rng = rng
+        self.kinetics = kinetics if kinetics is not None else GrowthKinetics()
+        self.tau_cat = tau_cat
+        self._delta_ratio = None if delta is not None else 0.01
+        self._delta = float(delta) if delta is not None else None
+        self._geo = None
+
+    # -- geometry (lazy, host) ------------------------------------------------
+    @property
+    def X(self):
+        return self._X
+
+    @X.setter
+    def X(self, value):
+        self._X = np.asarray(value, dtype=float).copy()
+        self._geo = None
+
+    def refresh_geometry(self):
+        s, s_alpha, L, t = spectral.fiber_geometry(self._X, self.p)
+        self._geo = dict(s=s, s_alpha=s_alpha, L=L, tangents=t)
+
+    def _g(self, key):
+        if self._geo is None:
+            self.refresh_geometry()
+        return self._geo[key]
+
+    @property
+    def s(self):
+        return self._g("s")
+
+    @property
+    def s_alpha(self):
+        return self._g("s_alpha")
+
+    @property
+    def L(self):
+        return self._g("L")
+
+    @property
+    def tangents(self):
+        return self._g("tangents")
+
+    @property
+    def n_nodes(self):
+        return self._X.shape[0]
+
+    @property
+    def p(self):
+        return self._X.shape[0] - 1
+
+    @property
+    def grid(self):
+        return spectral.grid(self.p)
+
+    @property
+    def delta(self):
+        return self._delta_ratio * self.L if self._delta_ratio is not None else self._delta
+
+    @delta.setter
+    def delta(self, value):
+        if value <= 0:
+            raise ValueError("regularization length must be positive")
+        self._delta = float(value)
+        self._delta_ratio = None
+
+    @property
+    def delta_ratio(self):
+        """0.01 for the reference default delta = 0.01 L, None if explicit."""
+        return self._delta_ratio
+
+    def end_index(self, plus):
+        return 0 if plus else self.p
+
+    def node_weights(self):
+        """Quadrature weights converting force density to point strengths (fiber.py:172-174)."""
+        return spectral.grid(self.p)[1] * self.s_alpha
+
+    def ds_powers(self):
+        """(Ds, Ds2, Ds3) on the host (fiber.py:140-143); API-path helper."""
+        D = spectral.grid(self.p)[2]
+        Ds = D / self.s_alpha[:, None]
+        Ds2 = Ds @ Ds
+        return Ds, Ds2, Ds2 @ Ds
+
+
+def straight_fiber(p, start, direction, length, eps=0.01, E=10.0, **kwargs):
+    """Straight fiber from start along a unit direction; minus end at start (fiber.py:225-232)."""
+    d = np.asarray(direction, dtype=float)
+    d = d / np.linalg.norm(d)
+    s = (spectral.cheb_nodes(p) + 1.0) * (length / 2.0)
+    X = np.asarray(start, dtype=float)[None, :] + s[:, None] * d[None, :]
+    return Fiber(X, eps=eps, E=E, **kwargs)
+
+
+def end_force_torque(fib, Xcand, Tcand):
+    """Minus-end force and torque on the attached body (fiber.py:361-372), host."""
+    Xcand = np.asarray(Xcand, dtype=float)
+    Tcand = np.asarray(Tcand, dtype=float)
+    k = fib.end_index(plus=False)
+    Ds, Ds2, Ds3 = fib.ds_powers()
+    Xsss = (Ds3 @ Xcand)[k]
+    Xss = (Ds2 @ Xcand)[k]
+    t = fib.tangents[k]
+    F = -fib.E * Xsss + Tcand[k] * t
+    L = fib.E * np.cross(Xss, t)
+    return F, L

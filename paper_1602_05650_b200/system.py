@@ -1,0 +1,458 @@
+"""System state and the complementary-velocity (HI) operator on the B200.
+
+Mirrors the reference's public API (/root/reference/pkg/src/slenderflow/
+system.py): SystemState, force models, the SummationBackend plugin,
+InteractionCache and complementary_velocities keep their names, arguments,
+return types and error behaviour.  The difference is where the work happens:
+InteractionCache freezes the geometry ON THE DEVICE (targets, groups,
+weights, doublet coefficients, surfaces, particle centres, near-field maps)
+and every application is one sf_hi_apply call into libsf_b200.so.
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, nearfield, spectral
+from ._native import SF_MODE_FP64
+from .fiber import InsideFiberError, end_force_torque
+from .kernels import MIN_SEPARATION, SingularEvaluationError
+
+
+class ConfigurationError(ValueError):
+    pass
+
+
+class OverlapError(ValueError):
+    """A target point lies inside another constituent's volume."""
+
+
+# -- force models (system.py:40-88) -------------------------------------------
+
+class UniformBodyForce:
+    kind = "uniformBodyForce"
+
+    def __init__(self, f0, direction=(0.0, 0.0, 1.0)):
+        d = np.asarray(direction, dtype=float)
+        nrm = np.linalg.norm(d)
+        if nrm == 0.0:
+            raise ConfigurationError("load direction must be nonzero")
+        self.f0 = float(f0)
+        self.direction = d / nrm
+
+
+class CytoplasmicPulling:
+    kind = "cytoplasmicPulling"
+
+    def __init__(self, motor_force=0.91, motor_density=0.04):
+        if motor_force < 0 or motor_density < 0:
+            raise ConfigurationError("motor force and density must be nonnegative")
+        self.motor_force = float(motor_force)
+        self.motor_density = float(motor_density)
+
+
+# -- summation backend plugin (system.py:93-105) -------------------------------
+
+class DeviceSummation:
+    """SummationBackend on the B200: exact pairwise Stokeslet summation.
+
+    Same contract as the reference's DirectSummation: .kind and
+    .stokeslet(sources, source_groups, strengths, targets, target_groups, mu)
+    -> (Nt,3), raising SingularEvaluationError on a cross-group coincidence.
+    """
+
+    kind = "direct"
+
+    def stokeslet(self, sources, source_groups, strengths, targets, target_groups, mu):
+        from . import kernels
+        out, bad = kernels.stokeslet_sum(targets, target_groups, sources, source_groups,
+                                         strengths, 1.0 / (8.0 * np.pi * mu))
+        if bad:
+            raise SingularEvaluationError(
+                "a target coincides with a source outside its own group")
+        return out
+
+
+DirectSummation = DeviceSummation
+
+
+# -- state (system.py:237-278) -------------------------------------------------
+
+class SystemState:
+    def __init__(self, fibers, particles=(), periphery=None, mu=1.0, time=0.0,
+                 force_models=(), seed=None):
+        if mu <= 0:
+            raise ConfigurationError("viscosity must be positive")
+        self.fibers = list(fibers)
+        self.particles = list(particles)
+        self.periphery = periphery
+        self.mu = float(mu)
+        self.time = float(time)
+        self.force_models = list(force_models)
+        self.seed = seed
+        self.rng = np.random.default_rng(seed)
+        self.validate()
+
+    def validate(self):
+        if self.periphery is not None:
+            for i, fib in enumerate(self.fibers):
+                if not np.all(self.periphery.contains(fib.X)):
+                    raise ConfigurationError(f"fiber {i} leaves the confining periphery")
+            for i, part in enumerate(self.particles):
+                if not np.all(self.periphery.contains(part.mesh.nodes)):
+                    raise ConfigurationError(f"particle {i} leaves the confining periphery")
+        for i, fib in enumerate(self.fibers):
+            if fib.bc_plus.kind == "clampedToBody":
+                raise ConfigurationError("plus-end clamping is not supported")
+            for bc in (fib.bc_minus, fib.bc_plus):
+                if bc.kind == "clampedToBody" and not 0 <= bc.body < len(self.particles):
+                    raise ConfigurationError(
+                        f"fiber {i} is clamped to a body outside the system")
+                if bc.kind == "hingedToSurface" and self.periphery is None:
+                    raise ConfigurationError(
+                        f"fiber {i} is hinged to a surface but no periphery is present")
+
+    def model(self, kind):
+        for m in self.force_models:
+            if m.kind == kind:
+                return m
+        return None
+
+
+def external_force_density(state, fib):
+    """Per-node external force density from the force models (system.py:297-305)."""
+    f = np.zeros((fib.n_nodes, 3))
+    for m in state.force_models:
+        if m.kind == "uniformBodyForce":
+            f += m.f0 * m.direction[None, :]
+        elif m.kind == "cytoplasmicPulling":
+            f += m.motor_force * m.motor_density * fib.tangents
+    return f
+
+
+def attachment_wrench(state, particle_index, candidates=None):
+    """Net force and torque on a particle from its clamped fibers (system.py:308-329)."""
+    part = state.particles[particle_index]
+    F = np.zeros(3)
+    L = np.zeros(3)
+    for k, fib in enumerate(state.fibers):
+        bc = fib.bc_minus
+        if bc.kind != "clampedToBody" or bc.body != particle_index:
+            continue
+        cand = None if candidates is None else candidates[k]
+        X, T = (fib.X, fib.T) if cand is None else cand
+        Fe, Le = end_force_torque(fib, X, T)
+        arm = fib.X[fib.end_index(plus=False)] - part.center
+        F += Fe
+        L += Le + np.cross(arm, Fe)
+    return F, L
+
+
+@dataclass
+class ComplementaryVelocities:
+    periphery: object
+    particles: list
+    fibers: list
+
+
+def _inside_star_surface(mesh, points):
+    pts = np.atleast_2d(points) - mesh.center
+    rho = np.linalg.norm(pts, axis=1)
+    safe = np.where(rho > 0, rho, 1.0)
+    th = np.arccos(np.clip(np.where(rho > 0, pts[:, 2] / safe, 1.0), -1.0, 1.0))
+    return rho < np.asarray(mesh.shape[2](th), dtype=float)
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def stack_fibers(fibers):
+    """(nf, n, 3) centrelines; the device layout needs one node count."""
+    if not fibers:
+        return np.zeros((0, 5, 3))
+    n = fibers[0].n_nodes
+    if any(f.n_nodes != n for f in fibers):
+        raise ConfigurationError("the device layout needs every fiber to have the same order p")
+    return np.stack([f.X for f in fibers])
+
+
+class FiberGeometry:
+    """Batched per-fiber geometry on the device (sf_fiber_geometry_batched)."""
+
+    def __init__(self, X, delta_ratio, delta, device):
+        import torch
+        dev = dict(dtype=torch.float64, device=device)
+        X = torch.as_tensor(X, **dev).contiguous()
+        nf, n, _ = X.shape
+        self.nf, self.n = nf, n
+        _, wcc, D, S = spectral.grid(n - 1)
+        self.X = X
+        self.wcc = torch.tensor(wcc, **dev)
+        self.D = torch.tensor(D, **dev)
+        self.S = torch.tensor(S, **dev)
+        self.s = torch.empty((nf, n), **dev)
+        self.s_alpha = torch.empty((nf, n), **dev)
+        self.tang = torch.empty((nf, n, 3), **dev)
+        self.wnode = torch.empty((nf, n), **dev)
+        self.L = torch.empty(nf, **dev)
+        self.delta = torch.as_tensor(np.asarray(delta, dtype=float), **dev).clone()
+        degenerate = torch.zeros(1, dtype=torch.int32, device=device)
+        if nf:
+            _native.call("sf_fiber_geometry_batched", _ptr(X), nf, n, _ptr(self.D), _ptr(self.S),
+                         _ptr(self.wcc), -1.0, _ptr(self.s), _ptr(self.s_alpha), _ptr(self.tang),
+                         _ptr(self.wnode), _ptr(self.L), None, _ptr(degenerate), _stream())
+            if int(degenerate.item()):
+                raise ValueError("centerline parametrization is degenerate")
+            # delta = ratio * L where the fiber uses the default ratio (fiber.py:127,144)
+            ratio = torch.as_tensor(np.asarray(delta_ratio, dtype=float), **dev)
+            self.delta = torch.where(ratio > 0, ratio * self.L, self.delta)
+
+
+class InteractionCache:
+    """Frozen-geometry layout of complementary_velocities, resident on the B200
+    (system.py:492-620).  Rebuild whenever any constituent moves."""
+
+    def __init__(self, state, include_doublet=True, device=None, mode=SF_MODE_FP64,
+                 near=True, fiber_geometry=None):
+        import torch
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        dev = dict(device=self.device)
+        f64 = dict(dtype=torch.float64, **dev)
+        self.include_doublet = include_doublet
+        self.mu = state.mu
+        nf = len(state.fibers)
+        np_ = len(state.particles)
+        self.nf, self.np = nf, np_
+
+        blocks, groups = [], []
+        self.particle_slices = []
+        off = 0
+        for i, part in enumerate(state.particles):
+            n = part.mesh.n_nodes
+            blocks.append(part.mesh.nodes)
+            groups.append(np.full(n, nf + i, dtype=np.int64))
+            self.particle_slices.append(slice(off, off + n))
+            off += n
+        self.periphery_slice = None
+        if state.periphery is not None:
+            n = state.periphery.mesh.n_nodes
+            blocks.append(state.periphery.mesh.nodes)
+            groups.append(np.full(n, nf + np_, dtype=np.int64))
+            self.periphery_slice = slice(off, off + n)
+            off += n
+        Xf = stack_fibers(state.fibers)
+        self.n_nodes = Xf.shape[1]
+        self.fiber_slice = slice(off, off + nf * self.n_nodes)
+        self.fiber_slices = [slice(off + m * self.n_nodes, off + (m + 1) * self.n_nodes)
+                             for m in range(nf)]
+        blocks.append(Xf.reshape(-1, 3))
+        groups.append(np.repeat(np.arange(nf, dtype=np.int64), self.n_nodes))
+        self.targets = np.vstack(blocks) if blocks else np.zeros((0, 3))
+        self.target_groups = np.concatenate(groups) if groups else np.zeros(0, np.int64)
+        self.n_targets = self.targets.shape[0]
+
+        # fibers: geometry, weights, doublet coefficients (device)
+        if fiber_geometry is None:
+            ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in state.fibers]
+            deltas = [0.0 if f.delta_ratio is not None else f.delta for f in state.fibers]
+            fiber_geometry = FiberGeometry(Xf, ratios, deltas, self.device)
+        self.geo = fiber_geometry
+        self.eps = torch.as_tensor([f.eps for f in state.fibers], **f64)
+        self.fsrc = self.geo.X.reshape(-1, 3)
+        self.fgrp = torch.as_tensor(np.repeat(np.arange(nf, dtype=np.int64), self.n_nodes), **dev)
+        self.fw = self.geo.wnode.reshape(-1)
+        self.fdcoef = (((self.eps * self.geo.L) ** 2 / 2.0).repeat_interleave(self.n_nodes)
+                       if include_doublet and nf else None)                   # system.py:542
+
+        # surfaces: particles then periphery (system.py:544-557)
+        self.surfaces = [(p.mesh, nf + i, False) for i, p in enumerate(state.particles)]
+        if state.periphery is not None:
+            self.surfaces.append((state.periphery.mesh, nf + np_, True))
+        self.surface_offsets = []
+        o = 0
+        for m, _, _ in self.surfaces:
+            self.surface_offsets.append(o)
+            o += m.n_nodes
+        self.nss = o
+        if self.surfaces:
+            self.ssrc = torch.as_tensor(np.vstack([m.nodes for m, _, _ in self.surfaces]), **f64)
+            self.snrm = torch.as_tensor(np.vstack([m.normals for m, _, _ in self.surfaces]), **f64)
+            self.sw = torch.as_tensor(np.concatenate([m.weights for m, _, _ in self.surfaces]), **f64)
+            self.sgrp = torch.as_tensor(np.concatenate(
+                [np.full(m.n_nodes, g, dtype=np.int64) for m, g, _ in self.surfaces]), **dev)
+        else:
+            self.ssrc = self.snrm = self.sw = self.sgrp = None
+        self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
+                        if np_ else None)
+        self.pgrp = torch.as_tensor(np.arange(nf, nf + np_, dtype=np.int64), **dev) if np_ else None
+
+        self.trg = torch.as_tensor(self.targets, **f64).contiguous()
+        self.tgrp = torch.as_tensor(self.target_groups, **dev)
+
+        self._check_surface_overlaps()
+        self.near_fiber = []
+        if near and nf:
+            try:
+                self.near_fiber = nearfield.find_fiber_pairs(
+                    state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
+            except InsideFiberError as err:
+                raise OverlapError(f"target node overlaps a fiber: {err}") from err
+        if near and self.surfaces:
+            self._check_no_near_surface()
+        self._build_near_map()
+        self.mode = int(mode)
+        self._layout()
+        self.bad = torch.zeros(3, dtype=torch.int64, **dev)
+
+    # -- construction helpers ------------------------------------------------
+    def _check_surface_overlaps(self):
+        for mesh, group, is_periphery in self.surfaces:
+            others = self.target_groups != group
+            if mesh.shape is not None:
+                inside = _inside_star_surface(mesh, self.targets)
+                if is_periphery and np.any(others & ~inside):
+                    raise OverlapError("a target lies outside the confining periphery")
+                if not is_periphery and np.any(others & inside):
+                    raise OverlapError("a target lies inside a rigid particle")
+
+    def _check_no_near_surface(self):
+        from scipy.spatial import cKDTree
+        for mesh, group, _ in self.surfaces:
+            shell = 1.5 * mesh.h
+            tree = cKDTree(mesh.nodes)
+            d, _ = tree.query(self.targets[self.target_groups != group], k=1)
+            if np.any(d < shell):
+                raise NotImplementedError(
+                    "near-surface correction maps are not built on this path yet "
+                    "(SURVEY.md §8f rank 1); keep targets outside 1.5 h of other surfaces")
+
+    def _build_near_map(self):
+        import torch
+        entries = self.near_fiber
+        self.near_nrows = 0
+        self.near_tensors = {}
+        if not entries:
+            return
+        t = np.array([e[0] for e in entries], dtype=np.int64)
+        l = np.array([e[1] for e in entries], dtype=np.int64)
+        W = np.stack([e[2] for e in entries])
+        order = np.argsort(t, kind="stable")
+        t, l, W = t[order], l[order], W[order]
+        rows, starts = np.unique(t, return_index=True)
+        L = 3 * self.n_nodes
+        dev = dict(device=self.device)
+        self.near_tensors = dict(
+            row_ptr=torch.as_tensor(np.append(starts, t.size).astype(np.int64), **dev),
+            rows=torch.as_tensor(rows, **dev),
+            w_off=torch.as_tensor(np.arange(t.size, dtype=np.int64) * 3 * L, **dev),
+            x_off=torch.as_tensor(l * L, **dev),           # into [fiber forces | densities]
+            x_len=torch.full((t.size,), L, dtype=torch.int64, **dev),
+            W=torch.as_tensor(np.ascontiguousarray(W), dtype=torch.float64, **dev))
+        self.near_nrows = rows.size
+
+    def _layout(self):
+        nt = self.near_tensors
+        self.layout = _native.HiLayout(
+            trg=_ptr(self.trg), tgrp=_ptr(self.tgrp), nt=self.n_targets,
+            fsrc=_ptr(self.fsrc), fgrp=_ptr(self.fgrp), fw=_ptr(self.fw),
+            fdcoef=_ptr(self.fdcoef), nfs=self.fsrc.shape[0],
+            ssrc=_ptr(self.ssrc), snrm=_ptr(self.snrm), sw=_ptr(self.sw), sgrp=_ptr(self.sgrp),
+            nss=self.nss, pcenter=_ptr(self.pcenter), pgrp=_ptr(self.pgrp), np=self.np,
+            near_row_ptr=_ptr(nt.get("row_ptr")), near_rows=_ptr(nt.get("rows")),
+            near_w_off=_ptr(nt.get("w_off")), near_x_off=_ptr(nt.get("x_off")),
+            near_x_len=_ptr(nt.get("x_len")), near_nrows=self.near_nrows,
+            near_W=_ptr(nt.get("W")), mu=self.mu, mode=self.mode)
+
+    # -- application ------------------------------------------------------------
+    @property
+    def pairs_per_apply(self):
+        """Non-excluded (target, source) pairs of one application."""
+        nfs = self.fsrc.shape[0]
+        own = self.nf * self.n_nodes * self.n_nodes
+        surf = sum(m.n_nodes * m.n_nodes for m, _, _ in self.surfaces)
+        return self.n_targets * nfs - own + self.n_targets * self.nss - surf
+
+    def apply(self, f, q=None, wrench=None, out=None, check=True):
+        """u (n_targets,3) on the device; f (nfs,3), q (nss,3), wrench (np,6)."""
+        import torch
+        f64 = dict(dtype=torch.float64, device=self.device)
+        f = torch.as_tensor(f, **f64).reshape(-1, 3).contiguous()
+        if q is not None:
+            q = torch.as_tensor(q, **f64).reshape(-1, 3).contiguous()
+        if wrench is not None:
+            wrench = torch.as_tensor(wrench, **f64).reshape(-1, 6).contiguous()
+        if out is None:
+            out = torch.empty((self.n_targets, 3), **f64)
+        x = None
+        if self.near_nrows:
+            x = f.reshape(-1) if q is None else torch.cat([f.reshape(-1), q.reshape(-1)])
+        _native.call("sf_hi_apply", ctypes.byref(self.layout), _ptr(f), _ptr(q), _ptr(wrench),
+                     _ptr(x), _ptr(out), _ptr(self.bad), _stream())
+        if check:
+            self.check_bad()
+        return out
+
+    def check_bad(self):
+        b = self.bad.tolist()
+        if b[0]:
+            raise SingularEvaluationError("a target coincides with another fiber's node")
+        if b[1]:
+            raise SingularEvaluationError("a target coincides with another surface's node")
+        if b[2]:
+            raise SingularEvaluationError("target at a particle center")
+
+    def split(self, u):
+        """Break a stacked velocity array into the evaluation families (system.py:615-620)."""
+        per = u[self.periphery_slice] if self.periphery_slice is not None else None
+        return ComplementaryVelocities(periphery=per,
+                                       particles=[u[s] for s in self.particle_slices],
+                                       fibers=[u[s] for s in self.fiber_slices])
+
+
+def complementary_velocities(state, periphery_density=None, particle_densities=None,
+                             fiber_forces=None, particle_wrenches=None, backend=None, cache=None,
+                             include_doublet=True):
+    """Flow induced at every constituent's nodes by all the others (system.py:623-709).
+
+    Same signature and results as the reference; the evaluation runs on the
+    B200 through the (device-resident) InteractionCache.  Host (numpy)
+    inputs give numpy outputs.
+    """
+    if backend is not None and getattr(backend, "kind", "direct") != "direct":
+        raise ConfigurationError(f"backend {backend.kind!r} is not available on the device path")
+    if cache is None:
+        cache = InteractionCache(state, include_doublet=include_doublet)
+    if fiber_forces is None:
+        from .solver import host_elastic_force_density
+        fiber_forces = [host_elastic_force_density(f, f.X, f.T) + external_force_density(state, f)
+                        for f in state.fibers]
+    if particle_densities is None:
+        particle_densities = [p.q for p in state.particles]
+    if periphery_density is None and state.periphery is not None:
+        periphery_density = state.periphery.q
+    if particle_wrenches is None:
+        particle_wrenches = []
+        for i, part in enumerate(state.particles):
+            Fa, La = attachment_wrench(state, i)
+            particle_wrenches.append((part.F_ext + Fa, part.L_ext + La))
+    f = (np.concatenate([np.asarray(x, dtype=float).reshape(-1, 3) for x in fiber_forces])
+         if state.fibers else np.zeros((0, 3)))
+    q = None
+    if cache.surfaces:
+        q = np.concatenate([np.asarray(periphery_density if isp else particle_densities[j],
+                                       dtype=float).reshape(-1, 3)
+                            for j, (_, _, isp) in enumerate(cache.surfaces)])
+    w = None
+    if state.particles:
+        w = np.concatenate([np.concatenate([np.asarray(F, dtype=float), np.asarray(L, dtype=float)])
+                            for F, L in particle_wrenches])
+    u = cache.apply(f, q, w).cpu().numpy()
+    return cache.split(u)

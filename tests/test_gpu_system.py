@@ -1,0 +1,68 @@
+"""complementary_velocities (system.py:623-709) on the device vs the reference."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle.ops import rel_l2
+from paper_1602_05650_b200 import body, system
+from paper_1602_05650_b200.fiber import Fiber
+
+pytestmark = pytest.mark.gpu
+
+
+def _surface_state(g):
+    per = body.Periphery(body.make_surface(body.sphere_shape(6.0), (8, 8)))
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(1.0), (6, 6)))
+    part.F_ext = g["F_ext"]
+    part.L_ext = g["L_ext"]
+    fibs = [Fiber(X, eps=0.01, E=10.0) for X in g["X"]]
+    return system.SystemState(fibs, [part], per), part
+
+
+def test_surfaces_fibers_particles(cuda):
+    g = golden("surfaces.npz")
+    st, part = _surface_state(g)
+    res = system.complementary_velocities(
+        st, periphery_density=g["q0"], particle_densities=[g["q1"]], fiber_forces=list(g["forces"]),
+        particle_wrenches=[(g["F_ext"], g["L_ext"])])
+    assert rel_l2(res.periphery, g["u_per"]) < 1e-12
+    assert rel_l2(res.particles[0], g["u_part"]) < 1e-12
+    assert rel_l2(np.vstack(res.fibers), g["u_fib"]) < 1e-12
+
+
+def test_c1_near_through_system_api(cuda):
+    g = golden("c1_near.npz")
+    fibs = [Fiber(X, eps=float(g["eps"]), E=1.0) for X in g["X"]]
+    st = system.SystemState(fibs, mu=float(g["mu"]))
+    cache = system.InteractionCache(st)
+    assert len(cache.near_fiber) == g["near_t"].size
+    res = system.complementary_velocities(st, fiber_forces=list(g["forces"]), cache=cache)
+    assert rel_l2(np.vstack(res.fibers), g["u_nl"]) < 1e-12
+    # cache reuse is bitwise identical to a fresh evaluation (test_system.py:221-232)
+    again = system.complementary_velocities(st, fiber_forces=list(g["forces"]), cache=cache)
+    assert np.array_equal(np.vstack(again.fibers), np.vstack(res.fibers))
+
+
+def test_lone_fiber_sees_nothing(cuda):
+    from paper_1602_05650_b200.fiber import straight_fiber
+    st = system.SystemState([straight_fiber(12, (0, 0, 0), (0, 0, 1.0), 2.0)])
+    res = system.complementary_velocities(st, fiber_forces=[np.ones((13, 3))])
+    assert res.periphery is None and res.particles == []
+    assert np.all(res.fibers[0] == 0.0)
+
+
+def test_fiber_inside_particle_raises(cuda):
+    from paper_1602_05650_b200.fiber import straight_fiber
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(1.0), (8, 8)))
+    st = system.SystemState([straight_fiber(12, (0.0, 0, 0.2), (0, 0, 1.0), 2.0)], [part])
+    with pytest.raises(system.OverlapError):
+        system.complementary_velocities(st, particle_densities=[part.q],
+                                        fiber_forces=[np.zeros((13, 3))])
+
+
+def test_device_summation_backend(cuda):
+    src = np.array([[0.0, 0, 0], [1.0, 0, 0]])
+    groups = np.array([0, 1], dtype=np.int64)
+    with pytest.raises(system.SingularEvaluationError):
+        system.DirectSummation().stokeslet(src, groups, np.ones((2, 3)), src[:1], groups[1:], 1.0)

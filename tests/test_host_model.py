@@ -1,0 +1,46 @@
+"""Host-side setup code (meshes, fibers, near-field maps) against the reference's
+own outputs (golden fixtures)."""
+
+import numpy as np
+
+from conftest import golden
+from paper_1602_05650_b200 import body, nearfield, spectral
+from paper_1602_05650_b200.fiber import Fiber, straight_fiber
+
+
+def test_surface_meshes_bitwise():
+    g = golden("surfaces.npz")
+    per = body.make_surface(body.sphere_shape(6.0), (8, 8))
+    part = body.make_surface(body.sphere_shape(1.0), (6, 6))
+    for m, k in ((per, "per"), (part, "part")):
+        assert np.array_equal(m.nodes, g[f"{k}_nodes"])
+        assert np.array_equal(m.normals, g[f"{k}_normals"])
+        assert np.array_equal(m.weights, g[f"{k}_weights"])
+
+
+def test_fiber_geometry_matches_reference():
+    g = golden("c1_near.npz")
+    for m in (0, 17, 63):
+        fib = Fiber(g["X"][m], eps=float(g["eps"]), E=1.0)
+        assert np.array_equal(fib.s_alpha, g["s_alpha"][m])
+        assert np.abs(fib.s - g["s"][m]).max() < 1e-15
+        assert np.abs(fib.tangents - g["tangents"][m]).max() < 1e-15
+        assert np.abs(fib.node_weights() - g["weights"][m]).max() < 1e-16
+        assert fib.delta == g["delta"][m]
+
+
+def test_straight_fiber_layout():
+    f = straight_fiber(31, (0.1, 0.2, 0.3), (1, 2, 3), 1.0)
+    assert np.allclose(f.X[-1], (0.1, 0.2, 0.3)) and f.end_index(False) == 31
+    assert abs(f.L - 1.0) < 1e-12
+
+
+def test_near_fiber_maps_match_reference():
+    g = golden("c1_near.npz")
+    fibers = [Fiber(X, eps=float(g["eps"]), E=1.0) for X in g["X"]]
+    targets = g["X"].reshape(-1, 3)
+    groups = np.repeat(np.arange(len(fibers)), g["X"].shape[1])
+    near = nearfield.find_fiber_pairs(fibers, targets, groups, float(g["mu"]), True)
+    assert [(t, l) for t, l, _ in near] == list(zip(g["near_t"].tolist(), g["near_l"].tolist()))
+    for (_, _, W), Wref in zip(near, g["near_W"]):
+        assert np.abs(W - Wref).max() <= 1e-12 * np.abs(Wref).max()
