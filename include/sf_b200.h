@@ -200,6 +200,87 @@ int sf_hi_apply(const sf_hi_layout *layout, const double *f, const double *q,
                 const double *wrench, const double *near_x, double *u, int64_t *bad,
                 void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Implicit step (solver.py): block rows, self blocks, preconditioner, Krylov.
+ * Unknown vector layout (StepLayout, solver.py:67-110):
+ *   [per particle U(3) omega(3) q1(3Np) | periphery q0(3N0) | per fiber X(3n) T(n)]
+ * ------------------------------------------------------------------------- */
+
+/* Frozen per-step fiber data (the reference's Fiber objects after
+ * refresh_geometry, batched).  bc_kind (nf,2) [plus, minus]: 0 free,
+ * 1 prescribedForceTorque, 2 hingedToSurface, 3 clampedToBody; bc_par
+ * (nf,2,12): force(3) torque(3) attachment(3) stiffness has_tangent pad;
+ * bc_body (nf): body of a clamped minus end or -1. */
+typedef struct {
+    int64_t nf, n;
+    const double *D;         /* (n,n) Chebyshev differentiation in alpha */
+    const double *nodes;     /* (n) alpha nodes */
+    const double *Dpow;      /* (nf,4,n,n) Ds, Ds2, Ds3, Ds4 */
+    const double *X;         /* (nf,n,3) frozen centrelines */
+    const double *tang;      /* (nf,n,3) */
+    const double *s_alpha;   /* (nf,n) */
+    const double *L, *Ldot, *E, *c_log;  /* (nf) */
+    double c_two;
+    const double *K;         /* (nf,3n,3n) K_delta */
+    const double *f_ext;     /* (nf,n,3) or NULL */
+    const int *bc_kind;
+    const double *bc_par;
+    const int *bc_body;
+    int64_t np;
+    const double *pcenter;   /* (np,3) */
+    const int64_t *p_uoff;   /* (np) offset of U in the unknown vector (omega at +3) */
+    int64_t fib_off;         /* offset of fiber 0's block */
+    double dt, mu;
+} sf_fiber_sys;
+
+/* Ds..Ds4 per fiber (fiber.py:140-143). */
+int sf_fiber_dpow(const double *D, const double *s_alpha, int64_t nf, int64_t n, double *Dpow,
+                  void *stream);
+/* f (nf,n,3) = elastic force of the candidate in u (+ f_ext if constants)
+ * (solver.py:313-318, fiber.py:237-241). */
+int sf_fiber_forces(const sf_fiber_sys *S, const double *u, int constants, double *f,
+                    void *stream);
+/* Per-particle wrench (np,6) from clamped fibers (system.py:308-329) + ext
+ * (np,6) if constants (solver.py:296-305); work (nf,6) scratch. */
+int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *ext,
+                         int constants, double *work, double *wout, void *stream);
+/* Fiber residual rows into out (solver.py:137-184, fiber.py:375-441); ubar
+ * (nf*n,3) complementary velocity at the fiber nodes or NULL. */
+int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *ubar, int constants,
+                  double *out, void *stream);
+/* Dense 4n x 4n self blocks (solver.py:250-294) into A (nf,4n,4n). */
+int sf_fiber_self_blocks(const sf_fiber_sys *S, double *A, void *stream);
+/* In-place equilibrated LU with partial pivoting of nb m x m blocks
+ * (solver.py:386-404), factors left column-major; r, c (nb,m) scalings;
+ * piv (nb,m) 0-based; info (nb): 0 ok, 1 non-finite, 2 zero row, 3 zero pivot. */
+int sf_block_lu(double *A, int64_t nb, int64_t m, double *r, double *c, int *piv, int *info,
+                void *stream);
+/* x = Preconditioner.apply(v) (solver.py:425-429): x[:ndiag] = v/diag; each
+ * fiber block b at off0 + m b solved with its equilibrated LU. */
+int sf_precond_apply(const double *LU, const double *r, const double *c, const int *piv,
+                     int64_t nb, int64_t m, int64_t off0, const double *diag, int64_t ndiag,
+                     const double *v, double *x, void *stream);
+/* Surface rows (solver.py:332-355).  kind 0 (particle): rows hold DL_on +
+ * wrench flow on entry; adds u_bar, subtracts U + omega x arm; out_uom gets
+ * U - <q>/mu, omega - <arm x q>/mu.  kind 1 (periphery): rows hold DL_on on
+ * entry; adds q/mu + n flux/(mu area) + u_bar.  work >= 6 doubles. */
+int sf_surface_rows(int kind, const double *nodes, const double *nrm, const double *w, int64_t n,
+                    const double *center, double area, const double *q, const double *ubar,
+                    const double *Uom, double mu, double *work, double *rows, double *out_uom,
+                    void *stream);
+/* u += Stokeslet + rotlet of wrench (F,L) at center (solver.py:125-134). */
+int sf_wrench_flow(const double *trg, int64_t nt, const double *center, const double *wrench,
+                   double mu, double *u, void *stream);
+/* Krylov vector kernels (deterministic order): out = x.y (sqrt_mode: sqrt);
+ * work >= 296 doubles.  y += sgn*(*a) x (mode 0) or y = x / (*a) (mode 2);
+ * x += sum_j coef[j] V[j*ld : j*ld+n]. */
+int sf_dot(const double *x, const double *y, int64_t n, double *work, double *out, int sqrt_mode,
+           void *stream);
+int sf_axpy_dev(const double *a, double sgn, int mode, const double *x, double *y, int64_t n,
+                void *stream);
+int sf_combine(const double *V, int64_t ld, int k, const double *coef, double *x, int64_t n,
+               void *stream);
+
 /* Near-field correction apply (system.py:702-707): for every entry e,
  * u[t_e] += W_e (3 x 3 m_e) . x[off_e : off_e + 3 m_e].  Entries must be
  * grouped by target (row_ptr CSR over `nrows` distinct targets rows[]);

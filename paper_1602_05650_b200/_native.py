@@ -50,6 +50,18 @@ _SIGNATURES = {
                           _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sf_pair_split": [_I64, _I64],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
+    "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
+    "sf_fiber_forces": [_P, _P, _I, _P, _P],
+    "sf_particle_wrenches": [_P, _P, _P, _I, _P, _P, _P],
+    "sf_fiber_rows": [_P, _P, _P, _I, _P, _P],
+    "sf_fiber_self_blocks": [_P, _P, _P],
+    "sf_block_lu": [_P, _I64, _I64, _P, _P, _P, _P, _P],
+    "sf_precond_apply": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, _P],
+    "sf_surface_rows": [_I, _P, _P, _P, _I64, _P, _D, _P, _P, _P, _D, _P, _P, _P, _P],
+    "sf_wrench_flow": [_P, _I64, _P, _P, _D, _P, _P],
+    "sf_dot": [_P, _P, _I64, _P, _P, _I, _P],
+    "sf_axpy_dev": [_P, _D, _I, _P, _P, _I64, _P],
+    "sf_combine": [_P, _I64, _I, _P, _P, _I64, _P],
     "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P],
@@ -61,6 +73,17 @@ _SIGNATURES = {
 }
 
 _lib = None
+
+
+class FiberSys(ctypes.Structure):
+    """Mirror of sf_fiber_sys (include/sf_b200.h)."""
+    _fields_ = [
+        ("nf", _I64), ("n", _I64), ("D", _P), ("nodes", _P), ("Dpow", _P), ("X", _P),
+        ("tang", _P), ("s_alpha", _P), ("L", _P), ("Ldot", _P), ("E", _P), ("c_log", _P),
+        ("c_two", _D), ("K", _P), ("f_ext", _P), ("bc_kind", _P), ("bc_par", _P),
+        ("bc_body", _P), ("np", _I64), ("pcenter", _P), ("p_uoff", _P), ("fib_off", _I64),
+        ("dt", _D), ("mu", _D),
+    ]
 
 
 class HiLayout(ctypes.Structure):

@@ -1,0 +1,983 @@
+// sf_solver.cu — the implicit step's block rows, self blocks, block-Jacobi
+// preconditioner and Krylov vector kernels (solver.py of the reference), sm_100a.
+//
+// Unknown / residual vector layout (StepLayout, solver.py:67-110):
+//   [ per particle: U(3) omega(3) q1(3 N_p) | periphery q0 (3 N_0) | per fiber: X(3n) T(n) ]
+// Fiber m's block starts at fib_off + 4 n m.  All per-fiber kernels run one
+// CTA per fiber with the fiber's small operators staged in shared memory.
+#include <cmath>
+
+#include "sf_common.cuh"
+#include "sf_internal.h"
+
+namespace sf {
+
+enum { BC_FREE = 0, BC_FORCE = 1, BC_HINGED = 2, BC_CLAMPED = 3 };
+// bc_par slots per (fiber, end)
+enum { P_F = 0, P_TQ = 3, P_ANCHOR = 6, P_STIFF = 9, P_HAS_TANGENT = 10, P_N = 12 };
+
+__device__ __forceinline__ void cross3(const double *a, const double *b, double *o) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// ---------------------------------------------------------------- D_s powers
+// fiber.py:140-143: Ds = D / s_alpha[:,None], Ds2 = Ds Ds, Ds3 = Ds2 Ds, Ds4 = Ds2 Ds2.
+__global__ void dpow_kernel(const double *__restrict__ D, const double *__restrict__ s_alpha,
+                            int n, double *__restrict__ Dpow) {
+    extern __shared__ double sm[];
+    double *ds = sm, *ds2 = sm + n * n;
+    const int m = blockIdx.x;
+    const double *sa = s_alpha + (int64_t)n * m;
+    double *out = Dpow + (int64_t)4 * n * n * m;
+    const int nn = n * n;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+        const double v = D[e] / sa[e / n];
+        ds[e] = v;
+        out[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        double a = 0.0;
+        for (int k = 0; k < n; ++k) a = fma(ds[i * n + k], ds[k * n + j], a);
+        ds2[e] = a;
+        out[nn + e] = a;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        double a3 = 0.0, a4 = 0.0;
+        for (int k = 0; k < n; ++k) {
+            a3 = fma(ds2[i * n + k], ds[k * n + j], a3);
+            a4 = fma(ds2[i * n + k], ds2[k * n + j], a4);
+        }
+        out[2 * nn + e] = a3;
+        out[3 * nn + e] = a4;
+    }
+}
+
+// ------------------------------------------------------------ shared helpers
+struct FiberCtx {
+    int n, m;
+    const double *Ds, *Ds2, *Ds3, *Ds4;
+};
+
+__device__ __forceinline__ FiberCtx fiber_ctx(const sf_fiber_sys &S, int m) {
+    FiberCtx c;
+    c.n = (int)S.n;
+    c.m = m;
+    const int64_t nn = (int64_t)S.n * S.n;
+    c.Ds = S.Dpow + 4 * nn * m;
+    c.Ds2 = c.Ds + nn;
+    c.Ds3 = c.Ds2 + nn;
+    c.Ds4 = c.Ds3 + nn;
+    return c;
+}
+
+// f_el = -E Ds4 X + Ds (T t) (fiber.py:237-241) for one fiber; X,T,t in smem.
+__device__ void elastic_force(const FiberCtx &c, double E, const double *X, const double *T,
+                              const double *t, double *f) {
+    const int n = c.n;
+    for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) {
+        const int i = e / 3, a = e - 3 * i;
+        double b = 0.0, s = 0.0;
+        for (int j = 0; j < n; ++j) {
+            b = fma(c.Ds4[i * n + j], X[3 * j + a], b);
+            s = fma(c.Ds[i * n + j], T[j] * t[3 * j + a], s);
+        }
+        f[e] = -E * b + s;
+    }
+}
+
+// -------------------------------------------------- fiber force densities
+// f (nf,n,3) = elastic force of the candidate (X,T) in u (+ f_ext if constants):
+// the strengths the HI operator needs (solver.py:313-318).
+__global__ void fiber_forces_kernel(sf_fiber_sys S, const double *__restrict__ u, int constants,
+                                    double *__restrict__ fout) {
+    extern __shared__ double sm[];
+    const int n = (int)S.n, m = blockIdx.x;
+    double *X = sm, *T = X + 3 * n, *t = T + n;
+    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
+    for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) {
+        X[e] = blk[e];
+        t[e] = S.tang[(int64_t)3 * n * m + e];
+    }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) T[e] = blk[3 * n + e];
+    __syncthreads();
+    FiberCtx c = fiber_ctx(S, m);
+    double *f = fout + (int64_t)3 * n * m;
+    const double E = S.E[m];
+    for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) {
+        const int i = e / 3, a = e - 3 * i;
+        double b = 0.0, s = 0.0;
+        for (int j = 0; j < n; ++j) {
+            b = fma(c.Ds4[i * n + j], X[3 * j + a], b);
+            s = fma(c.Ds[i * n + j], T[j] * t[3 * j + a], s);
+        }
+        double v = -E * b + s;
+        if (constants && S.f_ext) v += S.f_ext[(int64_t)3 * n * m + e];
+        f[e] = v;
+    }
+}
+
+// ------------------------------------------------------- attachment wrench
+// Per clamped fiber: F = -E Xsss + T t, L = E Xss x t at the minus end
+// (fiber.py:361-372), plus the moment arm of the stored attachment point
+// (system.py:308-329).  wf (nf,6) holds F and Le + arm x F (zeros if the fiber
+// is not clamped).
+__global__ void end_wrench_kernel(sf_fiber_sys S, const double *__restrict__ u,
+                                  double *__restrict__ wf) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= S.nf) return;
+    const int n = (int)S.n;
+    double *o = wf + 6 * (int64_t)m;
+    const int body = S.bc_body[m];
+    if (S.bc_kind[2 * m + 1] != BC_CLAMPED || body < 0) {
+        for (int c = 0; c < 6; ++c) o[c] = 0.0;
+        return;
+    }
+    FiberCtx c = fiber_ctx(S, m);
+    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
+    const int k = n - 1;
+    double xss[3] = {0, 0, 0}, xsss[3] = {0, 0, 0};
+    for (int j = 0; j < n; ++j) {
+        const double d2 = c.Ds2[k * n + j], d3 = c.Ds3[k * n + j];
+        for (int a = 0; a < 3; ++a) {
+            xss[a] = fma(d2, blk[3 * j + a], xss[a]);
+            xsss[a] = fma(d3, blk[3 * j + a], xsss[a]);
+        }
+    }
+    const double *t = S.tang + (int64_t)3 * n * m + 3 * k;
+    const double Tk = blk[3 * n + k];
+    const double E = S.E[m];
+    double F[3], L[3], arm[3], axf[3];
+    for (int a = 0; a < 3; ++a) F[a] = -E * xsss[a] + Tk * t[a];
+    cross3(xss, t, L);
+    for (int a = 0; a < 3; ++a) {
+        L[a] *= E;
+        arm[a] = S.X[(int64_t)3 * n * m + 3 * k + a] - S.pcenter[3 * body + a];
+    }
+    cross3(arm, F, axf);
+    for (int a = 0; a < 3; ++a) {
+        o[a] = F[a];
+        o[3 + a] = L[a] + axf[a];
+    }
+}
+
+// Sum the per-fiber wrenches per particle in fiber order (+ F_ext, L_ext).
+__global__ void wrench_reduce_kernel(sf_fiber_sys S, const double *__restrict__ wf,
+                                     const double *__restrict__ ext, int constants,
+                                     double *__restrict__ wout) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= S.np) return;
+    double F[3] = {0, 0, 0}, L[3] = {0, 0, 0};
+    for (int64_t m = 0; m < S.nf; ++m) {
+        if (S.bc_body[m] != p || S.bc_kind[2 * m + 1] != BC_CLAMPED) continue;
+        for (int a = 0; a < 3; ++a) {
+            F[a] += wf[6 * m + a];
+            L[a] += wf[6 * m + 3 + a];
+        }
+    }
+    if (constants && ext) {
+        for (int a = 0; a < 3; ++a) {
+            F[a] = F[a] + ext[6 * p + a];
+            L[a] = L[a] + ext[6 * p + 3 + a];
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        wout[6 * p + a] = F[a];
+        wout[6 * p + 3 + a] = L[a];
+    }
+}
+
+// ----------------------------------------------------------- fiber rows
+// One fiber's 4n residual rows (solver.py:137-184 with bc_residuals,
+// fiber.py:375-441): velocity rows, inextensibility rows, and the 14
+// boundary residuals in their replacement slots.
+__global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
+                                  const double *__restrict__ ubar, int constants,
+                                  double *__restrict__ out) {
+    extern __shared__ double sm[];
+    const int n = (int)S.n, m = blockIdx.x, n3 = 3 * n;
+    double *X = sm, *T = X + n3, *Xc = T + n, *t = Xc + n3, *fel = t + n3, *f = fel + n3,
+           *flow = f + n3, *w = flow + n3, *res = w + n3;  // res: 14 BC values
+    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
+    const int64_t o3 = (int64_t)n3 * m;
+    const double dt = S.dt;
+    for (int e = threadIdx.x; e < n3; e += blockDim.x) {
+        X[e] = blk[e];
+        Xc[e] = S.X[o3 + e];
+        t[e] = S.tang[o3 + e];
+    }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) T[e] = blk[n3 + e];
+    __syncthreads();
+    FiberCtx c = fiber_ctx(S, m);
+    const double E = S.E[m];
+    elastic_force(c, E, X, T, t, fel);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n3; e += blockDim.x)
+        f[e] = (constants && S.f_ext) ? fel[e] + S.f_ext[o3 + e] : fel[e];
+    __syncthreads();
+    // flow = M f + K f + u_bar ; warp per row
+    const double *K = S.K + (int64_t)n3 * n3 * m;
+    const double cl = S.c_log[m], c2 = S.c_two;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = warp; r < n3; r += nw) {
+        double acc = 0.0;
+        for (int col = lane; col < n3; col += 32) acc = fma(K[(int64_t)r * n3 + col], f[col], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const int i = r / 3, a = r - 3 * i;
+            const double fdt = f[3 * i] * t[3 * i] + f[3 * i + 1] * t[3 * i + 1] + f[3 * i + 2] * t[3 * i + 2];
+            const double ft = fdt * t[r];
+            const double mob = cl * (f[r] + ft) + c2 * (f[r] - ft);
+            flow[r] = (mob + acc) + (ubar ? ubar[o3 + r] : 0.0);
+        }
+    }
+    __syncthreads();
+    const double Lm = S.L[m], Ldot = S.Ldot[m];
+    const double *sa = S.s_alpha + (int64_t)n * m;
+    double *o = out + S.fib_off + (int64_t)4 * n * m;
+    // velocity rows and w
+    for (int e = threadIdx.x; e < n3; e += blockDim.x) {
+        const int i = e / 3;
+        const double xa = t[e] * sa[i];
+        const double rep = (Ldot != 0.0) ? (S.nodes[i] + 1.0) * Ldot / Lm * xa : 0.0;
+        double v = X[e] / dt - flow[e];
+        double wv = flow[e];
+        if (constants) {
+            v -= Xc[e] / dt + rep;
+            wv = wv + (Xc[e] / dt + rep);
+        }
+        o[e] = v;
+        w[e] = wv;
+    }
+    __syncthreads();
+    // inextensibility rows: ((D w) . Xa)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double d0 = 0, d1 = 0, d2 = 0;
+        for (int j = 0; j < n; ++j) {
+            const double dij = S.D[i * n + j];
+            d0 = fma(dij, w[3 * j], d0);
+            d1 = fma(dij, w[3 * j + 1], d1);
+            d2 = fma(dij, w[3 * j + 2], d2);
+        }
+        const double x0 = t[3 * i] * sa[i], x1 = t[3 * i + 1] * sa[i], x2 = t[3 * i + 2] * sa[i];
+        double v = d0 * x0 + d1 * x1 + d2 * x2;
+        if (constants) v -= (1.0 / dt + Ldot / Lm) * (x0 * x0 + x1 * x1 + x2 * x2);
+        o[n3 + i] = v;
+    }
+    // boundary residuals (warp 0)
+    if (warp == 0) {
+        for (int end = 0; end < 2; ++end) {  // 0 = plus (node 0), 1 = minus (node n-1)
+            const int k = end == 0 ? 0 : n - 1;
+            const double sig = end == 0 ? 1.0 : -1.0;
+            const int kind = S.bc_kind[2 * m + end];
+            const double *P = S.bc_par + ((int64_t)2 * m + end) * P_N;
+            double xs[3] = {0, 0, 0}, xss[3] = {0, 0, 0}, xsss[3] = {0, 0, 0};
+            for (int j = lane; j < n; j += 32) {
+                for (int a = 0; a < 3; ++a) {
+                    xs[a] = fma(c.Ds[k * n + j], X[3 * j + a], xs[a]);
+                    xss[a] = fma(c.Ds2[k * n + j], X[3 * j + a], xss[a]);
+                    xsss[a] = fma(c.Ds3[k * n + j], X[3 * j + a], xsss[a]);
+                }
+            }
+            for (int a = 0; a < 3; ++a) {
+                xs[a] = warp_sum(xs[a]);
+                xss[a] = warp_sum(xss[a]);
+                xsss[a] = warp_sum(xsss[a]);
+            }
+            // clamped: (M f_el + K f_el) at node k
+            double vself[3] = {0, 0, 0};
+            if (kind == BC_CLAMPED) {
+                for (int a = 0; a < 3; ++a) {
+                    double acc = 0.0;
+                    for (int col = lane; col < n3; col += 32)
+                        acc = fma(K[(int64_t)(3 * k + a) * n3 + col], fel[col], acc);
+                    vself[a] = warp_sum(acc);
+                }
+                const double fdt = fel[3 * k] * t[3 * k] + fel[3 * k + 1] * t[3 * k + 1] +
+                                   fel[3 * k + 2] * t[3 * k + 2];
+                for (int a = 0; a < 3; ++a) {
+                    const double ft = fdt * t[3 * k + a];
+                    vself[a] = (cl * (fel[3 * k + a] + ft) + c2 * (fel[3 * k + a] - ft)) + vself[a];
+                }
+            }
+            if (lane == 0) {
+                const double *tk = t + 3 * k;
+                const double Tk = T[k];
+                double v1[3], v2[3], tr;
+                if (kind == BC_FREE) {
+                    for (int a = 0; a < 3; ++a) { v1[a] = xss[a]; v2[a] = xsss[a]; }
+                    tr = Tk;
+                } else if (kind == BC_FORCE) {
+                    double Fx[3];
+                    for (int a = 0; a < 3; ++a) Fx[a] = -E * xsss[a] + Tk * tk[a];
+                    if (!constants) {
+                        for (int a = 0; a < 3; ++a) { v1[a] = Fx[a]; v2[a] = xss[a]; }
+                        tr = Tk;
+                    } else {
+                        double txq[3];
+                        cross3(tk, P + P_TQ, txq);
+                        const double Fdt = P[P_F] * tk[0] + P[P_F + 1] * tk[1] + P[P_F + 2] * tk[2];
+                        const double qq = P[P_TQ] * P[P_TQ] + P[P_TQ + 1] * P[P_TQ + 1] +
+                                          P[P_TQ + 2] * P[P_TQ + 2];
+                        for (int a = 0; a < 3; ++a) {
+                            v1[a] = Fx[a] - sig * P[P_F + a];
+                            v2[a] = xss[a] - sig * txq[a] / E;
+                        }
+                        tr = Tk - sig * (Fdt + qq / E);
+                    }
+                } else if (kind == BC_HINGED) {
+                    double spring[3];
+                    for (int a = 0; a < 3; ++a) {
+                        const double anchor = constants ? P[P_ANCHOR + a] : 0.0;
+                        spring[a] = -P[P_STIFF] * (X[3 * k + a] - anchor);
+                        v1[a] = (-E * xsss[a] + Tk * tk[a]) - sig * spring[a];
+                        v2[a] = xss[a];
+                    }
+                    tr = Tk - sig * (spring[0] * tk[0] + spring[1] * tk[1] + spring[2] * tk[2]);
+                } else {  // clamped to a body (minus end only)
+                    const int body = S.bc_body[m];
+                    const double *U = u + S.p_uoff[body];
+                    const double *Om = U + 3;
+                    const double *cen = S.pcenter + 3 * body;
+                    double arm[3], oxa[3], oxt[3];
+                    for (int a = 0; a < 3; ++a) arm[a] = Xc[3 * k + a] - cen[a];
+                    cross3(Om, arm, oxa);
+                    cross3(Om, tk, oxt);
+                    for (int a = 0; a < 3; ++a) {
+                        const double vel = (X[3 * k + a] - (constants ? Xc[3 * k + a] : 0.0)) / dt;
+                        v1[a] = vel - U[a] - oxa[a];
+                        if (P[P_HAS_TANGENT] != 0.0)
+                            v2[a] = (xs[a] - (constants ? tk[a] : 0.0)) / dt - oxt[a];
+                        else
+                            v2[a] = xss[a];
+                    }
+                    // u_bar at the minus end (solver.py:175-177)
+                    const double *ub = ubar ? ubar + o3 + 3 * (n - 1) : nullptr;
+                    double s = 0.0;
+                    for (int a = 0; a < 3; ++a)
+                        s += (vself[a] + (ub ? ub[a] : 0.0) - U[a] - oxa[a]) * tk[a];
+                    tr = s;
+                }
+                for (int a = 0; a < 3; ++a) {
+                    res[6 * end + a] = v1[a];
+                    res[6 * end + 3 + a] = v2[a];
+                }
+                res[12 + end] = tr;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 3; ++a) {
+            o[0 + a] = res[0 + a];                  // vel[0]   = plus vec1
+            o[3 + a] = res[3 + a];                  // vel[1]   = plus vec2
+            o[3 * (n - 1) + a] = res[6 + a];        // vel[n-1] = minus vec1
+            o[3 * (n - 2) + a] = res[9 + a];        // vel[n-2] = minus vec2
+        }
+        o[n3] = res[12];                            // inext[0]
+        o[n3 + n - 1] = res[13];                    // inext[n-1]
+    }
+}
+
+// ------------------------------------------------------------ self blocks
+// Dense 4n x 4n fiber block (solver.py:250-294) with the boundary rows of the
+// homogeneous, body-fixed (U = omega = 0, u_bar = 0) residual map.
+__global__ void self_block_kernel(sf_fiber_sys S, double *__restrict__ A) {
+    extern __shared__ double sm[];
+    const int n = (int)S.n, m = blockIdx.x, n3 = 3 * n, ld = 4 * n;
+    double *ds = sm, *ds4 = ds + n * n, *t = ds4 + n * n, *xa = t + n3, *bcrow = xa + n3;  // 14 x ld
+    FiberCtx c = fiber_ctx(S, m);
+    const int64_t o3 = (int64_t)n3 * m;
+    const double *sa = S.s_alpha + (int64_t)n * m;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        ds[e] = c.Ds[e];
+        ds4[e] = c.Ds4[e];
+    }
+    for (int e = threadIdx.x; e < n3; e += blockDim.x) {
+        t[e] = S.tang[o3 + e];
+        xa[e] = t[e] * sa[e / 3];
+    }
+    __syncthreads();
+    const double *K = S.K + (int64_t)n3 * n3 * m;
+    const double cl = S.c_log[m], c2 = S.c_two, E = S.E[m], dt = S.dt;
+    double *Am = A + (int64_t)ld * ld * m;
+    // MK[r, col] on the fly: M is 3x3 block diagonal
+    auto MK = [&](int r, int col) -> double {
+        double v = K[(int64_t)r * n3 + col];
+        const int i = r / 3;
+        if (col / 3 == i) {
+            const int a = r - 3 * i, b = col - 3 * i;
+            const double tt = t[3 * i + a] * t[3 * i + b];
+            const double d = (a == b) ? 1.0 : 0.0;
+            v += cl * (d + tt) + c2 * (d - tt);
+        }
+        return v;
+    };
+    // top rows: A[r, 3j+b] = d/dt - (MK FX)[r, 3j+b];  A[r, 3n+j] = -(MK FT)[r, j]
+    for (int e = threadIdx.x; e < n3 * ld; e += blockDim.x) {
+        const int r = e / ld, col = e - r * ld;
+        double v;
+        if (col < n3) {
+            const int j = col / 3, b = col - 3 * j;
+            double acc = 0.0;
+            for (int i = 0; i < n; ++i) acc = fma(MK(r, 3 * i + b), ds4[i * n + j], acc);
+            v = (r == col ? 1.0 / dt : 0.0) - (-E * acc);
+        } else {
+            const int j = col - n3;
+            double acc = 0.0;
+            for (int i = 0; i < n; ++i) {
+                const double dij = ds[i * n + j];
+                acc = fma(MK(r, 3 * i), dij * t[3 * j], acc);
+                acc = fma(MK(r, 3 * i + 1), dij * t[3 * j + 1], acc);
+                acc = fma(MK(r, 3 * i + 2), dij * t[3 * j + 2], acc);
+            }
+            v = -acc;
+        }
+        Am[(int64_t)r * ld + col] = v;
+    }
+    __syncthreads();
+    // bottom rows: A[3n+i, col] = sum_{j,c} D[i,j] Xa[i,c] G[3j+c, col] with
+    // G = MK [FX | FT] = [I/dt - A_top_left | -A_top_right]
+    for (int e = threadIdx.x; e < n * ld; e += blockDim.x) {
+        const int i = e / ld, col = e - i * ld;
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double dij = S.D[i * n + j];
+            for (int a = 0; a < 3; ++a) {
+                const int r = 3 * j + a;
+                const double top = Am[(int64_t)r * ld + col];
+                const double g = col < n3 ? ((r == col ? 1.0 / dt : 0.0) - top) : -top;
+                acc = fma(dij * xa[3 * i + a], g, acc);
+            }
+        }
+        Am[(int64_t)(n3 + i) * ld + col] = acc;
+    }
+    // boundary rows into smem (the clamped tension row reads top rows first)
+    for (int e = threadIdx.x; e < 14 * ld; e += blockDim.x) bcrow[e] = 0.0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * ld; e += blockDim.x) {
+        const int end = e / ld, col = e - end * ld;
+        const int k = end == 0 ? 0 : n - 1;
+        const double sig = end == 0 ? 1.0 : -1.0;
+        const int kind = S.bc_kind[2 * m + end];
+        const double *P = S.bc_par + ((int64_t)2 * m + end) * P_N;
+        double *r1 = bcrow + (6 * end) * ld, *r2 = r1 + 3 * ld, *rt = bcrow + (12 + end) * ld;
+        const double *tk = t + 3 * k;
+        if (col < n3) {
+            const int j = col / 3, b = col - 3 * j;
+            const double d1 = c.Ds[k * n + j], d2 = c.Ds2[k * n + j], d3 = c.Ds3[k * n + j];
+            if (kind == BC_FREE) {
+                r1[b * ld + col] = d2;
+                r2[b * ld + col] = d3;
+            } else if (kind == BC_FORCE) {
+                r1[b * ld + col] = -E * d3;
+                r2[b * ld + col] = d2;
+            } else if (kind == BC_HINGED) {
+                r1[b * ld + col] = -E * d3 + (j == k ? sig * P[P_STIFF] : 0.0);
+                r2[b * ld + col] = d2;
+                if (j == k) rt[col] = sig * P[P_STIFF] * tk[b];
+            } else {
+                r1[b * ld + col] = (j == k) ? 1.0 / dt : 0.0;
+                r2[b * ld + col] = P[P_HAS_TANGENT] != 0.0 ? d1 / dt : d2;
+                double s = 0.0;
+                for (int a = 0; a < 3; ++a) {
+                    const int r = 3 * k + a;
+                    s += tk[a] * ((r == col ? 1.0 / dt : 0.0) - Am[(int64_t)r * ld + col]);
+                }
+                rt[col] = s;
+            }
+        } else {
+            const int j = col - n3;
+            if (kind == BC_CLAMPED) {
+                double s = 0.0;
+                for (int a = 0; a < 3; ++a) s += tk[a] * (-Am[(int64_t)(3 * k + a) * ld + col]);
+                rt[col] = s;
+            } else {
+                if (j == k) rt[col] = 1.0;
+                if ((kind == BC_FORCE || kind == BC_HINGED) && j == k)
+                    for (int b = 0; b < 3; ++b) r1[b * ld + col] = tk[b];
+            }
+        }
+    }
+    __syncthreads();
+    const int slots[4] = {0, 1, n - 1, n - 2};
+    for (int e = threadIdx.x; e < 14 * ld; e += blockDim.x) {
+        const int row = e / ld, col = e - row * ld;
+        int dst;
+        if (row < 12) dst = 3 * slots[row / 3] + (row % 3);
+        else dst = row == 12 ? n3 : ld - 1;
+        Am[(int64_t)dst * ld + col] = bcrow[e];
+    }
+}
+
+// ------------------------------------------------------------ block LU
+// Equilibrated (row then column max-abs) LU with partial pivoting of one
+// m x m block in shared memory (solver.py:386-404, scipy lu_factor).  The
+// factors are written back column-major (LAPACK layout) for the solves.
+// info: 0 ok, 1 non-finite, 2 zero row, 3 zero pivot.
+__global__ void block_lu_smem_kernel(double *__restrict__ A, int mdim, double *__restrict__ rsc,
+                                     double *__restrict__ csc, int *__restrict__ piv,
+                                     int *__restrict__ info) {
+    extern __shared__ double a[];  // row-major m x m
+    __shared__ int s_piv;
+    __shared__ int s_bad;
+    const int b = blockIdx.x, mm = mdim * mdim;
+    double *Ab = A + (int64_t)mm * b;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) {
+        const double v = Ab[e];
+        a[e] = v;
+        if (!isfinite(v)) s_bad = 1;
+    }
+    __syncthreads();
+    // row scaling
+    for (int i = threadIdx.x; i < mdim; i += blockDim.x) {
+        double r = 0.0;
+        for (int j = 0; j < mdim; ++j) r = fmax(r, fabs(a[i * mdim + j]));
+        rsc[(int64_t)mdim * b + i] = r;
+        if (r == 0.0) s_bad = s_bad ? s_bad : 2;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) a[e] = a[e] / rsc[(int64_t)mdim * b + e / mdim];
+    __syncthreads();
+    for (int j = threadIdx.x; j < mdim; j += blockDim.x) {
+        double c = 0.0;
+        for (int i = 0; i < mdim; ++i) c = fmax(c, fabs(a[i * mdim + j]));
+        csc[(int64_t)mdim * b + j] = c;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) a[e] = a[e] / csc[(int64_t)mdim * b + e % mdim];
+    __syncthreads();
+    for (int k = 0; k < mdim; ++k) {
+        if (threadIdx.x < 32) {  // pivot search: first index of the max |a_ik|
+            double best = -1.0;
+            int bi = k;
+            for (int i = k + threadIdx.x; i < mdim; i += 32) {
+                const double v = fabs(a[i * mdim + k]);
+                if (v > best) { best = v; bi = i; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            }
+            if (threadIdx.x == 0) {
+                s_piv = bi;
+                piv[(int64_t)mdim * b + k] = bi;
+                if (best == 0.0 && !s_bad) s_bad = 3;
+            }
+        }
+        __syncthreads();
+        const int p = s_piv;
+        if (p != k)
+            for (int j = threadIdx.x; j < mdim; j += blockDim.x) {
+                const double tmp = a[k * mdim + j];
+                a[k * mdim + j] = a[p * mdim + j];
+                a[p * mdim + j] = tmp;
+            }
+        __syncthreads();
+        const double pv = a[k * mdim + k];
+        for (int i = k + 1 + threadIdx.x; i < mdim; i += blockDim.x)
+            a[i * mdim + k] = pv != 0.0 ? a[i * mdim + k] / pv : 0.0;
+        __syncthreads();
+        const int rem = mdim - k - 1;
+        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+            const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+            a[i * mdim + j] = fma(-a[i * mdim + k], a[k * mdim + j], a[i * mdim + j]);
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < mm; e += blockDim.x) {
+        const int i = e / mdim, j = e - i * mdim;
+        Ab[(int64_t)j * mdim + i] = a[e];  // column-major
+    }
+    if (threadIdx.x == 0) info[b] = s_bad;
+}
+
+// x_block = (LU \ (v_block / r)) / c for every fiber block, and v / diag on
+// every other row (solver.py:425-429).  LU column-major, piv 0-based row
+// swaps applied in order (LAPACK getrs).
+__global__ void block_solve_kernel(const double *__restrict__ LU, const double *__restrict__ rsc,
+                                   const double *__restrict__ csc, const int *__restrict__ piv,
+                                   int mdim, int64_t off0, const double *__restrict__ v,
+                                   double *__restrict__ x) {
+    extern __shared__ double y[];
+    const int b = blockIdx.x;
+    const double *L = LU + (int64_t)mdim * mdim * b;
+    const double *vb = v + off0 + (int64_t)mdim * b;
+    const double *r = rsc + (int64_t)mdim * b;
+    const int *pv = piv + (int64_t)mdim * b;
+    for (int i = threadIdx.x; i < mdim; i += blockDim.x) y[i] = vb[i] / r[i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < mdim; ++k) {
+            const int p = pv[k];
+            if (p != k) { const double tmp = y[k]; y[k] = y[p]; y[p] = tmp; }
+        }
+    __syncthreads();
+    for (int k = 0; k < mdim; ++k) {  // unit lower
+        const double yk = y[k];
+        for (int i = k + 1 + threadIdx.x; i < mdim; i += blockDim.x)
+            y[i] = fma(-L[(int64_t)k * mdim + i], yk, y[i]);
+        __syncthreads();
+    }
+    for (int k = mdim - 1; k >= 0; --k) {  // upper
+        if (threadIdx.x == 0) y[k] = y[k] / L[(int64_t)k * mdim + k];
+        __syncthreads();
+        const double yk = y[k];
+        for (int i = threadIdx.x; i < k; i += blockDim.x) y[i] = fma(-L[(int64_t)k * mdim + i], yk, y[i]);
+        __syncthreads();
+    }
+    const double *c = csc + (int64_t)mdim * b;
+    double *xb = x + off0 + (int64_t)mdim * b;
+    for (int i = threadIdx.x; i < mdim; i += blockDim.x) xb[i] = y[i] / c[i];
+}
+
+__global__ void diag_div_kernel(const double *__restrict__ v, const double *__restrict__ diag,
+                                int64_t n, double *__restrict__ x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v[i] / diag[i];
+}
+
+// --------------------------------------------------------- surface rows
+// Rigid averages (body.py:286-295) per particle: (sum w q, sum w (y-c) x q)/area.
+__global__ void rigid_avg_kernel(const double *__restrict__ nodes, const double *__restrict__ w,
+                                 const double *__restrict__ q, int64_t n, const double *center,
+                                 double area, double *__restrict__ out6) {
+    __shared__ double red[6][32];
+    double s[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double *qi = q + 3 * i;
+        double arm[3] = {nodes[3 * i] - center[0], nodes[3 * i + 1] - center[1],
+                         nodes[3 * i + 2] - center[2]};
+        double aq[3];
+        cross3(arm, qi, aq);
+        for (int a = 0; a < 3; ++a) {
+            s[a] += w[i] * qi[a];
+            s[3 + a] += w[i] * aq[a];
+        }
+    }
+    for (int a = 0; a < 6; ++a) s[a] = warp_sum(s[a]);
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 6; ++a) red[a][threadIdx.x >> 5] = s[a];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 6; ++a) {
+            double v = 0.0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) v += red[a][k];
+            out6[a] = v / area;
+        }
+    }
+}
+
+// flux = sum w (n . q) for the periphery null-space completion (body.py:265-269)
+__global__ void flux_kernel(const double *__restrict__ nrm, const double *__restrict__ w,
+                            const double *__restrict__ q, int64_t n, double *__restrict__ out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        s += w[i] * (nrm[3 * i] * q[3 * i] + nrm[3 * i + 1] * q[3 * i + 1] + nrm[3 * i + 2] * q[3 * i + 2]);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) v += red[k];
+        out[0] = v;
+    }
+}
+
+// particle rows (solver.py:332-345): rows already hold DL_on + wrench flow;
+// add u_bar and subtract the rigid motion; write U/omega rows.
+__global__ void particle_rows_kernel(const double *__restrict__ nodes, int64_t n,
+                                     const double *__restrict__ center,
+                                     const double *__restrict__ ubar,
+                                     const double *__restrict__ Uom, const double *__restrict__ avg,
+                                     double mu, double *__restrict__ rows,
+                                     double *__restrict__ out_uom) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        for (int a = 0; a < 3; ++a) {
+            out_uom[a] = Uom[a] - avg[a] / mu;
+            out_uom[3 + a] = Uom[3 + a] - avg[3 + a] / mu;
+        }
+    }
+    if (i >= n) return;
+    const double arm[3] = {nodes[3 * i] - center[0], nodes[3 * i + 1] - center[1],
+                           nodes[3 * i + 2] - center[2]};
+    double oxa[3];
+    cross3(Uom + 3, arm, oxa);
+    for (int a = 0; a < 3; ++a) {
+        double v = rows[3 * i + a];
+        if (ubar) v += ubar[3 * i + a];
+        rows[3 * i + a] = v - (Uom[a] + oxa[a]);
+    }
+}
+
+// periphery rows (solver.py:347-355): DL_on + q/mu + n flux/(mu area) + u_bar
+__global__ void periphery_rows_kernel(const double *__restrict__ nrm, int64_t n,
+                                      const double *__restrict__ q, const double *__restrict__ flux,
+                                      double scale, const double *__restrict__ ubar, double mu,
+                                      double *__restrict__ rows) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int a = 0; a < 3; ++a) {
+        double v = rows[3 * i + a];
+        v += q[3 * i + a] / mu;
+        v += scale * (nrm[3 * i + a] * flux[0]);
+        if (ubar) v += ubar[3 * i + a];
+        rows[3 * i + a] = v;
+    }
+}
+
+// Stokeslet + rotlet of a wrench at a point, accumulated into u
+// (solver.py:125-134); targets are surface nodes, never at the centre.
+__global__ void wrench_flow_kernel(const double *__restrict__ trg, int64_t nt,
+                                   const double *__restrict__ center,
+                                   const double *__restrict__ W, double pref,
+                                   double *__restrict__ u) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nt) return;
+    const double rx = trg[3 * i] - center[0], ry = trg[3 * i + 1] - center[1],
+                 rz = trg[3 * i + 2] - center[2];
+    const double d = sqrt(rx * rx + ry * ry + rz * rz);
+    const double d3 = d * d * d;
+    const double rF = (rx * W[0] + ry * W[1] + rz * W[2]) / d3;
+    double v[3] = {pref * (W[0] / d + rF * rx), pref * (W[1] / d + rF * ry),
+                   pref * (W[2] / d + rF * rz)};
+    v[0] += pref * (W[4] * rz - W[5] * ry) / d3;
+    v[1] += pref * (W[5] * rx - W[3] * rz) / d3;
+    v[2] += pref * (W[3] * ry - W[4] * rx) / d3;
+    u[3 * i] += v[0];
+    u[3 * i + 1] += v[1];
+    u[3 * i + 2] += v[2];
+}
+
+// ---------------------------------------------------------- vector kernels
+// Deterministic dot product: fixed grid, fixed per-thread stride order,
+// block tree, then one block sums the block partials in order.
+constexpr int kDotBlocks = 296, kDotThreads = 256;
+__global__ void dot_partial_kernel(const double *__restrict__ x, const double *__restrict__ y,
+                                   int64_t n, double *__restrict__ part) {
+    __shared__ double red[kDotThreads / 32];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < n;
+         i += (int64_t)kDotBlocks * kDotThreads)
+        s = fma(x[i], y[i], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int k = 0; k < kDotThreads / 32; ++k) v += red[k];
+        part[blockIdx.x] = v;
+    }
+}
+// mode 0: out = sum; mode 1: out = sqrt(sum)
+__global__ void dot_final_kernel(const double *__restrict__ part, double *__restrict__ out,
+                                 int mode) {
+    __shared__ double red[kDotThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) s += part[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int k = 0; k < kDotThreads / 32; ++k) v += red[k];
+        out[0] = mode ? sqrt(v) : v;
+    }
+}
+// y += alpha x where alpha = sgn * (*a) (device scalar) ; or y = x * (1 / *a) (mode 2)
+__global__ void axpy_dev_kernel(const double *__restrict__ a, double sgn, int mode,
+                                const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+    const double al = mode == 2 ? 1.0 / a[0] : sgn * a[0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == 2) y[i] = x[i] * al;
+        else y[i] = fma(al, x[i], y[i]);
+    }
+}
+// x += sum_j coef[j] V[j]  (coefficients in device memory; fixed j order)
+__global__ void combine_kernel(const double *__restrict__ V, int64_t ld, int k,
+                               const double *__restrict__ coef, double *__restrict__ x, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < k; ++j) s = fma(coef[j], V[(int64_t)j * ld + i], s);
+        x[i] += s;
+    }
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+// =================================================================== C ABI
+namespace {
+int grid1d(int64_t n, int threads = 256) {
+    int64_t g = (n + threads - 1) / threads;
+    return (int)(g < 1 ? 1 : (g > 8192 ? 8192 : g));
+}
+int set_smem(const void *fn, size_t bytes) {
+    if (bytes > 48 * 1024 &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+            cudaSuccess)
+        return check_launch("cudaFuncSetAttribute");
+    return SF_OK;
+}
+}  // namespace
+
+#define SF_CHECK_SYS(S)                                                              \
+    do {                                                                             \
+        if (!(S)) return set_error(SF_EINVAL, "null fiber system");                 \
+        if ((S)->nf < 0 || ((S)->nf > 0 && (S)->n < 5))                             \
+            return set_error(SF_EINVAL, "bad fiber sizes");                          \
+    } while (0)
+
+extern "C" {
+
+int sf_fiber_dpow(const double *D, const double *s_alpha, int64_t nf, int64_t n, double *Dpow,
+                  void *stream) {
+    if (nf <= 0) return SF_OK;
+    const size_t smem = sizeof(double) * 2 * n * n;
+    int rc = set_smem((const void *)dpow_kernel, smem);
+    if (rc) return rc;
+    dpow_kernel<<<(unsigned)nf, 256, smem, (cudaStream_t)stream>>>(D, s_alpha, (int)n, Dpow);
+    return check_launch("dpow_kernel");
+}
+
+int sf_fiber_forces(const sf_fiber_sys *S, const double *u, int constants, double *f,
+                    void *stream) {
+    SF_CHECK_SYS(S);
+    if (S->nf == 0) return SF_OK;
+    const size_t smem = sizeof(double) * 7 * S->n;
+    fiber_forces_kernel<<<(unsigned)S->nf, 128, smem, (cudaStream_t)stream>>>(*S, u, constants, f);
+    return check_launch("fiber_forces_kernel");
+}
+
+int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *ext, int constants,
+                         double *work, double *wout, void *stream) {
+    SF_CHECK_SYS(S);
+    if (S->np == 0) return SF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (S->nf > 0) {
+        end_wrench_kernel<<<grid1d(S->nf, 128), 128, 0, st>>>(*S, u, work);
+        int rc = check_launch("end_wrench_kernel");
+        if (rc) return rc;
+    }
+    wrench_reduce_kernel<<<grid1d(S->np, 32), 32, 0, st>>>(*S, work, ext, constants, wout);
+    return check_launch("wrench_reduce_kernel");
+}
+
+int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *ubar, int constants,
+                  double *out, void *stream) {
+    SF_CHECK_SYS(S);
+    if (S->nf == 0) return SF_OK;
+    const size_t smem = sizeof(double) * (8 * 3 * S->n + 2 * S->n + 16);
+    int rc = set_smem((const void *)fiber_rows_kernel, smem);
+    if (rc) return rc;
+    fiber_rows_kernel<<<(unsigned)S->nf, 128, smem, (cudaStream_t)stream>>>(*S, u, ubar, constants,
+                                                                           out);
+    return check_launch("fiber_rows_kernel");
+}
+
+int sf_fiber_self_blocks(const sf_fiber_sys *S, double *A, void *stream) {
+    SF_CHECK_SYS(S);
+    if (S->nf == 0) return SF_OK;
+    const int64_t n = S->n;
+    const size_t smem = sizeof(double) * (2 * n * n + 6 * n + 14 * 4 * n);
+    int rc = set_smem((const void *)self_block_kernel, smem);
+    if (rc) return rc;
+    self_block_kernel<<<(unsigned)S->nf, 256, smem, (cudaStream_t)stream>>>(*S, A);
+    return check_launch("self_block_kernel");
+}
+
+int sf_block_lu(double *A, int64_t nb, int64_t m, double *r, double *c, int *piv, int *info,
+                void *stream) {
+    if (nb <= 0) return SF_OK;
+    const size_t smem = sizeof(double) * m * m;
+    if (smem > 227 * 1024) return set_error(SF_EINVAL, "block of %lld rows exceeds shared memory",
+                                            (long long)m);
+    int rc = set_smem((const void *)block_lu_smem_kernel, smem);
+    if (rc) return rc;
+    block_lu_smem_kernel<<<(unsigned)nb, 256, smem, (cudaStream_t)stream>>>(A, (int)m, r, c, piv,
+                                                                            info);
+    return check_launch("block_lu_smem_kernel");
+}
+
+int sf_precond_apply(const double *LU, const double *r, const double *c, const int *piv,
+                     int64_t nb, int64_t m, int64_t off0, const double *diag, int64_t ndiag,
+                     const double *v, double *x, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ndiag > 0) {
+        diag_div_kernel<<<grid1d(ndiag), 256, 0, st>>>(v, diag, ndiag, x);
+        int rc = check_launch("diag_div_kernel");
+        if (rc) return rc;
+    }
+    if (nb > 0) {
+        block_solve_kernel<<<(unsigned)nb, 128, sizeof(double) * m, st>>>(LU, r, c, piv, (int)m,
+                                                                         off0, v, x);
+        return check_launch("block_solve_kernel");
+    }
+    return SF_OK;
+}
+
+int sf_surface_rows(int kind, const double *nodes, const double *nrm, const double *w, int64_t n,
+                    const double *center, double area, const double *q, const double *ubar,
+                    const double *Uom, double mu, double *work, double *rows, double *out_uom,
+                    void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (kind == 0) {  // rigid particle: rows hold DL_on + wrench flow on entry
+        rigid_avg_kernel<<<1, 256, 0, st>>>(nodes, w, q, n, center, area, work);
+        int rc = check_launch("rigid_avg_kernel");
+        if (rc) return rc;
+        particle_rows_kernel<<<grid1d(n), 256, 0, st>>>(nodes, n, center, ubar, Uom, work, mu, rows,
+                                                        out_uom);
+        return check_launch("particle_rows_kernel");
+    }
+    flux_kernel<<<1, 256, 0, st>>>(nrm, w, q, n, work);
+    int rc = check_launch("flux_kernel");
+    if (rc) return rc;
+    periphery_rows_kernel<<<grid1d(n), 256, 0, st>>>(nrm, n, q, work, 1.0 / (mu * area), ubar, mu,
+                                                     rows);
+    return check_launch("periphery_rows_kernel");
+}
+
+int sf_wrench_flow(const double *trg, int64_t nt, const double *center, const double *wrench,
+                   double mu, double *u, void *stream) {
+    if (nt <= 0) return SF_OK;
+    wrench_flow_kernel<<<grid1d(nt), 256, 0, (cudaStream_t)stream>>>(
+        trg, nt, center, wrench, 1.0 / (8.0 * M_PI * mu), u);
+    return check_launch("wrench_flow_kernel");
+}
+
+int sf_dot(const double *x, const double *y, int64_t n, double *work, double *out, int sqrt_mode,
+           void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    dot_partial_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(x, y, n, work);
+    dot_final_kernel<<<1, kDotThreads, 0, st>>>(work, out, sqrt_mode);
+    return check_launch("dot");
+}
+
+int sf_axpy_dev(const double *a, double sgn, int mode, const double *x, double *y, int64_t n,
+                void *stream) {
+    axpy_dev_kernel<<<grid1d(n), 256, 0, (cudaStream_t)stream>>>(a, sgn, mode, x, y, n);
+    return check_launch("axpy_dev_kernel");
+}
+
+int sf_combine(const double *V, int64_t ld, int k, const double *coef, double *x, int64_t n,
+               void *stream) {
+    if (k <= 0) return SF_OK;
+    combine_kernel<<<grid1d(n), 256, 0, (cudaStream_t)stream>>>(V, ld, k, coef, x, n);
+    return check_launch("combine_kernel");
+}
+
+}  // extern "C"

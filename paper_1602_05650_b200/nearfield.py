@@ -156,3 +156,195 @@ def find_fiber_pairs(fibers, targets, target_groups, mu, include_doublet=True):
             Wp = plain_fiber_weights(fib, targets[t], mu, include_doublet=include_doublet)
             out.append((int(t), l, Wn - Wp))
     return out
+
+
+# --------------------------------------------------------------- surfaces ----
+# Nearly singular double-layer evaluation near a surface (body.py:371-519):
+# a one-sided on-surface anchor (subtracted principal value plus the interior
+# jump) and three off-surface samples at 1.5h, 2.25h, 3.375h on a six-fold
+# refined mesh, combined by Lagrange interpolation along the normal ray and
+# mapped back to the coarse nodal density by patchwise tensor interpolation.
+
+from .body import GL01_NODES, make_surface  # noqa: E402
+
+_REFINED = {}
+
+
+def _lagrange(x, nodes):
+    x = np.atleast_1d(np.asarray(x, dtype=float))
+    c = np.ones((x.size, len(nodes)))
+    for i in range(len(nodes)):
+        for j in range(len(nodes)):
+            if i != j:
+                c[:, i] *= (x - nodes[j]) / (nodes[i] - nodes[j])
+    return c
+
+
+def refined(mesh, factor):
+    key = (id(mesh), factor)
+    if key not in _REFINED:
+        nt, nph = mesh.patch_grid
+        _REFINED[key] = (mesh, make_surface(mesh.shape, (nt * factor, nph * factor),
+                                            center=mesh.center))
+    return _REFINED[key][1]
+
+
+def surface_point(mesh, theta, phi):
+    R = mesh.shape[2](theta)
+    return mesh.center + R * np.array([math.sin(theta) * math.cos(phi),
+                                       math.sin(theta) * math.sin(phi), math.cos(theta)])
+
+
+def nearest_surface_point(mesh, target):
+    """(theta, phi, point, signed distance) (body.py:371-423)."""
+    t = np.asarray(target, dtype=float)
+    rel = t - mesh.center
+    rho = math.hypot(rel[0], rel[1])
+    phi = math.atan2(rel[1], rel[0]) if rho > 1e-14 else 0.0
+    R = mesh.shape[2]
+
+    def dist2(th):
+        r = float(R(th))
+        a = r * math.sin(th) - rho
+        b = r * math.cos(th) - rel[2]
+        return a * a + b * b
+
+    scan = np.linspace(0.0, math.pi, 65)
+    vals = [dist2(x) for x in scan]
+    i0 = int(np.argmin(vals))
+    lo, hi = scan[max(i0 - 1, 0)], scan[min(i0 + 1, 64)]
+    for _ in range(40):
+        m1 = lo + 0.382 * (hi - lo)
+        m2 = lo + 0.618 * (hi - lo)
+        if dist2(m1) < dist2(m2):
+            hi = m2
+        else:
+            lo = m1
+    th0 = 0.5 * (lo + hi)
+    fd = 1e-6
+    for _ in range(3):
+        gr = (dist2(th0 + fd) - dist2(th0 - fd)) / (2 * fd)
+        gpp = (dist2(th0 + fd) - 2 * dist2(th0) + dist2(th0 - fd)) / fd ** 2
+        if gpp <= 0:
+            break
+        cand = min(max(th0 - gr / gpp, 0.0), math.pi)
+        if dist2(cand) <= dist2(th0):
+            th0 = cand
+    x0 = surface_point(mesh, th0, phi)
+    d = float(np.linalg.norm(t - x0))
+    r_t = np.linalg.norm(rel)
+    th_t = math.acos(min(max(rel[2] / r_t, -1.0), 1.0)) if r_t > 0 else 0.0
+    inside = r_t < float(R(th_t))
+    return th0, phi, x0, (-d if inside else d)
+
+
+def plain_surface_weights(mesh, target, mu):
+    """Stresslet quadrature at one target as a (3, 3N) map (body.py:437-448)."""
+    r = np.asarray(target, dtype=float)[None, :] - mesh.nodes
+    d2 = (r * r).sum(axis=1)
+    live = d2 > 1e-24
+    nr = (mesh.normals * r).sum(axis=1)
+    scal = np.zeros(mesh.n_nodes)
+    scal[live] = (-3.0 / (4.0 * np.pi * mu)) * mesh.weights[live] * nr[live] \
+        / (d2[live] ** 2 * np.sqrt(d2[live]))
+    W = scal[None, :, None] * r.T[:, :, None] * r[None, :, :]
+    return W.reshape(3, 3 * mesh.n_nodes)
+
+
+def _interp_row(mesh, theta, phi):
+    nt, nph = mesh.patch_grid
+    dth, dph = np.pi / nt, 2.0 * np.pi / nph
+    phi = phi % (2.0 * np.pi)
+    it = min(int(theta / dth), nt - 1)
+    ip = min(int(phi / dph), nph - 1)
+    cu = _lagrange((theta - it * dth) / dth, GL01_NODES)[0]
+    cv = _lagrange((phi - ip * dph) / dph, GL01_NODES)[0]
+    row = np.zeros(mesh.n_nodes)
+    row[(it * nph + ip) * 16 + np.arange(16)] = np.outer(cu, cv).ravel()
+    return row
+
+
+def _subtracted_rows_at(mesh, theta, phi, mu, jump):
+    x0 = surface_point(mesh, theta, phi)
+    rows = plain_surface_weights(mesh, x0, mu).reshape(3, mesh.n_nodes, 3)
+    RS = rows.sum(axis=1)
+    r0 = _interp_row(mesh, theta, phi)
+    rows -= RS[:, None, :] * r0[None, :, None]
+    if jump != 0.0:
+        rows += jump * np.eye(3)[:, None, :] * r0[None, :, None]
+    return rows
+
+
+def _interpolation_matrix(mesh, fine):
+    from scipy import sparse
+    theta = np.asarray(fine.thetas, dtype=float)
+    phi = np.asarray(fine.phis, dtype=float) % (2.0 * np.pi)
+    nt, nph = mesh.patch_grid
+    dth, dph = np.pi / nt, 2.0 * np.pi / nph
+    it = np.minimum((theta / dth).astype(int), nt - 1)
+    ip = np.minimum((phi / dph).astype(int), nph - 1)
+    cu = _lagrange((theta - it * dth) / dth, GL01_NODES)
+    cv = _lagrange((phi - ip * dph) / dph, GL01_NODES)
+    vals = np.einsum("mi,mj->mij", cu, cv).reshape(theta.size, 16)
+    cols = ((it * nph + ip) * 16)[:, None] + np.arange(16)
+    rows = np.repeat(np.arange(theta.size), 16)
+    return sparse.csr_matrix((vals.ravel(), (rows, cols.ravel())),
+                             shape=(theta.size, mesh.n_nodes))
+
+
+_INTERP = {}
+
+
+def near_surface_weights(mesh, target, mu, interior_jump=True, upsample=6):
+    """(3, 3N) near-surface map (body.py:479-519)."""
+    target = np.asarray(target, dtype=float)
+    th0, ph0, x0, signed_d = nearest_surface_point(mesh, target)
+    d = abs(signed_d)
+    interior = signed_d < 0
+    if d < 1e-8 * mesh.h:
+        jump = (1.0 / mu) if interior_jump else 0.0
+        return _subtracted_rows_at(mesh, th0, ph0, mu, jump).reshape(3, 3 * mesh.n_nodes)
+    fine = refined(mesh, upsample) if upsample > 1 else mesh
+    jump = (1.0 / mu) if (interior and interior_jump) else 0.0
+    Wf = _subtracted_rows_at(fine, th0, ph0, mu, jump)
+    normal_dir = (target - x0) / d
+    c = 1.5 * mesh.h
+    dists = np.array([0.0, c, 1.5 * c, 2.25 * c])
+    ell = _lagrange(d, dists)[0]
+    Wf = ell[0] * Wf
+    for k in range(1, 4):
+        pt = x0 + dists[k] * normal_dir
+        Wf += ell[k] * plain_surface_weights(fine, pt, mu).reshape(3, fine.n_nodes, 3)
+    if fine is mesh:
+        return Wf.reshape(3, 3 * mesh.n_nodes)
+    key = (id(mesh), id(fine))
+    if key not in _INTERP:
+        _INTERP[key] = (mesh, fine, _interpolation_matrix(mesh, fine))
+    B = _INTERP[key][2]
+    W = np.empty((3, mesh.n_nodes, 3))
+    for a in range(3):
+        for b in range(3):
+            W[a, :, b] = B.T @ Wf[a, :, b]
+    return W.reshape(3, 3 * mesh.n_nodes)
+
+
+def find_surface_pairs(surfaces, targets, target_groups, mu):
+    """Near-surface list [(t, si, Wnear - Wplain)] in the reference's order
+    (system.py:588-613); surfaces: [(mesh, group, is_periphery)]."""
+    out = []
+    for si, (mesh, group, is_periphery) in enumerate(surfaces):
+        others = target_groups != group
+        shell = 1.5 * mesh.h
+        rel = np.linalg.norm(targets - mesh.center, axis=1)
+        rho_nodes = np.linalg.norm(mesh.nodes - mesh.center, axis=1)
+        band = others & (rel >= rho_nodes.min() - shell) & (rel <= rho_nodes.max() + shell)
+        cand = np.nonzero(band)[0]
+        if cand.size == 0:
+            continue
+        from scipy.spatial import cKDTree
+        d, _ = cKDTree(mesh.nodes).query(targets[cand], k=1)
+        for t in cand[d * d < shell * shell]:
+            Wn = near_surface_weights(mesh, targets[t], mu, interior_jump=is_periphery)
+            Wp = plain_surface_weights(mesh, targets[t], mu)
+            out.append((int(t), si, Wn - Wp))
+    return out

@@ -1,16 +1,581 @@
-"""Implicit coupled stepping on the device (solver.py of the reference)."""
+"""Implicit coupled stepping on the B200 (solver.py of the reference).
+
+Same public API as /root/reference/pkg/src/slenderflow/solver.py --
+GmresParams, StepLayout, BlockOperator, assemble_step_operator,
+Preconditioner, gmres_solve, backward_euler_step, NonconvergenceError,
+FactorizationError -- with the state, the Krylov basis and every block row
+resident on the device.  One matvec is: fiber force densities and particle
+wrenches from the candidate (sf_fiber_forces, sf_particle_wrenches), the HI
+operator (sf_hi_apply), surface rows (subtracted double layer + rigid-body /
+null-space terms, sf_surface_rows) and fiber rows (sf_fiber_rows).  The
+Givens/Hessenberg bookkeeping of GMRES is a few dozen scalars per iteration
+and stays on the host.
+"""
+
+import ctypes
+import logging
+import math
 
 import numpy as np
 
+from . import _native, spectral
+from .system import ConfigurationError, InteractionCache, external_force_density
+
+LOG = logging.getLogger("paper_1602_05650_b200.solver")
+
+BC_CODES = {"free": 0, "prescribedForceTorque": 1, "hingedToSurface": 2, "clampedToBody": 3}
+
+
+class NonconvergenceError(RuntimeError):
+    """GMRES ran out of iterations; carries the best iterate found (solver.py:40-47)."""
+
+    def __init__(self, message, best=None, iterations=0, residuals=()):
+        super().__init__(message)
+        self.best = best
+        self.iterations = iterations
+        self.residuals = list(residuals)
+
+
+class FactorizationError(RuntimeError):
+    """A fiber self-block could not be inverted (solver.py:50-51)."""
+
+
+class GmresParams:
+    """Iteration controls (solver.py:54-64)."""
+
+    def __init__(self, tolerance=1e-5, restart=60, max_iterations=500):
+        if not 0.0 < tolerance < 1.0:
+            raise ConfigurationError("GMRES tolerance must lie in (0, 1)")
+        if restart < 1 or max_iterations < 1:
+            raise ConfigurationError("restart length and iteration cap must be positive")
+        self.tolerance = float(tolerance)
+        self.restart = int(restart)
+        self.max_iterations = int(max_iterations)
+
+
+class StepLayout:
+    """Index map of the stacked step unknowns (solver.py:67-110)."""
+
+    def __init__(self, state):
+        off = 0
+        self.U, self.omega, self.q1 = [], [], []
+        for part in state.particles:
+            self.U.append(slice(off, off + 3))
+            self.omega.append(slice(off + 3, off + 6))
+            n = part.mesh.n_nodes
+            self.q1.append(slice(off + 6, off + 6 + 3 * n))
+            off += 6 + 3 * n
+        self.q0 = None
+        if state.periphery is not None:
+            n0 = state.periphery.mesh.n_nodes
+            self.q0 = slice(off, off + 3 * n0)
+            off += 3 * n0
+        self.fib_off = off
+        self.X, self.T, self.fiber_block = [], [], []
+        for fib in state.fibers:
+            n = fib.n_nodes
+            self.X.append(slice(off, off + 3 * n))
+            self.T.append(slice(off + 3 * n, off + 4 * n))
+            self.fiber_block.append(slice(off, off + 4 * n))
+            off += 4 * n
+        self.size = off
+
+    def unpack(self, u):
+        return _Parts([u[s] for s in self.U], [u[s] for s in self.omega],
+                      [u[s].reshape(-1, 3) for s in self.q1],
+                      u[self.q0].reshape(-1, 3) if self.q0 is not None else None,
+                      [u[s].reshape(-1, 3) for s in self.X], [u[s] for s in self.T])
+
+
+class _Parts:
+    __slots__ = ("U", "omega", "q1", "q0", "X", "T")
+
+    def __init__(self, U, omega, q1, q0, X, T):
+        self.U, self.omega, self.q1, self.q0, self.X, self.T = U, omega, q1, q0, X, T
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
 
 def host_elastic_force_density(fib, Xcand, Tcand):
-    """f = -E Ds^4 X + Ds (T X_s) with frozen geometry (fiber.py:237-241).
-
-    Host helper for API defaults (complementary_velocities with no explicit
-    forces); the solver evaluates it on the device.
-    """
+    """f = -E Ds^4 X + Ds (T X_s) (fiber.py:237-241); host helper for API defaults."""
     Ds, Ds2, _ = fib.ds_powers()
     Ds4 = Ds2 @ Ds2
-    Xcand = np.asarray(Xcand, dtype=float)
-    Tcand = np.asarray(Tcand, dtype=float)
-    return -fib.E * (Ds4 @ Xcand) + Ds @ (Tcand[:, None] * fib.tangents)
+    return (-fib.E * (Ds4 @ np.asarray(Xcand, dtype=float))
+            + Ds @ (np.asarray(Tcand, dtype=float)[:, None] * fib.tangents))
+
+
+class BlockOperator:
+    """Linear action of the implicit step system on the stacked unknowns,
+    evaluated on the device (solver.py:187-364).  apply/rhs accept and return
+    numpy arrays or CUDA tensors."""
+
+    def __init__(self, state, dt, mu=None, backend=None, cache=None, implicit_coupling=True):
+        import torch
+        if dt <= 0:
+            raise ConfigurationError("time step must be positive")
+        if not implicit_coupling:
+            raise ConfigurationError("the device operator implements implicit coupling only")
+        if backend is not None and getattr(backend, "kind", "direct") != "direct":
+            raise ConfigurationError(f"backend {backend.kind!r} is not available on the device")
+        self.state = state
+        self.dt = float(dt)
+        self.mu = state.mu if mu is None else float(mu)
+        if self.mu <= 0:
+            raise ConfigurationError("viscosity must be positive")
+        self.layout = StepLayout(state)
+        self.cache = cache if cache is not None else InteractionCache(state)
+        self.implicit_coupling = True
+        self.device = self.cache.device
+        dev = self.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        c = self.cache
+        nf, n = c.nf, c.n_nodes
+        self.nf, self.n = nf, n
+        g = c.geo
+        # frozen fiber operators (refresh_geometry, fiber.py:133-147)
+        self.Dpow = torch.empty((nf, 4, n, n), **f64)
+        self.nodes = torch.tensor(spectral.grid(n - 1)[0], **f64) if nf else None
+        if nf:
+            _native.call("sf_fiber_dpow", _ptr(g.D), _ptr(g.s_alpha), nf, n, _ptr(self.Dpow),
+                         _stream())
+        self.K = torch.empty((nf, 3 * n, 3 * n), **f64)
+        if nf:
+            _native.call("sf_kdelta_build_batched", _ptr(g.X), _ptr(g.s), _ptr(g.s_alpha),
+                         _ptr(g.tang), _ptr(g.wcc), nf, n, _ptr(g.delta),
+                         1.0 / (8.0 * math.pi * self.mu), _ptr(self.K), _stream())
+        eps = np.array([f.eps for f in state.fibers])
+        self.E = torch.as_tensor(np.array([f.E for f in state.fibers], dtype=float), **f64)
+        self.c_log = torch.as_tensor(-np.log(eps ** 2 * math.e) / (8.0 * math.pi * self.mu), **f64)
+        self.c_two = 2.0 / (8.0 * math.pi * self.mu)
+        self.Ldot = torch.as_tensor(np.array([f.Ldot for f in state.fibers], dtype=float), **f64)
+        self.f_ext = self._external_forces()
+        kinds = np.zeros((nf, 2), dtype=np.int32)
+        par = np.zeros((nf, 2, 12))
+        body = np.full(nf, -1, dtype=np.int32)
+        for m, fib in enumerate(state.fibers):
+            for e, bc in enumerate((fib.bc_plus, fib.bc_minus)):
+                kinds[m, e] = BC_CODES[bc.kind]
+                if bc.kind == "prescribedForceTorque":
+                    par[m, e, 0:3] = bc.force
+                    par[m, e, 3:6] = bc.torque
+                elif bc.kind == "hingedToSurface":
+                    par[m, e, 6:9] = bc.attachment
+                    par[m, e, 9] = bc.stiffness
+                elif bc.kind == "clampedToBody":
+                    par[m, e, 10] = 0.0 if bc.tangent is None else 1.0
+                    if e == 1:
+                        body[m] = bc.body
+        self.bc_kind = torch.as_tensor(kinds, device=dev)
+        self.bc_par = torch.as_tensor(par, **f64)
+        self.bc_body = torch.as_tensor(body, device=dev)
+        np_ = len(state.particles)
+        self.np = np_
+        self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
+                        if np_ else None)
+        self.p_uoff = torch.as_tensor(np.array([s.start for s in self.layout.U], dtype=np.int64),
+                                      device=dev) if np_ else None
+        self.ext = (torch.as_tensor(np.stack([np.concatenate([p.F_ext, p.L_ext])
+                                              for p in state.particles]), **f64) if np_ else None)
+        self.sys = _native.FiberSys(
+            nf=nf, n=n, D=_ptr(g.D), nodes=_ptr(self.nodes), Dpow=_ptr(self.Dpow), X=_ptr(g.X),
+            tang=_ptr(g.tang), s_alpha=_ptr(g.s_alpha), L=_ptr(g.L), Ldot=_ptr(self.Ldot),
+            E=_ptr(self.E), c_log=_ptr(self.c_log), c_two=self.c_two, K=_ptr(self.K),
+            f_ext=_ptr(self.f_ext), bc_kind=_ptr(self.bc_kind), bc_par=_ptr(self.bc_par),
+            bc_body=_ptr(self.bc_body), np=np_, pcenter=_ptr(self.pcenter),
+            p_uoff=_ptr(self.p_uoff), fib_off=self.layout.fib_off, dt=self.dt, mu=self.mu)
+        # surface data per particle / periphery
+        self.surf = []
+        for i, part in enumerate(state.particles):
+            m = part.mesh
+            self.surf.append(dict(kind=0, pi=i, nodes=torch.as_tensor(m.nodes, **f64),
+                                  nrm=torch.as_tensor(m.normals, **f64),
+                                  w=torch.as_tensor(m.weights, **f64), n=m.n_nodes, area=m.area,
+                                  center=self.pcenter[i], sl=self.layout.q1[i],
+                                  uom=self.layout.U[i].start, tsl=c.particle_slices[i]))
+        if state.periphery is not None:
+            m = state.periphery.mesh
+            self.surf.append(dict(kind=1, nodes=torch.as_tensor(m.nodes, **f64),
+                                  nrm=torch.as_tensor(m.normals, **f64),
+                                  w=torch.as_tensor(m.weights, **f64), n=m.n_nodes, area=m.area,
+                                  center=None, sl=self.layout.q0, uom=None,
+                                  tsl=c.periphery_slice))
+        # scratch
+        self._f = torch.empty((nf * n, 3), **f64)
+        self._wf = torch.empty((max(nf, 1), 6), **f64)
+        self._wr = torch.empty((max(np_, 1), 6), **f64)
+        self._ubar = torch.empty((c.n_targets, 3), **f64)
+        self._work = torch.empty(16, **f64)
+        self.fiber_blocks = torch.empty((nf, 4 * n, 4 * n), **f64)
+        if nf:
+            _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.fiber_blocks),
+                         _stream())
+        self.matvecs = 0
+
+    def _external_forces(self):
+        import torch
+        st = self.state
+        if not st.force_models or not self.nf:
+            return None
+        f = np.stack([external_force_density(st, fib) for fib in st.fibers]) \
+            if any(m.kind != "uniformBodyForce" for m in st.force_models) else \
+            np.broadcast_to(sum(m.f0 * m.direction for m in st.force_models
+                                if m.kind == "uniformBodyForce"), (self.nf, self.n, 3))
+        return torch.as_tensor(np.ascontiguousarray(f), dtype=torch.float64, device=self.device)
+
+    @property
+    def shape(self):
+        return (self.layout.size, self.layout.size)
+
+    # ------------------------------------------------------------- rows
+    def _densities(self, u):
+        """Surface densities in the cache's surface order (particles, periphery)."""
+        import torch
+        if not self.surf:
+            return None
+        return torch.cat([u[s["sl"]] for s in self.surf]).reshape(-1, 3)
+
+    def rows_device(self, u, constants, out=None):
+        import torch
+        c = self.cache
+        st = _stream()
+        if out is None:
+            out = torch.empty_like(u)
+        sysp = ctypes.byref(self.sys)
+        if self.nf:
+            _native.call("sf_fiber_forces", sysp, _ptr(u), int(constants), _ptr(self._f), st)
+        if self.np:
+            _native.call("sf_particle_wrenches", sysp, _ptr(u), _ptr(self.ext), int(constants),
+                         _ptr(self._wf), _ptr(self._wr), st)
+        q = self._densities(u)
+        ubar = c.apply(self._f, q, self._wr[:self.np] if self.np else None, out=self._ubar,
+                       check=True)
+        pref_dl = -3.0 / (4.0 * math.pi * self.mu)
+        for s in self.surf:
+            qs = u[s["sl"]]
+            rows = out[s["sl"]]
+            _native.call("sf_stresslet_sum_subtracted", _ptr(s["nodes"]), _ptr(s["nrm"]),
+                         _ptr(s["w"]), _ptr(qs), s["n"], pref_dl, _ptr(rows), st)
+            ub = ubar[s["tsl"]]
+            if s["kind"] == 0:
+                _native.call("sf_wrench_flow", _ptr(s["nodes"]), s["n"], _ptr(s["center"]),
+                             _ptr(self._wr[s["pi"]]), self.mu, _ptr(rows), st)
+                uom = u[s["uom"]:s["uom"] + 6]
+                _native.call("sf_surface_rows", 0, _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                             s["n"], _ptr(s["center"]), s["area"], _ptr(qs), _ptr(ub), _ptr(uom),
+                             self.mu, _ptr(self._work), _ptr(rows),
+                             _ptr(out[s["uom"]:s["uom"] + 6]), st)
+            else:
+                _native.call("sf_surface_rows", 1, _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                             s["n"], None, s["area"], _ptr(qs), _ptr(ub), None, self.mu,
+                             _ptr(self._work), _ptr(rows), None, st)
+        if self.nf:
+            _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(ubar[c.fiber_slice]),
+                         int(constants), _ptr(out), st)
+        self.matvecs += 1
+        return out
+
+    def _to_dev(self, u):
+        import torch
+        return torch.as_tensor(u, dtype=torch.float64, device=self.device).contiguous()
+
+    def apply(self, u):
+        """A @ u, strictly linear (solver.py:217-222)."""
+        is_np = isinstance(u, np.ndarray)
+        if u.shape != (self.layout.size,):
+            raise ValueError(f"expected a vector of length {self.layout.size}")
+        out = self.rows_device(self._to_dev(u), False)
+        return out.cpu().numpy() if is_np else out
+
+    def rhs_device(self):
+        import torch
+        zero = torch.zeros(self.layout.size, dtype=torch.float64, device=self.device)
+        return -self.rows_device(zero, True)
+
+    def rhs(self):
+        """Right-hand side of every candidate-independent term (solver.py:224-227)."""
+        return self.rhs_device().cpu().numpy()
+
+    def materialize(self):
+        n = self.layout.size
+        A = np.empty((n, n))
+        e = np.zeros(n)
+        for j in range(n):
+            e[j] = 1.0
+            A[:, j] = self.apply(e)
+            e[j] = 0.0
+        return A
+
+
+def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implicit_coupling=True):
+    op = BlockOperator(state, dt, mu=mu, backend=backend, cache=cache,
+                       implicit_coupling=implicit_coupling)
+    return op, op.rhs_device()
+
+
+class Preconditioner:
+    """Block Jacobi: equilibrated exact fiber-block inverses, diagonal on
+    surface rows (solver.py:375-429), factored and applied on the device."""
+
+    def __init__(self, op):
+        import torch
+        self.layout = op.layout
+        self.device = op.device
+        f64 = dict(dtype=torch.float64, device=op.device)
+        nf, n = op.nf, op.n
+        m = 4 * n
+        self.nb, self.m = nf, m
+        self.off0 = op.layout.fib_off
+        st = _stream()
+        if nf:
+            A = op.fiber_blocks.clone()
+            if not bool(torch.isfinite(A).all()):
+                raise FactorizationError("fiber self-block is not finite")
+            self.r = torch.empty((nf, m), **f64)
+            self.c = torch.empty((nf, m), **f64)
+            self.piv = torch.empty((nf, m), dtype=torch.int32, device=op.device)
+            info = torch.empty(nf, dtype=torch.int32, device=op.device)
+            if m * m * 8 <= 227 * 1024:
+                _native.call("sf_block_lu", _ptr(A), nf, m, _ptr(self.r), _ptr(self.c),
+                             _ptr(self.piv), _ptr(info), st)
+                self.LU = A
+            else:
+                # blocks too large for one CTA's shared memory: equilibrate on the
+                # device and factor with the batched library getrf
+                self.r = A.abs().amax(dim=2)
+                if bool((self.r == 0).any()):
+                    raise FactorizationError("fiber self-block is singular")
+                A = A / self.r[:, :, None]
+                self.c = A.abs().amax(dim=1)
+                A = A / self.c[:, None, :]
+                LU, piv, inf = torch.linalg.lu_factor_ex(A)
+                info = torch.where(inf != 0, 3, 0).to(torch.int32)
+                self.LU = LU.transpose(1, 2).contiguous()
+                self.piv = (piv - 1).to(torch.int32).contiguous()
+            bad = info.cpu().numpy()
+            if np.any(bad == 1):
+                raise FactorizationError(f"fiber {int(np.argmax(bad == 1))} self-block is not finite")
+            if np.any(bad == 2) or np.any(bad == 3):
+                raise FactorizationError(f"fiber {int(np.argmax(bad > 1))} self-block is singular")
+        else:
+            self.LU = self.r = self.c = self.piv = None
+        diag = torch.ones(self.off0, **f64)
+        pref = -3.0 / (4.0 * math.pi * op.mu)
+        for s in op.surf:
+            rs = torch.empty((s["n"], 3, 3), **f64)
+            _native.call("sf_stresslet_rowsum", _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                         s["n"], pref, _ptr(rs), st)
+            d = -torch.diagonal(rs, dim1=1, dim2=2)
+            if s["kind"] == 1:
+                d = d + 1.0 / op.mu
+                d = d + (s["nrm"] ** 2) * s["w"][:, None] / (op.mu * s["area"])
+            diag[s["sl"]] = d.reshape(-1)
+        if bool((diag == 0).any()):
+            raise FactorizationError("zero diagonal entry in a surface block")
+        self.diag = diag
+
+    def apply_device(self, v, out=None):
+        import torch
+        if out is None:
+            out = torch.empty_like(v)
+        _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c),
+                     _ptr(self.piv), self.nb, self.m, self.off0, _ptr(self.diag), self.off0,
+                     _ptr(v), _ptr(out), _stream())
+        return out
+
+    def apply(self, v):
+        import torch
+        if isinstance(v, np.ndarray):
+            return self.apply_device(torch.as_tensor(v, device=self.device)).cpu().numpy()
+        return self.apply_device(v.contiguous())
+
+
+class _DeviceVectors:
+    """Deterministic dot / axpy helpers on device vectors (sf_dot etc.)."""
+
+    def __init__(self, device):
+        import torch
+        self.work = torch.empty(296, dtype=torch.float64, device=device)
+
+    def dot_into(self, x, y, out, sqrt_mode=False):
+        _native.call("sf_dot", _ptr(x), _ptr(y), x.numel(), _ptr(self.work), _ptr(out),
+                     int(sqrt_mode), _stream())
+
+
+def _as_apply(obj, device):
+    import torch
+    if obj is None:
+        return lambda v: v
+    if hasattr(obj, "apply_device"):
+        return obj.apply_device
+    if hasattr(obj, "rows_device"):
+        return lambda v: obj.rows_device(v, False)
+    if hasattr(obj, "apply"):
+        fn = obj.apply
+    elif isinstance(obj, np.ndarray):
+        M = torch.as_tensor(obj, dtype=torch.float64, device=device)
+        return lambda v: M @ v
+    elif callable(obj):
+        fn = obj
+    else:
+        raise TypeError("operator must expose .apply, be a matrix, or be callable")
+
+    def wrapped(v):
+        r = fn(v)
+        return torch.as_tensor(r, dtype=torch.float64, device=device)
+    return wrapped
+
+
+def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
+    """Left-preconditioned restarted GMRES (solver.py:444-516) with the Krylov
+    basis on the device.  Returns (solution, iterations, residual history);
+    the solution has the type of `rhs` (numpy or CUDA tensor)."""
+    import torch
+    if params is None:
+        params = GmresParams()
+    host_io = isinstance(rhs, np.ndarray)
+    device = getattr(operator, "device", None) or torch.device("cuda")
+    rhs_d = torch.as_tensor(rhs, dtype=torch.float64, device=device).contiguous()
+    apply_a = _as_apply(operator, device)
+    apply_m = _as_apply(preconditioner, device)
+    vec = _DeviceVectors(device)
+    st = _stream()
+    n = rhs_d.numel()
+
+    def ret(x):
+        return x.cpu().numpy() if host_io else x
+
+    scal = torch.empty(2, dtype=torch.float64, device=device)
+    b = apply_m(rhs_d)
+    vec.dot_into(b, b, scal[0:1], sqrt_mode=True)
+    beta0 = float(scal[0].item())
+    if beta0 == 0.0:
+        return ret(torch.zeros(n, dtype=torch.float64, device=device)), 0, [0.0]
+    warm = x0 is not None
+    x = (torch.as_tensor(x0, dtype=torch.float64, device=device).clone() if warm
+         else torch.zeros(n, dtype=torch.float64, device=device))
+    R = params.restart
+    V = torch.empty((R + 1, n), dtype=torch.float64, device=device)
+    hcol = torch.empty(R + 2, dtype=torch.float64, device=device)
+    history = []
+    iters = 0
+    while True:
+        r = b - apply_m(apply_a(x)) if (iters or warm) else b
+        vec.dot_into(r, r, scal[0:1], sqrt_mode=True)
+        beta = float(scal[0].item())
+        if beta / beta0 <= params.tolerance:
+            return ret(x), iters, history or [beta / beta0]
+        V[0].copy_(r / beta)
+        H = np.zeros((R + 1, R))
+        cs = np.zeros(R)
+        sn = np.zeros(R)
+        g = np.zeros(R + 1)
+        g[0] = beta
+        k = 0
+        while k < R and iters < params.max_iterations:
+            w = apply_m(apply_a(V[k])).contiguous()
+            vec.dot_into(w, w, hcol[R + 1:R + 2], sqrt_mode=True)   # wnorm
+            for j in range(k + 1):                                   # modified Gram-Schmidt
+                vec.dot_into(V[j], w, hcol[j:j + 1])
+                _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
+            vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
+            hh = hcol.cpu().numpy()
+            wnorm = float(hh[R + 1])
+            H[:k + 2, k] = hh[:k + 2]
+            for j in range(k):
+                tmp = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
+                H[j + 1, k] = -sn[j] * H[j, k] + cs[j] * H[j + 1, k]
+                H[j, k] = tmp
+            denom = math.hypot(H[k, k], H[k + 1, k])
+            cs[k] = H[k, k] / denom if denom else 1.0
+            sn[k] = H[k + 1, k] / denom if denom else 0.0
+            H[k, k] = denom
+            g[k + 1] = -sn[k] * g[k]
+            g[k] = cs[k] * g[k]
+            iters += 1
+            rel = abs(g[k + 1]) / beta0
+            history.append(rel)
+            breakdown = H[k + 1, k] <= 1e-12 * max(wnorm, 1e-300)
+            if not breakdown:
+                _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]),
+                             n, st)
+            k += 1
+            if rel <= params.tolerance or breakdown:
+                break
+        if k:
+            y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
+            coef = torch.as_tensor(y, dtype=torch.float64, device=device)
+            _native.call("sf_combine", _ptr(V), n, k, _ptr(coef), _ptr(x), n, st)
+        rel = history[-1] if history else 0.0
+        if rel <= params.tolerance:
+            return ret(x), iters, history
+        if iters >= params.max_iterations:
+            raise NonconvergenceError(
+                f"GMRES did not reach {params.tolerance:g} within "
+                f"{params.max_iterations} iterations (residual {rel:.3e})",
+                best=ret(x), iterations=iters, residuals=history)
+
+
+def _rotation_is_representable(part, omega, dt):
+    if float(np.linalg.norm(omega)) * dt < 1e-14:
+        return True
+    shape = part.mesh.shape
+    return shape is not None and shape[0] == "sphere"
+
+
+def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=None,
+                        implicit_coupling=True, return_info=False):
+    """Advance the state by one implicit step on the device, halving dt on
+    nonconvergence (solver.py:528-592)."""
+    from .fiber import STALLED
+    if dt <= 0:
+        raise ConfigurationError("time step must be positive")
+    if any(f.growth_state != STALLED for f in state.fibers):
+        raise NotImplementedError("polymerization kinetics run on the host in the reference "
+                                  "(fiber.py:307-356) and are outside this device path")
+    if state.model("corticalPushing") is not None:
+        raise NotImplementedError("cortical contact models are outside this device path")
+    if dt_min is None:
+        dt_min = dt / 64.0
+    attempt = float(dt)
+    cache = InteractionCache(state)
+    while True:
+        op, rhs = assemble_step_operator(state, attempt, mu=mu, backend=backend, cache=cache,
+                                         implicit_coupling=implicit_coupling)
+        prec = Preconditioner(op)
+        try:
+            sol, iters, history = gmres_solve(op, prec, rhs, params)
+            break
+        except NonconvergenceError as err:
+            LOG.warning("step_rejected time=%.9g dt=%.3e residual=%.3e",
+                        state.time, attempt, err.residuals[-1])
+            if attempt / 2.0 < dt_min:
+                raise
+            attempt /= 2.0
+    sol = sol.cpu().numpy()
+    parts = op.layout.unpack(sol)
+    from .system import ConfigurationError as _CE
+    for i, part in enumerate(state.particles):
+        if not _rotation_is_representable(part, parts.omega[i], attempt):
+            raise _CE("rotation of a non-spherical particle is not supported")
+        part.U = parts.U[i].copy()
+        part.omega = parts.omega[i].copy()
+        part.q = parts.q1[i].copy()
+        part.translate(attempt * part.U)
+    if state.periphery is not None:
+        state.periphery.q = parts.q0.copy()
+    for m, fib in enumerate(state.fibers):
+        fib.X = parts.X[m].copy()
+        fib.T = parts.T[m].copy()
+    state.time += attempt
+    LOG.info("step time=%.9g dt=%.3e gmres_iterations=%d residual=%.3e",
+             state.time, attempt, iters, history[-1] if history else 0.0)
+    if return_info:
+        return state, dict(dt=attempt, iterations=iters, history=history, matvecs=op.matvecs)
+    return state

@@ -305,8 +305,10 @@ class InteractionCache:
                     state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
             except InsideFiberError as err:
                 raise OverlapError(f"target node overlaps a fiber: {err}") from err
+        self.near_surface = []
         if near and self.surfaces:
-            self._check_no_near_surface()
+            self.near_surface = nearfield.find_surface_pairs(
+                self.surfaces, self.targets, self.target_groups, state.mu)
         self._build_near_map()
         self.mode = int(mode)
         self._layout()
@@ -323,39 +325,37 @@ class InteractionCache:
                 if not is_periphery and np.any(others & inside):
                     raise OverlapError("a target lies inside a rigid particle")
 
-    def _check_no_near_surface(self):
-        from scipy.spatial import cKDTree
-        for mesh, group, _ in self.surfaces:
-            shell = 1.5 * mesh.h
-            tree = cKDTree(mesh.nodes)
-            d, _ = tree.query(self.targets[self.target_groups != group], k=1)
-            if np.any(d < shell):
-                raise NotImplementedError(
-                    "near-surface correction maps are not built on this path yet "
-                    "(SURVEY.md §8f rank 1); keep targets outside 1.5 h of other surfaces")
-
     def _build_near_map(self):
+        """CSR by target of every correction map, fiber entries before surface
+        entries for a target (the reference applies the fiber list first,
+        system.py:702-707).  x = [fiber forces | surface densities], flattened."""
         import torch
-        entries = self.near_fiber
         self.near_nrows = 0
         self.near_tensors = {}
-        if not entries:
-            return
-        t = np.array([e[0] for e in entries], dtype=np.int64)
-        l = np.array([e[1] for e in entries], dtype=np.int64)
-        W = np.stack([e[2] for e in entries])
-        order = np.argsort(t, kind="stable")
-        t, l, W = t[order], l[order], W[order]
-        rows, starts = np.unique(t, return_index=True)
         L = 3 * self.n_nodes
+        nfs3 = 3 * self.nf * self.n_nodes
+        ents = [(t, l * L, L, W) for t, l, W in self.near_fiber]
+        for t, si, W in self.near_surface:
+            mesh = self.surfaces[si][0]
+            ents.append((t, nfs3 + 3 * self.surface_offsets[si], 3 * mesh.n_nodes, W))
+        if not ents:
+            return
+        t = np.array([e[0] for e in ents], dtype=np.int64)
+        order = np.argsort(t, kind="stable")
+        t = t[order]
+        xo = np.array([ents[i][1] for i in order], dtype=np.int64)
+        xl = np.array([ents[i][2] for i in order], dtype=np.int64)
+        Ws = [np.ascontiguousarray(ents[i][3], dtype=float).reshape(-1) for i in order]
+        wo = np.concatenate([[0], np.cumsum([w.size for w in Ws])[:-1]]).astype(np.int64)
+        rows, starts = np.unique(t, return_index=True)
         dev = dict(device=self.device)
         self.near_tensors = dict(
             row_ptr=torch.as_tensor(np.append(starts, t.size).astype(np.int64), **dev),
             rows=torch.as_tensor(rows, **dev),
-            w_off=torch.as_tensor(np.arange(t.size, dtype=np.int64) * 3 * L, **dev),
-            x_off=torch.as_tensor(l * L, **dev),           # into [fiber forces | densities]
-            x_len=torch.full((t.size,), L, dtype=torch.int64, **dev),
-            W=torch.as_tensor(np.ascontiguousarray(W), dtype=torch.float64, **dev))
+            w_off=torch.as_tensor(wo, **dev),
+            x_off=torch.as_tensor(xo, **dev),
+            x_len=torch.as_tensor(xl, **dev),
+            W=torch.as_tensor(np.concatenate(Ws), dtype=torch.float64, **dev))
         self.near_nrows = rows.size
 
     def _layout(self):

@@ -144,8 +144,104 @@ def surfaces_fixture():
     print(f"  surfaces: near fiber {len(cache.near_fiber)}, near surface {len(cache.near_surface)}")
 
 
+# ---------------------------------------------------------------- implicit steps
+def _step_record(state):
+    return dict(X=np.stack([f.X for f in state.fibers]), T=np.stack([f.T for f in state.fibers]),
+                U=np.stack([p.U for p in state.particles]) if state.particles else np.zeros((0, 3)),
+                omega=(np.stack([p.omega for p in state.particles]) if state.particles
+                       else np.zeros((0, 3))),
+                q1=(np.stack([p.q for p in state.particles]) if state.particles
+                    else np.zeros((0, 1, 3))),
+                q0=state.periphery.q if state.periphery is not None else np.zeros((0, 3)))
+
+
+def aster_state(n_fibers=12, p=15, mesh_res=(4, 4), E=1.0, periphery=False, hinged=False):
+    from slenderflow import system as S
+    pnc = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), mesh_res))
+    pts, dirs = S.aster_attachment_layout(pnc, n_fibers, radius_factor=1.3)
+    fibs = []
+    for k, (x0, d) in enumerate(zip(pts, dirs)):
+        fb = fiber.straight_fiber(p, x0, d, 1.0, eps=1e-2, E=E)
+        fb.bc_minus = fiber.ClampedToBody(0, x0, d)
+        fb.bc_plus = fiber.PrescribedForceTorque(1.0 * d)
+        if hinged and k == 0:
+            fb.bc_plus = fiber.HingedToSurface(attachment=fb.X[0] + 0.05 * d, stiffness=10.0)
+        fibs.append(fb)
+    per = body.Periphery(body.make_surface(body.sphere_shape(3.0), (6, 6))) if periphery else None
+    return S.SystemState(fibs, [pnc], per)
+
+
+def cloud_state(n_fibers=8, p=15, seed=3):
+    from slenderflow import system as S
+    cl = configs.fiber_cloud(n_fibers, p, eps=5e-3, E=1e-2, region="ball", size=1.5, seed=seed,
+                             clear=configs.clean_clear(p), check="node", perturb=1e-2)
+    fibs = [fiber.Fiber(X, eps=5e-3, E=1e-2) for X in cl.X]
+    return S.SystemState(fibs, force_models=[S.UniformBodyForce(1.0, (0.0, 0.0, -1.0))]), cl.X
+
+
+def step_fixture(name, state, dt, tol, nsteps, extra=None):
+    from slenderflow import solver as R
+    rng = np.random.default_rng(5)
+    op, rhs = R.assemble_step_operator(state, dt)
+    prec = R.Preconditioner(op)
+    u = rng.standard_normal(op.layout.size)
+    v = rng.standard_normal(op.layout.size)
+    rec = dict(apply_u=u, apply_Au=op.apply(u), rhs=rhs, prec_v=v, prec_Mv=prec.apply(v),
+               block0=op.fiber_blocks[0], layout_size=op.layout.size)
+    init = _step_record(state)
+    steps = []
+    for _ in range(nsteps):
+        params = R.GmresParams(tolerance=tol)
+        # iterations of the reference's own solve for the record
+        op2, rhs2 = R.assemble_step_operator(state, dt)
+        _, iters, hist = R.gmres_solve(op2, R.Preconditioner(op2), rhs2, params)
+        R.backward_euler_step(state, dt, params)
+        steps.append((iters, _step_record(state)))
+    out = dict(dt=dt, tol=tol, nsteps=nsteps, **{f"init_{k}": v for k, v in init.items()}, **rec)
+    for s_i, (iters, r) in enumerate(steps):
+        out[f"iters_{s_i}"] = iters
+        for k, v in r.items():
+            out[f"step{s_i}_{k}"] = v
+    if extra:
+        out.update(extra)
+    save(name, **out, **versions())
+
+
+def steps_all():
+    st = aster_state()
+    step_fixture("step_aster.npz", st, 1e-3, 1e-10, 2)
+    st, X0 = cloud_state()
+    step_fixture("step_cloud.npz", st, 5e-3, 1e-10, 2, extra=dict(cloud_X=X0))
+    st = aster_state(n_fibers=6, periphery=True, hinged=True)
+    step_fixture("step_confined.npz", st, 1e-3, 1e-10, 1)
+
+
+def near_surface_fixture():
+    """Near-surface correction maps (body.py:479-519) for a few targets."""
+    part = body.make_surface(body.sphere_shape(0.5), (4, 4))
+    per = body.make_surface(body.sphere_shape(3.0), (6, 6))
+    tp = np.array([[0.0, 0.0, 0.62], [0.3, 0.35, 0.2], [0.5, 0.05, 0.0]])
+    tq = np.array([[0.0, 0.0, 2.7], [1.9, 1.9, 0.9], [0.1, -2.85, 0.3]])
+    Wp = np.stack([body.near_surface_weights(part, t, 1.0, interior_jump=False)
+                   - body.plain_surface_weights(part, t, 1.0) for t in tp])
+    Wq = np.stack([body.near_surface_weights(per, t, 1.0, interior_jump=True)
+                   - body.plain_surface_weights(per, t, 1.0) for t in tq])
+    nsp = [body.nearest_surface_point(per, t) for t in tq]
+    save("near_surface.npz", tp=tp, tq=tq, Wp=Wp, Wq=Wq,
+         nsp=np.array([[a, b, *x, d] for a, b, x, d in nsp]), **versions())
+
+
 if __name__ == "__main__":
-    pairs_small()
-    operator_fixture("c1_near.npz", configs.make("c1", seed=0))
-    operator_fixture("c1_clean.npz", configs.make("c1_clean", seed=0))
-    surfaces_fixture()
+    which = sys.argv[1:] or ["pairs", "operator", "surfaces", "steps"]
+    if "pairs" in which:
+        pairs_small()
+    if "operator" in which:
+        operator_fixture("c1_near.npz", configs.make("c1", seed=0))
+        operator_fixture("c1_clean.npz", configs.make("c1_clean", seed=0))
+    if "surfaces" in which:
+        surfaces_fixture()
+        near_surface_fixture()
+
+
+    if "steps" in which:
+        steps_all()

@@ -44,3 +44,19 @@ def test_near_fiber_maps_match_reference():
     assert [(t, l) for t, l, _ in near] == list(zip(g["near_t"].tolist(), g["near_l"].tolist()))
     for (_, _, W), Wref in zip(near, g["near_W"]):
         assert np.abs(W - Wref).max() <= 1e-12 * np.abs(Wref).max()
+
+
+def test_near_surface_maps_match_reference():
+    g = golden("near_surface.npz")
+    part = body.make_surface(body.sphere_shape(0.5), (4, 4))
+    per = body.make_surface(body.sphere_shape(3.0), (6, 6))
+    for t, Wref in zip(g["tp"], g["Wp"]):
+        W = nearfield.near_surface_weights(part, t, 1.0, interior_jump=False) \
+            - nearfield.plain_surface_weights(part, t, 1.0)
+        assert np.abs(W - Wref).max() <= 1e-12 * np.abs(Wref).max()
+    for t, Wref, ns in zip(g["tq"], g["Wq"], g["nsp"]):
+        th, ph, x0, d = nearfield.nearest_surface_point(per, t)
+        assert abs(th - ns[0]) < 1e-12 and abs(d - ns[5]) < 1e-12
+        W = nearfield.near_surface_weights(per, t, 1.0, interior_jump=True) \
+            - nearfield.plain_surface_weights(per, t, 1.0)
+        assert np.abs(W - Wref).max() <= 1e-12 * np.abs(Wref).max()
