@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--mode", default="fp64", choices=["fp64", "fp32c"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step-config", default="c2", help="implicit-step workload ('' to skip)")
+    ap.add_argument("--step-count", type=int, default=3)
     return ap.parse_args()
 
 
@@ -152,6 +154,39 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------- implicit steps ----
+def measure_steps(config, count):
+    """Implicit steps/s of the full device step (cache, self blocks, block LU,
+    GMRES to tol 1e-10, state update) on BASELINE config 2 (1024-fiber aster)
+    or a sedimenting cloud; one warm-up step, then `count` timed steps."""
+    import torch
+
+    from paper_1602_05650_b200 import configs, solver
+    if config == "c2":
+        st = configs.aster(n_fibers=1024)
+        dt, tol = 1e-3, 1e-10
+        desc = "c2: 1024 fibers x 32 nodes clamped to a sphere (8x8 patches), plus-end force 1"
+    else:
+        st = configs.cloud_state(config)
+        dt, tol = 5e-3, 1e-10
+        desc = f"{config}: sedimenting cloud, {len(st.fibers)} fibers"
+    params = solver.GmresParams(tolerance=tol)
+    st, info = solver.backward_euler_step(st, dt, params, return_info=True)
+    times, iters = [], []
+    for _ in range(count):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st, info = solver.backward_euler_step(st, dt, params, return_info=True)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        iters.append(info["iterations"])
+    return {"config": desc, "dt": dt, "gmres_tol": tol, "steps": count,
+            "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
+            "gmres_iterations": iters,
+            "timing": "wall clock around each full step (host orchestration included), "
+                      "after one warm-up step"}
+
+
 # ---------------------------------------------------------------- ours (GPU) ----
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -241,6 +276,10 @@ def run_ours(args, rank, world, local_rank):
     peak_flops, _ = kernels.dfma_peak(1 << 15)
     achieved = op.pairs_per_apply * FLOPS_PER_PAIR / (pair_ms * 1e-3)
 
+    steps = None
+    if args.step_config and world == 1:
+        steps = measure_steps(args.step_config, args.step_count)
+
     lines = None
     if rank == 0:
         cpu = None
@@ -278,6 +317,7 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": int(2 * cloud.n_points * 3 * 8)},
             "gpu_launches": args.steps * op.launches_per_apply,
             "clocks": clocks,
+            "implicit_steps": steps,
         }
         print(json.dumps(lines), flush=True)
     barrier()

@@ -8,7 +8,11 @@ laws follow BASELINE.json and SURVEY.md §8(d):
 * directions: normalised standard normals; ball centres R u^(1/3) dir, cube
   centres uniform (the cloud_init law, system.py:458-467);
 * optional centreline perturbation X(alpha) += sum_k c_k T_k(alpha),
-  c_k ~ N(0, sigma^2) per component (reading "~N(0,1e-2)" as sigma = 1e-2);
+  c_k ~ N(0, sigma^2) per component with sigma = 1e-2 (our reading of
+  "~N(0,1e-2)") on the lowest PERTURB_MODES = 4 Chebyshev modes.  Drawing all
+  p+1 coefficients with that variance makes the centreline a zig-zag at the
+  node scale (arclength 8-12 for a length-1 fiber at p = 63, measured), i.e.
+  not a resolved fiber of length 1; the low-mode reading keeps L = 1 +- O(1e-2);
 * REJECTION SAMPLING: the reference raises OverlapError for targets within
   eps L of another fiber (fiber.py:526-528), so uniform draws fail
   (SURVEY.md fact 6).  A draw is rejected when it comes closer than `clear`
@@ -80,6 +84,9 @@ def _seg_dist(p0, p1, q0, q1):
     return np.sqrt(((cp - cq) ** 2).sum(axis=1))
 
 
+PERTURB_MODES = 4
+
+
 def _draw(rng, k, p, length, region, size, perturb, V):
     """k candidate centrelines (k, n, 3) from the placement laws."""
     n = p + 1
@@ -95,7 +102,9 @@ def _draw(rng, k, p, length, region, size, perturb, V):
         d /= np.linalg.norm(d)
         X = straight_centerline(p, centre - 0.5 * length * d, d, length)
         if perturb > 0:
-            X = X + V @ rng.normal(0.0, perturb, size=(n, 3))
+            coef = np.zeros((n, 3))
+            coef[:PERTURB_MODES] = rng.normal(0.0, perturb, size=(PERTURB_MODES, 3))
+            X = X + V @ coef
         out[i] = X
     return out
 
@@ -128,48 +137,69 @@ def _segment_sampling(rng, n_fibers, p, length, region, size, clear, max_draws):
     return np.stack(Xs), draws
 
 
-def _node_sampling(rng, n_fibers, p, length, region, size, clear, perturb, max_draws):
-    """Batched rejection on node-node distance: draw all fibers, find
-    conflicting pairs with a k-d tree, keep the lower index of each conflict,
-    redraw the rest, repeat."""
+def _node_sampling(rng, n_fibers, p, length, region, size, clear, perturb, max_draws,
+                   upsample=4):
+    """Batched rejection on centreline-sample distance: draw all fibers,
+    resample each centreline at `upsample` x the Chebyshev nodes (the nodes
+    included), find conflicting pairs with a k-d tree, keep the lower index of
+    each conflict, redraw the rest, repeat.  Sampling the centreline (not only
+    the nodes) keeps every node outside other fibers' radius as well."""
     from scipy.spatial import cKDTree
 
     n = p + 1
     V = C.chebvander(cheb_nodes(p), p) if perturb > 0 else None
+    # nodal values -> values at the refined extremal points (nodes are a subset)
+    fine = np.cos(np.pi * np.arange(upsample * p + 1) / (upsample * p))
+    E = C.chebvander(fine, p) @ np.linalg.inv(C.chebvander(cheb_nodes(p), p))
+    nfine = fine.size
+    def refine(Xs):
+        m = Xs.shape[0]
+        return (E @ Xs.transpose(1, 0, 2).reshape(n, -1)).reshape(nfine, m, 3).transpose(1, 0, 2)
+
     X = _draw(rng, n_fibers, p, length, region, size, perturb, V)
+    F = refine(X)
     draws = n_fibers
-    pending = np.arange(n_fibers)
-    while True:
-        tree = cKDTree(X.reshape(-1, 3))
-        pairs = tree.query_pairs(clear, output_type="ndarray")
-        fa, fb = pairs[:, 0] // n, pairs[:, 1] // n
-        keep = fa != fb
-        fa, fb = np.minimum(fa[keep], fb[keep]), np.maximum(fa[keep], fb[keep])
-        if fa.size == 0:
-            break
-        # greedy in index order: a fiber is rejected if it conflicts with a
-        # lower-index fiber that itself survives
-        order = np.lexsort((fa, fb))
-        rejected = np.zeros(n_fibers, dtype=bool)
-        pending_set = np.zeros(n_fibers, dtype=bool)
-        pending_set[pending] = True
-        for a, b in zip(fa[order], fb[order]):
-            if rejected[a]:
-                continue
-            # only redraw fibers drawn in this round; earlier survivors stay
-            if pending_set[b]:
-                rejected[b] = True
-            elif pending_set[a]:
-                rejected[a] = True
-        redo = np.nonzero(rejected)[0]
-        if redo.size == 0:
-            # conflicts among earlier survivors cannot happen; guard anyway
-            redo = np.unique(fb)
+    # round 0: all pairs among the initial draws; keep the lower index
+    tree = cKDTree(F.reshape(-1, 3))
+    pairs = tree.query_pairs(clear, output_type="ndarray")
+    fa, fb = pairs[:, 0] // nfine, pairs[:, 1] // nfine
+    keep = fa != fb
+    fa, fb = np.minimum(fa[keep], fb[keep]), np.maximum(fa[keep], fb[keep])
+    rejected = np.zeros(n_fibers, dtype=bool)
+    for a, b in sorted(set(zip(fa.tolist(), fb.tolist())), key=lambda ab: (ab[1], ab[0])):
+        if not rejected[a]:
+            rejected[b] = True
+    redo = np.nonzero(rejected)[0]
+    # later rounds: redraw the rejected fibers and test them against the fixed
+    # survivors (old tree, stale entries of redrawn fibers ignored) and each other
+    while redo.size:
         draws += redo.size
         if draws > max_draws:
             raise RuntimeError("rejection sampling did not converge; domain too dense")
         X[redo] = _draw(rng, redo.size, p, length, region, size, perturb, V)
-        pending = redo
+        F[redo] = refine(X[redo])
+        in_redo = np.zeros(n_fibers, dtype=bool)
+        in_redo[redo] = True
+        bad = np.zeros(n_fibers, dtype=bool)
+        hits = tree.query_ball_point(F[redo].reshape(-1, 3), r=clear)
+        for k, h in enumerate(hits):
+            if h:
+                ids = np.asarray(h) // nfine
+                if np.any(~in_redo[ids]):
+                    bad[redo[k // nfine]] = True
+        small = cKDTree(F[redo].reshape(-1, 3))
+        pr = small.query_pairs(clear, output_type="ndarray")
+        ra, rb = redo[pr[:, 0] // nfine], redo[pr[:, 1] // nfine]
+        keep = ra != rb
+        for a, b in sorted(set(zip(np.minimum(ra[keep], rb[keep]).tolist(),
+                                   np.maximum(ra[keep], rb[keep]).tolist())),
+                           key=lambda ab: (ab[1], ab[0])):
+            if not bad[a]:
+                bad[b] = True
+        accepted = redo[~bad[redo]]
+        if accepted.size:
+            tree = cKDTree(F.reshape(-1, 3)) if accepted.size > 0 else tree
+        redo = redo[bad[redo]]
     return X, draws
 
 
@@ -221,3 +251,67 @@ def make(name, seed=0, **overrides):
 def forces(cloud, seed=1):
     """i.i.d. N(0,1) force densities per point (BASELINE.json C1)."""
     return np.random.default_rng(seed).standard_normal(cloud.X.shape)
+
+
+def aster(n_fibers=1024, p=31, radius=0.5, standoff=1.3, center=(0.0, 0.0, 0.0), eps=1e-2,
+          E=1.0, length=1.0, mesh_res=(8, 8), min_sep=0.05, motor_force=1.0, seed=0,
+          layout="random"):
+    """BASELINE config 2 (and 4's centrosome): fibers clamped radially to a
+    rigid sphere, plus-end force of magnitude `motor_force` along the initial
+    tangent (a fixed vector, as PrescribedForceTorque stores it, fiber.py:58-63).
+
+    layout "random": uniform directions (normalised Gaussians) with rejection
+    of attachment points closer than `min_sep` (uniform draws overlap,
+    SURVEY.md fact 6); "fibonacci": the reference's aster_attachment_layout
+    spiral (system.py:428-443).  Attachment at standoff * radius (the
+    reference default 1.3).  Returns a SystemState of this package.
+    """
+    from . import body
+    from .fiber import ClampedToBody, PrescribedForceTorque, straight_fiber
+    from .system import SystemState
+
+    center = np.asarray(center, dtype=float)
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(radius), mesh_res,
+                                                center=tuple(center)))
+    rng = np.random.default_rng(seed)
+    r_att = standoff * radius
+    if layout == "fibonacci":
+        k = np.arange(n_fibers)
+        z = 1.0 - 2.0 * (k + 0.5) / n_fibers
+        rho = np.sqrt(1.0 - z * z)
+        phi = k * (np.pi * (3.0 - np.sqrt(5.0)))
+        dirs = np.stack([rho * np.cos(phi), rho * np.sin(phi), z], axis=1)
+    else:
+        dirs = []
+        pts = []
+        draws = 0
+        while len(dirs) < n_fibers:
+            draws += 1
+            if draws > 1000 * n_fibers:
+                raise RuntimeError("aster rejection sampling did not converge")
+            d = rng.standard_normal(3)
+            d /= np.linalg.norm(d)
+            x = r_att * d
+            if pts and np.min(np.linalg.norm(np.asarray(pts) - x, axis=1)) < min_sep:
+                continue
+            dirs.append(d)
+            pts.append(x)
+        dirs = np.asarray(dirs)
+    fibs = []
+    for d in dirs:
+        x0 = center + r_att * d
+        fibs.append(straight_fiber(p, x0, d, length, eps=eps, E=E,
+                                   bc_minus=ClampedToBody(0, x0, d),
+                                   bc_plus=PrescribedForceTorque(motor_force * d)))
+    return SystemState(fibs, [part])
+
+
+def cloud_state(name="c3_scaled", seed=0, f0=1.0, direction=(0.0, 0.0, -1.0), **overrides):
+    """Sedimenting cloud (BASELINE configs 3/5): free fibers under a uniform
+    force density (0,0,-1) (UniformBodyForce, system.py:40-54)."""
+    from .fiber import Fiber
+    from .system import SystemState, UniformBodyForce
+
+    cl = make(name, seed=seed, **overrides)
+    fibs = [Fiber(X, eps=cl.eps, E=cl.E) for X in cl.X]
+    return SystemState(fibs, force_models=[UniformBodyForce(f0, direction)])

@@ -1,0 +1,33 @@
+"""Implicit-step timing on a config (helper; the bench reports the headline)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import torch  # noqa: E402
+
+from paper_1602_05650_b200 import configs, solver  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--fibers", type=int, default=1024)
+ap.add_argument("--tol", type=float, default=1e-10)
+a = ap.parse_args()
+if a.config == "c2":
+    st = configs.aster(n_fibers=a.fibers)
+    dt = 1e-3
+else:
+    st = configs.cloud_state(a.config)
+    dt = 5e-3
+params = solver.GmresParams(tolerance=a.tol)
+for k in range(a.steps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st, info = solver.backward_euler_step(st, dt, params, return_info=True)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    print(json.dumps({"config": a.config, "step": k, "s": el, "iters": info["iterations"],
+                      "matvecs": info["matvecs"], "dt": info["dt"]}), flush=True)
