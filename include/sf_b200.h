@@ -38,8 +38,12 @@ enum {
 
 /* Arithmetic mode of the pair kernels. */
 enum {
-    SF_MODE_FP64 = 0,  /* FP64 compute, FP64 accumulate */
-    SF_MODE_FP32C = 1  /* FP32 pair arithmetic, FP64 accumulation per tile */
+    SF_MODE_FP64 = 0,        /* FP64 compute and accumulation; where targets == sources
+                                (the fiber x fiber block, >= 8192 points) each pair's
+                                geometry is evaluated once for both directions */
+    SF_MODE_FP32C = 1,       /* FP32 pair arithmetic, FP64 accumulation per tile */
+    SF_MODE_FP64_DIRECT = 2  /* FP64, every target summed over sources in index
+                                order (the reference's loop order) */
 };
 
 int sf_abi_version(void);
@@ -189,7 +193,10 @@ typedef struct {
     int64_t near_nrows;
     const double *near_W;
     double mu;
-    int mode;                /* SF_MODE_FP64 / SF_MODE_FP32C for the fiber pair sum */
+    int mode;                /* SF_MODE_* for the fiber pair sum */
+    int64_t fiber_target_off; /* targets [off, off+nfs) ARE the fiber sources
+                                 (same points, order, groups), or -1 */
+    int64_t fiber_group_size; /* nodes per fiber (unit alignment), 0 if unknown */
 } sf_hi_layout;
 
 /* u (nt,3) = complementary velocities for fiber force densities f (nfs,3),

@@ -12,6 +12,7 @@ from .build import LIB
 SF_OK = 0
 SF_MODE_FP64 = 0
 SF_MODE_FP32C = 1
+SF_MODE_FP64_DIRECT = 2
 
 
 class NativeUnavailable(RuntimeError):
@@ -95,7 +96,7 @@ class HiLayout(ctypes.Structure):
         ("pcenter", _P), ("pgrp", _P), ("np", _I64),
         ("near_row_ptr", _P), ("near_rows", _P), ("near_w_off", _P), ("near_x_off", _P),
         ("near_x_len", _P), ("near_nrows", _I64), ("near_W", _P),
-        ("mu", _D), ("mode", _I),
+        ("mu", _D), ("mode", _I), ("fiber_target_off", _I64), ("fiber_group_size", _I64),
     ]
 
 

@@ -233,12 +233,19 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
                "target fiber range outside [0, nf)");
     SF_REQUIRE(nf == 0 || (X && wnode && f && out_nl), "null pointer");
     SF_REQUIRE(!out_self || (K && tang && c_log), "self terms need K, tangents and c_log");
-    SF_REQUIRE(mode == SF_MODE_FP64 || mode == SF_MODE_FP32C, "unknown mode");
+    SF_REQUIRE(mode == SF_MODE_FP64 || mode == SF_MODE_FP32C || mode == SF_MODE_FP64_DIRECT,
+               "unknown mode");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = nf * n;
     const int64_t t0 = t_fiber0 * n, nt = t_nfibers * n;
-    int rc = pairs_sbt_weighted(X + 3 * t0, grp ? grp + t0 : nullptr, nt, X, grp, N, f, wnode,
-                                dcoef, pref, mode, out_nl, bad, st, workspace_for(st));
+    int rc;
+    if (t_fiber0 == 0 && t_nfibers == nf && use_symmetric(mode, N))
+        rc = pairs_sbt_symmetric(X, grp, N, n, f, wnode, dcoef, pref, out_nl, bad, 0, st,
+                                 workspace_for(st));
+    else
+        rc = pairs_sbt_weighted(X + 3 * t0, grp ? grp + t0 : nullptr, nt, X, grp, N, f, wnode,
+                                dcoef, pref, mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64,
+                                out_nl, bad, st, workspace_for(st));
     if (rc) return rc;
     if (near_nrows > 0) {
         rc = near_apply(near_row_ptr, near_rows, near_nrows, near_w_off, near_x_off, near_x_len,

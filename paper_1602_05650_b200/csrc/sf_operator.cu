@@ -52,6 +52,13 @@ __global__ void completion_kernel(const double *__restrict__ trg, const int64_t 
     if ((threadIdx.x & 31) == 0 && nbad && bad) atomicAdd(bad, (unsigned long long)nbad);
 }
 
+__global__ void add_counter_kernel(int64_t *dst, const int64_t *src) { dst[0] += src[0]; }
+
+int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st) {
+    add_counter_kernel<<<1, 1, 0, st>>>(dst, src);
+    return check_launch("add_counter_kernel");
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -78,9 +85,30 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
     if (L->nt == 0) return SF_OK;
     const double pref = 1.0 / (8.0 * M_PI * L->mu);
     int rc;
-    if (L->nfs > 0) {
+    const int64_t off = L->fiber_target_off;
+    if (L->nfs > 0 && off >= 0 && off + L->nfs == L->nt && use_symmetric(L->mode, L->nfs)) {
+        // non-fiber targets against fiber sources, then the fiber block symmetrically
+        if (off > 0) {
+            rc = pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f, L->fw,
+                                    L->fdcoef, pref, SF_MODE_FP64, u, bad_f, st, ws, 0);
+            if (rc) return rc;
+        }
+        int64_t *bad_sym = nullptr;
+        if (bad) {
+            bad_sym = (int64_t *)ws.get(6, sizeof(int64_t), st);
+            if (!bad_sym) return SF_ENOMEM;
+        }
+        rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
+                                 L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws);
+        if (rc) return rc;
+        if (bad) {
+            rc = add_counter(bad_f, bad_sym, st);
+            if (rc) return rc;
+        }
+    } else if (L->nfs > 0) {
         rc = pairs_sbt_weighted(L->trg, L->tgrp, L->nt, L->fsrc, L->fgrp, L->nfs, f, L->fw,
-                                L->fdcoef, pref, L->mode, u, bad_f, st, ws, 0);
+                                L->fdcoef, pref, L->mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64,
+                                u, bad_f, st, ws, 0);
         if (rc) return rc;
     } else if (cudaMemsetAsync(u, 0, sizeof(double) * 3 * L->nt, st) != cudaSuccess) {
         return check_launch("memset");

@@ -1,0 +1,439 @@
+// sf_sym.cu — symmetric evaluation of the fiber-fiber Stokeslet + doublet sum.
+//
+// When the targets are exactly the sources (the fiber x fiber block of
+// complementary_velocities, system.py:656-671), the pair geometry r, r^2,
+// 1/r, 1/r^3, 1/r^5 of (i,j) is shared with (j,i): the kernel r_ij r_ij^T /r^3
+// is even in r.  Computing both directions from one geometry evaluation costs
+// 14 + 2 x 12 = 38 FP64 instructions per unordered pair (19 per pair
+// interaction) instead of 2 x 26.
+//
+// Determinism without atomics: points are split into G units of M points
+// (M a multiple of the fiber size, so units align to fibers).  A task is an
+// unordered unit pair {g,h}; the CTA computes every (i in g, j in h) pair in
+// both directions and writes two partial sums:
+//     part[h][points of g] = sum over j in h   (owner direction)
+//     part[g][points of h] = sum over i in g   (transposed direction)
+// Diagonal tasks {g,g} write only the owner direction.  A final pass sums the
+// G partials of every point in slot order.  Every partial is produced by one
+// CTA in a fixed loop order, so results are bitwise reproducible.
+//
+// Inside a task: 4 warps share an i-sub-block of 64 points (2 per lane, in
+// registers with their owner accumulators); j runs in 32-point slabs, slab
+// k owned by warp k % 4.  Within a slab each lane holds one j (data and
+// transposed accumulator) and the 32 j's rotate around the warp with
+// shuffles, so every (i, j) of the 64 x 32 block is visited once and each
+// j's transposed sum stays in registers; after 32 rotations it is added to
+// the task's shared-memory accumulator for that j (always by the same warp,
+// in i-sub-block order).
+#include <cstdlib>
+
+#include "sf_common.cuh"
+#include "sf_internal.h"
+
+namespace sf {
+
+struct __align__(16) SymSrc {  // same 80-byte record as the pair engine's Src80
+    double v[9];
+    int g;
+    int pad;
+};
+static_assert(sizeof(SymSrc) == 80, "record must be 80 bytes");
+
+struct __align__(16) SlabMeta {  // bounding box + group range of 32 points
+    double lo[3], hi[3];
+    int gmin, gmax;
+};
+
+struct SymArgs {
+    const SymSrc *src;
+    const SlabMeta *slab;
+    int64_t N;
+    int M;
+    int G;
+    int64_t ntasks;
+    double *part;  // (G, N, 3)
+    unsigned long long *bad;
+};
+
+constexpr int kSymThreads = 128;
+constexpr int kSymI = 64;  // i points per sub-block (2 per lane)
+
+struct PData {
+    double x, y, z, fx, fy, fz, c, c3;
+    int g;
+};
+
+__device__ __forceinline__ PData load_point(const SymArgs &a, int64_t k, bool valid) {
+    PData p;
+    if (valid) {
+        const double2 *q = reinterpret_cast<const double2 *>(a.src + k);
+        const double2 a0 = q[0], a1 = q[1], a2 = q[2], a3 = q[3];
+        p.x = a0.x; p.y = a0.y; p.z = a1.x; p.fx = a1.y; p.fy = a2.x; p.fz = a2.y;
+        p.c = a3.x; p.c3 = a3.y;
+        p.g = a.src[k].g;
+    } else {  // far away and strengthless: contributes exactly 0 both ways
+        p.x = p.y = p.z = 1e30;
+        p.fx = p.fy = p.fz = p.c = p.c3 = 0.0;
+        p.g = -3;
+    }
+    return p;
+}
+
+// One unordered pair, both directions.  ui += (j -> i), uj += (i -> j).
+template <bool CHECK, bool BOTH>
+__device__ __forceinline__ void sym_pair(const PData &pi, const PData &pj, double *ui, double *uj,
+                                         int &nb) {
+    const double rx = pi.x - pj.x, ry = pi.y - pj.y, rz = pi.z - pj.z;
+    const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
+    double y0 = rsq_seed(r2);
+    if (CHECK) {
+        const bool excl = (pi.g == pj.g) && pi.g >= 0;
+        const bool small = below_min_sep(r2);
+        nb += (small && !excl) ? (BOTH ? 2 : 1) : 0;
+        y0 = (excl || small) ? 0.0 : y0;
+    }
+    const double ir = rsq_refine(r2, y0);
+    const double ir2 = ir * ir;
+    const double ir3 = ir * ir2;
+    const double ir5 = ir3 * ir2;
+    {   // j -> i
+        const double a = fma(pj.c, ir3, ir);
+        const double bb = fma(-pj.c3, ir5, ir3);
+        const double rf = fma(rz, pj.fz, fma(ry, pj.fy, rx * pj.fx));
+        const double b = rf * bb;
+        ui[0] = fma(a, pj.fx, ui[0]);
+        ui[1] = fma(a, pj.fy, ui[1]);
+        ui[2] = fma(a, pj.fz, ui[2]);
+        ui[0] = fma(b, rx, ui[0]);
+        ui[1] = fma(b, ry, ui[1]);
+        ui[2] = fma(b, rz, ui[2]);
+    }
+    if (BOTH) {  // i -> j: (r_ji.f) r_ji = (r_ij.f) r_ij
+        const double a = fma(pi.c, ir3, ir);
+        const double bb = fma(-pi.c3, ir5, ir3);
+        const double rf = fma(rz, pi.fz, fma(ry, pi.fy, rx * pi.fx));
+        const double b = rf * bb;
+        uj[0] = fma(a, pi.fx, uj[0]);
+        uj[1] = fma(a, pi.fy, uj[1]);
+        uj[2] = fma(a, pi.fz, uj[2]);
+        uj[0] = fma(b, rx, uj[0]);
+        uj[1] = fma(b, ry, uj[1]);
+        uj[2] = fma(b, rz, uj[2]);
+    }
+}
+
+__device__ __forceinline__ PData shfl_next(const PData &p, int src_lane) {
+    PData q;
+    q.x = __shfl_sync(0xffffffffu, p.x, src_lane);
+    q.y = __shfl_sync(0xffffffffu, p.y, src_lane);
+    q.z = __shfl_sync(0xffffffffu, p.z, src_lane);
+    q.fx = __shfl_sync(0xffffffffu, p.fx, src_lane);
+    q.fy = __shfl_sync(0xffffffffu, p.fy, src_lane);
+    q.fz = __shfl_sync(0xffffffffu, p.fz, src_lane);
+    q.c = __shfl_sync(0xffffffffu, p.c, src_lane);
+    q.c3 = __shfl_sync(0xffffffffu, p.c3, src_lane);
+    q.g = __shfl_sync(0xffffffffu, p.g, src_lane);
+    return q;
+}
+
+__device__ __forceinline__ void task_units(int64_t t, int G, int &g, int &h) {
+    // tasks enumerate {g <= h} row by row: row g has G - g entries
+    // solve for the row with a float estimate, then fix up
+    double Gd = (double)G;
+    double disc = (2.0 * Gd + 1.0) * (2.0 * Gd + 1.0) - 8.0 * (double)t;
+    int r = (int)floor(((2.0 * Gd + 1.0) - sqrt(disc)) * 0.5);
+    if (r < 0) r = 0;
+    auto start = [&](int row) { return (int64_t)row * G - (int64_t)row * (row - 1) / 2; };
+    while (r > 0 && start(r) > t) --r;
+    while (r + 1 < G && start(r + 1) <= t) ++r;
+    g = r;
+    h = r + (int)(t - start(r));
+}
+
+__device__ __forceinline__ bool boxes_far(const double *blo, const double *bhi, const SlabMeta &m) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double gap = fmax(0.0, fmax(m.lo[c] - bhi[c], blo[c] - m.hi[c]));
+        d2 = fma(gap, gap, d2);
+    }
+    return d2 > 1e-20;
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) {
+    extern __shared__ double jacc_s[];           // M x 3 transposed accumulators
+    __shared__ double ui_s[4][kSymI][3];          // per-warp owner partials
+    __shared__ double2 js_xy[4][32], js_zf[4][32], js_ff[4][32], js_cc[4][32];  // j slabs
+    __shared__ int js_g[4][32];
+    const int64_t t = blockIdx.x;
+    if (t >= a.ntasks) return;
+    int g, h;
+    task_units(t, a.G, g, h);
+    const bool both = g != h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g0 = (int64_t)g * a.M, h0 = (int64_t)h * a.M;
+    const int ng = (int)min((int64_t)a.M, a.N - g0), nh = (int)min((int64_t)a.M, a.N - h0);
+    const int nslab = (nh + 31) / 32;
+    if (both)
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    int nb = 0;
+    for (int ib = 0; ib < ng; ib += kSymI) {
+        const bool v0 = ib + lane < ng, v1 = ib + 32 + lane < ng;
+        const PData p0 = load_point(a, g0 + ib + lane, v0);
+        const PData p1 = load_point(a, g0 + ib + 32 + lane, v1);
+        double u0[3] = {0, 0, 0}, u1[3] = {0, 0, 0};
+        // bounding box + groups of this i-sub-block from its two slab metas
+        double blo[3], bhi[3];
+        int gmn, gmx;
+        {
+            const SlabMeta &m0 = a.slab[(g0 + ib) / 32];
+            blo[0] = m0.lo[0]; blo[1] = m0.lo[1]; blo[2] = m0.lo[2];
+            bhi[0] = m0.hi[0]; bhi[1] = m0.hi[1]; bhi[2] = m0.hi[2];
+            gmn = m0.gmin; gmx = m0.gmax;
+            if (ib + 32 < ng) {
+                const SlabMeta &m1 = a.slab[(g0 + ib) / 32 + 1];
+                for (int c = 0; c < 3; ++c) {
+                    blo[c] = fmin(blo[c], m1.lo[c]);
+                    bhi[c] = fmax(bhi[c], m1.hi[c]);
+                }
+                gmn = min(gmn, m1.gmin);
+                gmx = max(gmx, m1.gmax);
+            }
+        }
+        for (int sl = warp; sl < nslab; sl += 4) {
+            const int jl = sl * 32 + lane;
+            {   // stage this warp's slab in shared memory (double2 SoA, conflict-free)
+                const PData q = load_point(a, h0 + jl, jl < nh);
+                js_xy[warp][lane] = make_double2(q.x, q.y);
+                js_zf[warp][lane] = make_double2(q.z, q.fx);
+                js_ff[warp][lane] = make_double2(q.fy, q.fz);
+                js_cc[warp][lane] = make_double2(q.c, q.c3);
+                js_g[warp][lane] = q.g;
+            }
+            __syncwarp();
+            double uj[3] = {0, 0, 0};
+            const SlabMeta &mj = a.slab[h0 / 32 + sl];
+            const bool fast = boxes_far(blo, bhi, mj) && (mj.gmax < gmn || mj.gmin > gmx);
+            const int nxt = (lane + 1) & 31;
+            // step s: this lane pairs its i's with j = (lane + s) mod 32 and
+            // carries that j's transposed accumulator (rotated by shuffles)
+            if (both && fast) {
+#pragma unroll 4
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PData pj;
+                    const double2 xy = js_xy[warp][k], zf = js_zf[warp][k], ff = js_ff[warp][k],
+                                  cc = js_cc[warp][k];
+                    pj.x = xy.x; pj.y = xy.y; pj.z = zf.x; pj.fx = zf.y; pj.fy = ff.x; pj.fz = ff.y;
+                    pj.c = cc.x; pj.c3 = cc.y; pj.g = 0;
+                    sym_pair<false, true>(p0, pj, u0, uj, nb);
+                    sym_pair<false, true>(p1, pj, u1, uj, nb);
+                    uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                    uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                    uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                }
+            } else {
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PData pj;
+                    const double2 xy = js_xy[warp][k], zf = js_zf[warp][k], ff = js_ff[warp][k],
+                                  cc = js_cc[warp][k];
+                    pj.x = xy.x; pj.y = xy.y; pj.z = zf.x; pj.fx = zf.y; pj.fy = ff.x; pj.fz = ff.y;
+                    pj.c = cc.x; pj.c3 = cc.y; pj.g = js_g[warp][k];
+                    int nbi = 0;
+                    if (both) {
+                        sym_pair<true, true>(p0, pj, u0, uj, nbi);
+                        sym_pair<true, true>(p1, pj, u1, uj, nbi);
+                        uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                        uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                        uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                    } else if (fast) {
+                        sym_pair<false, false>(p0, pj, u0, uj, nbi);
+                        sym_pair<false, false>(p1, pj, u1, uj, nbi);
+                    } else {
+                        sym_pair<true, false>(p0, pj, u0, uj, nbi);
+                        sym_pair<true, false>(p1, pj, u1, uj, nbi);
+                    }
+                    // count only pairs whose both ends are real points
+                    if (pj.g != -3) nb += nbi;
+                }
+            }
+            __syncwarp();
+            // after 32 rotations each lane again holds its own j's accumulator
+            if (both && jl < nh) {
+                double *dst = jacc_s + 3 * jl;
+                dst[0] += uj[0];
+                dst[1] += uj[1];
+                dst[2] += uj[2];
+            }
+        }
+        // combine the 4 warps' owner partials in warp order, write slot h
+        ui_s[warp][lane][0] = u0[0]; ui_s[warp][lane][1] = u0[1]; ui_s[warp][lane][2] = u0[2];
+        ui_s[warp][32 + lane][0] = u1[0]; ui_s[warp][32 + lane][1] = u1[1];
+        ui_s[warp][32 + lane][2] = u1[2];
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * kSymI; e += blockDim.x) {
+            const int il = e / 3, c = e - 3 * il;
+            if (ib + il < ng) {
+                const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
+                a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c] = s;
+            }
+        }
+        __syncthreads();
+    }
+    if (both) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
+            a.part[((int64_t)g * a.N + h0) * 3 + e] = jacc_s[e];
+    }
+    // invalid i lanes never count (their g is -3 and they sit at 1e30)
+    if (a.bad) {
+        nb = warp_sum_int(nb);
+        if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
+    }
+}
+
+__global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
+                                 SlabMeta *__restrict__ meta) {
+    const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s * 32 >= N) return;
+    const int64_t j = s * 32 + lane;
+    double v[6];
+    int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    if (j < N) {
+        const SymSrc &q = src[j];
+        v[0] = v[3] = q.v[0];
+        v[1] = v[4] = q.v[1];
+        v[2] = v[5] = q.v[2];
+        if (q.g >= 0) { gmn = q.g; gmx = q.g; }
+    } else {
+        v[0] = v[1] = v[2] = 1e300;
+        v[3] = v[4] = v[5] = -1e300;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            v[c] = fmin(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+            v[3 + c] = fmax(v[3 + c], __shfl_xor_sync(0xffffffffu, v[3 + c], o));
+        }
+        gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+        gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+    }
+    if (lane == 0) {
+        SlabMeta m;
+        for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
+        m.gmin = gmn;
+        m.gmax = gmx;
+        meta[s] = m;
+    }
+}
+
+// out[i] (+)= pref * sum_{s < G} part[s][i], slots in order.
+__global__ void sym_reduce_kernel(const double *__restrict__ part, int G, int64_t N, double pref,
+                                  double *__restrict__ out, int accumulate) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= 3 * N) return;
+    double s = 0.0;
+    for (int k = 0; k < G; ++k) s += part[(int64_t)k * 3 * N + e];
+    out[e] = accumulate ? out[e] + pref * s : pref * s;
+}
+
+// Packing identical to the pair engine's (x y z, w f, c, 3c, group).
+__global__ void sym_pack_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
+                                const double *__restrict__ f, const double *__restrict__ w,
+                                const double *__restrict__ dcoef, int64_t N,
+                                SymSrc *__restrict__ out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        SymSrc s;
+        const double wj = w ? w[j] : 1.0;
+        s.v[0] = x[3 * j]; s.v[1] = x[3 * j + 1]; s.v[2] = x[3 * j + 2];
+        s.v[3] = wj * f[3 * j]; s.v[4] = wj * f[3 * j + 1]; s.v[5] = wj * f[3 * j + 2];
+        const double c = dcoef ? dcoef[j] : 0.0;
+        s.v[6] = c; s.v[7] = 3.0 * c; s.v[8] = 0.0;
+        s.g = grp ? pack_source_group(grp[j]) : -1;
+        s.pad = 0;
+        out[j] = s;
+    }
+}
+
+int sym_unit_size(int64_t group_size) {
+    // units of ~2048 points: a multiple of the 32-point slab, and of the
+    // fiber size when that keeps them near 2048 (units then align to fibers,
+    // so off-diagonal unit pairs never share a group)
+    const char *e = getenv("SF_SYM_UNIT");
+    int target = e ? atoi(e) : 2048;
+    target = (target / 32) * 32;
+    if (target < 64) target = 64;
+    if (group_size > 0) {
+        int64_t a = group_size, b = 32;
+        while (b) { const int64_t t = a % b; a = b; b = t; }
+        const int64_t l = group_size / a * 32;  // lcm(group_size, 32)
+        if (l <= target) return (int)((target / l) * l);
+    }
+    return target;
+}
+
+// mode SF_MODE_FP64 picks the symmetric evaluation for large enough blocks;
+// SF_MODE_FP64_DIRECT forces the per-target order of the reference.
+bool use_symmetric(int mode, int64_t N) {
+    if (mode != SF_MODE_FP64) return false;
+    const char *e = getenv("SF_SYMMETRIC");
+    if (e && atoi(e) == 0) return false;
+    return N >= 8192;
+}
+
+int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
+                        const double *f, const double *w, const double *dcoef, double pref,
+                        double *out, int64_t *bad, int accumulate, cudaStream_t st,
+                        Workspace &ws) {
+    if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
+        return check_launch("memset");
+    if (N == 0) return SF_OK;
+    const int M = sym_unit_size(group_size);
+    const int G = (int)((N + M - 1) / M);
+    SymSrc *packed = (SymSrc *)ws.get(3, sizeof(SymSrc) * (size_t)N, st);
+    SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)((N + 31) / 32 + 1), st);
+    double *part = (double *)ws.get(5, sizeof(double) * 3 * (size_t)N * G, st);
+    if (!packed || !meta || !part) return SF_ENOMEM;
+    int64_t pg = (N + 255) / 256;
+    sym_pack_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef, N,
+                                                                     packed);
+    const int64_t nslab = (N + 31) / 32;
+    slab_meta_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
+    SymArgs a;
+    a.src = packed;
+    a.slab = meta;
+    a.N = N;
+    a.M = M;
+    a.G = G;
+    a.ntasks = (int64_t)G * (G + 1) / 2;
+    a.part = part;
+    a.bad = (unsigned long long *)bad;
+    const size_t smem = sizeof(double) * 3 * M;
+    static const int minb = [] {
+        const char *e = getenv("SF_SYM_MINB");
+        return e ? atoi(e) : 3;
+    }();
+    if (minb != 4) {
+        if (cudaFuncSetAttribute(sym_task_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        sym_task_kernel<3><<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
+    } else {
+        if (cudaFuncSetAttribute(sym_task_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        sym_task_kernel<4><<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
+    }
+    int rc = check_launch("sym_task_kernel");
+    if (rc) return rc;
+    sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(part, G, N, pref, out,
+                                                                      accumulate);
+    return check_launch("sym_reduce_kernel");
+}
+
+}  // namespace sf

@@ -369,7 +369,9 @@ class InteractionCache:
             near_row_ptr=_ptr(nt.get("row_ptr")), near_rows=_ptr(nt.get("rows")),
             near_w_off=_ptr(nt.get("w_off")), near_x_off=_ptr(nt.get("x_off")),
             near_x_len=_ptr(nt.get("x_len")), near_nrows=self.near_nrows,
-            near_W=_ptr(nt.get("W")), mu=self.mu, mode=self.mode)
+            near_W=_ptr(nt.get("W")), mu=self.mu, mode=self.mode,
+            fiber_target_off=self.fiber_slice.start if self.nf else -1,
+            fiber_group_size=self.n_nodes)
 
     # -- application ------------------------------------------------------------
     @property
