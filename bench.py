@@ -306,7 +306,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_flops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_flops, "traffic": None,
-                         "kernel": "pack + pair_kernel<SbtP<true>> + reduce_partials",
+                         "kernel": "pack + slab meta + sym_task_kernel (symmetric fiber-fiber "
+                                   "pairs) + ordered partial reduce",
                          "flops_per_pair": FLOPS_PER_PAIR,
                          "peak_source": "measured DFMA microbenchmark (sf_dfma_peak) on this GPU; "
                                         f"nominal {NOMINAL_FP64_TFLOPS:.1f} TFLOP/s at 1965 MHz",

@@ -160,10 +160,11 @@ __device__ __forceinline__ bool boxes_far(const double *blo, const double *bhi, 
     return d2 > 1e-20;
 }
 
-template <int MINB>
+template <int MINB, int TBI>
 __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) {
+    constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];           // M x 3 transposed accumulators
-    __shared__ double ui_s[4][kSymI][3];          // per-warp owner partials
+    __shared__ double ui_s[4][kI][3];             // per-warp owner partials
     __shared__ double2 js_xy[4][32], js_zf[4][32], js_ff[4][32], js_cc[4][32];  // j slabs
     __shared__ int js_g[4][32];
     const int64_t t = blockIdx.x;
@@ -178,11 +179,14 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     if (both)
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
     int nb = 0;
-    for (int ib = 0; ib < ng; ib += kSymI) {
-        const bool v0 = ib + lane < ng, v1 = ib + 32 + lane < ng;
-        const PData p0 = load_point(a, g0 + ib + lane, v0);
-        const PData p1 = load_point(a, g0 + ib + 32 + lane, v1);
-        double u0[3] = {0, 0, 0}, u1[3] = {0, 0, 0};
+    for (int ib = 0; ib < ng; ib += kI) {
+        PData pi[TBI];
+        double ui[TBI][3];
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            pi[k] = load_point(a, g0 + ib + 32 * k + lane, ib + 32 * k + lane < ng);
+            ui[k][0] = ui[k][1] = ui[k][2] = 0.0;
+        }
         // bounding box + groups of this i-sub-block from its two slab metas
         double blo[3], bhi[3];
         int gmn, gmx;
@@ -191,8 +195,9 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             blo[0] = m0.lo[0]; blo[1] = m0.lo[1]; blo[2] = m0.lo[2];
             bhi[0] = m0.hi[0]; bhi[1] = m0.hi[1]; bhi[2] = m0.hi[2];
             gmn = m0.gmin; gmx = m0.gmax;
-            if (ib + 32 < ng) {
-                const SlabMeta &m1 = a.slab[(g0 + ib) / 32 + 1];
+            for (int k = 1; k < TBI; ++k) {
+                if (ib + 32 * k >= ng) break;
+                const SlabMeta &m1 = a.slab[(g0 + ib) / 32 + k];
                 for (int c = 0; c < 3; ++c) {
                     blo[c] = fmin(blo[c], m1.lo[c]);
                     bhi[c] = fmax(bhi[c], m1.hi[c]);
@@ -227,8 +232,8 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
                                   cc = js_cc[warp][k];
                     pj.x = xy.x; pj.y = xy.y; pj.z = zf.x; pj.fx = zf.y; pj.fy = ff.x; pj.fz = ff.y;
                     pj.c = cc.x; pj.c3 = cc.y; pj.g = 0;
-                    sym_pair<false, true>(p0, pj, u0, uj, nb);
-                    sym_pair<false, true>(p1, pj, u1, uj, nb);
+#pragma unroll
+                    for (int q = 0; q < TBI; ++q) sym_pair<false, true>(pi[q], pj, ui[q], uj, nb);
                     uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
                     uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
                     uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
@@ -243,17 +248,17 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
                     pj.c = cc.x; pj.c3 = cc.y; pj.g = js_g[warp][k];
                     int nbi = 0;
                     if (both) {
-                        sym_pair<true, true>(p0, pj, u0, uj, nbi);
-                        sym_pair<true, true>(p1, pj, u1, uj, nbi);
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) sym_pair<true, true>(pi[q], pj, ui[q], uj, nbi);
                         uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
                         uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
                         uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
                     } else if (fast) {
-                        sym_pair<false, false>(p0, pj, u0, uj, nbi);
-                        sym_pair<false, false>(p1, pj, u1, uj, nbi);
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) sym_pair<false, false>(pi[q], pj, ui[q], uj, nbi);
                     } else {
-                        sym_pair<true, false>(p0, pj, u0, uj, nbi);
-                        sym_pair<true, false>(p1, pj, u1, uj, nbi);
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) sym_pair<true, false>(pi[q], pj, ui[q], uj, nbi);
                     }
                     // count only pairs whose both ends are real points
                     if (pj.g != -3) nb += nbi;
@@ -269,11 +274,14 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             }
         }
         // combine the 4 warps' owner partials in warp order, write slot h
-        ui_s[warp][lane][0] = u0[0]; ui_s[warp][lane][1] = u0[1]; ui_s[warp][lane][2] = u0[2];
-        ui_s[warp][32 + lane][0] = u1[0]; ui_s[warp][32 + lane][1] = u1[1];
-        ui_s[warp][32 + lane][2] = u1[2];
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            ui_s[warp][32 * k + lane][0] = ui[k][0];
+            ui_s[warp][32 * k + lane][1] = ui[k][1];
+            ui_s[warp][32 * k + lane][2] = ui[k][2];
+        }
         __syncthreads();
-        for (int e = threadIdx.x; e < 3 * kSymI; e += blockDim.x) {
+        for (int e = threadIdx.x; e < 3 * kI; e += blockDim.x) {
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
@@ -414,21 +422,32 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
     a.part = part;
     a.bad = (unsigned long long *)bad;
     const size_t smem = sizeof(double) * 3 * M;
-    static const int minb = [] {
-        const char *e = getenv("SF_SYM_MINB");
-        return e ? atoi(e) : 3;
+    static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
+        const char *e = getenv("SF_SYM_VARIANT");
+        return e ? atoi(e) : 24;
     }();
-    if (minb != 4) {
-        if (cudaFuncSetAttribute(sym_task_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
+    auto launch = [&](auto kern) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        sym_task_kernel<3><<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
-    } else {
-        if (cudaFuncSetAttribute(sym_task_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-            return check_launch("cudaFuncSetAttribute");
-        sym_task_kernel<4><<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
+        kern<<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
+        return SF_OK;
+    };
+    int lrc;
+    switch (variant) {
+        case 41: lrc = launch(sym_task_kernel<4, 1>); break;
+        case 42: lrc = launch(sym_task_kernel<4, 2>); break;
+        case 22: lrc = launch(sym_task_kernel<2, 2>); break;
+        case 23: lrc = launch(sym_task_kernel<2, 3>); break;
+        case 33: lrc = launch(sym_task_kernel<3, 3>); break;
+        case 32: lrc = launch(sym_task_kernel<3, 2>); break;
+        case 25: lrc = launch(sym_task_kernel<2, 5>); break;
+        case 26: lrc = launch(sym_task_kernel<2, 6>); break;
+        case 16: lrc = launch(sym_task_kernel<1, 6>); break;
+        case 18: lrc = launch(sym_task_kernel<1, 8>); break;
+        default: lrc = launch(sym_task_kernel<2, 4>); break;
     }
+    if (lrc) return lrc;
     int rc = check_launch("sym_task_kernel");
     if (rc) return rc;
     sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(part, G, N, pref, out,

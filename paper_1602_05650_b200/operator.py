@@ -147,11 +147,24 @@ class FiberHIOperator:
         return self.Nown * self.N - self.nown * self.n * self.n
 
     @property
+    def symmetric(self):
+        """Whether the fiber pair sum runs the symmetric evaluation
+        (SF_MODE_FP64, whole system on this rank, >= 8192 points)."""
+        import os
+        return (self.mode == SF_MODE_FP64 and self.world == 1 and self.N >= 8192
+                and os.environ.get("SF_SYMMETRIC", "1") != "0")
+
+    @property
     def launches_per_apply(self):
-        """Kernels one apply launches: pack, pair (+ ordered split reduce),
-        near (if any), self terms."""
-        split = _native.load().sf_pair_split(self.Nown, self.N)
-        return 3 + (1 if split > 1 else 0) + (1 if self.near.nrows else 0)
+        """Kernels one apply launches: symmetric path = pack, slab meta, task
+        kernel, ordered reduce; direct path = pack, tile meta, pair kernel
+        (+ ordered split reduce); then near (if any) and self terms."""
+        if self.symmetric:
+            pair = 4
+        else:
+            split = _native.load().sf_pair_split(self.Nown, self.N)
+            pair = 3 + (1 if split > 1 else 0)
+        return pair + (1 if self.near.nrows else 0) + 1
 
     def apply(self, f, out_nl=None, out_self=None, self_terms=True):
         """u_nl and u_self (each (Nown,3); u_self None if self_terms=False)
