@@ -288,6 +288,27 @@ int sf_axpy_dev(const double *a, double sgn, int mode, const double *x, double *
 int sf_combine(const double *V, int64_t ld, int k, const double *coef, double *x, int64_t n,
                void *stream);
 
+/* Near-field map construction on the device.
+ * sf_near_search: (fiber, target) pairs whose minimum node distance is below
+ * the fiber's shell 1.5 L/p, target outside the fiber's group
+ * (system.py:564-577); pairs (cap,2) as [l, t], *count = number found (may
+ * exceed cap: call again with a larger buffer); order unspecified.
+ * center/bound/shell (nf): node centroid, max node distance + shell, shell.
+ * sf_near_fiber_weights: W (npairs,3,3n) = near_fiber_weights -
+ * plain_fiber_weights (fiber.py:514-575) for pairs (pt[e], pl[e]); Cmat (n,n)
+ * maps nodal values to Chebyshev coefficients, gl = 10 Gauss-Legendre nodes
+ * then weights on [-1,1]; info (npairs): 0 ok, 1 target inside the fiber
+ * (InsideFiberError, fiber.py:527-528), 2 panel overflow.  n <= 128. */
+int sf_near_search(const double *trg, const int64_t *tgrp, int64_t nt, const double *X,
+                   int64_t nf, int64_t n, const double *center, const double *bound,
+                   const double *shell, int64_t cap, int64_t *pairs,
+                   unsigned long long *count, void *stream);
+int sf_near_fiber_weights(const int64_t *pt, const int64_t *pl, int64_t npairs,
+                          const double *targets, const double *X, const double *s_alpha,
+                          const double *wcc, const double *Cmat, const double *nodes,
+                          const double *gl, const double *eps, const double *L, int64_t n,
+                          double mu, int include_doublet, double *W, int *info, void *stream);
+
 /* Near-field correction apply (system.py:702-707): for every entry e,
  * u[t_e] += W_e (3 x 3 m_e) . x[off_e : off_e + 3 m_e].  Entries must be
  * grouped by target (row_ptr CSR over `nrows` distinct targets rows[]);

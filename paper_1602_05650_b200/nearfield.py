@@ -348,3 +348,71 @@ def find_surface_pairs(surfaces, targets, target_groups, mu):
             Wp = plain_surface_weights(mesh, targets[t], mu)
             out.append((int(t), si, Wn - Wp))
     return out
+
+
+# ------------------------------------------------------------------ device ----
+
+def device_fiber_pairs(geo, eps, targets, target_groups, mu, include_doublet=True):
+    """Fiber near maps built on the device (sf_near_search + sf_near_fiber_weights).
+
+    geo: system.FiberGeometry (device centrelines, s_alpha, L, weights);
+    eps (nf,) device tensor; targets (nt,3) / target_groups (nt,) device.
+    Returns (t, l, W): numpy pair indices in the reference's order (fibers in
+    order, targets ascending, system.py:566-586) and the device tensor W
+    (npairs, 3, 3n) of Wnear - Wplain.  Raises InsideFiberError like
+    near_fiber_weights when a target overlaps a fiber.
+    """
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    def ptr(t):
+        return t.data_ptr() if t is not None and t.numel() else None
+
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    dev = geo.X.device
+    nf, n = geo.nf, geo.n
+    nt = targets.shape[0]
+    if nf == 0 or nt == 0:
+        return (np.zeros(0, np.int64), np.zeros(0, np.int64),
+                torch.zeros((0, 3, 3 * n), dtype=torch.float64, device=dev))
+    p = n - 1
+    center = geo.X.mean(dim=1).contiguous()
+    shell = (NEAR_SHELL_FACTOR * geo.L / p).contiguous()
+    bound = ((geo.X - center[:, None, :]).norm(dim=2).amax(dim=1) + shell).contiguous()
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    cap = max(1024, nt // 8)
+    while True:
+        pairs = torch.empty((cap, 2), dtype=torch.int64, device=dev)
+        _native.call("sf_near_search", ptr(targets), ptr(target_groups), nt, ptr(geo.X), nf, n,
+                     ptr(center), ptr(bound), ptr(shell), cap, ptr(pairs), ptr(count), st)
+        found = int(count.item())
+        if found <= cap:
+            break
+        cap = found + 1024
+    pl_np, pt_np = (pairs[:found].cpu().numpy().T if found else (np.zeros(0, np.int64),) * 2)
+    order = np.lexsort((pt_np, pl_np))
+    pl_np, pt_np = pl_np[order], pt_np[order]
+    W = torch.empty((found, 3, 3 * n), dtype=torch.float64, device=dev)
+    if found:
+        from . import spectral
+        nodes, _, _, _ = spectral.grid(p)
+        glx, glw = np.polynomial.legendre.leggauss(10)
+        consts = dict(Cmat=torch.tensor(spectral.coeff_matrix(p), dtype=torch.float64, device=dev),
+                      nodes=torch.tensor(nodes, dtype=torch.float64, device=dev),
+                      gl=torch.tensor(np.concatenate([glx, glw]), dtype=torch.float64, device=dev))
+        pt = torch.as_tensor(pt_np, device=dev)
+        pl = torch.as_tensor(pl_np, device=dev)
+        info = torch.empty(found, dtype=torch.int32, device=dev)
+        _native.call("sf_near_fiber_weights", ptr(pt), ptr(pl), found, ptr(targets), ptr(geo.X),
+                     ptr(geo.s_alpha), ptr(geo.wcc), ptr(consts["Cmat"]), ptr(consts["nodes"]),
+                     ptr(consts["gl"]), ptr(eps), ptr(geo.L), n, float(mu), int(include_doublet),
+                     ptr(W), ptr(info), st)
+        bad = info.cpu().numpy()
+        if np.any(bad == 1):
+            raise InsideFiberError("target overlaps the fiber surface")
+        if np.any(bad == 2):
+            raise RuntimeError("near-field panel refinement overflowed its buffer")
+    return pt_np.astype(np.int64), pl_np.astype(np.int64), W

@@ -76,3 +76,14 @@ def fiber_geometry(X, p):
     anti = C.chebint(values_to_coeffs(s_alpha))
     s = C.chebval(nodes, anti) - C.chebval(-1.0, anti)
     return s, s_alpha, float(s[0]), Xa / s_alpha[:, None]
+
+
+@functools.lru_cache(maxsize=None)
+def coeff_matrix(p):
+    """(n,n) map from nodal values to Chebyshev coefficients (DCT-I, as
+    cheb_transform in spectral.py:37-50), column by column."""
+    n = int(p) + 1
+    eye = np.eye(n)
+    Cm = np.stack([values_to_coeffs(eye[:, j]) for j in range(n)], axis=1)
+    Cm.setflags(write=False)
+    return Cm

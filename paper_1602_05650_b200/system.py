@@ -221,7 +221,7 @@ class InteractionCache:
     (system.py:492-620).  Rebuild whenever any constituent moves."""
 
     def __init__(self, state, include_doublet=True, device=None, mode=SF_MODE_FP64,
-                 near=True, fiber_geometry=None):
+                 near="device", fiber_geometry=None):
         import torch
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         dev = dict(device=self.device)
@@ -292,17 +292,24 @@ class InteractionCache:
             self.ssrc = self.snrm = self.sw = self.sgrp = None
         self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
                         if np_ else None)
-        self.pgrp = torch.as_tensor(np.arange(nf, nf + np_, dtype=np.int64), **dev) if np_ else None
-
         self.trg = torch.as_tensor(self.targets, **f64).contiguous()
         self.tgrp = torch.as_tensor(self.target_groups, **dev)
+        self.pgrp = torch.as_tensor(np.arange(nf, nf + np_, dtype=np.int64), **dev) if np_ else None
 
         self._check_surface_overlaps()
+        # near maps: fibers on the device (default) or the host restatement
         self.near_fiber = []
+        self._near_dev = None
         if near and nf:
             try:
-                self.near_fiber = nearfield.find_fiber_pairs(
-                    state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
+                if near == "host":
+                    self.near_fiber = nearfield.find_fiber_pairs(
+                        state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
+                else:
+                    t, l, W = nearfield.device_fiber_pairs(self.geo, self.eps, self.trg, self.tgrp,
+                                                           state.mu, include_doublet)
+                    self._near_dev = (t, l, W)
+                    self.near_fiber = list(zip(t.tolist(), l.tolist(), W))
             except InsideFiberError as err:
                 raise OverlapError(f"target node overlaps a fiber: {err}") from err
         self.near_surface = []
@@ -334,28 +341,39 @@ class InteractionCache:
         self.near_tensors = {}
         L = 3 * self.n_nodes
         nfs3 = 3 * self.nf * self.n_nodes
-        ents = [(t, l * L, L, W) for t, l, W in self.near_fiber]
-        for t, si, W in self.near_surface:
-            mesh = self.surfaces[si][0]
-            ents.append((t, nfs3 + 3 * self.surface_offsets[si], 3 * mesh.n_nodes, W))
-        if not ents:
+        nfib = len(self.near_fiber)
+        t = np.array([e[0] for e in self.near_fiber] + [e[0] for e in self.near_surface],
+                     dtype=np.int64)
+        if t.size == 0:
             return
-        t = np.array([e[0] for e in ents], dtype=np.int64)
+        xo = np.array([e[1] * L for e in self.near_fiber]
+                      + [nfs3 + 3 * self.surface_offsets[e[1]] for e in self.near_surface],
+                      dtype=np.int64)
+        xl = np.array([L] * nfib + [3 * self.surfaces[e[1]][0].n_nodes for e in self.near_surface],
+                      dtype=np.int64)
         order = np.argsort(t, kind="stable")
-        t = t[order]
-        xo = np.array([ents[i][1] for i in order], dtype=np.int64)
-        xl = np.array([ents[i][2] for i in order], dtype=np.int64)
-        Ws = [np.ascontiguousarray(ents[i][3], dtype=float).reshape(-1) for i in order]
-        wo = np.concatenate([[0], np.cumsum([w.size for w in Ws])[:-1]]).astype(np.int64)
-        rows, starts = np.unique(t, return_index=True)
         dev = dict(device=self.device)
+        f64 = dict(dtype=torch.float64, **dev)
+        if self._near_dev is not None and not self.near_surface:
+            Wall = self._near_dev[2][torch.as_tensor(order, **dev)].reshape(-1)
+            wo = np.arange(t.size, dtype=np.int64) * 3 * L
+        else:
+            pieces = []
+            for i in order:
+                W = (self.near_fiber[i][2] if i < nfib else self.near_surface[i - nfib][2])
+                pieces.append(torch.as_tensor(W, **f64).reshape(-1))
+            sizes = np.array([x.numel() for x in pieces], dtype=np.int64)
+            wo = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+            Wall = torch.cat(pieces)
+        t = t[order]
+        rows, starts = np.unique(t, return_index=True)
         self.near_tensors = dict(
             row_ptr=torch.as_tensor(np.append(starts, t.size).astype(np.int64), **dev),
             rows=torch.as_tensor(rows, **dev),
             w_off=torch.as_tensor(wo, **dev),
-            x_off=torch.as_tensor(xo, **dev),
-            x_len=torch.as_tensor(xl, **dev),
-            W=torch.as_tensor(np.concatenate(Ws), dtype=torch.float64, **dev))
+            x_off=torch.as_tensor(xo[order], **dev),
+            x_len=torch.as_tensor(xl[order], **dev),
+            W=Wall.contiguous())
         self.near_nrows = rows.size
 
     def _layout(self):

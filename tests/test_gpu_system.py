@@ -66,3 +66,43 @@ def test_device_summation_backend(cuda):
     groups = np.array([0, 1], dtype=np.int64)
     with pytest.raises(system.SingularEvaluationError):
         system.DirectSummation().stokeslet(src, groups, np.ones((2, 3)), src[:1], groups[1:], 1.0)
+
+
+def test_device_near_maps_match_reference(cuda):
+    """sf_near_search + sf_near_fiber_weights reproduce the reference's near
+    list (same pairs, same order) and maps (fiber.py:514-575)."""
+    g = golden("c1_near.npz")
+    fibs = [Fiber(X, eps=float(g["eps"]), E=1.0) for X in g["X"]]
+    st = system.SystemState(fibs, mu=float(g["mu"]))
+    cache = system.InteractionCache(st, near="device")
+    got = [(t, l) for t, l, _ in cache.near_fiber]
+    assert got == list(zip(g["near_t"].tolist(), g["near_l"].tolist()))
+    for (_, _, W), Wref in zip(cache.near_fiber, g["near_W"]):
+        W = W.cpu().numpy()
+        assert np.abs(W - Wref).max() <= 1e-10 * np.abs(Wref).max()
+
+
+def test_device_near_maps_detect_overlap(cuda):
+    from paper_1602_05650_b200.fiber import straight_fiber
+    fa = straight_fiber(16, (0, 0, -1.0), (0, 0, 1.0), 2.0)
+    fb = straight_fiber(16, (0.004, 0.0, -1.0), (0, 0, 1.0), 2.0)   # 0.004 < eps L = 0.02
+    st = system.SystemState([fa, fb])
+    with pytest.raises(system.OverlapError):
+        system.InteractionCache(st, near="device")
+
+
+def test_near_fiber_pair_routes_through_near_evaluation(cuda):
+    # test_system.py:176-185: a close parallel pair is evaluated through the
+    # near maps; device and host constructions agree
+    from paper_1602_05650_b200.fiber import straight_fiber
+    fa = straight_fiber(16, (0, 0, -1.0), (0, 0, 1.0), 2.0)
+    fb = straight_fiber(16, (0.06, 0, -1.0), (0, 0, 1.0), 2.0)
+    rng = np.random.default_rng(5)
+    f = [rng.standard_normal((17, 3)), np.zeros((17, 3))]
+    st = system.SystemState([fa, fb])
+    dev = system.complementary_velocities(st, fiber_forces=f,
+                                          cache=system.InteractionCache(st, near="device"))
+    host = system.complementary_velocities(st, fiber_forces=f,
+                                           cache=system.InteractionCache(st, near="host"))
+    assert len(system.InteractionCache(st).near_fiber) > 0
+    assert rel_l2(dev.fibers[1], host.fibers[1]) < 1e-12
