@@ -315,3 +315,19 @@ def cloud_state(name="c3_scaled", seed=0, f0=1.0, direction=(0.0, 0.0, -1.0), **
     cl = make(name, seed=seed, **overrides)
     fibs = [Fiber(X, eps=cl.eps, E=cl.E) for X in cl.X]
     return SystemState(fibs, force_models=[UniformBodyForce(f0, direction)])
+
+
+def confined_aster(n_fibers=2048, p=31, centrosome_radius=0.3, centrosome_center=(0.5, 0.0, 0.0),
+                   centrosome_res=(8, 8), periphery_radius=2.0, periphery_res=(40, 64),
+                   standoff=1.3, eps=1e-2, E=1.0, motor_force=1.0):
+    """BASELINE config 4: fibers clamped radially (reference Fibonacci layout,
+    system.py:428-443) to a centrosome sphere inside a confining sphere.  The
+    icosphere of the baseline is not expressible in the reference; the
+    (40,64)-patch sphere has 40,960 nodes."""
+    from . import body
+    st = aster(n_fibers=n_fibers, p=p, radius=centrosome_radius, standoff=standoff,
+               center=centrosome_center, eps=eps, E=E, mesh_res=centrosome_res,
+               motor_force=motor_force, layout="fibonacci")
+    per = body.Periphery(body.make_surface(body.sphere_shape(periphery_radius), periphery_res))
+    from .system import SystemState
+    return SystemState(st.fibers, st.particles, per)

@@ -845,13 +845,13 @@ constexpr int kTargetsPerCta = kNT * kTB;
 
 // Split factor from (nt, ns) only: aim for >= 16384 (target block x source
 // chunk) work units so the last wave is a small fraction of the grid, while
-// keeping every chunk >= 32 tiles.
+// keeping every chunk >= 4 tiles.
 int choose_split(int64_t nt, int64_t ns) {
     const int64_t blocks = (nt + kTargetsPerCta - 1) / kTargetsPerCta;
     int64_t s = (16384 + blocks - 1) / blocks;
-    const int64_t max_s = ns / (32 * kTS);
+    const int64_t max_s = ns / (4 * kTS);
     if (s > max_s) s = max_s;
-    if (s > 64) s = 64;
+    if (s > 256) s = 256;
     return s < 1 ? 1 : (int)s;
 }
 

@@ -166,29 +166,32 @@ __global__ void end_wrench_kernel(sf_fiber_sys S, const double *__restrict__ u,
     }
 }
 
-// Sum the per-fiber wrenches per particle in fiber order (+ F_ext, L_ext).
+// Sum the per-fiber wrenches per particle (+ F_ext, L_ext): one CTA per
+// particle, each thread sums a fixed strided subset of fibers in order, then
+// a fixed-order tree — deterministic.
 __global__ void wrench_reduce_kernel(sf_fiber_sys S, const double *__restrict__ wf,
                                      const double *__restrict__ ext, int constants,
                                      double *__restrict__ wout) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= S.np) return;
-    double F[3] = {0, 0, 0}, L[3] = {0, 0, 0};
-    for (int64_t m = 0; m < S.nf; ++m) {
+    __shared__ double red[6][32];
+    const int p = blockIdx.x;
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t m = threadIdx.x; m < S.nf; m += blockDim.x) {
         if (S.bc_body[m] != p || S.bc_kind[2 * m + 1] != BC_CLAMPED) continue;
-        for (int a = 0; a < 3; ++a) {
-            F[a] += wf[6 * m + a];
-            L[a] += wf[6 * m + 3 + a];
-        }
+        for (int a = 0; a < 6; ++a) v[a] += wf[6 * m + a];
     }
-    if (constants && ext) {
-        for (int a = 0; a < 3; ++a) {
-            F[a] = F[a] + ext[6 * p + a];
-            L[a] = L[a] + ext[6 * p + 3 + a];
+    for (int a = 0; a < 6; ++a) v[a] = warp_sum(v[a]);
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 6; ++a) red[a][threadIdx.x >> 5] = v[a];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double F[6];
+        for (int a = 0; a < 6; ++a) {
+            double s = 0.0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[a][k];
+            F[a] = s;
         }
-    }
-    for (int a = 0; a < 3; ++a) {
-        wout[6 * p + a] = F[a];
-        wout[6 * p + 3 + a] = L[a];
+        for (int a = 0; a < 6; ++a)
+            wout[6 * p + a] = (constants && ext) ? F[a] + ext[6 * p + a] : F[a];
     }
 }
 
@@ -873,7 +876,7 @@ int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *e
         int rc = check_launch("end_wrench_kernel");
         if (rc) return rc;
     }
-    wrench_reduce_kernel<<<grid1d(S->np, 32), 32, 0, st>>>(*S, work, ext, constants, wout);
+    wrench_reduce_kernel<<<(unsigned)S->np, 256, 0, st>>>(*S, work, ext, constants, wout);
     return check_launch("wrench_reduce_kernel");
 }
 

@@ -368,21 +368,29 @@ __global__ void sym_pack_kernel(const double *__restrict__ x, const int64_t *__r
     }
 }
 
-int sym_unit_size(int64_t group_size) {
-    // units of ~2048 points: a multiple of the 32-point slab, and of the
-    // fiber size when that keeps them near 2048 (units then align to fibers,
-    // so off-diagonal unit pairs never share a group)
+int sym_unit_size(int64_t N, int64_t group_size) {
+    // units: a multiple of the 32-point slab (and of the fiber size when that
+    // keeps them near the target, so units align to fibers), at most 2048
+    // points, and small enough that the G(G+1)/2 unit-pair tasks fill the GPU
+    // several times over (G >= 48 -> >= 1176 tasks) for mid-size systems
     const char *e = getenv("SF_SYM_UNIT");
-    int target = e ? atoi(e) : 2048;
-    target = (target / 32) * 32;
-    if (target < 64) target = 64;
+    int64_t target = e ? atoi(e) : 2048;
+    if (!e) {
+        const int64_t fill = N / 48;
+        if (fill < target) target = fill;
+        if (target < 256) target = 256;
+    }
+    // multiple of the 128-point i-sub-block (4 per lane x 32 lanes) so no
+    // sub-block runs part-empty, and of the fiber size when possible
+    target = (target / 128) * 128;
+    if (target < 128) target = 128;
     if (group_size > 0) {
-        int64_t a = group_size, b = 32;
+        int64_t a = group_size, b = 128;
         while (b) { const int64_t t = a % b; a = b; b = t; }
-        const int64_t l = group_size / a * 32;  // lcm(group_size, 32)
+        const int64_t l = group_size / a * 128;  // lcm(group_size, 128)
         if (l <= target) return (int)((target / l) * l);
     }
-    return target;
+    return (int)target;
 }
 
 // mode SF_MODE_FP64 picks the symmetric evaluation for large enough blocks;
@@ -401,7 +409,7 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
-    const int M = sym_unit_size(group_size);
+    const int M = sym_unit_size(N, group_size);
     const int G = (int)((N + M - 1) / M);
     SymSrc *packed = (SymSrc *)ws.get(3, sizeof(SymSrc) * (size_t)N, st);
     SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)((N + 31) / 32 + 1), st);

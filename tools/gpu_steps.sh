@@ -1,2 +1,1 @@
-timeout 900 python tools/step_perf.py --config c3_scaled --steps 2 2>&1 | tail -3
-timeout 900 python tools/step_perf.py --config c3 --steps 2 2>&1 | tail -3
+timeout 1200 python tools/step_perf.py --config c4 --steps 2 --tol 1e-8 2>&1 | tail -3
