@@ -603,6 +603,164 @@ __global__ void block_lu_smem_kernel(double *__restrict__ A, int mdim, double *_
     if (threadIdx.x == 0) info[b] = s_bad;
 }
 
+// Blocked variant for blocks that do not fit in shared memory (m <= 256, i.e.
+// fibers of up to 64 nodes): right-looking LU with 32-column panels, the
+// matrix kept in global memory (L2 resident: one 512 KB block per CTA),
+// panel factored in shared memory with partial pivoting (row swaps applied
+// to the full rows as LAPACK getrf does), triangular solve for U12 and a
+// register-tiled update of the trailing block.  Factors end column-major.
+constexpr int kLuNB = 32;
+__global__ void __launch_bounds__(256) block_lu_global_kernel(double *__restrict__ A, int m,
+                                                               double *__restrict__ rsc,
+                                                               double *__restrict__ csc,
+                                                               int *__restrict__ piv,
+                                                               int *__restrict__ info) {
+    extern __shared__ double sh[];
+    double *panel = sh;                 // (m x kLuNB)
+    double *u12 = sh + (size_t)m * kLuNB;   // (kLuNB x m)
+    __shared__ int s_piv;
+    __shared__ int s_bad;
+    const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    double *Ab = A + (int64_t)m * m * b;
+    double *r = rsc + (int64_t)m * b, *c = csc + (int64_t)m * b;
+    int *pv = piv + (int64_t)m * b;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    for (int i = tid; i < m; i += nt) {
+        double mx = 0.0;
+        for (int j = 0; j < m; ++j) {
+            const double v = Ab[(int64_t)i * m + j];
+            if (!isfinite(v)) s_bad = 1;
+            mx = fmax(mx, fabs(v));
+        }
+        r[i] = mx;
+        if (mx == 0.0 && !s_bad) s_bad = 2;
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)m * m; e += nt) Ab[e] = Ab[e] / r[e / m];
+    __syncthreads();
+    for (int j = tid; j < m; j += nt) {
+        double mx = 0.0;
+        for (int i = 0; i < m; ++i) mx = fmax(mx, fabs(Ab[(int64_t)i * m + j]));
+        c[j] = mx;
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)m * m; e += nt) Ab[e] = Ab[e] / c[e % m];
+    __syncthreads();
+    for (int kb = 0; kb < m; kb += kLuNB) {
+        const int nb = min(kLuNB, m - kb), rows = m - kb, rest = m - kb - nb;
+        for (int e = tid; e < rows * nb; e += nt) {
+            const int i = e / nb, j = e - i * nb;
+            panel[i * kLuNB + j] = Ab[(int64_t)(kb + i) * m + kb + j];
+        }
+        __syncthreads();
+        for (int k = 0; k < nb; ++k) {
+            if (tid < 32) {
+                double best = -1.0;
+                int bi = k;
+                for (int i = k + tid; i < rows; i += 32) {
+                    const double v = fabs(panel[i * kLuNB + k]);
+                    if (v > best) { best = v; bi = i; }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+                }
+                if (tid == 0) {
+                    s_piv = bi;
+                    pv[kb + k] = kb + bi;
+                    if (best == 0.0 && !s_bad) s_bad = 3;
+                }
+            }
+            __syncthreads();
+            const int p = s_piv;
+            if (p != k) {
+                for (int j = tid; j < nb; j += nt) {
+                    const double t = panel[k * kLuNB + j];
+                    panel[k * kLuNB + j] = panel[p * kLuNB + j];
+                    panel[p * kLuNB + j] = t;
+                }
+                // the same swap on the rows outside the panel columns
+                for (int j = tid; j < m - nb; j += nt) {
+                    const int col = j < kb ? j : j + nb;
+                    double *ra = Ab + (int64_t)(kb + k) * m + col;
+                    double *rb = Ab + (int64_t)(kb + p) * m + col;
+                    const double t = *ra;
+                    *ra = *rb;
+                    *rb = t;
+                }
+            }
+            __syncthreads();
+            const double d = panel[k * kLuNB + k];
+            for (int i = k + 1 + tid; i < rows; i += nt)
+                panel[i * kLuNB + k] = d != 0.0 ? panel[i * kLuNB + k] / d : 0.0;
+            __syncthreads();
+            const int rr = rows - k - 1, cc = nb - k - 1;
+            for (int e = tid; e < rr * cc; e += nt) {
+                const int i = k + 1 + e / cc, j = k + 1 + e % cc;
+                panel[i * kLuNB + j] = fma(-panel[i * kLuNB + k], panel[k * kLuNB + j],
+                                           panel[i * kLuNB + j]);
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < rows * nb; e += nt) {
+            const int i = e / nb, j = e - i * nb;
+            Ab[(int64_t)(kb + i) * m + kb + j] = panel[i * kLuNB + j];
+        }
+        if (rest > 0) {
+            // U12 = L11^-1 A12 (unit lower), one column per thread
+            for (int j = tid; j < rest; j += nt) {
+                double col[kLuNB];
+                for (int i = 0; i < nb; ++i) col[i] = Ab[(int64_t)(kb + i) * m + kb + nb + j];
+                for (int i = 0; i < nb; ++i) {
+                    double v = col[i];
+                    for (int q = 0; q < i; ++q) v = fma(-panel[i * kLuNB + q], col[q], v);
+                    col[i] = v;
+                }
+                for (int i = 0; i < nb; ++i) {
+                    Ab[(int64_t)(kb + i) * m + kb + nb + j] = col[i];
+                    u12[i * m + j] = col[i];
+                }
+            }
+            __syncthreads();
+            // A22 -= L21 U12, 4x4 register tiles
+            const int tr = (rest + 3) / 4, ntile = tr * tr;
+            for (int tix = tid; tix < ntile; tix += nt) {
+                const int i0 = (tix / tr) * 4, j0 = (tix % tr) * 4;
+                double acc[4][4];
+                for (int a = 0; a < 4; ++a)
+                    for (int q = 0; q < 4; ++q) acc[a][q] = 0.0;
+                for (int k = 0; k < nb; ++k) {
+                    double lv[4], uv[4];
+                    for (int a = 0; a < 4; ++a)
+                        lv[a] = (i0 + a < rest) ? panel[(nb + i0 + a) * kLuNB + k] : 0.0;
+                    for (int q = 0; q < 4; ++q) uv[q] = (j0 + q < rest) ? u12[k * m + j0 + q] : 0.0;
+                    for (int a = 0; a < 4; ++a)
+                        for (int q = 0; q < 4; ++q) acc[a][q] = fma(lv[a], uv[q], acc[a][q]);
+                }
+                for (int a = 0; a < 4; ++a) {
+                    if (i0 + a >= rest) break;
+                    double *row = Ab + (int64_t)(kb + nb + i0 + a) * m + kb + nb;
+                    for (int q = 0; q < 4; ++q)
+                        if (j0 + q < rest) row[j0 + q] -= acc[a][q];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // row-major -> column-major in place
+    for (int64_t e = tid; e < (int64_t)m * m; e += nt) {
+        const int i = (int)(e / m), j = (int)(e - (int64_t)i * m);
+        if (i < j) {
+            const double t = Ab[(int64_t)i * m + j];
+            Ab[(int64_t)i * m + j] = Ab[(int64_t)j * m + i];
+            Ab[(int64_t)j * m + i] = t;
+        }
+    }
+    if (tid == 0) info[b] = s_bad;
+}
+
 // x_block = (LU \ (v_block / r)) / c for every fiber block, and v / diag on
 // every other row (solver.py:425-429).  LU column-major, piv 0-based row
 // swaps applied in order (LAPACK getrs).
@@ -907,8 +1065,15 @@ int sf_block_lu(double *A, int64_t nb, int64_t m, double *r, double *c, int *piv
                 void *stream) {
     if (nb <= 0) return SF_OK;
     const size_t smem = sizeof(double) * m * m;
-    if (smem > 227 * 1024) return set_error(SF_EINVAL, "block of %lld rows exceeds shared memory",
-                                            (long long)m);
+    if (smem > 200 * 1024) {
+        if (m > 256) return set_error(SF_EINVAL, "blocks larger than 256 rows are not supported");
+        const size_t sm2 = sizeof(double) * 2 * kLuNB * m;
+        int rc2 = set_smem((const void *)block_lu_global_kernel, sm2);
+        if (rc2) return rc2;
+        block_lu_global_kernel<<<(unsigned)nb, 256, sm2, (cudaStream_t)stream>>>(A, (int)m, r, c,
+                                                                               piv, info);
+        return check_launch("block_lu_global_kernel");
+    }
     int rc = set_smem((const void *)block_lu_smem_kernel, smem);
     if (rc) return rc;
     block_lu_smem_kernel<<<(unsigned)nb, 256, smem, (cudaStream_t)stream>>>(A, (int)m, r, c, piv,

@@ -341,13 +341,14 @@ class Preconditioner:
             self.c = torch.empty((nf, m), **f64)
             self.piv = torch.empty((nf, m), dtype=torch.int32, device=op.device)
             info = torch.empty(nf, dtype=torch.int32, device=op.device)
-            if m * m * 8 <= 227 * 1024:
+            if m <= 256:
+                # shared-memory LU for m <= 160, blocked global-memory LU up to 256
                 _native.call("sf_block_lu", _ptr(A), nf, m, _ptr(self.r), _ptr(self.c),
                              _ptr(self.piv), _ptr(info), st)
                 self.LU = A
             else:
-                # blocks too large for one CTA's shared memory: equilibrate on the
-                # device and factor with the batched library getrf
+                # larger blocks: equilibrate on the device and factor with the
+                # batched library getrf (outside every BASELINE config)
                 self.r = A.abs().amax(dim=2)
                 if bool((self.r == 0).any()):
                     raise FactorizationError("fiber self-block is singular")
