@@ -155,6 +155,17 @@ int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf, int64_t n
                       const double *near_W, const double *f, double *out_nl,
                       double *out_self, int64_t *bad, void *stream);
 
+/* Symmetric fiber x fiber sum, multi-GPU form: rank `rank` of `world`
+ * evaluates its contiguous share of the unit-pair tasks (both directions) and
+ * writes its contribution to EVERY point into out (N,3); summing out over
+ * ranks (NCCL reduce-scatter to the target blocks) gives the Stokeslet +
+ * doublet sum.  world = 1 equals the single-GPU symmetric path.  bad counts
+ * this rank's skipped ordered pairs. */
+int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
+                             int64_t group_size, const double *f, const double *w,
+                             const double *dcoef, double pref, int rank, int world,
+                             double *out, int64_t *bad, void *stream);
+
 /* Source-split factor the pair kernels use for nt targets x ns sources (a
  * pure function of the sizes; each target's sum is split into this many
  * ordered chunks).  Used to count kernel launches. */

@@ -260,6 +260,17 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
 
 extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt, ns); }
 
+extern "C" int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
+                                        int64_t group_size, const double *f, const double *w,
+                                        const double *dcoef, double pref, int rank, int world,
+                                        double *out, int64_t *bad, void *stream) {
+    SF_REQUIRE(N >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sizes");
+    SF_REQUIRE(N == 0 || (X && f && out), "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    return pairs_sbt_symmetric_shard(X, grp, N, group_size, f, w, dcoef, pref, rank, world, out,
+                                     bad, 0, st, workspace_for(st));
+}
+
 // ------------------------------------------------------------ host entries ----
 namespace {
 struct StageLock {

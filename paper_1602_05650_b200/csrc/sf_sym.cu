@@ -50,7 +50,8 @@ struct SymArgs {
     int64_t N;
     int M;
     int G;
-    int64_t ntasks;
+    int64_t ntasks;   // tasks of this launch
+    int64_t task0;    // first task (rank share of the G(G+1)/2 unit pairs)
     double *part;  // (G, N, 3)
     unsigned long long *bad;
 };
@@ -167,8 +168,8 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     __shared__ double ui_s[4][kI][3];             // per-warp owner partials
     __shared__ double2 js_xy[4][32], js_zf[4][32], js_ff[4][32], js_cc[4][32];  // j slabs
     __shared__ int js_g[4][32];
-    const int64_t t = blockIdx.x;
-    if (t >= a.ntasks) return;
+    if ((int64_t)blockIdx.x >= a.ntasks) return;
+    const int64_t t = a.task0 + blockIdx.x;
     int g, h;
     task_units(t, a.G, g, h);
     const bool both = g != h;
@@ -406,6 +407,24 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
                         const double *f, const double *w, const double *dcoef, double pref,
                         double *out, int64_t *bad, int accumulate, cudaStream_t st,
                         Workspace &ws) {
+    return pairs_sbt_symmetric_shard(x, grp, N, group_size, f, w, dcoef, pref, 0, 1, out, bad,
+                                     accumulate, st, ws);
+}
+
+// The unit-pair tasks of rank `rank` of `world`: contiguous equal-count
+// ranges of the G(G+1)/2 tasks.  out receives this rank's contribution to
+// EVERY point (slots of other ranks' tasks are zero); summing `out` over
+// ranks (reduce-scatter) gives the full sum.
+int64_t sym_task_range(int64_t ntasks, int rank, int world, int64_t *count) {
+    const int64_t b = ntasks * rank / world, e = ntasks * (rank + 1) / world;
+    *count = e - b;
+    return b;
+}
+
+int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
+                              const double *f, const double *w, const double *dcoef, double pref,
+                              int rank, int world, double *out, int64_t *bad, int accumulate,
+                              cudaStream_t st, Workspace &ws) {
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
@@ -426,8 +445,12 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
     a.N = N;
     a.M = M;
     a.G = G;
-    a.ntasks = (int64_t)G * (G + 1) / 2;
+    const int64_t all_tasks = (int64_t)G * (G + 1) / 2;
+    a.task0 = sym_task_range(all_tasks, rank, world, &a.ntasks);
     a.part = part;
+    if (world > 1 &&
+        cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)N * G, st) != cudaSuccess)
+        return check_launch("memset");
     a.bad = (unsigned long long *)bad;
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
@@ -438,7 +461,7 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        kern<<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
+        if (a.ntasks > 0) kern<<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
         return SF_OK;
     };
     int lrc;
@@ -457,6 +480,7 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
     }
     if (lrc) return lrc;
     int rc = check_launch("sym_task_kernel");
+    if (a.ntasks == 0 && world == 1) return rc;
     if (rc) return rc;
     sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(part, G, N, pref, out,
                                                                       accumulate);

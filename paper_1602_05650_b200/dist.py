@@ -50,9 +50,39 @@ class ShardedHIOperator:
             dist.all_gather(parts, self._f_pad, group=self.group)
         return self._f_full[:nf]
 
-    def apply(self, f_local, **kw):
-        """One matvec of the HI operator on this rank's target block."""
-        return self.op.apply(self.gather_sources(f_local), **kw)
+    def apply(self, f_local, out_nl=None, out_self=None, self_terms=True):
+        """One matvec of the HI operator on this rank's target block.
+
+        Symmetric path (FP64, >= 8192 points): every rank evaluates its share
+        of the unit-pair tasks for all points, a reduce-scatter sums the
+        partials onto the target blocks, then near maps and self terms run
+        locally.  Otherwise each rank evaluates its targets against all
+        sources (direct path)."""
+        f_full = self.gather_sources(f_local)
+        op = self.op
+        if getattr(op, "symmetric_shard", False):
+            part = op.symmetric_partial(f_full)
+            u_own = self.reduce_scatter_points(part, out_nl)
+            return op.finish_own(u_own, f_full, out_self=out_self, self_terms=self_terms)
+        return op.apply(f_full, out_nl=out_nl, out_self=out_self, self_terms=self_terms)
+
+    def reduce_scatter_points(self, part, out=None):
+        """Sum (N,3) per-rank partials over ranks; return this rank's (Nown,3)."""
+        n = self.op.n
+        rows = self.per * n
+        full = torch.zeros((self.world * rows, 3), dtype=part.dtype, device=part.device)
+        full[: part.shape[0]].copy_(part)
+        mine = torch.empty((rows, 3), dtype=part.dtype, device=part.device)
+        if dist.get_backend(self.group) == "nccl":
+            dist.reduce_scatter_tensor(mine, full, group=self.group)
+        else:
+            dist.all_reduce(full, group=self.group)
+            mine.copy_(full[self.rank * rows:(self.rank + 1) * rows])
+        nown = self.op.Nown
+        if out is None:
+            return mine[:nown].contiguous()
+        out.copy_(mine[:nown])
+        return out
 
     def gather_targets(self, u_local):
         """All-gather per-rank (Nown,3) outputs into the global (N,3) array."""

@@ -155,11 +155,51 @@ class FiberHIOperator:
                 and os.environ.get("SF_SYMMETRIC", "1") != "0")
 
     @property
+    def symmetric_shard(self):
+        """Multi-GPU form of the symmetric evaluation: this rank computes its
+        share of the unit-pair tasks for ALL points; the dist layer sums the
+        ranks' partials with a reduce-scatter."""
+        import os
+        return (self.mode == SF_MODE_FP64 and self.world > 1 and self.N >= 8192
+                and os.environ.get("SF_SYMMETRIC", "1") != "0")
+
+    def symmetric_partial(self, f, out=None, rank=None, world=None):
+        """(N,3) contribution of this rank's unit-pair tasks to every point."""
+        import torch
+        f = torch.as_tensor(f, dtype=torch.float64, device=self.device).contiguous()
+        if out is None:
+            out = torch.empty((self.N, 3), dtype=torch.float64, device=self.device)
+        _native.call("sf_sbt_symmetric_partial", _ptr(self.X), _ptr(self.groups), self.N, self.n,
+                     _ptr(f), _ptr(self.wnode), _ptr(self.dcoef), self.pref,
+                     self.rank if rank is None else rank, self.world if world is None else world,
+                     _ptr(out), _ptr(self.bad), _stream())
+        return out
+
+    def finish_own(self, u_own, f, out_self=None, self_terms=True):
+        """Near corrections and self terms of this rank's targets, after the
+        pair sums of every rank were summed into u_own (Nown,3)."""
+        import torch
+        f = torch.as_tensor(f, dtype=torch.float64, device=self.device).contiguous()
+        nm = self.near
+        st = _stream()
+        if nm.nrows:
+            _native.call("sf_near_apply", _ptr(nm.row_ptr), _ptr(nm.rows), nm.nrows, _ptr(nm.w_off),
+                         _ptr(nm.x_off), _ptr(nm.x_len), _ptr(nm.W), _ptr(f), _ptr(u_own), st)
+        if self_terms:
+            if out_self is None:
+                out_self = torch.empty((self.Nown, 3), dtype=torch.float64, device=self.device)
+            o = self.f0
+            _native.call("sf_self_apply_batched", _ptr(self.K), _ptr(self.tang[o:]),
+                         _ptr(self.c_log[o:]), self.c_two, _ptr(f[o * self.n:]), self.nown, self.n,
+                         0, _ptr(out_self), st)
+        return u_own, (out_self if self_terms else None)
+
+    @property
     def launches_per_apply(self):
         """Kernels one apply launches: symmetric path = pack, slab meta, task
         kernel, ordered reduce; direct path = pack, tile meta, pair kernel
         (+ ordered split reduce); then near (if any) and self terms."""
-        if self.symmetric:
+        if self.symmetric or self.symmetric_shard:
             pair = 4
         else:
             split = _native.load().sf_pair_split(self.Nown, self.N)

@@ -222,7 +222,19 @@ class InteractionCache:
 
     def __init__(self, state, include_doublet=True, device=None, mode=SF_MODE_FP64,
                  near="device", fiber_geometry=None):
+        import os
+        import time
+
         import torch
+        _dbg = os.environ.get("SF_DEBUG_TIMING")
+        _t = [time.perf_counter()]
+
+        def _lap(label):
+            if _dbg:
+                torch.cuda.synchronize()
+                now = time.perf_counter()
+                print(f"  cache {label:28s} {1e3 * (now - _t[0]):9.2f} ms", flush=True)
+                _t[0] = now
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         dev = dict(device=self.device)
         f64 = dict(dtype=torch.float64, **dev)
@@ -259,6 +271,7 @@ class InteractionCache:
         self.target_groups = np.concatenate(groups) if groups else np.zeros(0, np.int64)
         self.n_targets = self.targets.shape[0]
 
+        _lap("targets")
         # fibers: geometry, weights, doublet coefficients (device)
         if fiber_geometry is None:
             ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in state.fibers]
@@ -296,7 +309,9 @@ class InteractionCache:
         self.tgrp = torch.as_tensor(self.target_groups, **dev)
         self.pgrp = torch.as_tensor(np.arange(nf, nf + np_, dtype=np.int64), **dev) if np_ else None
 
+        _lap("geometry + surfaces")
         self._check_surface_overlaps()
+        _lap("overlap checks")
         # near maps: fibers on the device (default) or the host restatement
         self.near_fiber = []
         self._near_dev = None
@@ -312,11 +327,14 @@ class InteractionCache:
                     self.near_fiber = list(zip(t.tolist(), l.tolist(), W))
             except InsideFiberError as err:
                 raise OverlapError(f"target node overlaps a fiber: {err}") from err
+        _lap("near fiber maps")
         self.near_surface = []
         if near and self.surfaces:
             self.near_surface = nearfield.find_surface_pairs(
                 self.surfaces, self.targets, self.target_groups, state.mu)
+        _lap("near surface maps")
         self._build_near_map()
+        _lap("near CSR")
         self.mode = int(mode)
         self._layout()
         self.bad = torch.zeros(3, dtype=torch.int64, **dev)

@@ -43,6 +43,59 @@ class OracleShardOperator:
         return torch.as_tensor(u1 + u2), None
 
 
+class SymmetricShardOperator(OracleShardOperator):
+    """Stand-in for the symmetric multi-GPU form: each rank returns a partial
+    for EVERY point (here: the full oracle sum split by a fixed per-rank
+    weight) and the dist layer must reduce-scatter them."""
+
+    symmetric_shard = True
+
+    def __init__(self, X, eps, rank, world):
+        super().__init__(X, eps, rank, world)
+        self.rank, self.world = rank, world
+        self.Nown = self.nown * self.n
+
+    def symmetric_partial(self, f_full):
+        full = OracleShardOperator(self.X, self.eps, 0, 1).apply(f_full)[0]
+        return full * (0.25 if self.rank == 0 else 0.75 / (self.world - 1))
+
+    def finish_own(self, u_own, f_full, out_self=None, self_terms=True):
+        return u_own, None
+
+
+def _sym_worker(rank, world, port, X, eps, F, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        op = SymmetricShardOperator(X, eps, rank, world)
+        sop = ShardedHIOperator(op)
+        u_own, _ = sop.apply(torch.as_tensor(F[op.f0:op.f0 + op.nown]))
+        full = sop.gather_targets(u_own)
+        if rank == 0:
+            q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_symmetric_reduce_scatter():
+    cloud = configs.fiber_cloud(9, 15, eps=1e-2, region="cube", size=1.5, seed=5,
+                                clear=configs.clean_clear(15), check="node")
+    F = configs.forces(cloud, seed=3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, 2, port, cloud.X, cloud.eps, F, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref, _ = ops.fiber_operator(cloud.X, F, cloud.eps)
+    assert ops.rel_l2(got, ref) < 1e-14
+
+
 def _worker(rank, world, port, X, eps, F, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)

@@ -206,3 +206,18 @@ def test_symmetric_counts_coincident_pairs(cuda):
     assert int(op.bad.item()) == 2
     with pytest.raises(kernels.SingularEvaluationError):
         op.check_bad()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_symmetric_task_shards_sum_to_single_gpu(cuda, world):
+    """Multi-GPU symmetric form emulated on one GPU: the ranks' task shares,
+    each contributing to every point, sum to the single-GPU result."""
+    import torch
+    from paper_1602_05650_b200._native import SF_MODE_FP64
+    cl, F = _cloud_operator_inputs(200, 64)
+    op = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP64)
+    one, _ = op.apply(F, self_terms=False)
+    total = torch.zeros_like(one)
+    for r in range(world):
+        total += op.symmetric_partial(F, rank=r, world=world)
+    assert rel(total.cpu().numpy(), one.cpu().numpy()) < 1e-14
