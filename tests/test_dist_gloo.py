@@ -31,7 +31,7 @@ class OracleShardOperator:
         self.w = np.concatenate([g["weights"] for g in geos])
         self.c = np.repeat([(eps * g["L"]) ** 2 / 2.0 for g in geos], self.n)
 
-    def apply(self, f_full):
+    def apply(self, f_full, out_nl=None, out_self=None, self_terms=True):
         f = f_full.numpy().reshape(-1, 3)
         src = self.X.reshape(-1, 3)
         grp = np.repeat(np.arange(self.nf, dtype=np.int64), self.n)
