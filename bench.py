@@ -275,6 +275,13 @@ def run_ours(args, rank, world, local_rank):
     pair_ms = r_s.elapsed_time(r_e) / reps
     peak_flops, _ = kernels.dfma_peak(1 << 15)
     achieved = op.pairs_per_apply * FLOPS_PER_PAIR / (pair_ms * 1e-3)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_sym_c5_metrics.json")
+    if args.config == "c5" and world == 1 and op.symmetric and os.path.exists(prof):
+        m = json.load(open(prof))
+        gb = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
+        traffic = sum(float(m[k][1].replace(",", "")) * gb.get(m[k][0], 1.0)
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
 
     steps = None
     if args.step_config and world == 1:
@@ -305,7 +312,11 @@ def run_ours(args, rank, world, local_rank):
                        "steps_per_s": 1e3 / ms_step},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_flops / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / peak_flops, "traffic": None,
+                         "frac": achieved / peak_flops, "traffic": traffic,
+                         "traffic_note": "DRAM bytes per launch of the symmetric kernel from "
+                                         "profiles/r01_ncu_sym_kernel_notes.md: the unit-pair "
+                                         "partial buffer (written once, read once); algorithmic "
+                                         "inputs are 80 MB",
                          "kernel": "pack + slab meta + sym_task_kernel (symmetric fiber-fiber "
                                    "pairs) + ordered partial reduce",
                          "flops_per_pair": FLOPS_PER_PAIR,
