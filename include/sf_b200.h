@@ -41,7 +41,8 @@ enum {
     SF_MODE_FP64 = 0,        /* FP64 compute and accumulation; where targets == sources
                                 (the fiber x fiber block, >= 8192 points) each pair's
                                 geometry is evaluated once for both directions */
-    SF_MODE_FP32C = 1,       /* FP32 pair arithmetic, FP64 accumulation per tile */
+    SF_MODE_FP32C = 1,       /* FP32 pair arithmetic, FP64 accumulation per tile / slab
+                                (symmetric where SF_MODE_FP64 would be) */
     SF_MODE_FP64_DIRECT = 2  /* FP64, every target summed over sources in index
                                 order (the reference's loop order) */
 };
@@ -163,7 +164,7 @@ int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf, int64_t n
  * this rank's skipped ordered pairs. */
 int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
                              int64_t group_size, const double *f, const double *w,
-                             const double *dcoef, double pref, int rank, int world,
+                             const double *dcoef, double pref, int mode, int rank, int world,
                              double *out, int64_t *bad, void *stream);
 
 /* Source-split factor the pair kernels use for nt targets x ns sources (a

@@ -50,7 +50,7 @@ _SIGNATURES = {
     "sf_fiber_hi_apply": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _D, _I, _P, _P, _P, _D, _P,
                           _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sf_pair_split": [_I64, _I64],
-    "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _P, _P, _P],
+    "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
     "sf_near_search": [_P, _P, _I64, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P],

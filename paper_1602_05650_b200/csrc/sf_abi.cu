@@ -241,7 +241,7 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
     int rc;
     if (t_fiber0 == 0 && t_nfibers == nf && use_symmetric(mode, N))
         rc = pairs_sbt_symmetric(X, grp, N, n, f, wnode, dcoef, pref, out_nl, bad, 0, st,
-                                 workspace_for(st));
+                                 workspace_for(st), mode);
     else
         rc = pairs_sbt_weighted(X + 3 * t0, grp ? grp + t0 : nullptr, nt, X, grp, N, f, wnode,
                                 dcoef, pref, mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64,
@@ -262,13 +262,14 @@ extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt,
 
 extern "C" int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
                                         int64_t group_size, const double *f, const double *w,
-                                        const double *dcoef, double pref, int rank, int world,
-                                        double *out, int64_t *bad, void *stream) {
+                                        const double *dcoef, double pref, int mode, int rank,
+                                        int world, double *out, int64_t *bad, void *stream) {
     SF_REQUIRE(N >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sizes");
     SF_REQUIRE(N == 0 || (X && f && out), "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     return pairs_sbt_symmetric_shard(X, grp, N, group_size, f, w, dcoef, pref, rank, world, out,
-                                     bad, 0, st, workspace_for(st));
+                                     bad, 0, st, workspace_for(st),
+                                     mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64);
 }
 
 // ------------------------------------------------------------ host entries ----

@@ -59,12 +59,12 @@ int pair_split(int64_t nt, int64_t ns);
 int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                         const double *f, const double *w, const double *dcoef, double pref,
                         double *out, int64_t *bad, int accumulate, cudaStream_t st,
-                        Workspace &ws);
+                        Workspace &ws, int mode = SF_MODE_FP64);
 bool use_symmetric(int mode, int64_t N);
 int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
-                              cudaStream_t st, Workspace &ws);
+                              cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,

@@ -99,7 +99,7 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
             if (!bad_sym) return SF_ENOMEM;
         }
         rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
-                                 L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws);
+                                 L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws, L->mode);
         if (rc) return rc;
         if (bad) {
             rc = add_counter(bad_f, bad_sym, st);

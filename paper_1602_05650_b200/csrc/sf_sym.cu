@@ -340,6 +340,266 @@ __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
     }
 }
 
+
+// ------------------------------------------------ FP32-compute variant ----
+// Same task structure; pair arithmetic in FP32 with positions split into
+// float hi + lo parts (r = (x_hi - y_hi) + (x_lo - y_lo) keeps FP32 relative
+// accuracy in r), FP32 sums over one 32-point slab, FP64 accumulation across
+// slabs (owner sums in registers, transposed sums in shared memory).
+// Record floats: xh yh zh xl yl zl fx fy fz c c3, int g at the record's end.
+struct PDataF {
+    float xh, yh, zh, xl, yl, zl, fx, fy, fz, c, c3;
+    int g;
+};
+
+__device__ __forceinline__ PDataF load_point_f(const SymSrc *src, int64_t k, bool valid) {
+    PDataF p;
+    if (valid) {
+        const float4 *q = reinterpret_cast<const float4 *>(src + k);
+        const float4 a0 = q[0], a1 = q[1], a2 = q[2];
+        p.xh = a0.x; p.yh = a0.y; p.zh = a0.z; p.xl = a0.w;
+        p.yl = a1.x; p.zl = a1.y; p.fx = a1.z; p.fy = a1.w;
+        p.fz = a2.x; p.c = a2.y; p.c3 = a2.z;
+        p.g = src[k].g;
+    } else {
+        p.xh = p.yh = p.zh = 1e30f;
+        p.xl = p.yl = p.zl = 0.f;
+        p.fx = p.fy = p.fz = p.c = p.c3 = 0.f;
+        p.g = -3;
+    }
+    return p;
+}
+
+template <bool CHECK, bool BOTH>
+__device__ __forceinline__ void sym_pair_f(const PDataF &pi, const PDataF &pj, float *ui,
+                                           float *uj, int &nb) {
+    const float rx = (pi.xh - pj.xh) + (pi.xl - pj.xl);
+    const float ry = (pi.yh - pj.yh) + (pi.yl - pj.yl);
+    const float rz = (pi.zh - pj.zh) + (pi.zl - pj.zl);
+    const float r2 = fmaf(rx, rx, fmaf(ry, ry, rz * rz));
+    float ir = rsqrtf(r2);
+    if (CHECK) {
+        const bool excl = (pi.g == pj.g) && pi.g >= 0;
+        const bool small = r2 < 1e-24f;
+        nb += (small && !excl) ? (BOTH ? 2 : 1) : 0;
+        ir = (excl || small) ? 0.f : ir;
+    }
+    const float ir2 = ir * ir;
+    const float ir3 = ir * ir2;
+    const float ir5 = ir3 * ir2;
+    {
+        const float a = fmaf(pj.c, ir3, ir);
+        const float b = fmaf(rz, pj.fz, fmaf(ry, pj.fy, rx * pj.fx)) * fmaf(-pj.c3, ir5, ir3);
+        ui[0] = fmaf(a, pj.fx, fmaf(b, rx, ui[0]));
+        ui[1] = fmaf(a, pj.fy, fmaf(b, ry, ui[1]));
+        ui[2] = fmaf(a, pj.fz, fmaf(b, rz, ui[2]));
+    }
+    if (BOTH) {
+        const float a = fmaf(pi.c, ir3, ir);
+        const float b = fmaf(rz, pi.fz, fmaf(ry, pi.fy, rx * pi.fx)) * fmaf(-pi.c3, ir5, ir3);
+        uj[0] = fmaf(a, pi.fx, fmaf(b, rx, uj[0]));
+        uj[1] = fmaf(a, pi.fy, fmaf(b, ry, uj[1]));
+        uj[2] = fmaf(a, pi.fz, fmaf(b, rz, uj[2]));
+    }
+}
+
+template <int MINB, int TBI>
+__global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs a) {
+    constexpr int kI = 32 * TBI;
+    extern __shared__ double jacc_s[];
+    __shared__ double ui_s[4][kI][3];
+    __shared__ float4 js_a[4][32], js_b[4][32];
+    __shared__ float js_c[4][32][4];
+    __shared__ int js_g[4][32];
+    if ((int64_t)blockIdx.x >= a.ntasks) return;
+    const int64_t t = a.task0 + blockIdx.x;
+    int g, h;
+    task_units(t, a.G, g, h);
+    const bool both = g != h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g0 = (int64_t)g * a.M, h0 = (int64_t)h * a.M;
+    const int ng = (int)min((int64_t)a.M, a.N - g0), nh = (int)min((int64_t)a.M, a.N - h0);
+    const int nslab = (nh + 31) / 32;
+    if (both)
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    int nb = 0;
+    for (int ib = 0; ib < ng; ib += kI) {
+        PDataF pi[TBI];
+        double ud[TBI][3];
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            pi[k] = load_point_f(a.src, g0 + ib + 32 * k + lane, ib + 32 * k + lane < ng);
+            ud[k][0] = ud[k][1] = ud[k][2] = 0.0;
+        }
+        double blo[3], bhi[3];
+        int gmn, gmx;
+        {
+            const SlabMeta &m0 = a.slab[(g0 + ib) / 32];
+            for (int c = 0; c < 3; ++c) { blo[c] = m0.lo[c]; bhi[c] = m0.hi[c]; }
+            gmn = m0.gmin; gmx = m0.gmax;
+            for (int k = 1; k < TBI; ++k) {
+                if (ib + 32 * k >= ng) break;
+                const SlabMeta &m1 = a.slab[(g0 + ib) / 32 + k];
+                for (int c = 0; c < 3; ++c) {
+                    blo[c] = fmin(blo[c], m1.lo[c]);
+                    bhi[c] = fmax(bhi[c], m1.hi[c]);
+                }
+                gmn = min(gmn, m1.gmin);
+                gmx = max(gmx, m1.gmax);
+            }
+        }
+        for (int sl = warp; sl < nslab; sl += 4) {
+            const int jl = sl * 32 + lane;
+            {
+                const PDataF q = load_point_f(a.src, h0 + jl, jl < nh);
+                js_a[warp][lane] = make_float4(q.xh, q.yh, q.zh, q.xl);
+                js_b[warp][lane] = make_float4(q.yl, q.zl, q.fx, q.fy);
+                js_c[warp][lane][0] = q.fz;
+                js_c[warp][lane][1] = q.c;
+                js_c[warp][lane][2] = q.c3;
+                js_g[warp][lane] = q.g;
+            }
+            __syncwarp();
+            float uf[TBI][3];
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
+            float uj[3] = {0.f, 0.f, 0.f};
+            const SlabMeta &mj = a.slab[h0 / 32 + sl];
+            const bool fast = boxes_far(blo, bhi, mj) && (mj.gmax < gmn || mj.gmin > gmx);
+            const int nxt = (lane + 1) & 31;
+            for (int s = 0; s < 32; ++s) {
+                const int k = (lane + s) & 31;
+                PDataF pj;
+                const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
+                pj.xh = A0.x; pj.yh = A0.y; pj.zh = A0.z; pj.xl = A0.w;
+                pj.yl = B0.x; pj.zl = B0.y; pj.fx = B0.z; pj.fy = B0.w;
+                pj.fz = js_c[warp][k][0]; pj.c = js_c[warp][k][1]; pj.c3 = js_c[warp][k][2];
+                pj.g = js_g[warp][k];
+                int nbi = 0;
+                if (fast) {
+#pragma unroll
+                    for (int q = 0; q < TBI; ++q) {
+                        if (both) sym_pair_f<false, true>(pi[q], pj, uf[q], uj, nbi);
+                        else sym_pair_f<false, false>(pi[q], pj, uf[q], uj, nbi);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < TBI; ++q) {
+                        if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi);
+                        else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi);
+                    }
+                }
+                if (pj.g != -3) nb += nbi;
+                if (both) {
+                    uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                    uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                    uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) {
+                ud[k][0] += (double)uf[k][0];
+                ud[k][1] += (double)uf[k][1];
+                ud[k][2] += (double)uf[k][2];
+            }
+            if (both && jl < nh) {
+                double *dst = jacc_s + 3 * jl;
+                dst[0] += (double)uj[0];
+                dst[1] += (double)uj[1];
+                dst[2] += (double)uj[2];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            ui_s[warp][32 * k + lane][0] = ud[k][0];
+            ui_s[warp][32 * k + lane][1] = ud[k][1];
+            ui_s[warp][32 * k + lane][2] = ud[k][2];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * kI; e += blockDim.x) {
+            const int il = e / 3, c = e - 3 * il;
+            if (ib + il < ng) {
+                const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
+                a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c] = sv;
+            }
+        }
+        __syncthreads();
+    }
+    if (both) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
+            a.part[((int64_t)g * a.N + h0) * 3 + e] = jacc_s[e];
+    }
+    if (a.bad) {
+        nb = warp_sum_int(nb);
+        if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
+    }
+}
+
+// FP32 record packing: float hi/lo positions, weighted strengths, c, 3c.
+__global__ void sym_pack_f32_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
+                                    const double *__restrict__ f, const double *__restrict__ w,
+                                    const double *__restrict__ dcoef, int64_t N,
+                                    SymSrc *__restrict__ out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        SymSrc s;
+        float *pf = reinterpret_cast<float *>(&s);
+        const double wj = w ? w[j] : 1.0;
+        for (int c = 0; c < 3; ++c) {
+            const double v = x[3 * j + c];
+            const float hf = __double2float_rn(v);
+            pf[c] = hf;
+            pf[3 + c] = __double2float_rn(v - (double)hf);
+            pf[6 + c] = __double2float_rn(wj * f[3 * j + c]);
+        }
+        const double c = dcoef ? dcoef[j] : 0.0;
+        pf[9] = __double2float_rn(c);
+        pf[10] = __double2float_rn(3.0 * c);
+        for (int k = 11; k < 18; ++k) pf[k] = 0.f;
+        s.g = grp ? pack_source_group(grp[j]) : -1;
+        s.pad = 0;
+        out[j] = s;
+    }
+}
+
+// Slab bounds from FP32 records (coordinate = hi + lo).
+__global__ void slab_meta_f32_kernel(const SymSrc *__restrict__ src, int64_t N,
+                                     SlabMeta *__restrict__ meta) {
+    const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s * 32 >= N) return;
+    const int64_t j = s * 32 + lane;
+    double v[6];
+    int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    if (j < N) {
+        const float *pf = reinterpret_cast<const float *>(src + j);
+        for (int c = 0; c < 3; ++c) v[c] = v[3 + c] = (double)pf[c] + (double)pf[3 + c];
+        if (src[j].g >= 0) { gmn = src[j].g; gmx = src[j].g; }
+    } else {
+        v[0] = v[1] = v[2] = 1e300;
+        v[3] = v[4] = v[5] = -1e300;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            v[c] = fmin(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+            v[3 + c] = fmax(v[3 + c], __shfl_xor_sync(0xffffffffu, v[3 + c], o));
+        }
+        gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+        gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+    }
+    if (lane == 0) {
+        SlabMeta m;
+        for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
+        m.gmin = gmn;
+        m.gmax = gmx;
+        meta[s] = m;
+    }
+}
+
 // out[i] (+)= pref * sum_{s < G} part[s][i], slots in order.
 __global__ void sym_reduce_kernel(const double *__restrict__ part, int G, int64_t N, double pref,
                                   double *__restrict__ out, int accumulate) {
@@ -397,7 +657,7 @@ int sym_unit_size(int64_t N, int64_t group_size) {
 // mode SF_MODE_FP64 picks the symmetric evaluation for large enough blocks;
 // SF_MODE_FP64_DIRECT forces the per-target order of the reference.
 bool use_symmetric(int mode, int64_t N) {
-    if (mode != SF_MODE_FP64) return false;
+    if (mode != SF_MODE_FP64 && mode != SF_MODE_FP32C) return false;
     const char *e = getenv("SF_SYMMETRIC");
     if (e && atoi(e) == 0) return false;
     return N >= 8192;
@@ -406,9 +666,9 @@ bool use_symmetric(int mode, int64_t N) {
 int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                         const double *f, const double *w, const double *dcoef, double pref,
                         double *out, int64_t *bad, int accumulate, cudaStream_t st,
-                        Workspace &ws) {
+                        Workspace &ws, int mode) {
     return pairs_sbt_symmetric_shard(x, grp, N, group_size, f, w, dcoef, pref, 0, 1, out, bad,
-                                     accumulate, st, ws);
+                                     accumulate, st, ws, mode);
 }
 
 // The unit-pair tasks of rank `rank` of `world`: contiguous equal-count
@@ -424,7 +684,8 @@ int64_t sym_task_range(int64_t ntasks, int rank, int world, int64_t *count) {
 int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
-                              cudaStream_t st, Workspace &ws) {
+                              cudaStream_t st, Workspace &ws, int mode) {
+    const bool f32 = mode == SF_MODE_FP32C;
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
@@ -435,10 +696,16 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     double *part = (double *)ws.get(5, sizeof(double) * 3 * (size_t)N * G, st);
     if (!packed || !meta || !part) return SF_ENOMEM;
     int64_t pg = (N + 255) / 256;
-    sym_pack_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef, N,
-                                                                     packed);
     const int64_t nslab = (N + 31) / 32;
-    slab_meta_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
+    if (f32) {
+        sym_pack_f32_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef,
+                                                                             N, packed);
+        slab_meta_f32_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
+    } else {
+        sym_pack_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef, N,
+                                                                         packed);
+        slab_meta_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
+    }
     SymArgs a;
     a.src = packed;
     a.slab = meta;
@@ -465,7 +732,21 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         return SF_OK;
     };
     int lrc;
-    switch (variant) {
+    if (f32) {
+        static const int fvariant = [] {
+            const char *e = getenv("SF_SYM_F32_VARIANT");
+            return e ? atoi(e) : 34;
+        }();
+        switch (fvariant) {
+            case 32: lrc = launch(sym_task_kernel_f32<3, 2>); break;
+            case 33: lrc = launch(sym_task_kernel_f32<3, 3>); break;
+            case 24: lrc = launch(sym_task_kernel_f32<2, 4>); break;
+            case 26: lrc = launch(sym_task_kernel_f32<2, 6>); break;
+            case 28: lrc = launch(sym_task_kernel_f32<2, 8>); break;
+            case 44: lrc = launch(sym_task_kernel_f32<4, 4>); break;
+            default: lrc = launch(sym_task_kernel_f32<3, 4>); break;
+        }
+    } else switch (variant) {
         case 41: lrc = launch(sym_task_kernel<4, 1>); break;
         case 42: lrc = launch(sym_task_kernel<4, 2>); break;
         case 22: lrc = launch(sym_task_kernel<2, 2>); break;

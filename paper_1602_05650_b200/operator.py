@@ -19,7 +19,7 @@ import math
 import numpy as np
 
 from . import _native, spectral
-from ._native import SF_MODE_FP64
+from ._native import SF_MODE_FP32C, SF_MODE_FP64
 
 
 def _ptr(t):
@@ -151,7 +151,7 @@ class FiberHIOperator:
         """Whether the fiber pair sum runs the symmetric evaluation
         (SF_MODE_FP64, whole system on this rank, >= 8192 points)."""
         import os
-        return (self.mode == SF_MODE_FP64 and self.world == 1 and self.N >= 8192
+        return (self.mode in (SF_MODE_FP64, SF_MODE_FP32C) and self.world == 1 and self.N >= 8192
                 and os.environ.get("SF_SYMMETRIC", "1") != "0")
 
     @property
@@ -160,7 +160,7 @@ class FiberHIOperator:
         share of the unit-pair tasks for ALL points; the dist layer sums the
         ranks' partials with a reduce-scatter."""
         import os
-        return (self.mode == SF_MODE_FP64 and self.world > 1 and self.N >= 8192
+        return (self.mode in (SF_MODE_FP64, SF_MODE_FP32C) and self.world > 1 and self.N >= 8192
                 and os.environ.get("SF_SYMMETRIC", "1") != "0")
 
     def symmetric_partial(self, f, out=None, rank=None, world=None):
@@ -170,7 +170,7 @@ class FiberHIOperator:
         if out is None:
             out = torch.empty((self.N, 3), dtype=torch.float64, device=self.device)
         _native.call("sf_sbt_symmetric_partial", _ptr(self.X), _ptr(self.groups), self.N, self.n,
-                     _ptr(f), _ptr(self.wnode), _ptr(self.dcoef), self.pref,
+                     _ptr(f), _ptr(self.wnode), _ptr(self.dcoef), self.pref, self.mode,
                      self.rank if rank is None else rank, self.world if world is None else world,
                      _ptr(out), _ptr(self.bad), _stream())
         return out

@@ -221,3 +221,22 @@ def test_symmetric_task_shards_sum_to_single_gpu(cuda, world):
     for r in range(world):
         total += op.symmetric_partial(F, rank=r, world=world)
     assert rel(total.cpu().numpy(), one.cpu().numpy()) < 1e-14
+
+
+def test_symmetric_fp32c_variant(cuda):
+    """FP32-compute / FP64-accumulate symmetric evaluation within 1e-5 of FP64."""
+    from paper_1602_05650_b200._native import SF_MODE_FP32C, SF_MODE_FP64
+    cl, F = _cloud_operator_inputs(200, 64)
+    a, _ = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP64).apply(F, self_terms=False)
+    op32 = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP32C)
+    assert op32.symmetric
+    b, _ = op32.apply(F, self_terms=False)
+    c, _ = op32.apply(F, self_terms=False)
+    assert torch_equal(b, c)
+    e = rel(b.cpu().numpy(), a.cpu().numpy())
+    assert e < 1e-5, e
+
+
+def torch_equal(x, y):
+    import torch
+    return bool(torch.equal(x, y))
