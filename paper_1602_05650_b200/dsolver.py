@@ -1,0 +1,528 @@
+"""Multi-GPU implicit step: sharded block rows, all-reduced GMRES.
+
+One process per GPU.  Rank r owns a contiguous block of fibers (their X, T
+unknowns and rows); rank 0 also owns the particle and periphery unknowns
+(U, omega, q1, q0) and rows.  Every vector is allocated full length on every
+rank but only the owned entries are meaningful; the Krylov bookkeeping
+(Hessenberg, Givens) is replicated.
+
+Per matvec:
+  1. broadcast the surface/particle unknowns from rank 0;
+  2. fiber force densities of the own fibers, all-gathered (NCCL) to all;
+  3. particle wrenches: per-rank partial sums, all-reduced;
+  4. fiber x fiber Stokeslet + doublet: the symmetric unit-pair tasks split
+     over ranks + reduce-scatter (>= 8192 points), or own targets against
+     all sources (direct);
+  5. the other families (surface double layers, completion flow, near maps)
+     for the rank's own targets;
+  6. own fiber rows; surface rows on rank 0.
+Per GMRES iteration the MGS dot products are all-reduced (one collective per
+inner product, preserving modified Gram-Schmidt).
+
+`Comm` hides the transport: TorchComm uses torch.distributed (NCCL on the
+GPU box, gloo on the CPU), ThreadComm runs the ranks as threads on ONE GPU
+(host-side barriers only; no kernel waits on another) for tests.
+"""
+
+import ctypes
+import math
+import threading
+
+import numpy as np
+
+from . import _native, spectral
+from .dist import shard_range
+from .solver import (BC_CODES, FactorizationError, GmresParams, NonconvergenceError,
+                     StepLayout, _ptr, _stream)
+from .system import (ConfigurationError, SingularEvaluationError, FiberGeometry, InteractionCache, external_force_density,
+                     stack_fibers)
+
+
+# ------------------------------------------------------------------ comms ----
+class TorchComm:
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def all_reduce_sum(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def broadcast(self, t, src=0):
+        self.dist.broadcast(t, src=src, group=self.group)
+        return t
+
+    def all_gather(self, out, inp):
+        if self.nccl:
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
+        else:
+            self.dist.all_gather(list(out.chunk(self.world)), inp, group=self.group)
+        return out
+
+    def reduce_scatter_sum(self, out, inp):
+        if self.nccl:
+            self.dist.reduce_scatter_tensor(out, inp, group=self.group)
+        else:
+            self.dist.all_reduce(inp, group=self.group)
+            out.copy_(inp.chunk(self.world)[self.rank])
+        return out
+
+
+class ThreadHub:
+    """Shared state of ThreadComm ranks (one process, one GPU)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+
+class ThreadComm:
+    """Collectives between threads of one process; sums in rank order."""
+
+    def __init__(self, hub, rank):
+        self.hub, self.rank, self.world = hub, rank, hub.world
+
+    def _exchange(self, t):
+        import torch
+        if t.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        self.hub.slots[self.rank] = t
+        self.hub.barrier.wait()
+        return self.hub.slots
+
+    def _done(self):
+        import torch
+        if self.hub.slots[self.rank].is_cuda:
+            torch.cuda.current_stream().synchronize()
+        self.hub.barrier.wait()
+
+    def all_reduce_sum(self, t):
+        slots = self._exchange(t.clone())
+        acc = slots[0].clone()
+        for k in range(1, self.world):
+            acc += slots[k]
+        self._done()
+        t.copy_(acc)
+        return t
+
+    def broadcast(self, t, src=0):
+        slots = self._exchange(t.clone())
+        v = slots[src].clone()
+        self._done()
+        t.copy_(v)
+        return t
+
+    def all_gather(self, out, inp):
+        slots = self._exchange(inp.clone())
+        parts = [s.clone() for s in slots]
+        self._done()
+        for k, p in enumerate(parts):
+            out.chunk(self.world)[k].copy_(p)
+        return out
+
+    def reduce_scatter_sum(self, out, inp):
+        slots = self._exchange(inp.clone())
+        acc = slots[0].chunk(self.world)[self.rank].clone()
+        for k in range(1, self.world):
+            acc += slots[k].chunk(self.world)[self.rank]
+        self._done()
+        out.copy_(acc)
+        return out
+
+
+# --------------------------------------------------------------- operator ----
+class DistBlockOperator:
+    """This rank's rows of the implicit step system (solver.py:187-364)."""
+
+    def __init__(self, state, dt, comm, mu=None, symmetric=None):
+        import torch
+        if dt <= 0:
+            raise ConfigurationError("time step must be positive")
+        self.state, self.comm = state, comm
+        self.dt = float(dt)
+        self.mu = state.mu if mu is None else float(mu)
+        self.layout = lay = StepLayout(state)
+        self.device = dev = torch.device("cuda")
+        f64 = dict(dtype=torch.float64, device=dev)
+        nf = len(state.fibers)
+        n = state.fibers[0].n_nodes if nf else 5
+        self.nf, self.n = nf, n
+        rank, world = comm.rank, comm.world
+        self.f0, self.nown = shard_range(nf, rank, world)
+        self.per = -(-nf // world) if nf else 0
+        fo = lay.fib_off
+        # target share: rank 0 [surfaces | own fibers], others own fibers
+        n_surf_t = sum(p.mesh.n_nodes for p in state.particles) + \
+            (state.periphery.mesh.n_nodes if state.periphery is not None else 0)
+        self.n_surf_t = n_surf_t
+        N = nf * n
+        if symmetric is None:
+            import os
+            symmetric = N >= 8192 and os.environ.get("SF_SYMMETRIC", "1") != "0"
+        self.symmetric = bool(symmetric) and nf > 0
+        lo_f = n_surf_t + self.f0 * n
+        hi_f = lo_f + self.nown * n
+        ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in state.fibers]
+        deltas = [0.0 if f.delta_ratio is not None else f.delta for f in state.fibers]
+        geo = FiberGeometry(stack_fibers(state.fibers), ratios, deltas, dev)
+        self.geo = geo
+        eps_all = torch.as_tensor([f.eps for f in state.fibers], **f64)
+        self.fdcoef = ((eps_all * geo.L) ** 2 / 2.0).repeat_interleave(n).contiguous() \
+            if nf else None
+        self.fgrp = torch.as_tensor(np.repeat(np.arange(nf, dtype=np.int64), n), device=dev)
+        # fiber targets: symmetric -> fiber pair sums come from the task split
+        self.cache_fib = (InteractionCache(state, target_range=(lo_f, hi_f), fiber_geometry=geo,
+                                           fiber_pairs=not self.symmetric) if self.nown else None)
+        self.cache_surf = (InteractionCache(state, target_range=(0, n_surf_t), fiber_geometry=geo)
+                           if rank == 0 and n_surf_t else None)
+        # frozen fiber operators of the OWN fibers
+        o, no = self.f0, self.nown
+        self.Dpow = torch.empty((no, 4, n, n), **f64)
+        if no:
+            _native.call("sf_fiber_dpow", _ptr(geo.D), _ptr(geo.s_alpha[o:]), no, n,
+                         _ptr(self.Dpow), _stream())
+        self.K = torch.empty((no, 3 * n, 3 * n), **f64)
+        if no:
+            _native.call("sf_kdelta_build_batched", _ptr(geo.X[o:]), _ptr(geo.s[o:]),
+                         _ptr(geo.s_alpha[o:]), _ptr(geo.tang[o:]), _ptr(geo.wcc), no, n,
+                         _ptr(geo.delta[o:]), 1.0 / (8.0 * math.pi * self.mu), _ptr(self.K),
+                         _stream())
+        own = state.fibers[o:o + no]
+        eps = np.array([f.eps for f in own])
+        self.E = torch.as_tensor(np.array([f.E for f in own], dtype=float), **f64)
+        self.c_log = torch.as_tensor(-np.log(eps ** 2 * math.e) / (8.0 * math.pi * self.mu), **f64)
+        self.c_two = 2.0 / (8.0 * math.pi * self.mu)
+        self.Ldot = torch.as_tensor(np.array([f.Ldot for f in own], dtype=float), **f64)
+        self.f_ext = (torch.as_tensor(np.ascontiguousarray(np.stack(
+            [external_force_density(state, f) for f in own])), **f64)
+            if (state.force_models and no) else None)
+        kinds = np.zeros((no, 2), dtype=np.int32)
+        par = np.zeros((no, 2, 12))
+        body = np.full(no, -1, dtype=np.int32)
+        for m, fib in enumerate(own):
+            for e, bc in enumerate((fib.bc_plus, fib.bc_minus)):
+                kinds[m, e] = BC_CODES[bc.kind]
+                if bc.kind == "prescribedForceTorque":
+                    par[m, e, 0:3], par[m, e, 3:6] = bc.force, bc.torque
+                elif bc.kind == "hingedToSurface":
+                    par[m, e, 6:9], par[m, e, 9] = bc.attachment, bc.stiffness
+                elif bc.kind == "clampedToBody":
+                    par[m, e, 10] = 0.0 if bc.tangent is None else 1.0
+                    if e == 1:
+                        body[m] = bc.body
+        self.bc_kind = torch.as_tensor(kinds, device=dev)
+        self.bc_par = torch.as_tensor(par, **f64)
+        self.bc_body = torch.as_tensor(body, device=dev)
+        np_ = len(state.particles)
+        self.np = np_
+        self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
+                        if np_ else None)
+        self.p_uoff = (torch.as_tensor(np.array([s.start for s in lay.U], dtype=np.int64), device=dev)
+                       if np_ else None)
+        self.ext = (torch.as_tensor(np.stack([np.concatenate([p.F_ext, p.L_ext])
+                                              for p in state.particles]), **f64)
+                    if (np_ and rank == 0) else None)
+        self.nodes = torch.tensor(spectral.grid(n - 1)[0], **f64)
+        self.sys = _native.FiberSys(
+            nf=no, n=n, D=_ptr(geo.D), nodes=_ptr(self.nodes), Dpow=_ptr(self.Dpow),
+            X=_ptr(geo.X[o:]), tang=_ptr(geo.tang[o:]), s_alpha=_ptr(geo.s_alpha[o:]),
+            L=_ptr(geo.L[o:]), Ldot=_ptr(self.Ldot), E=_ptr(self.E), c_log=_ptr(self.c_log),
+            c_two=self.c_two, K=_ptr(self.K), f_ext=_ptr(self.f_ext), bc_kind=_ptr(self.bc_kind),
+            bc_par=_ptr(self.bc_par), bc_body=_ptr(self.bc_body), np=np_, pcenter=_ptr(self.pcenter),
+            p_uoff=_ptr(self.p_uoff), fib_off=fo + 4 * n * o, dt=self.dt, mu=self.mu)
+        # surfaces (rank 0 rows)
+        self.surf = []
+        if rank == 0:
+            for i, part in enumerate(state.particles):
+                m = part.mesh
+                self.surf.append(dict(kind=0, pi=i, nodes=torch.as_tensor(m.nodes, **f64),
+                                      nrm=torch.as_tensor(m.normals, **f64),
+                                      w=torch.as_tensor(m.weights, **f64), n=m.n_nodes,
+                                      area=m.area, center=self.pcenter[i], sl=lay.q1[i],
+                                      uom=lay.U[i].start,
+                                      tsl=self.cache_surf.particle_slices[i]))
+            if state.periphery is not None:
+                m = state.periphery.mesh
+                self.surf.append(dict(kind=1, nodes=torch.as_tensor(m.nodes, **f64),
+                                      nrm=torch.as_tensor(m.normals, **f64),
+                                      w=torch.as_tensor(m.weights, **f64), n=m.n_nodes,
+                                      area=m.area, center=None, sl=lay.q0, uom=None,
+                                      tsl=self.cache_surf.periphery_slice))
+        # surface densities in cache order: (slice in u) for every surface, every rank
+        self.dens_sl = list(lay.q1) + ([lay.q0] if lay.q0 is not None else [])
+        # owned index ranges of the unknown vector
+        self.owned = []
+        if rank == 0 and fo:
+            self.owned.append((0, fo))
+        if no:
+            self.owned.append((fo + 4 * n * o, fo + 4 * n * (o + no)))
+        # scratch
+        self._f_pad = torch.zeros((max(self.per, 1) * n, 3), **f64)
+        self._f_full = torch.zeros((world * max(self.per, 1) * n, 3), **f64)
+        self._wf = torch.empty((max(no, 1), 6), **f64)
+        self._wr = torch.empty((max(np_, 1), 6), **f64)
+        self._work = torch.empty(16, **f64)
+        self._part = torch.empty((N, 3), **f64) if self.symmetric else None
+        self._rs_in = torch.zeros((world * max(self.per, 1) * n, 3), **f64)
+        self._rs_out = torch.zeros((max(self.per, 1) * n, 3), **f64)
+        self._bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.fiber_blocks = torch.empty((no, 4 * n, 4 * n), **f64)
+        if no:
+            _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.fiber_blocks),
+                         _stream())
+        self.matvecs = 0
+
+    @property
+    def shape(self):
+        return (self.layout.size, self.layout.size)
+
+    def rows_device(self, u, constants, out=None):
+        import torch
+        c = self.comm
+        st = _stream()
+        n, fo, no = self.n, self.layout.fib_off, self.nown
+        if out is None:
+            out = torch.zeros_like(u)
+        if fo:
+            c.broadcast(u[:fo], src=0)               # U, omega, q1, q0 from rank 0
+        sysp = ctypes.byref(self.sys)
+        # own fiber forces -> all fibers
+        self._f_pad.zero_()
+        if no:
+            _native.call("sf_fiber_forces", sysp, _ptr(u), int(constants), _ptr(self._f_pad), st)
+        c.all_gather(self._f_full, self._f_pad)
+        N = self.nf * n
+        f_full = self._f_full[:N].contiguous()
+        # particle wrenches: partial sums over own fibers, all-reduced
+        if self.np:
+            if no:
+                _native.call("sf_particle_wrenches", sysp, _ptr(u), _ptr(self.ext), int(constants),
+                             _ptr(self._wf), _ptr(self._wr), st)
+            else:
+                self._wr.zero_()
+                if self.ext is not None and constants:
+                    self._wr[:self.np].copy_(self.ext)
+            c.all_reduce_sum(self._wr)
+        q = (torch.cat([u[sl] for sl in self.dens_sl]).reshape(-1, 3) if self.dens_sl else None)
+        wr = self._wr[:self.np] if self.np else None
+        # fiber targets: the other families (and the fiber pairs when direct)
+        ub_f = self.cache_fib.apply(f_full, q, wr, check=True) if no else None
+        if self.symmetric:
+            g = self.geo
+            _native.call("sf_sbt_symmetric_partial", _ptr(g.X), _ptr(self.fgrp), N, n,
+                         _ptr(f_full), _ptr(g.wnode), _ptr(self.fdcoef),
+                         1.0 / (8.0 * math.pi * self.mu), _native.SF_MODE_FP64, c.rank, c.world,
+                         _ptr(self._part), _ptr(self._bad), st)
+            self._rs_in[:N].copy_(self._part)
+            c.reduce_scatter_sum(self._rs_out, self._rs_in)
+            if int(self._bad.item()):
+                raise SingularEvaluationError("a target coincides with another fiber's node")
+            if no:
+                ub_f = ub_f + self._rs_out[:no * n]
+        if no:
+            _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(ub_f), int(constants), _ptr(out), st)
+        # surfaces (rank 0)
+        if self.surf:
+            ub_s = self.cache_surf.apply(f_full, q, wr, check=True)
+            pref_dl = -3.0 / (4.0 * math.pi * self.mu)
+            for s in self.surf:
+                qs = u[s["sl"]]
+                rows = out[s["sl"]]
+                _native.call("sf_stresslet_sum_subtracted", _ptr(s["nodes"]), _ptr(s["nrm"]),
+                             _ptr(s["w"]), _ptr(qs), s["n"], pref_dl, _ptr(rows), st)
+                ub = ub_s[s["tsl"]]
+                if s["kind"] == 0:
+                    _native.call("sf_wrench_flow", _ptr(s["nodes"]), s["n"], _ptr(s["center"]),
+                                 _ptr(self._wr[s["pi"]]), self.mu, _ptr(rows), st)
+                    uom = u[s["uom"]:s["uom"] + 6]
+                    _native.call("sf_surface_rows", 0, _ptr(s["nodes"]), _ptr(s["nrm"]),
+                                 _ptr(s["w"]), s["n"], _ptr(s["center"]), s["area"], _ptr(qs),
+                                 _ptr(ub), _ptr(uom), self.mu, _ptr(self._work), _ptr(rows),
+                                 _ptr(out[s["uom"]:s["uom"] + 6]), st)
+                else:
+                    _native.call("sf_surface_rows", 1, _ptr(s["nodes"]), _ptr(s["nrm"]),
+                                 _ptr(s["w"]), s["n"], None, s["area"], _ptr(qs), _ptr(ub), None,
+                                 self.mu, _ptr(self._work), _ptr(rows), None, st)
+        self.matvecs += 1
+        return out
+
+    def rhs_device(self):
+        import torch
+        zero = torch.zeros(self.layout.size, dtype=torch.float64, device=self.device)
+        return -self.rows_device(zero, True)
+
+
+class DistPreconditioner:
+    """Own fiber blocks (equilibrated LU) + surface diagonal on rank 0."""
+
+    def __init__(self, op):
+        import torch
+        f64 = dict(dtype=torch.float64, device=op.device)
+        self.op = op
+        no, n = op.nown, op.n
+        m = 4 * n
+        self.m = m
+        if m > 256:
+            raise ConfigurationError("the distributed preconditioner factors blocks up to 4n = 256")
+        self.off0 = op.layout.fib_off + 4 * n * op.f0
+        st = _stream()
+        self.LU = self.r = self.c = self.piv = None
+        if no:
+            A = op.fiber_blocks.clone()
+            self.r = torch.empty((no, m), **f64)
+            self.c = torch.empty((no, m), **f64)
+            self.piv = torch.empty((no, m), dtype=torch.int32, device=op.device)
+            info = torch.empty(no, dtype=torch.int32, device=op.device)
+            _native.call("sf_block_lu", _ptr(A), no, m, _ptr(self.r), _ptr(self.c),
+                         _ptr(self.piv), _ptr(info), st)
+            bad = info.cpu().numpy()
+            if np.any(bad > 0):
+                raise FactorizationError(f"fiber {op.f0 + int(np.argmax(bad > 0))} self-block "
+                                         "is not invertible")
+            self.LU = A
+        fo = op.layout.fib_off
+        self.ndiag = fo if op.comm.rank == 0 else 0
+        self.diag = torch.ones(max(self.ndiag, 1), **f64)
+        pref = -3.0 / (4.0 * math.pi * op.mu)
+        for s in op.surf:
+            rs = torch.empty((s["n"], 3, 3), **f64)
+            _native.call("sf_stresslet_rowsum", _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                         s["n"], pref, _ptr(rs), st)
+            d = -torch.diagonal(rs, dim1=1, dim2=2)
+            if s["kind"] == 1:
+                d = d + 1.0 / op.mu + (s["nrm"] ** 2) * s["w"][:, None] / (op.mu * s["area"])
+            self.diag[s["sl"]] = d.reshape(-1)
+
+    def apply_device(self, v, out=None):
+        import torch
+        if out is None:
+            out = torch.zeros_like(v)
+        _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c), _ptr(self.piv),
+                     self.op.nown, self.m, self.off0, _ptr(self.diag), self.ndiag, _ptr(v),
+                     _ptr(out), _stream())
+        return out
+
+
+# ----------------------------------------------------------------- GMRES ----
+def dist_gmres_solve(op, prec, rhs, params=None):
+    """solver.gmres_solve (solver.py:444-516) over the ranks' owned entries:
+    every inner product is a local deterministic dot plus an all-reduce."""
+    import torch
+    if params is None:
+        params = GmresParams()
+    comm = op.comm
+    dev = op.device
+    n = rhs.numel()
+    work = torch.empty(296, dtype=torch.float64, device=dev)
+    loc = torch.zeros(4, dtype=torch.float64, device=dev)
+    st = _stream()
+
+    def dot(x, y):
+        loc.zero_()
+        for k, (a, b) in enumerate(op.owned):
+            _native.call("sf_dot", _ptr(x[a:b]), _ptr(y[a:b]), b - a, _ptr(work), _ptr(loc[k:k + 1]),
+                         0, st)
+        s = loc[0:1] + loc[1:2]
+        return comm.all_reduce_sum(s)
+
+    def M(v):
+        return prec.apply_device(v)
+
+    def A(v):
+        return op.rows_device(v, False)
+
+    b = M(rhs)
+    beta0 = math.sqrt(float(dot(b, b).item()))
+    if beta0 == 0.0:
+        return torch.zeros(n, dtype=torch.float64, device=dev), 0, [0.0]
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    R = params.restart
+    V = torch.zeros((R + 1, n), dtype=torch.float64, device=dev)
+    history, iters = [], 0
+    while True:
+        r = b - M(A(x)) if iters else b
+        beta = math.sqrt(float(dot(r, r).item()))
+        if beta / beta0 <= params.tolerance:
+            return x, iters, history or [beta / beta0]
+        V[0].copy_(r / beta)
+        H = np.zeros((R + 1, R))
+        cs, sn, g = np.zeros(R), np.zeros(R), np.zeros(R + 1)
+        g[0] = beta
+        k = 0
+        while k < R and iters < params.max_iterations:
+            w = M(A(V[k])).contiguous()
+            wnorm = math.sqrt(float(dot(w, w).item()))
+            for j in range(k + 1):
+                h = dot(V[j], w)
+                _native.call("sf_axpy_dev", _ptr(h), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
+                H[j, k] = float(h.item())
+            H[k + 1, k] = math.sqrt(float(dot(w, w).item()))
+            for j in range(k):
+                tmp = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
+                H[j + 1, k] = -sn[j] * H[j, k] + cs[j] * H[j + 1, k]
+                H[j, k] = tmp
+            denom = math.hypot(H[k, k], H[k + 1, k])
+            cs[k] = H[k, k] / denom if denom else 1.0
+            sn[k] = H[k + 1, k] / denom if denom else 0.0
+            H[k, k] = denom
+            g[k + 1] = -sn[k] * g[k]
+            g[k] = cs[k] * g[k]
+            iters += 1
+            rel = abs(g[k + 1]) / beta0
+            history.append(rel)
+            breakdown = H[k + 1, k] <= 1e-12 * max(wnorm, 1e-300)
+            if not breakdown:
+                V[k + 1].copy_(w / H[k + 1, k])
+            k += 1
+            if rel <= params.tolerance or breakdown:
+                break
+        if k:
+            y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
+            coef = torch.as_tensor(y, dtype=torch.float64, device=dev)
+            _native.call("sf_combine", _ptr(V), n, k, _ptr(coef), _ptr(x), n, st)
+        rel = history[-1] if history else 0.0
+        if rel <= params.tolerance:
+            return x, iters, history
+        if iters >= params.max_iterations:
+            raise NonconvergenceError(
+                f"GMRES did not reach {params.tolerance:g} within {params.max_iterations} "
+                f"iterations (residual {rel:.3e})", best=x, iterations=iters, residuals=history)
+
+
+def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, symmetric=None):
+    """backward_euler_step (solver.py:528-592) over `comm`'s ranks.  The host
+    state is replicated; every rank ends with the same updated state."""
+    import torch
+    from .fiber import STALLED
+    if any(f.growth_state != STALLED for f in state.fibers):
+        raise NotImplementedError("polymerization kinetics are outside the device path")
+    op = DistBlockOperator(state, dt, comm, symmetric=symmetric)
+    rhs = op.rhs_device()
+    prec = DistPreconditioner(op)
+    x, iters, history = dist_gmres_solve(op, prec, rhs, params)
+    # assemble the full solution on every rank: owned ranges summed (others 0)
+    full = torch.zeros_like(x)
+    for a, b in op.owned:
+        full[a:b] = x[a:b]
+    comm.all_reduce_sum(full)
+    sol = full.cpu().numpy()
+    parts = op.layout.unpack(sol)
+    for i, part in enumerate(state.particles):
+        part.U = parts.U[i].copy()
+        part.omega = parts.omega[i].copy()
+        part.q = parts.q1[i].copy()
+        part.translate(dt * part.U)
+    if state.periphery is not None:
+        state.periphery.q = parts.q0.copy()
+    for m, fib in enumerate(state.fibers):
+        fib.X = parts.X[m].copy()
+        fib.T = parts.T[m].copy()
+    state.time += dt
+    if return_info:
+        return state, dict(iterations=iters, history=history, matvecs=op.matvecs)
+    return state

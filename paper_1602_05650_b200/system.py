@@ -221,7 +221,12 @@ class InteractionCache:
     (system.py:492-620).  Rebuild whenever any constituent moves."""
 
     def __init__(self, state, include_doublet=True, device=None, mode=SF_MODE_FP64,
-                 near="device", fiber_geometry=None):
+                 near="device", fiber_geometry=None, target_range=None, fiber_pairs=True):
+        """target_range (lo, hi): evaluate only the targets [lo, hi) of the
+        global [particles | periphery | fibers] list (a rank's share in a
+        multi-GPU step).  fiber_pairs=False leaves the fiber-source pair sum
+        out of the layout (evaluated elsewhere, e.g. symmetrically across
+        ranks); the near corrections of fiber sources stay in."""
         import os
         import time
 
@@ -269,7 +274,23 @@ class InteractionCache:
         groups.append(np.repeat(np.arange(nf, dtype=np.int64), self.n_nodes))
         self.targets = np.vstack(blocks) if blocks else np.zeros((0, 3))
         self.target_groups = np.concatenate(groups) if groups else np.zeros(0, np.int64)
+        self.target_offset = 0
+        if target_range is not None:
+            lo, hi = target_range
+            self.targets = self.targets[lo:hi]
+            self.target_groups = self.target_groups[lo:hi]
+            self.target_offset = lo
+
+            def clip(sl):
+                a, b = max(sl.start, lo), min(sl.stop, hi)
+                return slice(a - lo, b - lo) if a < b else slice(0, 0)
+            self.particle_slices = [clip(x) for x in self.particle_slices]
+            if self.periphery_slice is not None:
+                self.periphery_slice = clip(self.periphery_slice)
+            self.fiber_slice = clip(self.fiber_slice)
+            self.fiber_slices = [clip(x) for x in self.fiber_slices]
         self.n_targets = self.targets.shape[0]
+        self.fiber_pairs = bool(fiber_pairs)
 
         _lap("targets")
         # fibers: geometry, weights, doublet coefficients (device)
@@ -396,26 +417,32 @@ class InteractionCache:
 
     def _layout(self):
         nt = self.near_tensors
+        nfs = self.fsrc.shape[0] if self.fiber_pairs else 0
+        whole = self.target_offset == 0 and self.fiber_slice.stop == self.n_targets and \
+            self.fiber_slice.stop - self.fiber_slice.start == self.fsrc.shape[0]
         self.layout = _native.HiLayout(
             trg=_ptr(self.trg), tgrp=_ptr(self.tgrp), nt=self.n_targets,
             fsrc=_ptr(self.fsrc), fgrp=_ptr(self.fgrp), fw=_ptr(self.fw),
-            fdcoef=_ptr(self.fdcoef), nfs=self.fsrc.shape[0],
+            fdcoef=_ptr(self.fdcoef), nfs=nfs,
             ssrc=_ptr(self.ssrc), snrm=_ptr(self.snrm), sw=_ptr(self.sw), sgrp=_ptr(self.sgrp),
             nss=self.nss, pcenter=_ptr(self.pcenter), pgrp=_ptr(self.pgrp), np=self.np,
             near_row_ptr=_ptr(nt.get("row_ptr")), near_rows=_ptr(nt.get("rows")),
             near_w_off=_ptr(nt.get("w_off")), near_x_off=_ptr(nt.get("x_off")),
             near_x_len=_ptr(nt.get("x_len")), near_nrows=self.near_nrows,
             near_W=_ptr(nt.get("W")), mu=self.mu, mode=self.mode,
-            fiber_target_off=self.fiber_slice.start if self.nf else -1,
+            fiber_target_off=self.fiber_slice.start if (self.nf and whole) else -1,
             fiber_group_size=self.n_nodes)
 
     # -- application ------------------------------------------------------------
     @property
     def pairs_per_apply(self):
         """Non-excluded (target, source) pairs of one application."""
-        nfs = self.fsrc.shape[0]
-        own = self.nf * self.n_nodes * self.n_nodes
-        surf = sum(m.n_nodes * m.n_nodes for m, _, _ in self.surfaces)
+        nfs = self.fsrc.shape[0] if self.fiber_pairs else 0
+        ln = lambda sl: sl.stop - sl.start                                 # noqa: E731
+        own = sum(ln(s) for s in self.fiber_slices) * self.n_nodes if self.fiber_pairs else 0
+        tsl = list(self.particle_slices) + ([self.periphery_slice]
+                                             if self.periphery_slice is not None else [])
+        surf = sum(ln(s) * m.n_nodes for s, (m, _, _) in zip(tsl, self.surfaces))
         return self.n_targets * nfs - own + self.n_targets * self.nss - surf
 
     def apply(self, f, q=None, wrench=None, out=None, check=True):

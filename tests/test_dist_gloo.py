@@ -147,3 +147,70 @@ def test_shard_ranges_cover_all_fibers():
             spans = [shard_range(nf, r, world) for r in range(world)]
             covered = [m for f0, c in spans for m in range(f0, f0 + c)]
             assert covered == list(range(nf))
+
+
+# ----------------------------------------------- dsolver Comm semantics ----
+def _comm_ops(comm):
+    """The four collectives dsolver uses, on rank-dependent inputs."""
+    from paper_1602_05650_b200.dsolver import ThreadComm  # noqa: F401 (import check)
+    r, w = comm.rank, comm.world
+    a = torch.arange(6, dtype=torch.float64) * (r + 1)
+    comm.all_reduce_sum(a)
+    b = torch.full((3,), float(r + 10), dtype=torch.float64)
+    comm.broadcast(b, src=0)
+    c = torch.empty((2 * w, 3), dtype=torch.float64)
+    comm.all_gather(c, torch.full((2, 3), float(r), dtype=torch.float64))
+    d = torch.empty((2, 3), dtype=torch.float64)
+    comm.reduce_scatter_sum(d, torch.arange(6 * w, dtype=torch.float64).reshape(2 * w, 3) + r)
+    return [x.numpy().copy() for x in (a, b, c, d)]
+
+
+def _expected(r, w):
+    a = np.arange(6.0) * sum(k + 1 for k in range(w))
+    b = np.full(3, 10.0)
+    c = np.repeat(np.arange(w, dtype=float), 2)[:, None] * np.ones(3)
+    d = sum(np.arange(6.0 * w).reshape(2 * w, 3) + k for k in range(w))[2 * r:2 * r + 2]
+    return [a, b, c, d]
+
+
+def _comm_worker(rank, world, port, q):
+    from paper_1602_05650_b200.dsolver import TorchComm
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, _comm_ops(TorchComm())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_comm_collectives_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        for x, e in zip(got[r], _expected(r, 2)):
+            assert np.array_equal(x, e)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_thread_comm_collectives(world):
+    import threading
+    from paper_1602_05650_b200.dsolver import ThreadComm, ThreadHub
+    hub = ThreadHub(world)
+    got = [None] * world
+    th = [threading.Thread(target=lambda r=r: got.__setitem__(r, _comm_ops(ThreadComm(hub, r))))
+          for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(60)
+    for r in range(world):
+        for x, e in zip(got[r], _expected(r, world)):
+            assert np.array_equal(x, e)

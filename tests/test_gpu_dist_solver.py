@@ -1,0 +1,94 @@
+"""Distributed implicit step (dsolver.py) with 2-3 ranks emulated as threads
+on one GPU (ThreadComm: host-side exchanges only, no kernel waits on another
+rank).  Each rank's rows must equal the single-GPU operator's rows, and the
+sharded step must reproduce the reference's golden steps (tolerances of
+test_gpu_solver.py)."""
+
+import copy
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle.ops import rel_l2
+from paper_1602_05650_b200 import dsolver, solver
+from test_gpu_solver import CASES
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(world, fn):
+    """fn(comm) on `world` threads, each with its own CUDA stream."""
+    import torch
+    hub = dsolver.ThreadHub(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = fn(dsolver.ThreadComm(hub, r))
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:       # noqa: BLE001 - re-raised below
+            errs.append(e)
+            hub.barrier.abort()
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("symmetric", [False, True])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_dist_rows_match_single_gpu(cuda, name, world, symmetric):
+    import torch
+    g = golden(name)
+    st = CASES[name](g)
+    dt = float(g["dt"])
+    op1 = solver.BlockOperator(st, dt)
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal(op1.layout.size)
+    ref = op1.apply(u)
+    ref_rhs = op1.rhs()
+
+    def fn(comm):
+        op = dsolver.DistBlockOperator(copy.deepcopy(st), dt, comm, symmetric=symmetric)
+        a = op.rows_device(torch.as_tensor(u, device=cuda), False).cpu().numpy()
+        b = op.rhs_device().cpu().numpy()
+        return op.owned, a, b
+    for owned, a, b in run_ranks(world, fn):
+        for lo, hi in owned:
+            assert rel_l2(a[lo:hi], ref[lo:hi]) < 1e-12
+            assert rel_l2(b[lo:hi], ref_rhs[lo:hi]) < 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_dist_steps_match_reference(cuda, name, world):
+    g = golden(name)
+    st0 = CASES[name](g)
+    params = solver.GmresParams(tolerance=float(g["tol"]))
+    dt = float(g["dt"])
+
+    def fn(comm):
+        st = copy.deepcopy(st0)
+        res = []
+        for _ in range(int(g["nsteps"])):
+            st, info = dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True)
+            res.append((np.stack([f.X for f in st.fibers]), np.stack([f.T for f in st.fibers]),
+                        info["iterations"]))
+        return res
+    results = run_ranks(world, fn)
+    for s in range(int(g["nsteps"])):
+        X, T, it = results[0][s]
+        for r in range(1, world):                      # replicated state agrees
+            assert np.array_equal(results[r][s][0], X)
+        ref = g[f"step{s}_X"]
+        assert np.linalg.norm(X - ref) / np.linalg.norm(ref) < 1e-8
+        assert rel_l2(T, g[f"step{s}_T"]) < 1e-6
+        assert abs(it - int(g[f"iters_{s}"])) <= 1
