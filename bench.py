@@ -155,7 +155,7 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------- implicit steps ----
-def measure_steps(config, count):
+def measure_steps(config, count, comm=None):
     """Implicit steps/s of the full device step (cache, self blocks, block LU,
     GMRES to tol 1e-10, state update) on BASELINE config 2 (1024-fiber aster)
     or a sedimenting cloud; one warm-up step, then `count` timed steps."""
@@ -171,20 +171,39 @@ def measure_steps(config, count):
         dt, tol = 5e-3, 1e-10
         desc = f"{config}: sedimenting cloud, {len(st.fibers)} fibers"
     params = solver.GmresParams(tolerance=tol)
-    st, info = solver.backward_euler_step(st, dt, params, return_info=True)
+    if comm is None:
+        def one(st):
+            return solver.backward_euler_step(st, dt, params, return_info=True)
+    else:
+        from paper_1602_05650_b200 import dsolver
+
+        def one(st):
+            return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True)
+
+    def sync():
+        torch.cuda.synchronize()
+        if comm is not None:
+            import torch.distributed as dist
+            dist.barrier()
+    st, info = one(st)
     times, iters = [], []
     for _ in range(count):
-        torch.cuda.synchronize()
+        sync()
         t0 = time.perf_counter()
-        st, info = solver.backward_euler_step(st, dt, params, return_info=True)
+        st, info = one(st)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
         iters.append(info["iterations"])
+    if comm is not None:                       # max over ranks, per step
+        t = torch.tensor(times, dtype=torch.float64, device="cuda")
+        comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
+        times = t.tolist()
     return {"config": desc, "dt": dt, "gmres_tol": tol, "steps": count,
+            "ranks": 1 if comm is None else comm.world,
             "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
             "gmres_iterations": iters,
             "timing": "wall clock around each full step (host orchestration included), "
-                      "after one warm-up step"}
+                      "after one warm-up step; max over ranks"}
 
 
 # ---------------------------------------------------------------- ours (GPU) ----
@@ -284,8 +303,10 @@ def run_ours(args, rank, world, local_rank):
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
 
     steps = None
-    if args.step_config and world == 1:
-        steps = measure_steps(args.step_config, args.step_count)
+    if args.step_config:
+        from paper_1602_05650_b200.dsolver import TorchComm
+        steps = measure_steps(args.step_config, args.step_count,
+                              TorchComm() if world > 1 else None)
 
     lines = None
     if rank == 0:

@@ -255,12 +255,11 @@ class DistBlockOperator:
                                       tsl=self.cache_surf.periphery_slice))
         # surface densities in cache order: (slice in u) for every surface, every rank
         self.dens_sl = list(lay.q1) + ([lay.q0] if lay.q0 is not None else [])
-        # owned index ranges of the unknown vector
-        self.owned = []
-        if rank == 0 and fo:
-            self.owned.append((0, fo))
-        if no:
-            self.owned.append((fo + 4 * n * o, fo + 4 * n * (o + no)))
+        # owned entries of the unknown vector: one contiguous range per rank
+        # (rank 0's surface/particle block sits right before its fibers)
+        lo = 0 if rank == 0 else fo + 4 * n * o
+        self.own_lo, self.own_hi = lo, fo + 4 * n * (o + no)
+        self.owned = [(self.own_lo, self.own_hi)] if self.own_hi > self.own_lo else []
         # scratch
         self._f_pad = torch.zeros((max(self.per, 1) * n, 3), **f64)
         self._f_full = torch.zeros((world * max(self.per, 1) * n, 3), **f64)
@@ -410,25 +409,33 @@ class DistPreconditioner:
 
 # ----------------------------------------------------------------- GMRES ----
 def dist_gmres_solve(op, prec, rhs, params=None):
-    """solver.gmres_solve (solver.py:444-516) over the ranks' owned entries:
-    every inner product is a local deterministic dot plus an all-reduce."""
+    """solver.gmres_solve (solver.py:444-516) over the ranks' owned entries.
+    Every inner product is a local deterministic dot over the rank's range
+    plus an in-place all-reduce of the scalar, stream-ordered (NCCL), so the
+    modified Gram-Schmidt loop needs no host sync; the Hessenberg column
+    comes to the host once per iteration."""
     import torch
     if params is None:
         params = GmresParams()
     comm = op.comm
     dev = op.device
     n = rhs.numel()
+    lo, hi = op.own_lo, op.own_hi
     work = torch.empty(296, dtype=torch.float64, device=dev)
-    loc = torch.zeros(4, dtype=torch.float64, device=dev)
     st = _stream()
+    R = params.restart
+    hcol = torch.zeros(R + 2, dtype=torch.float64, device=dev)
+    scal = torch.zeros(1, dtype=torch.float64, device=dev)
 
-    def dot(x, y):
-        loc.zero_()
-        for k, (a, b) in enumerate(op.owned):
-            _native.call("sf_dot", _ptr(x[a:b]), _ptr(y[a:b]), b - a, _ptr(work), _ptr(loc[k:k + 1]),
+    def dot_into(x, y, out, root=False):
+        if hi > lo:
+            _native.call("sf_dot", _ptr(x[lo:hi]), _ptr(y[lo:hi]), hi - lo, _ptr(work), _ptr(out),
                          0, st)
-        s = loc[0:1] + loc[1:2]
-        return comm.all_reduce_sum(s)
+        else:
+            out.zero_()
+        comm.all_reduce_sum(out)
+        if root:
+            out.sqrt_()
 
     def M(v):
         return prec.apply_device(v)
@@ -437,16 +444,17 @@ def dist_gmres_solve(op, prec, rhs, params=None):
         return op.rows_device(v, False)
 
     b = M(rhs)
-    beta0 = math.sqrt(float(dot(b, b).item()))
+    dot_into(b, b, scal, root=True)
+    beta0 = float(scal.item())
     if beta0 == 0.0:
         return torch.zeros(n, dtype=torch.float64, device=dev), 0, [0.0]
     x = torch.zeros(n, dtype=torch.float64, device=dev)
-    R = params.restart
     V = torch.zeros((R + 1, n), dtype=torch.float64, device=dev)
     history, iters = [], 0
     while True:
         r = b - M(A(x)) if iters else b
-        beta = math.sqrt(float(dot(r, r).item()))
+        dot_into(r, r, scal, root=True)
+        beta = float(scal.item())
         if beta / beta0 <= params.tolerance:
             return x, iters, history or [beta / beta0]
         V[0].copy_(r / beta)
@@ -456,12 +464,14 @@ def dist_gmres_solve(op, prec, rhs, params=None):
         k = 0
         while k < R and iters < params.max_iterations:
             w = M(A(V[k])).contiguous()
-            wnorm = math.sqrt(float(dot(w, w).item()))
-            for j in range(k + 1):
-                h = dot(V[j], w)
-                _native.call("sf_axpy_dev", _ptr(h), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
-                H[j, k] = float(h.item())
-            H[k + 1, k] = math.sqrt(float(dot(w, w).item()))
+            dot_into(w, w, hcol[R + 1:R + 2], root=True)               # wnorm
+            for j in range(k + 1):                                       # modified Gram-Schmidt
+                dot_into(V[j], w, hcol[j:j + 1])
+                _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
+            dot_into(w, w, hcol[k + 1:k + 2], root=True)
+            hh = hcol.cpu().numpy()
+            wnorm = float(hh[R + 1])
+            H[:k + 2, k] = hh[:k + 2]
             for j in range(k):
                 tmp = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
                 H[j + 1, k] = -sn[j] * H[j, k] + cs[j] * H[j + 1, k]
@@ -477,7 +487,8 @@ def dist_gmres_solve(op, prec, rhs, params=None):
             history.append(rel)
             breakdown = H[k + 1, k] <= 1e-12 * max(wnorm, 1e-300)
             if not breakdown:
-                V[k + 1].copy_(w / H[k + 1, k])
+                _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]),
+                             n, st)
             k += 1
             if rel <= params.tolerance or breakdown:
                 break
