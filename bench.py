@@ -42,8 +42,11 @@ def parse():
     ap.add_argument("--mode", default="fp64", choices=["fp64", "fp32c"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--step-config", default="c2", help="implicit-step workload ('' to skip)")
-    ap.add_argument("--step-count", type=int, default=3)
+    ap.add_argument("--step-config", default="c2,c5",
+                    help="implicit-step workloads, comma separated ('' to skip)")
+    ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
+    ap.add_argument("--big-step-count", type=int, default=1,
+                    help="timed steps of c3/c5 (about 38 s each on one GPU at c5)")
     return ap.parse_args()
 
 
@@ -155,7 +158,7 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------- implicit steps ----
-def measure_steps(config, count, comm=None):
+def measure_steps(config, count, comm=None, warm=True):
     """Implicit steps/s of the full device step (cache, self blocks, block LU,
     GMRES to tol 1e-10, state update) on BASELINE config 2 (1024-fiber aster)
     or a sedimenting cloud; one warm-up step, then `count` timed steps."""
@@ -185,7 +188,8 @@ def measure_steps(config, count, comm=None):
         if comm is not None:
             import torch.distributed as dist
             dist.barrier()
-    st, info = one(st)
+    if warm:
+        st, info = one(st)
     times, iters = [], []
     for _ in range(count):
         sync()
@@ -203,7 +207,9 @@ def measure_steps(config, count, comm=None):
             "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
             "gmres_iterations": iters,
             "timing": "wall clock around each full step (host orchestration included), "
-                      "after one warm-up step; max over ranks"}
+                      + ("after one warm-up step" if warm else
+                         "no warm-up step of its own (the preceding step runs warmed the path)")
+                      + "; max over ranks"}
 
 
 # ---------------------------------------------------------------- ours (GPU) ----
@@ -302,17 +308,23 @@ def run_ours(args, rank, world, local_rank):
         traffic = sum(float(m[k][1].replace(",", "")) * gb.get(m[k][0], 1.0)
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
 
-    steps = None
+    steps = []
     if args.step_config:
         from paper_1602_05650_b200.dsolver import TorchComm
-        steps = measure_steps(args.step_config, args.step_count,
-                              TorchComm() if world > 1 else None)
+        comm = TorchComm() if world > 1 else None
+        for k, cfg in enumerate(c for c in args.step_config.split(",") if c):
+            big = cfg in ("c3", "c5")
+            try:
+                steps.append(measure_steps(cfg, args.big_step_count if big else args.step_count,
+                                           comm, warm=not (big and k > 0)))
+            except Exception as err:      # noqa: BLE001 - reported in the JSON line
+                steps.append({"config": cfg, "error": f"{type(err).__name__}: {err}"})
 
     lines = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rows = max(64, int(round(3e9 / cloud.n_points / 2)))
+            rows = max(64, int(round(2e10 / cloud.n_points)))     # ~13 s on 16 host cores
             rate, dt, npairs, threads = cpu_pair_rate(cloud.X, f_all, cloud.eps, rows)
             cpu = {"value": rate, "unit": "pair-interactions/s", "cores": threads, "kind": "port",
                    "sample": f"{rows} target rows x {cloud.n_points} sources, Stokeslet + doublet "

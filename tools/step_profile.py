@@ -15,7 +15,8 @@ st = {"c2": lambda: configs.aster(n_fibers=1024), "c4": lambda: configs.confined
 dt = 1e-3 if cfg in ("c2", "c4") else 5e-3
 tol = 1e-8 if cfg == "c4" else 1e-10
 params = solver.GmresParams(tolerance=tol)
-solver.backward_euler_step(st, dt, params)   # warm-up
+if os.environ.get("STEP_WARMUP", "1") != "0":
+    solver.backward_euler_step(st, dt, params)   # warm-up
 
 
 def lap(t0, label):
@@ -25,7 +26,7 @@ def lap(t0, label):
     return t
 
 
-for rep in range(2):
+for rep in range(int(os.environ.get("STEP_REPS", "2"))):
     t = time.perf_counter()
     cache = InteractionCache(st)
     t = lap(t, "InteractionCache")
