@@ -299,6 +299,13 @@ int sf_axpy_dev(const double *a, double sgn, int mode, const double *x, double *
                 void *stream);
 int sf_combine(const double *V, int64_t ld, int k, const double *coef, double *x, int64_t n,
                void *stream);
+/* One Arnoldi step's modified Gram-Schmidt (solver.py:472-486) in one
+ * cooperative launch: hcol[R+1] = |w|; for j <= k: hcol[j] = V_j.w,
+ * w -= hcol[j] V_j; hcol[k+1] = |w|; V_{k+1} = w / hcol[k+1].  Bitwise equal
+ * to the sf_dot / sf_axpy_dev sequence.  V rows of length ld (R+1 rows,
+ * k+1 <= R); work >= 4*296 doubles. */
+int sf_gmres_mgs(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol, int R,
+                 double *work, void *stream);
 
 /* Near-field map construction on the device.
  * sf_near_search: (fiber, target) pairs whose minimum node distance is below

@@ -67,6 +67,7 @@ _SIGNATURES = {
     "sf_dot": [_P, _P, _I64, _P, _P, _I, _P],
     "sf_axpy_dev": [_P, _D, _I, _P, _P, _I64, _P],
     "sf_combine": [_P, _I64, _I, _P, _P, _I64, _P],
+    "sf_gmres_mgs": [_P, _I64, _I, _P, _I64, _P, _I, _P, _P],
     "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P],

@@ -7,6 +7,8 @@
 // CTA per fiber with the fiber's small operators staged in shared memory.
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "sf_common.cuh"
 #include "sf_internal.h"
 
@@ -977,6 +979,97 @@ __global__ void combine_kernel(const double *__restrict__ V, int64_t ld, int k,
     }
 }
 
+// One GMRES Arnoldi orthogonalisation (solver.py:472-486, modified
+// Gram-Schmidt) in a single cooperative launch.  Bitwise equal to the
+// sequence sf_dot(w,w,sqrt) ; for j<=k { sf_dot(V_j,w) ; w -= h_j V_j } ;
+// sf_dot(w,w,sqrt) ; V_{k+1} = w / h_{k+1}: every block owns the same
+// index set as dot_partial_kernel, so the axpy of step j-1 and the partial
+// dot of step j fuse into one pass over the block's indices, and every
+// block reduces the block partials in dot_final_kernel's order.  One grid
+// barrier per inner product instead of three launches.
+__device__ __forceinline__ double block_reduce_dot(double s, double *red) {
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double v = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kDotThreads / 32; ++k) v += red[k];
+    __syncthreads();
+    return v;   // valid on thread 0
+}
+__device__ __forceinline__ double final_reduce(const double *part, double *red,
+                                               double *bcast) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) s += __ldcg(part + i);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int k = 0; k < kDotThreads / 32; ++k) v += red[k];
+        *bcast = v;
+    }
+    __syncthreads();
+    const double v = *bcast;
+    __syncthreads();
+    return v;
+}
+__global__ void __launch_bounds__(kDotThreads)
+mgs_kernel(double *__restrict__ V, int64_t ld, int k, double *__restrict__ w, int64_t n,
+           double *__restrict__ hcol, int R, double *__restrict__ part) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[kDotThreads / 32];
+    __shared__ double bc;
+    const int64_t i0 = (int64_t)blockIdx.x * kDotThreads + threadIdx.x;
+    const int64_t stride = (int64_t)kDotBlocks * kDotThreads;
+    // pass 0: |w|^2 and V_0 . w
+    {
+        double s0 = 0.0, s1 = 0.0;
+        for (int64_t i = i0; i < n; i += stride) {
+            const double wi = w[i];
+            s0 = fma(wi, wi, s0);
+            s1 = fma(V[i], wi, s1);
+        }
+        const double b0 = block_reduce_dot(s0, red);
+        const double b1 = block_reduce_dot(s1, red);
+        if (threadIdx.x == 0) {
+            part[blockIdx.x] = b0;
+            part[kDotBlocks + blockIdx.x] = b1;
+        }
+    }
+    grid.sync();
+    const double wn = sqrt(final_reduce(part, red, &bc));
+    double h = final_reduce(part + kDotBlocks, red, &bc);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        hcol[R + 1] = wn;
+        hcol[0] = h;
+    }
+    for (int j = 1; j <= k + 1; ++j) {
+        // w -= h_{j-1} V_{j-1}; then V_j . w (j <= k) or |w|^2 (j = k + 1)
+        const double al = -1.0 * h;
+        const double *Vp = V + (int64_t)(j - 1) * ld;
+        const double *Vj = V + (int64_t)(j <= k ? j : 0) * ld;
+        double s = 0.0;
+        for (int64_t i = i0; i < n; i += stride) {
+            const double wi = fma(al, Vp[i], w[i]);
+            w[i] = wi;
+            s = (j <= k) ? fma(Vj[i], wi, s) : fma(wi, wi, s);
+        }
+        double *pb = part + (int64_t)(2 + (j & 1)) * kDotBlocks;
+        const double b = block_reduce_dot(s, red);
+        if (threadIdx.x == 0) pb[blockIdx.x] = b;
+        grid.sync();
+        h = final_reduce(pb, red, &bc);
+        if (j == k + 1) h = sqrt(h);
+        if (blockIdx.x == 0 && threadIdx.x == 0) hcol[j] = h;
+    }
+    // V_{k+1} = w / h_{k+1}
+    const double inv = 1.0 / h;
+    double *Vn = V + (int64_t)(k + 1) * ld;
+    for (int64_t i = i0; i < n; i += stride) Vn[i] = w[i] * inv;
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -1133,6 +1226,26 @@ int sf_dot(const double *x, const double *y, int64_t n, double *work, double *ou
     dot_partial_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(x, y, n, work);
     dot_final_kernel<<<1, kDotThreads, 0, st>>>(work, out, sqrt_mode);
     return check_launch("dot");
+}
+
+int sf_gmres_mgs(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol, int R,
+                 double *work, void *stream) {
+    if (k < 0 || k + 1 > R || n < 0) return set_error(SF_EINVAL, "bad Arnoldi sizes");
+    if (n > 0 && (!V || !w || !hcol || !work)) return set_error(SF_EINVAL, "null pointer");
+    static int resident = -1;
+    if (resident < 0) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mgs_kernel, kDotThreads, 0);
+        resident = sms * per;
+    }
+    if (resident < kDotBlocks) return set_error(SF_ECUDA, "cooperative MGS grid not co-resident");
+    void *args[] = {&V, &ld, &k, &w, &n, &hcol, &R, &work};
+    if (cudaLaunchCooperativeKernel((const void *)mgs_kernel, dim3(kDotBlocks), dim3(kDotThreads),
+                                    args, 0, (cudaStream_t)stream) != cudaSuccess)
+        return check_launch("mgs_kernel");
+    return SF_OK;
 }
 
 int sf_axpy_dev(const double *a, double sgn, int mode, const double *x, double *y, int64_t n,

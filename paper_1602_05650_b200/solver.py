@@ -15,6 +15,7 @@ and stays on the host.
 import ctypes
 import logging
 import math
+import os
 
 import numpy as np
 
@@ -402,7 +403,7 @@ class _DeviceVectors:
 
     def __init__(self, device):
         import torch
-        self.work = torch.empty(296, dtype=torch.float64, device=device)
+        self.work = torch.empty(4 * 296, dtype=torch.float64, device=device)
 
     def dot_into(self, x, y, out, sqrt_mode=False):
         _native.call("sf_dot", _ptr(x), _ptr(y), x.numel(), _ptr(self.work), _ptr(out),
@@ -448,6 +449,7 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
     vec = _DeviceVectors(device)
     st = _stream()
     n = rhs_d.numel()
+    fused = os.environ.get("SF_GMRES_FUSED", "1") != "0"
 
     def ret(x):
         return x.cpu().numpy() if host_io else x
@@ -481,11 +483,17 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
         k = 0
         while k < R and iters < params.max_iterations:
             w = apply_m(apply_a(V[k])).contiguous()
-            vec.dot_into(w, w, hcol[R + 1:R + 2], sqrt_mode=True)   # wnorm
-            for j in range(k + 1):                                   # modified Gram-Schmidt
-                vec.dot_into(V[j], w, hcol[j:j + 1])
-                _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
-            vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
+            if fused:
+                # wnorm, modified Gram-Schmidt, |w| and V[k+1] = w/|w| in one launch
+                _native.call("sf_gmres_mgs", _ptr(V), n, k, _ptr(w), n, _ptr(hcol), R,
+                             _ptr(vec.work), st)
+            else:
+                vec.dot_into(w, w, hcol[R + 1:R + 2], sqrt_mode=True)   # wnorm
+                for j in range(k + 1):                                   # modified Gram-Schmidt
+                    vec.dot_into(V[j], w, hcol[j:j + 1])
+                    _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w),
+                                 n, st)
+                vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
             hh = hcol.cpu().numpy()
             wnorm = float(hh[R + 1])
             H[:k + 2, k] = hh[:k + 2]
@@ -503,7 +511,7 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
             rel = abs(g[k + 1]) / beta0
             history.append(rel)
             breakdown = H[k + 1, k] <= 1e-12 * max(wnorm, 1e-300)
-            if not breakdown:
+            if not breakdown and not fused:
                 _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]),
                              n, st)
             k += 1

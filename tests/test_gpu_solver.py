@@ -118,3 +118,39 @@ def test_c3_physics_step_uses_device_lu(cuda):
     assert hist[-1] <= 1e-10 and it < 60
     res = op.apply(x.cpu().numpy()) - rhs.cpu().numpy()
     assert np.linalg.norm(res) <= 1e-6 * np.linalg.norm(rhs.cpu().numpy())
+
+
+@pytest.mark.parametrize("k", [0, 1, 7])
+def test_fused_mgs_bitwise_equals_dot_axpy_sequence(cuda, k):
+    """sf_gmres_mgs (one cooperative launch) reproduces the sf_dot /
+    sf_axpy_dev modified Gram-Schmidt sequence bit for bit."""
+    import torch
+    from paper_1602_05650_b200 import _native
+    R, n = 10, 134_150
+    g = torch.Generator(device="cpu").manual_seed(k)
+    V = torch.randn((R + 1, n), generator=g, dtype=torch.float64).to(cuda)
+    w0 = torch.randn(n, generator=g, dtype=torch.float64).to(cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    work = torch.empty(4 * 296, dtype=torch.float64, device=cuda)
+    # reference sequence
+    V1, w1 = V.clone(), w0.clone()
+    h1 = torch.zeros(R + 2, dtype=torch.float64, device=cuda)
+    _native.call("sf_dot", w1.data_ptr(), w1.data_ptr(), n, work.data_ptr(), h1[R + 1:].data_ptr(),
+                 1, st)
+    for j in range(k + 1):
+        _native.call("sf_dot", V1[j].data_ptr(), w1.data_ptr(), n, work.data_ptr(),
+                     h1[j:].data_ptr(), 0, st)
+        _native.call("sf_axpy_dev", h1[j:].data_ptr(), -1.0, 0, V1[j].data_ptr(), w1.data_ptr(), n,
+                     st)
+    _native.call("sf_dot", w1.data_ptr(), w1.data_ptr(), n, work.data_ptr(), h1[k + 1:].data_ptr(),
+                 1, st)
+    _native.call("sf_axpy_dev", h1[k + 1:].data_ptr(), 1.0, 2, w1.data_ptr(), V1[k + 1].data_ptr(),
+                 n, st)
+    # fused
+    V2, w2 = V.clone(), w0.clone()
+    h2 = torch.zeros(R + 2, dtype=torch.float64, device=cuda)
+    _native.call("sf_gmres_mgs", V2.data_ptr(), n, k, w2.data_ptr(), n, h2.data_ptr(), R,
+                 work.data_ptr(), st)
+    assert torch.equal(h1, h2)
+    assert torch.equal(w1, w2)
+    assert torch.equal(V1, V2)
