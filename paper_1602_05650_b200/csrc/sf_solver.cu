@@ -802,6 +802,120 @@ __global__ void block_solve_kernel(const double *__restrict__ LU, const double *
     for (int i = threadIdx.x; i < mdim; i += blockDim.x) xb[i] = y[i] / c[i];
 }
 
+// Warp-per-block variant for m <= 32*MT: y lives in registers (row
+// i = 32 t + lane in y[t]), column k of the factor is read coalesced and
+// the pivot y_k is broadcast by shuffle, so a substitution step is one
+// shuffle + FMA instead of a block barrier; the fully unrolled column loop
+// lets the loads of later columns issue ahead of the dependency chain.
+// The upper solve multiplies by the reciprocal diagonal (computed off the
+// chain), equal to the division to rounding.
+constexpr int kSolveWarps = 4;
+template <int MT>
+__global__ void __launch_bounds__(32 * kSolveWarps)
+block_solve_warp_kernel(const double *__restrict__ LU, const double *__restrict__ rsc,
+                        const double *__restrict__ csc, const int *__restrict__ piv, int mdim,
+                        int64_t nb, int64_t off0, const double *__restrict__ v,
+                        double *__restrict__ x) {
+    __shared__ double ys_all[kSolveWarps][32 * MT];
+    __shared__ int ps_all[kSolveWarps][32 * MT];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * kSolveWarps + wid;
+    if (b >= nb) return;
+    double *ys = ys_all[wid];
+    int *ps = ps_all[wid];
+    const int m = mdim;
+    const double *L = LU + (int64_t)m * m * b;
+    const double *vb = v + off0 + (int64_t)m * b;
+    const double *r = rsc + (int64_t)m * b;
+    const int *pv = piv + (int64_t)m * b;
+    for (int i = lane; i < m; i += 32) {
+        ys[i] = vb[i] / r[i];
+        ps[i] = pv[i];
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int k = 0; k < m; ++k) {
+            const int p = ps[k];
+            if (p != k) { const double tmp = ys[k]; ys[k] = ys[p]; ys[p] = tmp; }
+        }
+    __syncwarp();
+    double y[MT], inv[MT];
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+        const int i = 32 * t + lane;
+        y[t] = i < m ? ys[i] : 0.0;
+        inv[t] = i < m ? 1.0 / __ldg(L + (int64_t)i * m + i) : 0.0;
+    }
+    constexpr int kSolveChunk = MT >= 7 ? 4 : 8;   // register budget at m = 256
+    // Columns are consumed in chunks of kSolveChunk: a chunk's factor values
+    // are loaded into registers up front (independent of the chain), so the
+    // load latency is paid once per chunk and overlaps the previous chunk.
+    // unit lower: y_i -= L_ik y_k for i > k
+#pragma unroll
+    for (int kt = 0; kt < MT; ++kt) {
+#pragma unroll
+        for (int kc = 0; kc < 32; kc += kSolveChunk) {
+            double Lc[kSolveChunk][MT];
+#pragma unroll
+            for (int q = 0; q < kSolveChunk; ++q) {
+                const int k = 32 * kt + kc + q;
+#pragma unroll
+                for (int t = kt; t < MT; ++t) {
+                    const int i = 32 * t + lane;
+                    Lc[q][t] = (k < m && i < m) ? __ldg(L + (int64_t)k * m + i) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kSolveChunk; ++q) {
+                const int k = 32 * kt + kc + q;
+                const double yk = __shfl_sync(0xffffffffu, y[kt], kc + q);
+#pragma unroll
+                for (int t = kt; t < MT; ++t) {
+                    const int i = 32 * t + lane;
+                    if (i > k) y[t] = fma(-Lc[q][t], yk, y[t]);
+                }
+            }
+        }
+    }
+    // upper: y_k /= U_kk; y_i -= U_ik y_k for i < k
+#pragma unroll
+    for (int kt = MT - 1; kt >= 0; --kt) {
+#pragma unroll
+        for (int kc = 32 - kSolveChunk; kc >= 0; kc -= kSolveChunk) {
+            double Uc[kSolveChunk][MT];
+#pragma unroll
+            for (int q = kSolveChunk - 1; q >= 0; --q) {
+                const int k = 32 * kt + kc + q;
+#pragma unroll
+                for (int t = 0; t <= kt; ++t) {
+                    const int i = 32 * t + lane;
+                    Uc[q][t] = (k < m && i < k) ? __ldg(L + (int64_t)k * m + i) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int q = kSolveChunk - 1; q >= 0; --q) {
+                const int k = 32 * kt + kc + q;
+                if (k < m) {
+                    if (lane == kc + q) y[kt] *= inv[kt];
+                    const double yk = __shfl_sync(0xffffffffu, y[kt], kc + q);
+#pragma unroll
+                    for (int t = 0; t <= kt; ++t) {
+                        const int i = 32 * t + lane;
+                        if (i < k) y[t] = fma(-Uc[q][t], yk, y[t]);
+                    }
+                }
+            }
+        }
+    }
+    const double *c = csc + (int64_t)m * b;
+    double *xb = x + off0 + (int64_t)m * b;
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+        const int i = 32 * t + lane;
+        if (i < m) xb[i] = y[t] / c[i];
+    }
+}
+
 __global__ void diag_div_kernel(const double *__restrict__ v, const double *__restrict__ diag,
                                 int64_t n, double *__restrict__ x) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1184,6 +1298,25 @@ int sf_precond_apply(const double *LU, const double *r, const double *c, const i
         if (rc) return rc;
     }
     if (nb > 0) {
+        static const bool warp_solve = [] {
+            const char *e = getenv("SF_BLOCK_SOLVE");
+            return !(e && e[0] == '0');
+        }();
+        const unsigned g = (unsigned)((nb + kSolveWarps - 1) / kSolveWarps);
+        const int mt = (int)((m + 31) / 32);
+        if (warp_solve && mt <= 8) {
+            switch (mt) {
+#define SF_SOLVE_CASE(T)                                                                     \
+    case T:                                                                                  \
+        block_solve_warp_kernel<T><<<g, 32 * kSolveWarps, 0, st>>>(LU, r, c, piv, (int)m, nb, \
+                                                                   off0, v, x);              \
+        break;
+                SF_SOLVE_CASE(1) SF_SOLVE_CASE(2) SF_SOLVE_CASE(3) SF_SOLVE_CASE(4)
+                SF_SOLVE_CASE(5) SF_SOLVE_CASE(6) SF_SOLVE_CASE(7) SF_SOLVE_CASE(8)
+#undef SF_SOLVE_CASE
+            }
+            return check_launch("block_solve_warp_kernel");
+        }
         block_solve_kernel<<<(unsigned)nb, 128, sizeof(double) * m, st>>>(LU, r, c, piv, (int)m,
                                                                          off0, v, x);
         return check_launch("block_solve_kernel");

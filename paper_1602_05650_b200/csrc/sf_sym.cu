@@ -633,11 +633,12 @@ int sym_unit_size(int64_t N, int64_t group_size) {
     // units: a multiple of the 32-point slab (and of the fiber size when that
     // keeps them near the target, so units align to fibers), at most 2048
     // points, and small enough that the G(G+1)/2 unit-pair tasks fill the GPU
-    // several times over (G >= 48 -> >= 1176 tasks) for mid-size systems
+    // many times over (G >= 128 -> >= 8256 tasks) for mid-size systems; the
+    // sweep (tools/gpu_unit_sweep.sh) peaks at N/128..N/85 for N = 32k-64k
     const char *e = getenv("SF_SYM_UNIT");
     int64_t target = e ? atoi(e) : 2048;
     if (!e) {
-        const int64_t fill = N / 48;
+        const int64_t fill = N / 128;
         if (fill < target) target = fill;
         if (target < 256) target = 256;
     }
