@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--mode", default="fp64", choices=["fp64", "fp32c"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
     ap.add_argument("--step-config", default="c2,c5",
                     help="implicit-step workloads, comma separated ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
@@ -308,6 +309,38 @@ def run_ours(args, rank, world, local_rank):
         traffic = sum(float(m[k][1].replace(",", "")) * gb.get(m[k][0], 1.0)
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
 
+    # ---- the FP32-compute / FP64-accumulate variant on the same workload
+    variant = None
+    if args.mode == "fp64" and not args.no_variant:
+        op32 = FiberHIOperator(cloud.X, cloud.eps, device=dev, mode=_native.SF_MODE_FP32C,
+                               shard=(rank, world))
+        sop32 = ShardedHIOperator(op32)
+        u32 = torch.empty_like(u_nl)
+        for _ in range(2):
+            sop32.apply(f_local, out_nl=u32, out_self=u_self)
+        barrier()
+        v_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        v_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            v_s[k].record()
+            sop32.apply(f_local, out_nl=u32, out_self=u_self)
+            v_e[k].record()
+        barrier()
+        vms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(v_s, v_e)) / args.steps],
+                           dtype=torch.float64, device=dev)
+        sop.apply(f_local, out_nl=u_nl, out_self=u_self)            # FP64 reference rows
+        err = torch.stack([((u32 - u_nl) ** 2).sum(), (u_nl ** 2).sum()])
+        if world > 1:
+            dist.all_reduce(vms, op=dist.ReduceOp.MAX)
+            dist.all_reduce(err)
+        vms = float(vms.item())
+        variant = {"dtype": "f32-compute/f64-accumulate", "value": total_pairs / (vms * 1e-3),
+                   "unit": "pair-interactions/s", "ms_per_step": vms,
+                   "rel_l2_vs_fp64": float((err[0] / err[1]).sqrt().item()),
+                   "tolerance": 1e-5}
+        del op32, sop32, u32
+
     steps = []
     if args.step_config:
         from paper_1602_05650_b200.dsolver import TorchComm
@@ -362,6 +395,7 @@ def run_ours(args, rank, world, local_rank):
                     "d2h_bytes_per_step": int(2 * cloud.n_points * 3 * 8)},
             "gpu_launches": args.steps * op.launches_per_apply,
             "clocks": clocks,
+            "variant_fp32c": variant,
             "implicit_steps": steps,
         }
         print(json.dumps(lines), flush=True)

@@ -849,7 +849,11 @@ constexpr int kTargetsPerCta = kNT * kTB;
 int choose_split(int64_t nt, int64_t ns) {
     const int64_t blocks = (nt + kTargetsPerCta - 1) / kTargetsPerCta;
     int64_t s = (16384 + blocks - 1) / blocks;
-    const int64_t max_s = ns / (4 * kTS);
+    int64_t max_s = ns / (4 * kTS);
+    // small problems: split down to one source tile per CTA if that is what
+    // it takes to give every SM two CTAs
+    const int64_t fill = (2 * 148 + blocks - 1) / blocks;
+    if (max_s < fill) max_s = fill < ns / kTS ? fill : ns / kTS;
     if (s > max_s) s = max_s;
     if (s > 256) s = 256;
     return s < 1 ? 1 : (int)s;
