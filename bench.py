@@ -291,16 +291,26 @@ def run_ours(args, rank, world, local_rank):
     fs = sop.gather_sources(f_local)
     r_s = torch.cuda.Event(enable_timing=True)
     r_e = torch.cuda.Event(enable_timing=True)
-    op.apply(fs, out_nl=u_nl, self_terms=False)
+    if op.symmetric_shard:       # N > 1: this rank's share of the unit-pair tasks
+        part = torch.empty((op.N, 3), dtype=torch.float64, device=dev)
+
+        def dominant():
+            op.symmetric_partial(fs, out=part)
+        rank_pairs = _native.load().sf_sym_shard_pairs(op.N, op.n, rank, world)
+    else:
+        def dominant():
+            op.apply(fs, out_nl=u_nl, self_terms=False)
+        rank_pairs = op.pairs_per_apply
+    dominant()
     torch.cuda.synchronize()
     r_s.record()
     for _ in range(reps):
-        op.apply(fs, out_nl=u_nl, self_terms=False)
+        dominant()
     r_e.record()
     torch.cuda.synchronize()
     pair_ms = r_s.elapsed_time(r_e) / reps
     peak_flops, _ = kernels.dfma_peak(1 << 15)
-    achieved = op.pairs_per_apply * FLOPS_PER_PAIR / (pair_ms * 1e-3)
+    achieved = rank_pairs * FLOPS_PER_PAIR / (pair_ms * 1e-3)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01_ncu_sym_c5_metrics.json")
     if args.config == "c5" and world == 1 and op.symmetric and os.path.exists(prof):
@@ -413,8 +423,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # SF_DIST_BACKEND=gloo: functional check of the multi-rank code path
+        # with host-side collectives (never a scaling number)
+        backend = os.environ.get("SF_DIST_BACKEND", "nccl")
+        if backend != "nccl":
+            local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -1,6 +1,7 @@
 // sf_abi.cu — the extern "C" boundary (include/sf_b200.h): argument checks,
 // error reporting, per-stream workspaces, host-buffer drop-ins, and the FP64
 // DFMA peak microbenchmark used as the roofline denominator.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -259,6 +260,41 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
 }
 
 extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt, ns); }
+
+extern "C" int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world) {
+    if (N <= 0 || world < 1 || rank < 0 || rank >= world) return 0;
+    const int64_t M = sf::sym_unit_size(N, group_size);
+    const int64_t G = (N + M - 1) / M;
+    int64_t count = 0;
+    const int64_t t0 = sf::sym_task_range(G, rank, world, &count);
+    auto units = [&](int64_t t, int64_t &g, int64_t &h) {   // row-major {g <= h}
+        int64_t r = 0, start = 0;
+        while (start + (G - r) <= t) { start += G - r; ++r; }
+        g = r;
+        h = r + (t - start);
+    };
+    // ordered pairs of a task minus the same-group ones (groups are the
+    // contiguous ranges [k*group_size, (k+1)*group_size))
+    auto excluded = [&](int64_t a0, int64_t a1, int64_t b0, int64_t b1) {
+        if (group_size <= 0) return (int64_t)0;
+        int64_t e = 0;
+        for (int64_t k = a0 / group_size; k * group_size < a1; ++k) {
+            const int64_t lo = k * group_size, hi = lo + group_size;
+            const int64_t oa = std::min(a1, hi) - std::max(a0, lo);
+            const int64_t ob = std::min(b1, hi) - std::max(b0, lo);
+            if (oa > 0 && ob > 0) e += oa * ob;
+        }
+        return e;
+    };
+    int64_t g, h, pairs = 0;
+    for (int64_t t = t0; t < t0 + count; ++t) {
+        units(t, g, h);
+        const int64_t a0 = g * M, a1 = std::min(N, a0 + M), b0 = h * M, b1 = std::min(N, b0 + M);
+        const int64_t all = (a1 - a0) * (b1 - b0) - excluded(a0, a1, b0, b1);
+        pairs += g != h ? 2 * all : all;
+    }
+    return pairs;
+}
 
 extern "C" int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
                                         int64_t group_size, const double *f, const double *w,

@@ -66,6 +66,8 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               int rank, int world, double *out, int64_t *bad, int accumulate,
                               cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
+int sym_unit_size(int64_t N, int64_t group_size);
+int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,
                double *u, cudaStream_t st);

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kNearThreads) near_weights_kernel(NearArgs A) 
     double *pb = pa + kMaxPanels;                        // kMaxPanels
     __shared__ double s_red[kNearThreads];
     __shared__ int s_idx[kNearThreads];
-    __shared__ double s_d, s_wb;
+    __shared__ double s_wb;
     __shared__ int s_np, s_fail;
 
     const double tx = A.targets[3 * t], ty = A.targets[3 * t + 1], tz = A.targets[3 * t + 2];
@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(kNearThreads) near_weights_kernel(NearArgs A) 
         const double dx = tx - clenshaw(cx, n, a0), dy = ty - clenshaw(cx + n, n, a0),
                      dz = tz - clenshaw(cx + 2 * n, n, a0);
         const double d = sqrt(dx * dx + dy * dy + dz * dz);
-        s_d = d;
         const double Lf = A.L[l];
         s_fail = d < A.eps[l] * Lf ? 1 : 0;
         // ---- adaptive panels (fiber.py:535-549), LIFO as the reference

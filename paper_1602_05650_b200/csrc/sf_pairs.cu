@@ -880,7 +880,6 @@ template <class P>
 static int launch_pairs(PairArgs a, cudaStream_t st, Workspace &ws) {
     if (a.nt == 0) return 0;
     a.nsplit = choose_split(a.nt, a.ns);
-    const int64_t blocks = (a.nt + kTargetsPerCta - 1) / kTargetsPerCta;
     a.chunk = (a.ns + a.nsplit - 1) / a.nsplit;
     a.chunk = ((a.chunk + kTS - 1) / kTS) * kTS;
     if (a.nsplit > 1) {

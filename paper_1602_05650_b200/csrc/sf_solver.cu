@@ -234,7 +234,7 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
         for (int col = lane; col < n3; col += 32) acc = fma(K[(int64_t)r * n3 + col], f[col], acc);
         acc = warp_sum(acc);
         if (lane == 0) {
-            const int i = r / 3, a = r - 3 * i;
+            const int i = r / 3;
             const double fdt = f[3 * i] * t[3 * i] + f[3 * i + 1] * t[3 * i + 1] + f[3 * i + 2] * t[3 * i + 2];
             const double ft = fdt * t[r];
             const double mob = cl * (f[r] + ft) + c2 * (f[r] - ft);

@@ -57,7 +57,6 @@ struct SymArgs {
 };
 
 constexpr int kSymThreads = 128;
-constexpr int kSymI = 64;  // i points per sub-block (2 per lane)
 
 struct PData {
     double x, y, z, fx, fy, fz, c, c3;
@@ -676,8 +675,34 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
 // ranges of the G(G+1)/2 tasks.  out receives this rank's contribution to
 // EVERY point (slots of other ranks' tasks are zero); summing `out` over
 // ranks (reduce-scatter) gives the full sum.
-int64_t sym_task_range(int64_t ntasks, int rank, int world, int64_t *count) {
-    const int64_t b = ntasks * rank / world, e = ntasks * (rank + 1) / world;
+// Contiguous task range of `rank`, balanced by cost: off-diagonal tasks
+// evaluate twice the pairs of a diagonal one.  Tasks run row by row, each row
+// g = {g,g}, {g,g+1}, ..., {g,G-1} starting with its diagonal, so the cost of
+// the first t tasks is 2t - (rows started before t).
+int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count) {
+    const int64_t ntasks = G * (G + 1) / 2;
+    auto start = [&](int64_t row) { return row * G - row * (row - 1) / 2; };
+    auto cost = [&](int64_t t) {   // cost of tasks [0, t)
+        int64_t lo = 0, hi = G;    // rows with start(row) < t
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (start(mid) < t) lo = mid + 1; else hi = mid;
+        }
+        return 2 * t - lo;
+    };
+    const int64_t total = 2 * ntasks - G;
+    auto boundary = [&](int r) {   // first task whose prefix cost reaches r/world of the total
+        if (r <= 0) return (int64_t)0;
+        if (r >= world) return ntasks;
+        const int64_t want = (total * r + world - 1) / world;
+        int64_t lo = 0, hi = ntasks;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (cost(mid) < want) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t b = boundary(rank), e = boundary(rank + 1);
     *count = e - b;
     return b;
 }
@@ -713,8 +738,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     a.N = N;
     a.M = M;
     a.G = G;
-    const int64_t all_tasks = (int64_t)G * (G + 1) / 2;
-    a.task0 = sym_task_range(all_tasks, rank, world, &a.ntasks);
+    a.task0 = sym_task_range(G, rank, world, &a.ntasks);
     a.part = part;
     if (world > 1 &&
         cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)N * G, st) != cudaSuccess)

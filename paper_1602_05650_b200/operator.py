@@ -179,7 +179,7 @@ class FiberHIOperator:
         """Near corrections and self terms of this rank's targets, after the
         pair sums of every rank were summed into u_own (Nown,3)."""
         import torch
-        f = torch.as_tensor(f, dtype=torch.float64, device=self.device).contiguous()
+        f = torch.as_tensor(f, dtype=torch.float64, device=self.device).reshape(-1, 3).contiguous()
         nm = self.near
         st = _stream()
         if nm.nrows:

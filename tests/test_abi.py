@@ -13,7 +13,7 @@ HEADER = os.path.join(os.path.dirname(__file__), "..", "include", "sf_b200.h")
 
 def declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(sf_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char \*)\s*(sf_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_abi():
@@ -36,3 +36,16 @@ def test_binding_covers_header():
 def test_abi_version_callable_without_gpu():
     lib = _native.load()
     assert lib.sf_abi_version() == 1
+
+
+def test_symmetric_shard_pair_counts_cover_all_pairs():
+    """sf_sym_shard_pairs (host function): the ranks' task shares of the
+    symmetric evaluation add up to every non-excluded ordered pair."""
+    lib = _native.load()
+    for N, n in ((1048576, 64), (32768, 32), (401 * 24, 24), (200 * 64, 64)):
+        full = N * N - (N // n) * n * n
+        for world in (1, 2, 3, 8):
+            parts = [lib.sf_sym_shard_pairs(N, n, r, world) for r in range(world)]
+            assert sum(parts) == full
+            if N >= 32768:            # balanced to within a task or two at real sizes
+                assert max(parts) - min(parts) <= 0.005 * full / world

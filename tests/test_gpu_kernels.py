@@ -240,3 +240,25 @@ def test_symmetric_fp32c_variant(cuda):
 def torch_equal(x, y):
     import torch
     return bool(torch.equal(x, y))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_operator_ranks_match_single_gpu(cuda, world):
+    """The multi-GPU operator flow of dist.ShardedHIOperator emulated on one
+    GPU: every rank's symmetric partial for all points, summed (the
+    reduce-scatter), then each rank's near + self terms for its own targets,
+    with the all-gathered (nf, n, 3) force array as the dist layer passes it."""
+    import torch
+    from paper_1602_05650_b200._native import SF_MODE_FP64
+    cl, F = _cloud_operator_inputs(200, 64)
+    Fd = torch.as_tensor(F, device=cuda).reshape(cl.X.shape[0], cl.X.shape[1], 3)
+    one = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP64)
+    u1, s1 = one.apply(Fd)
+    ops = [FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP64, shard=(r, world)) for r in range(world)]
+    assert all(op.symmetric_shard for op in ops)
+    total = sum(op.symmetric_partial(Fd) for op in ops)
+    for op in ops:
+        lo, hi = op.f0 * op.n, (op.f0 + op.nown) * op.n
+        u, s = op.finish_own(total[lo:hi].clone(), Fd)
+        assert rel(u.cpu().numpy(), u1[lo:hi].cpu().numpy()) < 1e-13
+        assert torch.equal(s, s1[lo:hi])
