@@ -333,6 +333,25 @@ int sf_near_fiber_weights(const int64_t *pt, const int64_t *pl, int64_t npairs,
                           const double *gl, const double *eps, const double *L, int64_t n,
                           double mu, int include_doublet, double *W, int *info, void *stream);
 
+/* Near-surface correction maps Wnear - Wplain (body.py:479-519,
+ * system.py:588-613) for npairs (target, surface) pairs of ONE surface.
+ * Coarse mesh: nt x nph patches of 16 Gauss-Legendre nodes (patch-major);
+ * fine mesh: the same surface at (f nt) x (f nph) patches; fcoef (Nf,8) the
+ * Lagrange coefficients (theta then phi) of each fine node in its coarse
+ * patch.  Per pair (host-computed, body.py:371-423 and :479-519): target,
+ * nearest surface point x0, the three off-surface points pts (3,3), their
+ * Lagrange weights ell (4), jump (1/mu inside a periphery, else 0), the
+ * fine patch index and 16 coefficients of the interpolation row at x0.
+ * f = 1 with the coarse mesh as "fine" mesh gives the on-surface map.
+ * work >= npairs * (9 + 148*9) doubles; W (npairs, 3, 3 Nc). */
+int sf_near_surface_weights(const double *cnodes, const double *cnrm, const double *cw,
+                            int64_t nt, int64_t nph, const double *fnodes, const double *fnrm,
+                            const double *fw, const double *fcoef, int f, int64_t npairs,
+                            const double *trg, const double *x0, const double *pts,
+                            const double *ell, const double *jump, const int64_t *r0patch,
+                            const double *r0coef, double mu, double *work, double *W,
+                            void *stream);
+
 /* Near-field correction apply (system.py:702-707): for every entry e,
  * u[t_e] += W_e (3 x 3 m_e) . x[off_e : off_e + 3 m_e].  Entries must be
  * grouped by target (row_ptr CSR over `nrows` distinct targets rows[]);

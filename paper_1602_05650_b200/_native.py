@@ -55,6 +55,8 @@ _SIGNATURES = {
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
     "sf_near_search": [_P, _P, _I64, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P],
+    "sf_near_surface_weights": [_P, _P, _P, _I64, _I64, _P, _P, _P, _P, _I, _I64, _P, _P, _P, _P,
+                                _P, _P, _P, _D, _P, _P, _P],
     "sf_near_fiber_weights": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _D, _I,
                               _P, _P, _P],
     "sf_fiber_forces": [_P, _P, _I, _P, _P],

@@ -336,3 +336,186 @@ extern "C" int sf_near_fiber_weights(const int64_t *pt, const int64_t *pl, int64
     near_weights_kernel<<<(unsigned)npairs, kNearThreads, smem, (cudaStream_t)stream>>>(A);
     return check_launch("near_weights_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Near-surface correction maps on the device (body.py:371-519 via
+// system.py:588-613): for each (target, surface) pair
+//   W = B^T [ ell_0 (P(x0) - RS (x) r0 + jump I (x) r0) + sum_k ell_k P(pt_k) ]
+//       - P_coarse(target)
+// where P(y) is the stresslet quadrature map of the upsampled ("fine") mesh
+// at the point y, RS the row sum of P(x0) over the fine nodes, r0 the fine
+// interpolation row at the nearest surface point (theta0, phi0), ell the
+// Lagrange weights of the off-surface extrapolation points and B the
+// fine-from-coarse patch interpolation.  The host supplies the per-pair
+// scalars (nearest point by the reference's golden-section search, ell,
+// pt_k, r0); the device does every O(N_fine) sum.  One CTA per (coarse
+// patch, pair): it evaluates the f*f*16 fine nodes inside its coarse patch
+// into shared memory and contracts them with their interpolation
+// coefficients in a fixed order (no atomics), so results are reproducible.
+namespace sf {
+namespace {
+constexpr int kSurfRsBlocks = 148, kSurfThreads = 160;
+
+struct SurfArgs {
+    const double *cnodes, *cnrm, *cw;   // coarse mesh (patch-major, 16 nodes per patch)
+    int64_t nt, nph;                    // coarse patch grid
+    const double *fnodes, *fnrm, *fw;   // fine mesh, patch grid (f nt, f nph)
+    const double *fcoef;                // (Nf, 8): cu[4], cv[4] of each fine node in its coarse patch
+    int f;
+    int64_t npairs;
+    const double *trg, *x0, *pts, *ell, *jump, *r0coef;   // (np,3) (np,3) (np,3,3) (np,4) (np) (np,16)
+    const int64_t *r0patch;             // (np) fine patch index of (theta0, phi0)
+    double pref;                        // -3 / (4 pi mu)
+    double *rs;                         // (np, 9) work: row sums
+    double *rs_part;                    // (np, kSurfRsBlocks, 9)
+    double *W;                          // (np, 3, 3 Nc)
+};
+
+__device__ __forceinline__ void plain_at(const double *y, const double *node, const double *nrm,
+                                         double w, double pref, double s[9]) {
+    const double r0 = y[0] - node[0], r1 = y[1] - node[1], r2 = y[2] - node[2];
+    const double d2 = r0 * r0 + r1 * r1 + r2 * r2;
+    double sc = 0.0;
+    if (d2 > 1e-24) {
+        const double nr = nrm[0] * r0 + nrm[1] * r1 + nrm[2] * r2;
+        sc = pref * w * nr / (d2 * d2 * sqrt(d2));
+    }
+    const double r[3] = {r0, r1, r2};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) s[3 * a + b] = sc * r[a] * r[b];
+}
+
+__global__ void surf_rs_partial(SurfArgs A, int64_t nf) {
+    const int64_t p = blockIdx.y;
+    const double *y = A.x0 + 3 * p;
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < nf;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double s[9];
+        plain_at(y, A.fnodes + 3 * m, A.fnrm + 3 * m, A.fw[m], A.pref, s);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) acc[e] += s[e];
+    }
+    __shared__ double red[9][kSurfThreads / 32];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+        const double v = warp_sum(acc[e]);
+        if ((threadIdx.x & 31) == 0) red[e][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        double v = 0.0;
+        for (int k = 0; k < kSurfThreads / 32; ++k) v += red[threadIdx.x][k];
+        A.rs_part[(p * kSurfRsBlocks + blockIdx.x) * 9 + threadIdx.x] = v;
+    }
+}
+
+__global__ void surf_rs_final(SurfArgs A) {
+    const int64_t p = blockIdx.x;
+    if (threadIdx.x < 9) {
+        double v = 0.0;
+        for (int k = 0; k < kSurfRsBlocks; ++k) v += A.rs_part[(p * kSurfRsBlocks + k) * 9 + threadIdx.x];
+        A.rs[p * 9 + threadIdx.x] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kSurfThreads) surf_patch_kernel(SurfArgs A) {
+    extern __shared__ double sm[];
+    const int f = A.f, nloc = f * f * 16;
+    double *Wf = sm;                    // nloc x 9
+    double *cf = sm + 9 * nloc;         // nloc x 8
+    const int64_t P = blockIdx.x, p = blockIdx.y;
+    const int64_t it = P / A.nph, ip = P - it * A.nph;
+    const int64_t nphf = A.nph * f;
+    const double *x0 = A.x0 + 3 * p, *pts = A.pts + 9 * p, *ell = A.ell + 4 * p;
+    const double jump = A.jump[p];
+    const int64_t r0p = A.r0patch[p];
+    double RS[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) RS[e] = A.rs[p * 9 + e];
+    for (int ml = threadIdx.x; ml < nloc; ml += blockDim.x) {
+        const int fl = ml >> 4, q = ml & 15;
+        const int64_t ft = it * f + fl / f, fp = ip * f + fl % f;
+        const int64_t fpatch = ft * nphf + fp;
+        const int64_t m = fpatch * 16 + q;
+        const double *node = A.fnodes + 3 * m, *nrm = A.fnrm + 3 * m;
+        const double w = A.fw[m];
+        double s0[9], sk[9], out[9];
+        plain_at(x0, node, nrm, w, A.pref, s0);
+        const double r0 = fpatch == r0p ? A.r0coef[p * 16 + q] : 0.0;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+            double v = s0[e] - RS[e] * r0;
+            if (e % 4 == 0) v += jump * r0;
+            out[e] = ell[0] * v;
+        }
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+            if (ell[k] == 0.0) continue;
+            plain_at(pts + 3 * (k - 1), node, nrm, w, A.pref, sk);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) out[e] += ell[k] * sk[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Wf[ml * 9 + e] = out[e];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cf[ml * 8 + e] = A.fcoef[m * 8 + e];
+    }
+    __syncthreads();
+    if (threadIdx.x < 144) {
+        const int n = threadIdx.x / 9, e = threadIdx.x - 9 * n;
+        const int un = n >> 2, vn = n & 3;
+        double acc = 0.0;
+        for (int ml = 0; ml < nloc; ++ml) acc += (cf[ml * 8 + un] * cf[ml * 8 + 4 + vn]) * Wf[ml * 9 + e];
+        const int64_t cn = (it * A.nph + ip) * 16 + n;
+        double sp[9];
+        plain_at(A.trg + 3 * p, A.cnodes + 3 * cn, A.cnrm + 3 * cn, A.cw[cn], A.pref, sp);
+        acc -= sp[e];
+        const int a = e / 3, b = e - 3 * a;
+        const int64_t Nc = A.nt * A.nph * 16;
+        A.W[(p * 3 + a) * 3 * Nc + 3 * cn + b] = acc;
+    }
+}
+}  // namespace
+
+}  // namespace sf
+
+extern "C" int sf_near_surface_weights(
+    const double *cnodes, const double *cnrm, const double *cw, int64_t nt, int64_t nph,
+    const double *fnodes, const double *fnrm, const double *fw, const double *fcoef, int f,
+    int64_t npairs, const double *trg, const double *x0, const double *pts, const double *ell,
+    const double *jump, const int64_t *r0patch, const double *r0coef, double mu, double *work,
+    double *W, void *stream) {
+    using namespace sf;
+    if (npairs <= 0) return SF_OK;
+    if (nt < 1 || nph < 1 || f < 1 || f > 8) return set_error(SF_EINVAL, "bad patch grid");
+    if (!cnodes || !cnrm || !cw || !fnodes || !fnrm || !fw || !fcoef || !trg || !x0 || !pts ||
+        !ell || !jump || !r0patch || !r0coef || !work || !W)
+        return set_error(SF_EINVAL, "null pointer");
+    if (!(mu > 0)) return set_error(SF_EINVAL, "viscosity must be positive");
+    cudaStream_t st = (cudaStream_t)stream;
+    SurfArgs A;
+    A.cnodes = cnodes; A.cnrm = cnrm; A.cw = cw; A.nt = nt; A.nph = nph;
+    A.fnodes = fnodes; A.fnrm = fnrm; A.fw = fw; A.fcoef = fcoef; A.f = f;
+    A.npairs = npairs; A.trg = trg; A.x0 = x0; A.pts = pts; A.ell = ell; A.jump = jump;
+    A.r0patch = r0patch; A.r0coef = r0coef; A.pref = -3.0 / (4.0 * M_PI * mu);
+    A.rs = work;
+    A.rs_part = work + 9 * npairs;
+    A.W = W;
+    const int64_t nfine = nt * nph * f * f * 16;
+    surf_rs_partial<<<dim3(kSurfRsBlocks, (unsigned)npairs), kSurfThreads, 0, st>>>(A, nfine);
+    int rc = check_launch("surf_rs_partial");
+    if (rc) return rc;
+    surf_rs_final<<<(unsigned)npairs, 32, 0, st>>>(A);
+    rc = check_launch("surf_rs_final");
+    if (rc) return rc;
+    const size_t smem = sizeof(double) * 17 * (size_t)f * f * 16;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(surf_patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("cudaFuncSetAttribute");
+    surf_patch_kernel<<<dim3((unsigned)(nt * nph), (unsigned)npairs), kSurfThreads, smem, st>>>(A);
+    return check_launch("surf_patch_kernel");
+}

@@ -416,3 +416,144 @@ def device_fiber_pairs(geo, eps, targets, target_groups, mu, include_doublet=Tru
         if np.any(bad == 2):
             raise RuntimeError("near-field panel refinement overflowed its buffer")
     return pt_np.astype(np.int64), pl_np.astype(np.int64), W
+
+
+_DEV_MESH = {}          # (id(mesh), factor, device) -> (mesh, tensors); small LRU
+
+
+def _device_mesh(mesh, factor, device):
+    """Device arrays of the coarse mesh, its factor-x refinement and the
+    fine-from-coarse interpolation coefficients (_interpolation_matrix)."""
+    import torch
+    key = (id(mesh), factor, str(device))
+    hit = _DEV_MESH.pop(key, None)
+    if hit is not None:
+        _DEV_MESH[key] = hit
+        return hit[1]
+    f64 = dict(dtype=torch.float64, device=device)
+    nt, nph = mesh.patch_grid
+    if factor == 1:
+        fine = mesh
+        coef = np.zeros((mesh.n_nodes, 8))
+        q = np.arange(mesh.n_nodes) % 16
+        coef[np.arange(mesh.n_nodes), q // 4] = 1.0
+        coef[np.arange(mesh.n_nodes), 4 + q % 4] = 1.0
+    else:
+        fine = refined(mesh, factor)
+        theta = np.asarray(fine.thetas, dtype=float)
+        phi = np.asarray(fine.phis, dtype=float) % (2.0 * np.pi)
+        dth, dph = np.pi / nt, 2.0 * np.pi / nph
+        it = np.minimum((theta / dth).astype(int), nt - 1)
+        ip = np.minimum((phi / dph).astype(int), nph - 1)
+        fpatch = np.arange(fine.n_nodes) // 16
+        if not (np.array_equal(it, (fpatch // (nph * factor)) // factor)
+                and np.array_equal(ip, (fpatch % (nph * factor)) // factor)):
+            raise RuntimeError("refined patches do not nest in the coarse patches")
+        coef = np.concatenate([_lagrange((theta - it * dth) / dth, GL01_NODES),
+                               _lagrange((phi - ip * dph) / dph, GL01_NODES)], axis=1)
+    t = dict(cnodes=torch.as_tensor(mesh.nodes, **f64).contiguous(),
+             cnrm=torch.as_tensor(mesh.normals, **f64).contiguous(),
+             cw=torch.as_tensor(mesh.weights, **f64).contiguous(),
+             fnodes=torch.as_tensor(fine.nodes, **f64).contiguous(),
+             fnrm=torch.as_tensor(fine.normals, **f64).contiguous(),
+             fw=torch.as_tensor(fine.weights, **f64).contiguous(),
+             fcoef=torch.as_tensor(np.ascontiguousarray(coef), **f64))
+    _DEV_MESH[key] = (mesh, t)
+    while len(_DEV_MESH) > 8:
+        _DEV_MESH.pop(next(iter(_DEV_MESH)))
+    return t
+
+
+def device_surface_weights(mesh, targets, mu, device, interior_jump=True, upsample=6):
+    """near_surface_weights - plain_surface_weights (body.py:479-519) for the
+    given targets of one mesh, built on the device (sf_near_surface_weights).
+    The nearest surface point (a scalar golden-section search on the
+    profile R(theta), body.py:371-423) and the per-target Lagrange scalars
+    are host work; every O(N_fine) sum runs on the B200.  Returns a device
+    tensor (k, 3, 3N)."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    def ptr(x):
+        return x.data_ptr() if x is not None and x.numel() else None
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    f64 = dict(dtype=torch.float64, device=device)
+    targets = np.atleast_2d(np.asarray(targets, dtype=float))
+    k_all = targets.shape[0]
+    W_all = torch.empty((k_all, 3, 3 * mesh.n_nodes), **f64)
+    groups = {1: [], upsample: []}
+    per_pair = []
+    nt_, nph_ = mesh.patch_grid
+    for j, tgt in enumerate(targets):
+        th0, ph0, x0, sd = nearest_surface_point(mesh, tgt)
+        dist = abs(sd)
+        if dist < 1e-8 * mesh.h:                      # on the surface: coarse map
+            fct, jump = 1, ((1.0 / mu) if interior_jump else 0.0)
+            ell = np.array([1.0, 0.0, 0.0, 0.0])
+            pts = np.zeros((3, 3))
+        else:
+            fct = upsample
+            jump = (1.0 / mu) if (sd < 0 and interior_jump) else 0.0
+            ndir = (tgt - x0) / dist
+            c = 1.5 * mesh.h
+            dists = np.array([0.0, c, 1.5 * c, 2.25 * c])
+            ell = _lagrange(dist, dists)[0]
+            pts = x0[None, :] + dists[1:, None] * ndir[None, :]
+        gt, gp = nt_ * fct, nph_ * fct
+        dth, dph = np.pi / gt, 2.0 * np.pi / gp
+        phw = ph0 % (2.0 * np.pi)
+        it = min(int(th0 / dth), gt - 1)
+        ip = min(int(phw / dph), gp - 1)
+        cu = _lagrange((th0 - it * dth) / dth, GL01_NODES)[0]
+        cv = _lagrange((phw - ip * dph) / dph, GL01_NODES)[0]
+        groups[fct].append(j)
+        per_pair.append((tgt, x0, pts, ell, jump, it * gp + ip, np.outer(cu, cv).ravel()))
+    for fct, js in groups.items():
+        if not js:
+            continue
+        m = _device_mesh(mesh, fct, device)
+        k = len(js)
+        cols = list(zip(*[per_pair[j] for j in js]))
+        trg = torch.as_tensor(np.stack(cols[0]), **f64)
+        x0 = torch.as_tensor(np.stack(cols[1]), **f64)
+        pts = torch.as_tensor(np.stack(cols[2]), **f64)
+        ell = torch.as_tensor(np.stack(cols[3]), **f64)
+        jump = torch.as_tensor(np.array(cols[4], dtype=float), **f64)
+        r0p = torch.as_tensor(np.array(cols[5], dtype=np.int64), device=device)
+        r0c = torch.as_tensor(np.stack(cols[6]), **f64)
+        work = torch.empty(k * (9 + 148 * 9), **f64)
+        W = torch.empty((k, 3, 3 * mesh.n_nodes), **f64)
+        _native.call("sf_near_surface_weights", ptr(m["cnodes"]), ptr(m["cnrm"]), ptr(m["cw"]),
+                     nt_, nph_, ptr(m["fnodes"]), ptr(m["fnrm"]), ptr(m["fw"]), ptr(m["fcoef"]),
+                     fct, k, ptr(trg), ptr(x0), ptr(pts), ptr(ell), ptr(jump), ptr(r0p), ptr(r0c),
+                     float(mu), ptr(work), ptr(W), st)
+        W_all[torch.as_tensor(js, device=device)] = W
+    return W_all
+
+
+def device_surface_pairs(surfaces, targets, target_groups, mu, device, upsample=6):
+    """find_surface_pairs with the maps built on the device
+    (device_surface_weights).  Returns [(t, si, W)] in the reference's order
+    (system.py:588-613) with W (3, 3N) device rows."""
+    out = []
+    for si, (mesh, group, is_periphery) in enumerate(surfaces):
+        others = target_groups != group
+        shell = 1.5 * mesh.h
+        rel = np.linalg.norm(targets - mesh.center, axis=1)
+        rho_nodes = np.linalg.norm(mesh.nodes - mesh.center, axis=1)
+        band = others & (rel >= rho_nodes.min() - shell) & (rel <= rho_nodes.max() + shell)
+        cand = np.nonzero(band)[0]
+        if cand.size == 0:
+            continue
+        from scipy.spatial import cKDTree
+        d, _ = cKDTree(mesh.nodes).query(targets[cand], k=1)
+        near = cand[d * d < shell * shell]
+        if near.size == 0:
+            continue
+        W = device_surface_weights(mesh, targets[near], mu, device,
+                                   interior_jump=is_periphery, upsample=upsample)
+        out.extend((int(t), si, W[j]) for j, t in enumerate(near))
+    return out

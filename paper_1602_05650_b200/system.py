@@ -351,8 +351,12 @@ class InteractionCache:
         _lap("near fiber maps")
         self.near_surface = []
         if near and self.surfaces:
-            self.near_surface = nearfield.find_surface_pairs(
-                self.surfaces, self.targets, self.target_groups, state.mu)
+            if near == "host":
+                self.near_surface = nearfield.find_surface_pairs(
+                    self.surfaces, self.targets, self.target_groups, state.mu)
+            else:
+                self.near_surface = nearfield.device_surface_pairs(
+                    self.surfaces, self.targets, self.target_groups, state.mu, self.device)
         _lap("near surface maps")
         self._build_near_map()
         _lap("near CSR")
