@@ -116,7 +116,8 @@ int sf_kdelta_build_batched(const double *X, const double *s,
 
 /* u = M f + K f (+ u if accumulate): local_mobility_apply (fiber.py:244-250)
  * plus nonlocal_Kdelta_apply (fiber.py:253-258) for every fiber.
- * c_log (nf) = -ln(eps^2 e)/(8 pi mu), c_two = 2/(8 pi mu). */
+ * c_log (nf) = -ln(eps^2 e)/(8 pi mu), c_two = 2/(8 pi mu).  K may be null
+ * (local mobility only); c_log = c_two = 0 gives K f alone. */
 int sf_self_apply_batched(const double *K, const double *tang,
                           const double *c_log, double c_two, const double *f,
                           int64_t nf, int64_t n, int accumulate, double *u,

@@ -132,3 +132,69 @@ class Periphery:
             th = np.arccos(np.clip(np.where(rho > 0, pts[:, 2] / np.where(rho > 0, rho, 1.0), 1.0),
                                    -1, 1))
         return rho <= np.asarray(self.mesh.shape[2](th), dtype=float) - margin
+
+
+# -- per-surface operator API (body.py:237-283, 522-527) on the device --------
+
+def double_layer_offsurface(mesh, q, targets, mu, allow_near=False):
+    """Stresslet quadrature at targets away from the surface (body.py:237-251)."""
+    from . import kernels
+    targets = np.atleast_2d(np.asarray(targets, dtype=float))
+    q = np.asarray(q, dtype=float)
+    if not allow_near:
+        d = targets[:, None, :] - mesh.nodes[None, :, :]
+        if np.any((d * d).sum(axis=2).min(axis=1) < (NEAR_SHELL_FACTOR * mesh.h) ** 2):
+            raise kernels.NearFieldError(
+                "target inside the near shell; route through near_surface_eval")
+    qw = q * mesh.weights[:, None]
+    out, bad = kernels.stresslet_sum(targets, kernels.no_groups(targets.shape[0]), mesh.nodes,
+                                     kernels.no_groups(mesh.n_nodes), mesh.normals, qw,
+                                     -3.0 / (4.0 * np.pi * mu))
+    if bad:
+        raise kernels.SingularEvaluationError("target coincides with a mesh node")
+    return out
+
+
+def double_layer_onsurface(mesh, q, mu):
+    """Singularity-subtracted on-surface double layer (body.py:254-262)."""
+    from . import kernels
+    return kernels.stresslet_sum_subtracted(mesh.nodes, mesh.normals, mesh.weights,
+                                            np.asarray(q, dtype=float), -3.0 / (4.0 * np.pi * mu))
+
+
+def completion_flow(particle, targets, mu):
+    """Stokeslet + rotlet of the particle's external wrench at its centre
+    (body.py:272-283), by the device kernel sf_wrench_flow."""
+    import ctypes
+
+    import torch
+
+    from . import _native, kernels
+    _native.load(require_device=True)
+    targets = np.atleast_2d(np.asarray(targets, dtype=float))
+    if np.any(np.linalg.norm(targets - particle.center, axis=1) < kernels.MIN_SEPARATION):
+        raise kernels.SingularEvaluationError("target at the particle center")
+    f64 = dict(dtype=torch.float64, device="cuda")
+    t = torch.as_tensor(targets, **f64).contiguous()
+    c = torch.as_tensor(particle.center, **f64)
+    w = torch.as_tensor(np.concatenate([particle.F_ext, particle.L_ext]), **f64)
+    u = torch.zeros_like(t)
+    _native.call("sf_wrench_flow", t.data_ptr(), t.shape[0], c.data_ptr(), w.data_ptr(), float(mu),
+                 u.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    return u.cpu().numpy()
+
+
+def near_surface_eval(mesh, q, target, mu, interior_jump=True, upsample=6):
+    """Velocity at a target close to the surface (body.py:522-527): the
+    device-built near map (nearfield.device_surface_weights) applied to q."""
+    import torch
+
+    from . import nearfield
+    Wn = nearfield.device_surface_weights(mesh, np.asarray(target, dtype=float)[None, :], mu,
+                                          torch.device("cuda"), interior_jump=interior_jump,
+                                          upsample=upsample)[0]
+    qd = torch.as_tensor(np.asarray(q, dtype=float).ravel(), dtype=torch.float64, device="cuda")
+    corr = (Wn @ qd).cpu().numpy()                       # (W_near - W_plain) q
+    plain = double_layer_offsurface(mesh, q, np.asarray(target, dtype=float)[None, :], mu,
+                                    allow_near=True)[0]  # W_plain q
+    return plain + corr

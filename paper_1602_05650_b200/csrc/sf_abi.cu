@@ -179,7 +179,7 @@ int sf_self_apply_batched(const double *K, const double *tang, const double *c_l
                           double c_two, const double *f, int64_t nf, int64_t n, int accumulate,
                           double *u, void *stream) {
     SF_REQUIRE(nf >= 0 && n >= 2, "bad fiber sizes");
-    SF_REQUIRE(nf == 0 || (K && tang && c_log && f && u), "null pointer");
+    SF_REQUIRE(nf == 0 || (tang && c_log && f && u), "null pointer");
     return fiber_self_apply(K, tang, c_log, c_two, f, nf, n, accumulate, u,
                             (cudaStream_t)stream);
 }

@@ -108,15 +108,17 @@ __global__ void self_apply_kernel(const double *__restrict__ K, const double *__
     const double *fm = f + (int64_t)ld * m;
     for (int c = threadIdx.x; c < ld; c += blockDim.x) fs[c] = fm[c];
     __syncthreads();
-    const double *Km = K + (int64_t)ld * ld * m;
+    const double *Km = K ? K + (int64_t)ld * ld * m : nullptr;
     const double *Tm = tang + (int64_t)ld * m;
     const double cl = c_log[m];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int r = warp; r < ld; r += nw) {
-        const double *row = Km + (int64_t)r * ld;
+        const double *row = Km ? Km + (int64_t)r * ld : nullptr;
         double acc = 0.0;
-        for (int c = lane; c < ld; c += 32) acc = fma(row[c], fs[c], acc);
-        acc = warp_sum(acc);
+        if (K) {   // K == nullptr: local mobility only
+            for (int c = lane; c < ld; c += 32) acc = fma(row[c], fs[c], acc);
+            acc = warp_sum(acc);
+        }
         if (lane == 0) {
             const int i = r / 3, a = r - 3 * (r / 3);
             const double tx = Tm[3 * i], ty = Tm[3 * i + 1], tz = Tm[3 * i + 2];

@@ -210,3 +210,119 @@ def end_force_torque(fib, Xcand, Tcand):
     F = -fib.E * Xsss + Tcand[k] * t
     L = fib.E * np.cross(Xss, t)
     return F, L
+
+
+# -- per-fiber operator API (fiber.py:237-289), evaluated on the device --------
+
+def _dev():
+    import torch
+
+    from . import _native
+    _native.load(require_device=True)
+    return torch.device("cuda")
+
+
+def _stream():
+    import ctypes
+
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
+def elastic_force_density(fib, Xcand, Tcand):
+    """f = -E Ds^4 X + Ds (T X_s) with the geometry frozen (fiber.py:237-241);
+    Ds^k built on the device (sf_fiber_dpow), products by the device BLAS."""
+    import torch
+
+    from . import _native
+    dev = _dev()
+    f64 = dict(dtype=torch.float64, device=dev)
+    n = fib.n_nodes
+    D = torch.tensor(spectral.grid(fib.p)[2], **f64)
+    sa = torch.as_tensor(fib.s_alpha, **f64)
+    Dpow = torch.empty((1, 4, n, n), **f64)
+    _native.call("sf_fiber_dpow", _ptr(D), _ptr(sa), 1, n, _ptr(Dpow), _stream())
+    X = torch.as_tensor(np.asarray(Xcand, dtype=float), **f64)
+    T = torch.as_tensor(np.asarray(Tcand, dtype=float), **f64)
+    t = torch.as_tensor(fib.tangents, **f64)
+    f = -fib.E * (Dpow[0, 3] @ X) + Dpow[0, 0] @ (T[:, None] * t)
+    return f.cpu().numpy()
+
+
+def local_mobility_apply(fib, f, mu):
+    """(1/8 pi mu)[-ln(eps^2 e)(I + tt) + 2(I - tt)] f (fiber.py:244-250),
+    the local half of sf_self_apply_batched."""
+    import torch
+
+    from . import _native
+    dev = _dev()
+    f64 = dict(dtype=torch.float64, device=dev)
+    n = fib.n_nodes
+    fd = torch.as_tensor(np.asarray(f, dtype=float).reshape(n, 3), **f64).contiguous()
+    t = torch.as_tensor(fib.tangents, **f64).contiguous()
+    c_log = torch.tensor([-math.log(fib.eps ** 2 * math.e) / (8.0 * math.pi * mu)], **f64)
+    u = torch.empty_like(fd)
+    _native.call("sf_self_apply_batched", None, _ptr(t), _ptr(c_log), 2.0 / (8.0 * math.pi * mu),
+                 _ptr(fd), 1, n, 0, _ptr(u), _stream())
+    return u.cpu().numpy()
+
+
+def nonlocal_Kdelta_apply(fib, f, mu):
+    """K_delta f (fiber.py:253-258): K built on the device by
+    sf_kdelta_build_batched and applied by sf_self_apply_batched."""
+    import torch
+
+    from . import _native
+    if fib.delta <= 0:
+        raise ValueError("regularization length must be positive")
+    dev = _dev()
+    f64 = dict(dtype=torch.float64, device=dev)
+    n = fib.n_nodes
+    X = torch.as_tensor(fib.X, **f64).contiguous()
+    s = torch.as_tensor(fib.s, **f64)
+    sa = torch.as_tensor(fib.s_alpha, **f64)
+    t = torch.as_tensor(fib.tangents, **f64).contiguous()
+    w = torch.as_tensor(spectral.grid(fib.p)[1], **f64)
+    delta = torch.tensor([fib.delta], **f64)
+    K = torch.empty((1, 3 * n, 3 * n), **f64)
+    st = _stream()
+    _native.call("sf_kdelta_build_batched", _ptr(X), _ptr(s), _ptr(sa), _ptr(t), _ptr(w), 1, n,
+                 _ptr(delta), 1.0 / (8.0 * math.pi * mu), _ptr(K), st)
+    fd = torch.as_tensor(np.asarray(f, dtype=float).reshape(n, 3), **f64).contiguous()
+    zero = torch.zeros(1, **f64)
+    u = torch.empty_like(fd)
+    _native.call("sf_self_apply_batched", _ptr(K), _ptr(t), _ptr(zero), 0.0, _ptr(fd), 1, n, 0,
+                 _ptr(u), st)
+    return u.cpu().numpy()
+
+
+def fiber_induced_velocity(fib, f, targets, mu, include_doublet=False, allow_near=False):
+    """Clenshaw-Curtis line quadrature of the Stokeslet (+ doublet) of one
+    fiber at distant targets (fiber.py:261-289), through the device kernels."""
+    from . import kernels
+    targets = np.atleast_2d(np.asarray(targets, dtype=float))
+    f = np.asarray(f, dtype=float)
+    if not allow_near:
+        h = fib.L / fib.p
+        d = targets[:, None, :] - fib.X[None, :, :]
+        if np.any((d * d).sum(axis=2).min(axis=1) < (1.5 * h) ** 2):
+            raise kernels.NearFieldError("target inside the fiber's near-field shell")
+    strengths = fib.node_weights()[:, None] * f
+    ng_t = kernels.no_groups(targets.shape[0])
+    ng_s = kernels.no_groups(fib.n_nodes)
+    out, bad = kernels.stokeslet_sum(targets, ng_t, fib.X, ng_s, strengths,
+                                     1.0 / (8.0 * np.pi * mu))
+    if bad:
+        raise kernels.SingularEvaluationError("target coincides with a fiber node")
+    if include_doublet:
+        coeff = (fib.eps * fib.L) ** 2 / 2.0
+        dbl, bad = kernels.doublet_sum(targets, ng_t, fib.X, ng_s, strengths,
+                                       coeff / (8.0 * np.pi * mu))
+        if bad:
+            raise kernels.SingularEvaluationError("target coincides with a fiber node")
+        out = out + dbl
+    return out

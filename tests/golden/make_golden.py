@@ -231,6 +231,41 @@ def near_surface_fixture():
          nsp=np.array([[a, b, *x, d] for a, b, x, d in nsp]), **versions())
 
 
+def api_ops_fixture():
+    """Per-constituent operator API of the reference (fiber.py:237-289,
+    body.py:237-283, 522-527) on seeded inputs: the functions a reference
+    user calls directly."""
+    rng = np.random.default_rng(11)
+    cl = configs.make("c1_clean", seed=0)
+    fib = fiber.Fiber(cl.X[3], eps=1e-2, E=0.7)
+    f = rng.standard_normal((fib.n_nodes, 3))
+    Xc = cl.X[3] + 1e-3 * rng.standard_normal(cl.X[3].shape)
+    Tc = rng.standard_normal(fib.n_nodes)
+    mu = 1.3
+    far = cl.X[3].mean(axis=0) + np.array([[2.0, 0.5, -1.0], [-1.5, 2.5, 0.3], [0.2, -0.1, 3.0]])
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), (4, 4)))
+    part.F_ext = np.array([0.3, -1.0, 0.5])
+    part.L_ext = np.array([-0.2, 0.1, 0.7])
+    per = body.make_surface(body.sphere_shape(3.0), (6, 6))
+    q = rng.standard_normal((per.n_nodes, 3))
+    qp = rng.standard_normal((part.mesh.n_nodes, 3))
+    tgt = np.array([[0.1, 0.2, 0.3], [1.0, -0.5, 0.4], [-0.7, 0.6, -1.1]])
+    near_t = np.array([0.1, -2.85, 0.3])
+    save("api_ops.npz", X=cl.X[3], eps=1e-2, E=0.7, mu=mu, f=f, Xc=Xc, Tc=Tc, far=far,
+         elastic=fiber.elastic_force_density(fib, Xc, Tc),
+         mobility=fiber.local_mobility_apply(fib, f, mu),
+         kdelta=fiber.nonlocal_Kdelta_apply(fib, f, mu),
+         induced=fiber.fiber_induced_velocity(fib, f, far, mu),
+         induced_dbl=fiber.fiber_induced_velocity(fib, f, far, mu, include_doublet=True),
+         q=q, qp=qp, tgt=tgt, near_t=near_t, F=part.F_ext, L=part.L_ext,
+         dl_off=body.double_layer_offsurface(per, q, tgt, mu),
+         dl_on=body.double_layer_onsurface(per, q, mu),
+         dl_on_p=body.double_layer_onsurface(part.mesh, qp, mu),
+         completion=body.completion_flow(part, tgt + 1.0, mu),
+         near_eval=body.near_surface_eval(per, q, near_t, mu, interior_jump=True),
+         **versions())
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pairs", "operator", "surfaces", "steps"]
     if "pairs" in which:
@@ -245,3 +280,5 @@ if __name__ == "__main__":
 
     if "steps" in which:
         steps_all()
+    if "api" in which:
+        api_ops_fixture()
