@@ -389,6 +389,24 @@ int sf_host_kdelta_matrix(const double *X, const double *s, const double *s_alph
                           double delta, double pref, double *K);
 
 /* ---------------------------------------------------------------------------
+ * Octree Stokeslet summation: the reference's TreeSummation backend
+ * (system.py:108-224).  Sources/strengths src, f (ns,3) permuted so node k
+ * owns [nbeg[k], nend[k]); children of k are nodes first_child[k] ..
+ * first_child[k] + nchild[k] - 1 in octant order (host-built topology,
+ * system.py:112-140).  Moments, traversal with the reference's opening test
+ * (theta, cell_tolerance, C2 = 16) and the same-group subtraction run on the
+ * device; group g's sources are gsrc/gf[gbeg[g] .. gend[g]).  work >=
+ * sf_tree_work_doubles(nnodes) doubles; out (nt,3) overwritten.
+ * ------------------------------------------------------------------------- */
+int sf_tree_stokeslet(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
+                      const double *f, int64_t ns, const int64_t *nbeg, const int64_t *nend,
+                      const int64_t *first_child, const int *nchild, int64_t nnodes,
+                      const double *gsrc, const double *gf, const int64_t *gbeg,
+                      const int64_t *gend, int64_t ngroups, double theta, double cell_tolerance,
+                      double mu, double *work, double *out, void *stream);
+int64_t sf_tree_work_doubles(int64_t nnodes);
+
+/* ---------------------------------------------------------------------------
  * Measurement helpers.
  * ------------------------------------------------------------------------- */
 

@@ -50,6 +50,9 @@ _SIGNATURES = {
     "sf_fiber_hi_apply": [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _D, _I, _P, _P, _P, _D, _P,
                           _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sf_pair_split": [_I64, _I64],
+    "sf_tree_stokeslet": [_P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64,
+                          _D, _D, _D, _P, _P, _P],
+    "sf_tree_work_doubles": [_I64],
     "sf_sym_shard_pairs": [_I64, _I64, _I, _I],
     "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
@@ -125,6 +128,7 @@ def load(require_device=False):
             fn.argtypes = argtypes
             fn.restype = _I
         lib.sf_sym_shard_pairs.restype = ctypes.c_int64
+        lib.sf_tree_work_doubles.restype = ctypes.c_int64
         lib.sf_last_error.argtypes = []
         lib.sf_last_error.restype = ctypes.c_char_p
         _lib = lib

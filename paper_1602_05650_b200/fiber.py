@@ -286,7 +286,7 @@ def nonlocal_Kdelta_apply(fib, f, mu):
     s = torch.as_tensor(fib.s, **f64)
     sa = torch.as_tensor(fib.s_alpha, **f64)
     t = torch.as_tensor(fib.tangents, **f64).contiguous()
-    w = torch.as_tensor(spectral.grid(fib.p)[1], **f64)
+    w = torch.tensor(spectral.grid(fib.p)[1], **f64)
     delta = torch.tensor([fib.delta], **f64)
     K = torch.empty((1, 3 * n, 3 * n), **f64)
     st = _stream()

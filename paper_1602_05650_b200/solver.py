@@ -123,15 +123,13 @@ class BlockOperator:
             raise ConfigurationError("time step must be positive")
         if not implicit_coupling:
             raise ConfigurationError("the device operator implements implicit coupling only")
-        if backend is not None and getattr(backend, "kind", "direct") != "direct":
-            raise ConfigurationError(f"backend {backend.kind!r} is not available on the device")
         self.state = state
         self.dt = float(dt)
         self.mu = state.mu if mu is None else float(mu)
         if self.mu <= 0:
             raise ConfigurationError("viscosity must be positive")
         self.layout = StepLayout(state)
-        self.cache = cache if cache is not None else InteractionCache(state)
+        self.cache = cache if cache is not None else InteractionCache(state, backend=backend)
         self.implicit_coupling = True
         self.device = self.cache.device
         dev = self.device
@@ -553,7 +551,7 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
     if dt_min is None:
         dt_min = dt / 64.0
     attempt = float(dt)
-    cache = InteractionCache(state)
+    cache = InteractionCache(state, backend=backend)
     while True:
         op, rhs = assemble_step_operator(state, attempt, mu=mu, backend=backend, cache=cache,
                                          implicit_coupling=implicit_coupling)

@@ -78,6 +78,60 @@ class DeviceSummation:
 DirectSummation = DeviceSummation
 
 
+class TreeSummation:
+    """The reference's octree Stokeslet backend (system.py:157-224) on the
+    device: same constructor, validation, opening test (theta, analytic
+    cell_tolerance gate with C2 = 16) and group-exclusion-by-subtraction;
+    the topology is built once per source geometry on the host, moments,
+    traversal and leaf sums run in sf_tree_stokeslet.  numpy in -> numpy out,
+    CUDA tensors in -> CUDA tensor out."""
+
+    kind = "treeAccelerated"
+    _C2 = 16.0
+
+    def __init__(self, theta=0.5, leaf_size=32, cell_tolerance=1e-8):
+        if not 0.0 < theta < 1.0:
+            raise ConfigurationError("opening parameter must lie in (0, 1)")
+        if leaf_size < 1:
+            raise ConfigurationError("leaf size must be at least 1")
+        if cell_tolerance <= 0:
+            raise ConfigurationError("cell tolerance must be positive")
+        self.theta = float(theta)
+        self.leaf_size = int(leaf_size)
+        self.cell_tolerance = float(cell_tolerance)
+        self._plans = {}
+
+    def plan(self, sources, source_groups, device=None):
+        import torch
+
+        from . import tree
+        src = sources.detach().cpu().numpy() if hasattr(sources, "detach") else sources
+        grp = source_groups.detach().cpu().numpy() if hasattr(source_groups, "detach") \
+            else source_groups
+        src = np.asarray(src, dtype=float).reshape(-1, 3)
+        key = tree.geometry_key(src, grp, self.leaf_size)
+        p = self._plans.pop(key, None)
+        if p is None:
+            p = tree.TreePlan(src, grp, self.leaf_size, device or torch.device("cuda"))
+        self._plans[key] = p
+        while len(self._plans) > 2:
+            self._plans.pop(next(iter(self._plans)))
+        return p
+
+    def stokeslet(self, sources, source_groups, strengths, targets, target_groups, mu):
+        import torch
+        _native.load(require_device=True)
+        dev_io = isinstance(strengths, torch.Tensor) and strengths.is_cuda
+        dev = torch.device("cuda")
+        p = self.plan(sources, source_groups, dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        f = torch.as_tensor(strengths, **f64).reshape(-1, 3).contiguous()
+        t = torch.as_tensor(targets, **f64).reshape(-1, 3).contiguous()
+        tg = torch.as_tensor(target_groups, dtype=torch.int64, device=dev).contiguous()
+        out = p.stokeslet(f, t, tg, mu, self.theta, self.cell_tolerance)
+        return out if dev_io else out.cpu().numpy()
+
+
 # -- state (system.py:237-278) -------------------------------------------------
 
 class SystemState:
@@ -221,7 +275,8 @@ class InteractionCache:
     (system.py:492-620).  Rebuild whenever any constituent moves."""
 
     def __init__(self, state, include_doublet=True, device=None, mode=SF_MODE_FP64,
-                 near="device", fiber_geometry=None, target_range=None, fiber_pairs=True):
+                 near="device", fiber_geometry=None, target_range=None, fiber_pairs=True,
+                 backend=None):
         """target_range (lo, hi): evaluate only the targets [lo, hi) of the
         global [particles | periphery | fibers] list (a rank's share in a
         multi-GPU step).  fiber_pairs=False leaves the fiber-source pair sum
@@ -290,7 +345,13 @@ class InteractionCache:
             self.fiber_slice = clip(self.fiber_slice)
             self.fiber_slices = [clip(x) for x in self.fiber_slices]
         self.n_targets = self.targets.shape[0]
-        self.fiber_pairs = bool(fiber_pairs)
+        kind = getattr(backend, "kind", "direct") if backend is not None else "direct"
+        if kind not in ("direct", "treeAccelerated"):
+            raise ConfigurationError(f"backend {kind!r} is not available on the device")
+        # tree backend: the fiber Stokeslet goes through the octree, the
+        # doublet stays a direct sum (system.py:659-671)
+        self.backend = backend if kind == "treeAccelerated" else None
+        self.fiber_pairs = bool(fiber_pairs) and self.backend is None
 
         _lap("targets")
         # fibers: geometry, weights, doublet coefficients (device)
@@ -467,7 +528,29 @@ class InteractionCache:
                      _ptr(x), _ptr(out), _ptr(self.bad), _stream())
         if check:
             self.check_bad()
+        if self.backend is not None and self.nf and self.n_targets:
+            self._tree_fiber_terms(f, out)
         return out
+
+    def _tree_fiber_terms(self, f, out):
+        """Fiber Stokeslet through the tree backend + direct doublet
+        (complementary_velocities, system.py:655-671)."""
+        import torch
+        s = self.fw[:, None] * f
+        if getattr(self, "_tree_plan", None) is None:      # topology once per geometry
+            self._tree_plan = self.backend.plan(self.fsrc, self.fgrp, self.device)
+        b = self.backend
+        out += self._tree_plan.stokeslet(s, self.trg, self.tgrp, self.mu, b.theta, b.cell_tolerance)
+        if self.fdcoef is not None:
+            dbl = (self.fdcoef[:, None] * s).contiguous()
+            tmp = torch.empty_like(out)
+            bad = torch.zeros(1, dtype=torch.int64, device=self.device)
+            _native.call("sf_doublet_sum", _ptr(self.trg), _ptr(self.tgrp), self.n_targets,
+                         _ptr(self.fsrc), _ptr(self.fgrp), self.fsrc.shape[0], _ptr(dbl),
+                         1.0 / (8.0 * math.pi * self.mu), _ptr(tmp), _ptr(bad), _stream())
+            if int(bad.item()):
+                raise SingularEvaluationError("a target coincides with another fiber's node")
+            out += tmp
 
     def check_bad(self):
         b = self.bad.tolist()
@@ -495,10 +578,8 @@ def complementary_velocities(state, periphery_density=None, particle_densities=N
     B200 through the (device-resident) InteractionCache.  Host (numpy)
     inputs give numpy outputs.
     """
-    if backend is not None and getattr(backend, "kind", "direct") != "direct":
-        raise ConfigurationError(f"backend {backend.kind!r} is not available on the device path")
     if cache is None:
-        cache = InteractionCache(state, include_doublet=include_doublet)
+        cache = InteractionCache(state, include_doublet=include_doublet, backend=backend)
     if fiber_forces is None:
         from .solver import host_elastic_force_density
         fiber_forces = [host_elastic_force_density(f, f.X, f.T) + external_force_density(state, f)

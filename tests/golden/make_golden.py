@@ -266,6 +266,36 @@ def api_ops_fixture():
          **versions())
 
 
+def tree_fixture():
+    """TreeSummation (system.py:157-224) outputs: the reference tests'
+    geometries plus a fiber cloud with groups, with loose and default
+    parameters, and complementary_velocities through the tree backend."""
+    rng = np.random.default_rng(2)
+    src = rng.standard_normal((200, 3))
+    src /= np.abs(src).max()
+    f = rng.standard_normal((200, 3))
+    far = 25.0 * np.array([[1.0, 0, 0], [0, 1.0, 0], [0.6, 0, 0.8], [-1.0, 0, 0], [0, 0, -1.0]])
+    ng = lambda k: kernels.no_groups(k)   # noqa: E731
+    loose = system.TreeSummation(theta=0.5, leaf_size=8, cell_tolerance=2e-2)
+    out = dict(src=src, f=f, far=far,
+               far_loose=loose.stokeslet(src, ng(200), f, far, ng(5), 1.0),
+               far_exact=system.DirectSummation().stokeslet(src, ng(200), f, far, ng(5), 1.0))
+    cl = configs.make("c1_clean", seed=0)
+    X = cl.X.reshape(-1, 3)
+    grp = np.repeat(np.arange(cl.X.shape[0], dtype=np.int64), cl.X.shape[1])
+    fc = rng.standard_normal(X.shape)
+    mid = system.TreeSummation(theta=0.6, leaf_size=16, cell_tolerance=1e-1)
+    out.update(cX=X, cgrp=grp, cf=fc,
+               cloud_mid=mid.stokeslet(X, grp, fc, X, grp, 1.3),
+               cloud_default=system.TreeSummation().stokeslet(X, grp, fc, X, grp, 1.3),
+               cloud_exact=system.DirectSummation().stokeslet(X, grp, fc, X, grp, 1.3))
+    st = system.SystemState([fiber.Fiber(x, eps=1e-2, E=1.0) for x in cl.X])
+    ff = rng.standard_normal(cl.X.shape)
+    cv = system.complementary_velocities(st, fiber_forces=list(ff), backend=mid)
+    out.update(cv_forces=ff, cv_mid=np.stack(cv.fibers))
+    save("tree.npz", **out, **versions())
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pairs", "operator", "surfaces", "steps"]
     if "pairs" in which:
@@ -282,3 +312,5 @@ if __name__ == "__main__":
         steps_all()
     if "api" in which:
         api_ops_fixture()
+    if "tree" in which:
+        tree_fixture()

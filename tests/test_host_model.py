@@ -60,3 +60,22 @@ def test_near_surface_maps_match_reference():
         W = nearfield.near_surface_weights(per, t, 1.0, interior_jump=True) \
             - nearfield.plain_surface_weights(per, t, 1.0)
         assert np.abs(W - Wref).max() <= 1e-12 * np.abs(Wref).max()
+
+
+def test_tree_topology_partitions_the_points():
+    """tree.build_topology: every node owns a contiguous permuted range that
+    its children tile in octant order; leaves hold <= leaf_size points."""
+    from paper_1602_05650_b200 import tree
+    rng = np.random.default_rng(0)
+    pts = np.vstack([rng.standard_normal((500, 3)), rng.standard_normal((300, 3)) + 8.0])
+    perm, nb, ne, first, nch = tree.build_topology(pts, 16)
+    assert sorted(perm.tolist()) == list(range(pts.shape[0]))
+    assert nb[0] == 0 and ne[0] == pts.shape[0]
+    for k in range(nb.size):
+        if nch[k] == 0:
+            assert ne[k] - nb[k] <= 16
+            assert list(perm[nb[k]:ne[k]]) == sorted(perm[nb[k]:ne[k]])   # reference idx order
+        else:
+            kids = range(first[k], first[k] + nch[k])
+            assert nb[first[k]] == nb[k] and ne[first[k] + nch[k] - 1] == ne[k]
+            assert all(ne[a] == nb[a + 1] for a in list(kids)[:-1])
