@@ -33,7 +33,7 @@ import numpy as np
 from . import _native, spectral
 from .dist import shard_range
 from .solver import (BC_CODES, FactorizationError, GmresParams, NonconvergenceError,
-                     StepLayout, _ptr, _stream)
+                     StepLayout, _kinetics_and_contacts, _ptr, _stream)
 from .system import (ConfigurationError, SingularEvaluationError, FiberGeometry, InteractionCache, external_force_density,
                      stack_fibers)
 
@@ -509,9 +509,6 @@ def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, sy
     """backward_euler_step (solver.py:528-592) over `comm`'s ranks.  The host
     state is replicated; every rank ends with the same updated state."""
     import torch
-    from .fiber import STALLED
-    if any(f.growth_state != STALLED for f in state.fibers):
-        raise NotImplementedError("polymerization kinetics are outside the device path")
     op = DistBlockOperator(state, dt, comm, symmetric=symmetric)
     rhs = op.rhs_device()
     prec = DistPreconditioner(op)
@@ -534,6 +531,7 @@ def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, sy
         fib.X = parts.X[m].copy()
         fib.T = parts.T[m].copy()
     state.time += dt
+    _kinetics_and_contacts(state, dt)          # replicated: same RNG streams on every rank
     if return_info:
         return state, dict(iterations=iters, history=history, matvecs=op.matvecs)
     return state

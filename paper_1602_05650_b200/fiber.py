@@ -326,3 +326,56 @@ def fiber_induced_velocity(fib, f, targets, mu, include_doublet=False, allow_nea
             raise kernels.SingularEvaluationError("target coincides with a fiber node")
         out = out + dbl
     return out
+
+
+# -- polymerization kinetics (fiber.py:297-356): per-fiber scalar host logic
+#    run after each device solve; the reparametrization velocity enters the
+#    device rows through Ldot (sf_fiber_rows) -----------------------------------
+
+def reparam_velocity(fib):
+    """((alpha + 1) Ldot / L) X_alpha (fiber.py:297-302)."""
+    nodes, _, D, _ = spectral.grid(fib.p)
+    coef = (nodes + 1.0) * fib.Ldot / fib.L
+    return coef[:, None] * (D @ fib.X)
+
+
+def growth_rate(fib, end_force, v_grow0, stall_force):
+    """Load-dependent plus-end polymerization speed (fiber.py:307-319)."""
+    if fib.growth_state == SHRINKING:
+        return -fib.kinetics.v_shrink
+    t_plus = fib.tangents[fib.end_index(plus=True)]
+    load = float(np.dot(np.asarray(end_force, dtype=float), t_plus))
+    return v_grow0 * math.exp(-(7.0 / 3.0) * load / stall_force)
+
+
+def catastrophe_rate(v_g, v_g0, f_cat0, tau_cat):
+    """Catastrophe rate, never below 1/tau_cat (fiber.py:322-328)."""
+    if v_g <= 0:
+        raise ValueError("catastrophe rate is defined for growing fibers only")
+    return max(f_cat0 * v_g0 / v_g, 1.0 / tau_cat)
+
+
+def polymerization_step(fib, dt, rng):
+    """Dynamic-instability transitions and growth rate (fiber.py:331-356):
+    one uniform draw per transition test, rescue at the minimum length."""
+    if dt <= 0:
+        raise ValueError("time step must be positive")
+    kin = fib.kinetics
+    if fib.growth_state in (GROWING, STALLED):
+        v_g = fib.Ldot if fib.Ldot > 0 else kin.v_grow
+        rate = catastrophe_rate(v_g, kin.v_grow, kin.f_cat, fib.tau_cat)
+        if rng.random() < -math.expm1(-rate * dt):
+            fib.growth_state = SHRINKING
+            fib.Ldot = -kin.v_shrink
+        elif fib.growth_state == GROWING and fib.Ldot <= 0:
+            fib.Ldot = kin.v_grow
+    elif fib.growth_state == SHRINKING:
+        if rng.random() < -math.expm1(-kin.f_res * dt):
+            fib.growth_state = GROWING
+            fib.Ldot = kin.v_grow
+        else:
+            fib.Ldot = -kin.v_shrink
+    if fib.Ldot < 0 and fib.L + fib.Ldot * dt < kin.min_length:
+        fib.growth_state = GROWING
+        fib.Ldot = (kin.min_length - fib.L) / dt
+    return fib.growth_state, fib.Ldot

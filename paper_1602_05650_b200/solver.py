@@ -529,6 +529,28 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
                 best=ret(x), iterations=iters, residuals=history)
 
 
+def _kinetics_and_contacts(state, dt):
+    """Polymerization kinetics and contact models after the geometry update
+    (solver.py:574-588): per-fiber scalar logic with the reference's RNG
+    draws; the resulting Ldot enters the next step's device rows."""
+    from . import fiber as fibers_
+    from .system import cortical_pull_catastrophe, cortical_push_update
+    for fib in state.fibers:
+        if fib.growth_state == fibers_.STALLED:
+            continue
+        load = np.zeros(3)
+        if fib.bc_plus.kind == "hingedToSurface":
+            load = fib.bc_plus.stiffness * (fib.X[0] - fib.bc_plus.attachment)
+        kin = fib.kinetics
+        fib.Ldot = fibers_.growth_rate(fib, load, kin.v_grow, kin.stall_force)
+        rng = fib.rng if fib.rng is not None else state.rng
+        fibers_.polymerization_step(fib, dt, rng)
+    if state.model("corticalPushing") is not None:
+        cortical_push_update(state)
+    if state.model("cytoplasmicPulling") is not None:
+        cortical_pull_catastrophe(state)
+
+
 def _rotation_is_representable(part, omega, dt):
     if float(np.linalg.norm(omega)) * dt < 1e-14:
         return True
@@ -540,14 +562,9 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
                         implicit_coupling=True, return_info=False):
     """Advance the state by one implicit step on the device, halving dt on
     nonconvergence (solver.py:528-592)."""
-    from .fiber import STALLED
+    from . import fiber as fibers_
     if dt <= 0:
         raise ConfigurationError("time step must be positive")
-    if any(f.growth_state != STALLED for f in state.fibers):
-        raise NotImplementedError("polymerization kinetics run on the host in the reference "
-                                  "(fiber.py:307-356) and are outside this device path")
-    if state.model("corticalPushing") is not None:
-        raise NotImplementedError("cortical contact models are outside this device path")
     if dt_min is None:
         dt_min = dt / 64.0
     attempt = float(dt)
@@ -581,6 +598,7 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
         fib.X = parts.X[m].copy()
         fib.T = parts.T[m].copy()
     state.time += attempt
+    _kinetics_and_contacts(state, attempt)
     LOG.info("step time=%.9g dt=%.3e gmres_iterations=%d residual=%.3e",
              state.time, attempt, iters, history[-1] if history else 0.0)
     if return_info:

@@ -43,6 +43,22 @@ class UniformBodyForce:
         self.direction = d / nrm
 
 
+class CorticalPushing:
+    """Hinged spring attachment of growing plus-ends at the periphery
+    (system.py:56-76)."""
+
+    kind = "corticalPushing"
+
+    def __init__(self, stiffness, contact_distance, tau_cat):
+        if stiffness < 0 or contact_distance < 0:
+            raise ConfigurationError("spring stiffness and contact distance must be nonnegative")
+        if tau_cat <= 0:
+            raise ConfigurationError("contact catastrophe time must be positive")
+        self.stiffness = float(stiffness)
+        self.contact_distance = float(contact_distance)
+        self.tau_cat = float(tau_cat)
+
+
 class CytoplasmicPulling:
     kind = "cytoplasmicPulling"
 
@@ -173,6 +189,65 @@ class SystemState:
             if m.kind == kind:
                 return m
         return None
+
+
+def cytoplasmic_pull_density(fib, motor_force, motor_density):
+    """Tangential motor force density and its integral (system.py:283-295)."""
+    if motor_force < 0 or motor_density < 0:
+        raise ConfigurationError("motor force and density must be nonnegative")
+    scale = motor_force * motor_density
+    density = scale * fib.tangents
+    total = scale * (fib.X[fib.end_index(plus=True)] - fib.X[fib.end_index(plus=False)])
+    return density, total
+
+
+def cortical_push_update(state):
+    """Attach growing plus-ends reaching the periphery, release on
+    catastrophe (system.py:334-362).  Host per-fiber logic after the solve."""
+    from . import fiber as fibers_
+    from .nearfield import nearest_surface_point
+    if state.periphery is None:
+        raise ConfigurationError("cortical pushing requires a periphery")
+    model = state.model("corticalPushing")
+    if model is None:
+        raise ConfigurationError("no cortical pushing model is configured")
+    mesh = state.periphery.mesh
+    out = []
+    for fib in state.fibers:
+        attached = fib.bc_plus.kind == "hingedToSurface"
+        if attached and fib.growth_state == fibers_.SHRINKING:
+            fib.bc_plus = fibers_.FreeEnd()
+            fib.tau_cat = math.inf
+        elif not attached and fib.growth_state == fibers_.GROWING:
+            tip = fib.X[fib.end_index(plus=True)]
+            _, _, _, signed_d = nearest_surface_point(mesh, tip)
+            if -signed_d <= model.contact_distance:
+                fib.bc_plus = fibers_.HingedToSurface(attachment=tip, stiffness=model.stiffness)
+                fib.tau_cat = model.tau_cat
+        out.append(fib.bc_plus)
+    return out
+
+
+def cortical_pull_catastrophe(state, standoff_fraction=0.95):
+    """Instant catastrophe at the periphery standoff shell (system.py:365-388)."""
+    from . import fiber as fibers_
+    if state.periphery is None:
+        raise ConfigurationError("cortical catastrophe requires a periphery")
+    mesh = state.periphery.mesh
+    switched = []
+    for fib in state.fibers:
+        if fib.growth_state == fibers_.SHRINKING:
+            continue
+        rel = fib.X[fib.end_index(plus=True)] - mesh.center
+        rho = float(np.linalg.norm(rel))
+        if rho == 0.0:
+            continue
+        th = math.acos(min(max(rel[2] / rho, -1.0), 1.0))
+        if rho >= standoff_fraction * float(mesh.shape[2](th)):
+            fib.growth_state = fibers_.SHRINKING
+            fib.Ldot = -fib.kinetics.v_shrink
+            switched.append(fib)
+    return switched
 
 
 def external_force_density(state, fib):

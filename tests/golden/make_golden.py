@@ -296,6 +296,47 @@ def tree_fixture():
     save("tree.npz", **out, **versions())
 
 
+KIN = dict(v_grow=0.5, v_shrink=0.8, f_cat=150.0, f_res=250.0, stall_force=4.4, min_length=0.5)
+
+
+def kinetics_state(pushing=True):
+    """Growing aster in a small cell: dynamic instability with fast rates,
+    and cortical pushing (hinged capture at the periphery) or cytoplasmic
+    pulling (standoff catastrophe), per-fiber seeded RNG streams."""
+    from slenderflow import system as S
+    pnc = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), (4, 4)))
+    pts, dirs = S.aster_attachment_layout(pnc, 8, radius_factor=1.3)
+    fibs = []
+    for k, (x0, d) in enumerate(zip(pts, dirs)):
+        fb = fiber.straight_fiber(15, x0, d, 1.0, eps=1e-2, E=1.0,
+                                  growth_state=fiber.GROWING, Ldot=KIN["v_grow"],
+                                  rng=np.random.default_rng(100 + k),
+                                  kinetics=fiber.GrowthKinetics(**KIN))
+        fb.bc_minus = fiber.ClampedToBody(0, x0, d)
+        fibs.append(fb)
+    per = body.Periphery(body.make_surface(body.sphere_shape(1.8), (6, 6)))
+    models = ([S.CorticalPushing(stiffness=5.0, contact_distance=0.2, tau_cat=0.5)] if pushing
+              else [S.CytoplasmicPulling(motor_force=0.91, motor_density=0.5)])
+    return S.SystemState(fibs, [pnc], per, force_models=models)
+
+
+def kinetics_fixture(name, pushing, nsteps=4, dt=1e-3):
+    from slenderflow import solver as R
+    st = kinetics_state(pushing)
+    out = dict(dt=dt, nsteps=nsteps, init_X=np.stack([f.X for f in st.fibers]),
+               init_d=np.stack([f.bc_minus.tangent for f in st.fibers]))
+    params = R.GmresParams(tolerance=1e-10)
+    for s_i in range(nsteps):
+        R.backward_euler_step(st, dt, params)
+        out[f"step{s_i}_X"] = np.stack([f.X for f in st.fibers])
+        out[f"step{s_i}_T"] = np.stack([f.T for f in st.fibers])
+        out[f"step{s_i}_Ldot"] = np.array([f.Ldot for f in st.fibers])
+        out[f"step{s_i}_state"] = np.array([f.growth_state for f in st.fibers])
+        out[f"step{s_i}_bcplus"] = np.array([f.bc_plus.kind for f in st.fibers])
+        out[f"step{s_i}_tau"] = np.array([f.tau_cat for f in st.fibers])
+    save(name, **out, **versions())
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pairs", "operator", "surfaces", "steps"]
     if "pairs" in which:
@@ -314,3 +355,6 @@ if __name__ == "__main__":
         api_ops_fixture()
     if "tree" in which:
         tree_fixture()
+    if "kinetics" in which:
+        kinetics_fixture("step_pushing.npz", True)
+        kinetics_fixture("step_pulling.npz", False)

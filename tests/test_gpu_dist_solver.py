@@ -92,3 +92,27 @@ def test_dist_steps_match_reference(cuda, name, world):
         assert np.linalg.norm(X - ref) / np.linalg.norm(ref) < 1e-8
         assert rel_l2(T, g[f"step{s}_T"]) < 1e-6
         assert abs(it - int(g[f"iters_{s}"])) <= 1
+
+
+def test_dist_kinetics_steps_match_reference(cuda):
+    """Kinetics + cortical pushing over 2 emulated ranks: replicated host
+    state, same RNG streams, same transitions as the reference."""
+    from test_gpu_kinetics import build
+    g = golden("step_pushing.npz")
+    params = solver.GmresParams(tolerance=1e-10)
+
+    def fn(comm):
+        st = build(g, True)
+        res = []
+        for _ in range(int(g["nsteps"])):
+            st = dsolver.dist_backward_euler_step(st, float(g["dt"]), comm, params)
+            res.append((np.stack([f.X for f in st.fibers]), [f.growth_state for f in st.fibers],
+                        [f.bc_plus.kind for f in st.fibers]))
+        return res
+    out = run_ranks(2, fn)
+    for s in range(int(g["nsteps"])):
+        X, states, bcs = out[0][s]
+        assert np.array_equal(out[1][s][0], X)
+        assert states == list(g[f"step{s}_state"]) and bcs == list(g[f"step{s}_bcplus"])
+        ref = g[f"step{s}_X"]
+        assert np.linalg.norm(X - ref) / np.linalg.norm(ref) < 1e-8
