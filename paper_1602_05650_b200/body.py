@@ -30,6 +30,51 @@ def sphere_shape(radius):
             lambda th: np.zeros_like(np.asarray(th, dtype=float)))
 
 
+def _profile(name, a, R, Rp):
+    return (name, a, R, Rp)
+
+
+def s1_shape(a):
+    """Asymmetric cell profile of the reference (body.py:37-41)."""
+    c3 = lambda th: np.cos(th) ** 3                                     # noqa: E731
+    s3 = lambda th: np.sin(th) ** 3                                     # noqa: E731
+    return _profile("s1", a, lambda th: a * (1.0 - 0.35 * c3(th) - 0.15 * s3(th)),
+                    lambda th: a * (1.05 * np.cos(th) ** 2 * np.sin(th)
+                                    - 0.45 * np.sin(th) ** 2 * np.cos(th)))
+
+
+def s2_shape(a):
+    """Tilted-ellipsoid-like profile (body.py:44-47)."""
+    return _profile("s2", a, lambda th: a * (1.0 + 0.2 * np.cos(2 * th) - 0.2 * np.sin(2 * th)),
+                    lambda th: a * (-0.4 * np.sin(2 * th) - 0.4 * np.cos(2 * th)))
+
+
+def s3_shape(a):
+    """Flattened (oblate) profile (body.py:50-53)."""
+    return _profile("s3", a, lambda th: a * (1.0 - 0.6 * np.sin(th) ** 4),
+                    lambda th: a * (-2.4 * np.sin(th) ** 3 * np.cos(th)))
+
+
+def profile_shape(R, Rp=None, name="profile", param=0.0):
+    """User profile R(theta); Rp by central differences when omitted (body.py:56-60)."""
+    if Rp is None:
+        def Rp(th, _R=R, h=1e-5):
+            th = np.asarray(th)
+            return (_R(th + h) - _R(th - h)) / (2 * h)
+    return (name, param, R, Rp)
+
+
+_NAMED = {"s1": s1_shape, "s2": s2_shape, "s3": s3_shape}
+
+
+def named_shape(kind, param):
+    if kind == "sphere":
+        return sphere_shape(param)
+    if kind in _NAMED:
+        return _NAMED[kind](param)
+    raise GeometryError(f"unknown shape {kind!r}")
+
+
 class SurfaceMesh:
     """Nodes, outward normals and Jacobian-folded weights (body.py:74-124)."""
 
@@ -62,9 +107,7 @@ def make_surface(shape, resolution, center=(0.0, 0.0, 0.0)):
     patch-major, each patch a 4x4 (theta, phi) tensor block.
     """
     if isinstance(shape, tuple) and len(shape) == 2:
-        if shape[0] != "sphere":
-            raise GeometryError(f"unknown shape {shape[0]!r}")
-        shape = sphere_shape(shape[1])
+        shape = named_shape(*shape)
     kind, param, R, Rp = shape
     nt, nph = (resolution, resolution) if isinstance(resolution, int) else resolution
     if nt < 2 or nph < 2:
@@ -198,3 +241,72 @@ def near_surface_eval(mesh, q, target, mu, interior_jump=True, upsample=6):
     plain = double_layer_offsurface(mesh, q, np.asarray(target, dtype=float)[None, :], mu,
                                     allow_near=True)[0]  # W_plain q
     return plain + corr
+
+
+# -- small host helpers and mesh text IO (body.py:186-193, 265-295, 567-618) --
+
+def surface_integral(mesh, f):
+    """Quadrature sum of scalar or vector nodal data."""
+    f = np.asarray(f, dtype=float)
+    if f.shape[0] != mesh.n_nodes:
+        raise ValueError("nodal data does not conform to the mesh")
+    return float(mesh.weights @ f) if f.ndim == 1 else mesh.weights @ f
+
+
+def nullspace_operator(periphery, q):
+    """n(x) times the flux of q through the periphery."""
+    mesh = periphery.mesh if isinstance(periphery, Periphery) else periphery
+    flux = float(mesh.weights @ (mesh.normals * np.asarray(q, dtype=float)).sum(axis=1))
+    return mesh.normals * flux
+
+
+def rigid_constraint_averages(particle, q):
+    """Area averages of q and of its moment about the centre."""
+    mesh = particle.mesh
+    if mesh.area <= 0:
+        raise GeometryError("zero-area surface")
+    q = np.asarray(q, dtype=float)
+    wq = mesh.weights[:, None] * q
+    return wq.sum(axis=0) / mesh.area, \
+        (mesh.weights[:, None] * np.cross(mesh.nodes - particle.center, q)).sum(axis=0) / mesh.area
+
+
+MESH_FORMAT_VERSION = 1
+
+
+def mesh_to_text(mesh):
+    """One node per line (x y z nx ny nz w) after a header that records the
+    parametrization, so a parametrized mesh round-trips exactly."""
+    out = [f"# surface-mesh v{MESH_FORMAT_VERSION}"]
+    if mesh.has_parametrization():
+        nt, nph = mesh.patch_grid
+        c = [float(v) for v in mesh.center]
+        out.append(f"# shape {mesh.shape[0]} {float(mesh.shape[1]):.17g} patches {nt} {nph} "
+                   f"center {c[0]:.17g} {c[1]:.17g} {c[2]:.17g}")
+    out.append("# columns: x y z nx ny nz w")
+    rows = np.column_stack([mesh.nodes, mesh.normals, mesh.weights])
+    out.extend(" ".join(f"{v:.17g}" for v in row) for row in rows)
+    return "\n".join(out) + "\n"
+
+
+def mesh_from_text(text):
+    """Inverse of mesh_to_text: a named parametrized shape is rebuilt exactly
+    (and checked against the data), otherwise a bare quadrature mesh."""
+    lines = text.splitlines()
+    if not lines or not lines[0].startswith("# surface-mesh v"):
+        raise ValueError("not a surface-mesh file")
+    if int(lines[0].rsplit("v", 1)[1]) > MESH_FORMAT_VERSION:
+        raise ValueError("unsupported mesh format version")
+    data = np.array([[float(t) for t in ln.split()] for ln in lines
+                     if ln and not ln.startswith("#")])
+    if data.ndim != 2 or data.shape[1] != 7:
+        raise ValueError("expected 7 columns: x y z nx ny nz w")
+    header = [ln.split() for ln in lines if ln.startswith("# shape ")]
+    if header:
+        h = header[0]
+        mesh = make_surface(named_shape(h[2], float(h[3])), (int(h[5]), int(h[6])),
+                            center=tuple(float(v) for v in h[8:11]))
+        if not np.allclose(mesh.nodes, data[:, 0:3], atol=1e-12):
+            raise ValueError("mesh data disagrees with its shape header")
+        return mesh
+    return SurfaceMesh(data[:, 0:3], data[:, 3:6], data[:, 6])

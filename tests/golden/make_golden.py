@@ -337,6 +337,25 @@ def kinetics_fixture(name, pushing, nsteps=4, dt=1e-3):
     save(name, **out, **versions())
 
 
+def shapes_fixture():
+    """Non-spherical profile meshes (body.py:37-72) and a near-surface map on
+    one of them (exercises the golden-section nearest point on R(theta))."""
+    out = {}
+    for k in ("s1", "s2", "s3"):
+        m = body.make_surface(body.named_shape(k, 2.0), (6, 8), center=(0.1, -0.2, 0.3))
+        out.update({f"{k}_nodes": m.nodes, f"{k}_normals": m.normals, f"{k}_weights": m.weights})
+    per = body.make_surface(body.s1_shape(2.0), (6, 8))
+    t = np.array([[0.2, 0.1, 1.2], [1.5, 0.3, -0.1]])
+    rho = [np.linalg.norm(x) for x in t]
+    out["near_t"] = t
+    out["near_W"] = np.stack([body.near_surface_weights(per, x, 1.0, interior_jump=True)
+                              - body.plain_surface_weights(per, x, 1.0) for x in t])
+    out["near_ns"] = np.array([[*body.nearest_surface_point(per, x)[:2],
+                                body.nearest_surface_point(per, x)[3]] for x in t])
+    print("  shapes: target radii", rho)
+    save("shapes.npz", **out, **versions())
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pairs", "operator", "surfaces", "steps"]
     if "pairs" in which:
@@ -355,6 +374,8 @@ if __name__ == "__main__":
         api_ops_fixture()
     if "tree" in which:
         tree_fixture()
+    if "shapes" in which:
+        shapes_fixture()
     if "kinetics" in which:
         kinetics_fixture("step_pushing.npz", True)
         kinetics_fixture("step_pulling.npz", False)

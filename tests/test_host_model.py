@@ -79,3 +79,19 @@ def test_tree_topology_partitions_the_points():
             kids = range(first[k], first[k] + nch[k])
             assert nb[first[k]] == nb[k] and ne[first[k] + nch[k] - 1] == ne[k]
             assert all(ne[a] == nb[a + 1] for a in list(kids)[:-1])
+
+
+def test_profile_shape_meshes_match_reference():
+    """s1/s2/s3 profile meshes (body.py:37-72) bitwise equal to the reference's,
+    and the mesh text format round-trips them."""
+    g = golden("shapes.npz")
+    for k in ("s1", "s2", "s3"):
+        m = body.make_surface(body.named_shape(k, 2.0), (6, 8), center=(0.1, -0.2, 0.3))
+        assert np.array_equal(m.nodes, g[f"{k}_nodes"])
+        assert np.array_equal(m.normals, g[f"{k}_normals"])
+        assert np.array_equal(m.weights, g[f"{k}_weights"])
+        assert np.array_equal(body.mesh_from_text(body.mesh_to_text(m)).nodes, m.nodes)
+    per = body.make_surface(body.s1_shape(2.0), (6, 8))
+    for t, ns in zip(g["near_t"], g["near_ns"]):
+        th, ph, _, d = nearfield.nearest_surface_point(per, t)
+        assert abs(th - ns[0]) < 1e-12 and abs(d - ns[2]) < 1e-12
