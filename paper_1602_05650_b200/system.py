@@ -279,6 +279,69 @@ def attachment_wrench(state, particle_index, candidates=None):
     return F, L
 
 
+# -- attachment layouts and initial conditions (system.py:392-466) --------------
+
+GOLDEN_ANGLE = math.pi * (3.0 - math.sqrt(5.0))
+
+
+def _fibonacci_cap(n, cap_angle):
+    """n quasi-uniform directions on the polar cap theta <= cap_angle."""
+    if n == 1:
+        return np.array([[0.0, 0.0, 1.0]])
+    k = np.arange(n)
+    z = 1.0 - (1.0 - math.cos(cap_angle)) * (k + 0.5) / n
+    rho = np.sqrt(1.0 - z * z)
+    return np.stack([rho * np.cos(k * GOLDEN_ANGLE), rho * np.sin(k * GOLDEN_ANGLE), z], axis=1)
+
+
+def _nominal_radius(pnc):
+    shape = pnc.mesh.shape
+    a = float(shape[1]) if shape is not None else 0.0
+    if a <= 0:
+        raise ConfigurationError("particle shape has no nominal radius")
+    return a
+
+
+def mtoc_attachment_layout(pnc, n_fibers, cap_angle=math.pi / 5.0, radius_factor=1.3):
+    """Attachment points / radial tangents on two opposite polar caps."""
+    if n_fibers <= 0 or n_fibers % 2:
+        raise ConfigurationError("attachment layout needs a positive even fiber count")
+    a = _nominal_radius(pnc)
+    north = _fibonacci_cap(n_fibers // 2, cap_angle)
+    dirs = np.vstack([north, north * np.array([1.0, 1.0, -1.0])])
+    return pnc.center[None, :] + radius_factor * a * dirs, dirs
+
+
+def aster_attachment_layout(pnc, n_fibers, radius_factor=1.3):
+    """One Fibonacci spiral over the whole sphere (radial asters)."""
+    if n_fibers <= 0:
+        raise ConfigurationError("attachment layout needs a positive fiber count")
+    a = _nominal_radius(pnc)
+    dirs = _fibonacci_cap(n_fibers, math.pi)
+    return pnc.center[None, :] + radius_factor * a * dirs, dirs
+
+
+def cloud_init(n_fibers, radius, length, eps, E, seed, p=16, mu=1.0, f0=1.0,
+               load_direction=(0.0, 0.0, 1.0)):
+    """Straight free fibers uniform in a ball under a uniform load, drawn from
+    a generator seeded by `seed` (same draws as the reference)."""
+    from .fiber import straight_fiber
+    if n_fibers <= 0:
+        raise ConfigurationError("need a positive number of fibers")
+    if radius <= 0 or length <= 0:
+        raise ConfigurationError("cloud radius and fiber length must be positive")
+    rng = np.random.default_rng(seed)
+    fibs = []
+    for _ in range(n_fibers):
+        cdir = rng.standard_normal(3)
+        cdir /= np.linalg.norm(cdir)
+        center = radius * rng.random() ** (1.0 / 3.0) * cdir
+        d = rng.standard_normal(3)
+        d /= np.linalg.norm(d)
+        fibs.append(straight_fiber(p, center - 0.5 * length * d, d, length, eps=eps, E=E))
+    return SystemState(fibs, mu=mu, seed=seed, force_models=[UniformBodyForce(f0, load_direction)])
+
+
 @dataclass
 class ComplementaryVelocities:
     periphery: object

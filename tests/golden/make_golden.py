@@ -337,6 +337,16 @@ def kinetics_fixture(name, pushing, nsteps=4, dt=1e-3):
     save(name, **out, **versions())
 
 
+def layouts_fixture():
+    """Attachment layouts and cloud initial condition (system.py:392-466)."""
+    pnc = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), (4, 4), center=(0.5, 0, 0)))
+    ap, ad = system.aster_attachment_layout(pnc, 37)
+    mp, md = system.mtoc_attachment_layout(pnc, 36)
+    cl = system.cloud_init(20, 3.0, 1.0, 1e-2, 1.0, seed=4)
+    save("layouts.npz", aster_p=ap, aster_d=ad, mtoc_p=mp, mtoc_d=md,
+         cloud_X=np.stack([f.X for f in cl.fibers]), **versions())
+
+
 def shapes_fixture():
     """Non-spherical profile meshes (body.py:37-72) and a near-surface map on
     one of them (exercises the golden-section nearest point on R(theta))."""
@@ -376,6 +386,7 @@ if __name__ == "__main__":
         tree_fixture()
     if "shapes" in which:
         shapes_fixture()
+        layouts_fixture()
     if "kinetics" in which:
         kinetics_fixture("step_pushing.npz", True)
         kinetics_fixture("step_pulling.npz", False)

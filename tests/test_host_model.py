@@ -95,3 +95,15 @@ def test_profile_shape_meshes_match_reference():
     for t, ns in zip(g["near_t"], g["near_ns"]):
         th, ph, _, d = nearfield.nearest_surface_point(per, t)
         assert abs(th - ns[0]) < 1e-12 and abs(d - ns[2]) < 1e-12
+
+
+def test_attachment_layouts_and_cloud_init_match_reference():
+    g = golden("layouts.npz")
+    from paper_1602_05650_b200 import system
+    pnc = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), (4, 4), center=(0.5, 0, 0)))
+    p, d = system.aster_attachment_layout(pnc, 37)
+    assert np.array_equal(p, g["aster_p"]) and np.array_equal(d, g["aster_d"])
+    p, d = system.mtoc_attachment_layout(pnc, 36)
+    assert np.array_equal(p, g["mtoc_p"]) and np.array_equal(d, g["mtoc_d"])
+    cl = system.cloud_init(20, 3.0, 1.0, 1e-2, 1.0, seed=4)
+    assert np.array_equal(np.stack([f.X for f in cl.fibers]), g["cloud_X"])
