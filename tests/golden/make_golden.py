@@ -347,6 +347,18 @@ def layouts_fixture():
          cloud_X=np.stack([f.X for f in cl.fibers]), **versions())
 
 
+def spectral_fixture():
+    """Spectral API values (spectral.py:24-154) on a p = 31 grid."""
+    from slenderflow import spectral as R
+    g = R.ChebyshevGrid(31)
+    X = configs.make("c1_clean", seed=0).X[5]
+    v = np.sin(3 * g.nodes) + 0.2 * g.nodes ** 5
+    s, sa, L = R.arclength_map(X, g)
+    save("spectral.npz", nodes=g.nodes, weights=g.weights, D=g.D, X=X, s=s, s_alpha=sa, L=L, v=v,
+         dv=R.cheb_diff(v, g), iv=R.cheb_integrate(v, g), cv=R.cheb_transform(v),
+         interp=np.array([R.cheb_interp(v, a) for a in (-1.0, -0.37, 0.3, 1.0)]), **versions())
+
+
 def shapes_fixture():
     """Non-spherical profile meshes (body.py:37-72) and a near-surface map on
     one of them (exercises the golden-section nearest point on R(theta))."""
@@ -387,6 +399,7 @@ if __name__ == "__main__":
     if "shapes" in which:
         shapes_fixture()
         layouts_fixture()
+        spectral_fixture()
     if "kinetics" in which:
         kinetics_fixture("step_pushing.npz", True)
         kinetics_fixture("step_pulling.npz", False)

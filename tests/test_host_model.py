@@ -2,6 +2,7 @@
 own outputs (golden fixtures)."""
 
 import numpy as np
+import pytest
 
 from conftest import golden
 from paper_1602_05650_b200 import body, nearfield, spectral
@@ -107,3 +108,21 @@ def test_attachment_layouts_and_cloud_init_match_reference():
     assert np.array_equal(p, g["mtoc_p"]) and np.array_equal(d, g["mtoc_d"])
     cl = system.cloud_init(20, 3.0, 1.0, 1e-2, 1.0, seed=4)
     assert np.array_equal(np.stack([f.X for f in cl.fibers]), g["cloud_X"])
+
+
+def test_spectral_api_matches_reference():
+    """ChebyshevGrid, arclength_map and the cheb_* helpers bitwise equal to
+    the reference's (spectral.py:24-154)."""
+    from paper_1602_05650_b200 import spectral as S
+    g = golden("spectral.npz")
+    grid = S.ChebyshevGrid(31)
+    for k in ("nodes", "weights", "D"):
+        assert np.array_equal(getattr(grid, k), g[k])
+    s, sa, L = S.arclength_map(g["X"], grid)
+    assert np.array_equal(s, g["s"]) and np.array_equal(sa, g["s_alpha"]) and L == float(g["L"])
+    assert np.array_equal(S.cheb_diff(g["v"], grid), g["dv"])
+    assert S.cheb_integrate(g["v"], grid) == float(g["iv"])
+    assert np.array_equal(S.cheb_transform(g["v"]), g["cv"])
+    assert np.array_equal([S.cheb_interp(g["v"], a) for a in (-1.0, -0.37, 0.3, 1.0)], g["interp"])
+    with pytest.raises(S.InvalidOrderError):
+        S.ChebyshevGrid(3)
