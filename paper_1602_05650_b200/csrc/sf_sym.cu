@@ -599,13 +599,23 @@ __global__ void slab_meta_f32_kernel(const SymSrc *__restrict__ src, int64_t N,
     }
 }
 
-// out[i] (+)= pref * sum_{s < G} part[s][i], slots in order.
-__global__ void sym_reduce_kernel(const double *__restrict__ part, int G, int64_t N, double pref,
-                                  double *__restrict__ out, int accumulate) {
+// out[i] (+)= pref * sum_{s < G} part[s][i], slots in order.  Slot s of a
+// point in unit u was written by task {min(u,s), max(u,s)}; slots whose task
+// is outside this launch's range [t0, t1) (another rank's share) are skipped
+// instead of being zero-filled and read back -- the sum is unchanged.
+__global__ void sym_reduce_kernel(const double *__restrict__ part, int G, int64_t N, int M,
+                                  int64_t t0, int64_t t1, double pref, double *__restrict__ out,
+                                  int accumulate) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= 3 * N) return;
+    const int64_t u = (e / 3) / M;
     double s = 0.0;
-    for (int k = 0; k < G; ++k) s += part[(int64_t)k * 3 * N + e];
+    for (int k = 0; k < G; ++k) {
+        const int64_t g = k < u ? k : u, h = k < u ? u : k;
+        const int64_t t = g * G - g * (g - 1) / 2 + (h - g);
+        if (t < t0 || t >= t1) continue;
+        s += part[(int64_t)k * 3 * N + e];
+    }
     out[e] = accumulate ? out[e] + pref * s : pref * s;
 }
 
@@ -740,9 +750,6 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     a.G = G;
     a.task0 = sym_task_range(G, rank, world, &a.ntasks);
     a.part = part;
-    if (world > 1 &&
-        cudaMemsetAsync(part, 0, sizeof(double) * 3 * (size_t)N * G, st) != cudaSuccess)
-        return check_launch("memset");
     a.bad = (unsigned long long *)bad;
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
@@ -788,8 +795,8 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     int rc = check_launch("sym_task_kernel");
     if (a.ntasks == 0 && world == 1) return rc;
     if (rc) return rc;
-    sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(part, G, N, pref, out,
-                                                                      accumulate);
+    sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(
+        part, G, N, M, a.task0, a.task0 + a.ntasks, pref, out, accumulate);
     return check_launch("sym_reduce_kernel");
 }
 
