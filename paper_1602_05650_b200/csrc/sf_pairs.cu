@@ -848,8 +848,12 @@ constexpr int kTargetsPerCta = kNT * kTB;
 // keeping every chunk >= 4 tiles.
 int choose_split(int64_t nt, int64_t ns) {
     const int64_t blocks = (nt + kTargetsPerCta - 1) / kTargetsPerCta;
+    static const int min_tiles = [] {   // source tiles per split (tuning knob)
+        const char *e = getenv("SF_SPLIT_TILES");
+        return e ? atoi(e) : 4;
+    }();
     int64_t s = (16384 + blocks - 1) / blocks;
-    int64_t max_s = ns / (4 * kTS);
+    int64_t max_s = ns / (min_tiles * kTS);
     // small problems: split down to one source tile per CTA if that is what
     // it takes to give every SM two CTAs
     const int64_t fill = (2 * 148 + blocks - 1) / blocks;
