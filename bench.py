@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
-    ap.add_argument("--step-config", default="c2,c5",
+    ap.add_argument("--step-config", default="c2,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
     ap.add_argument("--big-step-count", type=int, default=1,
@@ -166,6 +166,8 @@ def measure_steps(config, count, comm=None, warm=True):
     import torch
 
     from paper_1602_05650_b200 import configs, solver
+    config, _, precision = config.partition(":")
+    precision = precision or "fp64"
     if config == "c2":
         st = configs.aster(n_fibers=1024)
         dt, tol = 1e-3, 1e-10
@@ -177,12 +179,14 @@ def measure_steps(config, count, comm=None, warm=True):
     params = solver.GmresParams(tolerance=tol)
     if comm is None:
         def one(st):
-            return solver.backward_euler_step(st, dt, params, return_info=True)
+            return solver.backward_euler_step(st, dt, params, return_info=True,
+                                              precision=precision)
     else:
         from paper_1602_05650_b200 import dsolver
 
         def one(st):
-            return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True)
+            return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True,
+                                                    precision=precision)
 
     def sync():
         torch.cuda.synchronize()
@@ -203,7 +207,7 @@ def measure_steps(config, count, comm=None, warm=True):
         t = torch.tensor(times, dtype=torch.float64, device="cuda")
         comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
         times = t.tolist()
-    return {"config": desc, "dt": dt, "gmres_tol": tol, "steps": count,
+    return {"config": desc, "precision": precision, "dt": dt, "gmres_tol": tol, "steps": count,
             "ranks": 1 if comm is None else comm.world,
             "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
             "gmres_iterations": iters,
@@ -356,7 +360,7 @@ def run_ours(args, rank, world, local_rank):
         from paper_1602_05650_b200.dsolver import TorchComm
         comm = TorchComm() if world > 1 else None
         for k, cfg in enumerate(c for c in args.step_config.split(",") if c):
-            big = cfg in ("c3", "c5")
+            big = cfg.split(":")[0] in ("c3", "c5")
             try:
                 steps.append(measure_steps(cfg, args.big_step_count if big else args.step_count,
                                            comm, warm=not (big and k > 0)))

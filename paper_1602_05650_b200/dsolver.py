@@ -33,7 +33,7 @@ import numpy as np
 from . import _native, spectral
 from .dist import shard_range
 from .solver import (BC_CODES, FactorizationError, GmresParams, NonconvergenceError,
-                     StepLayout, _kinetics_and_contacts, _ptr, _stream)
+                     StepLayout, _kinetics_and_contacts, _precision_mode, _ptr, _stream)
 from .system import (ConfigurationError, SingularEvaluationError, FiberGeometry, InteractionCache, external_force_density,
                      stack_fibers)
 
@@ -139,7 +139,7 @@ class ThreadComm:
 class DistBlockOperator:
     """This rank's rows of the implicit step system (solver.py:187-364)."""
 
-    def __init__(self, state, dt, comm, mu=None, symmetric=None):
+    def __init__(self, state, dt, comm, mu=None, symmetric=None, precision="fp64"):
         import torch
         if dt <= 0:
             raise ConfigurationError("time step must be positive")
@@ -176,9 +176,12 @@ class DistBlockOperator:
             if nf else None
         self.fgrp = torch.as_tensor(np.repeat(np.arange(nf, dtype=np.int64), n), device=dev)
         # fiber targets: symmetric -> fiber pair sums come from the task split
+        self.mode = _precision_mode(precision)
         self.cache_fib = (InteractionCache(state, target_range=(lo_f, hi_f), fiber_geometry=geo,
-                                           fiber_pairs=not self.symmetric) if self.nown else None)
-        self.cache_surf = (InteractionCache(state, target_range=(0, n_surf_t), fiber_geometry=geo)
+                                           fiber_pairs=not self.symmetric, mode=self.mode)
+                          if self.nown else None)
+        self.cache_surf = (InteractionCache(state, target_range=(0, n_surf_t), fiber_geometry=geo,
+                                            mode=self.mode)
                            if rank == 0 and n_surf_t else None)
         # frozen fiber operators of the OWN fibers
         o, no = self.f0, self.nown
@@ -315,7 +318,7 @@ class DistBlockOperator:
             g = self.geo
             _native.call("sf_sbt_symmetric_partial", _ptr(g.X), _ptr(self.fgrp), N, n,
                          _ptr(f_full), _ptr(g.wnode), _ptr(self.fdcoef),
-                         1.0 / (8.0 * math.pi * self.mu), _native.SF_MODE_FP64, c.rank, c.world,
+                         1.0 / (8.0 * math.pi * self.mu), self.mode, c.rank, c.world,
                          _ptr(self._part), _ptr(self._bad), st)
             self._rs_in[:N].copy_(self._part)
             c.reduce_scatter_sum(self._rs_out, self._rs_in)
@@ -505,11 +508,12 @@ def dist_gmres_solve(op, prec, rhs, params=None):
                 f"iterations (residual {rel:.3e})", best=x, iterations=iters, residuals=history)
 
 
-def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, symmetric=None):
+def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, symmetric=None,
+                             precision="fp64"):
     """backward_euler_step (solver.py:528-592) over `comm`'s ranks.  The host
     state is replicated; every rank ends with the same updated state."""
     import torch
-    op = DistBlockOperator(state, dt, comm, symmetric=symmetric)
+    op = DistBlockOperator(state, dt, comm, symmetric=symmetric, precision=precision)
     rhs = op.rhs_device()
     prec = DistPreconditioner(op)
     x, iters, history = dist_gmres_solve(op, prec, rhs, params)

@@ -112,12 +112,24 @@ def host_elastic_force_density(fib, Xcand, Tcand):
             + Ds @ (np.asarray(Tcand, dtype=float)[:, None] * fib.tangents))
 
 
+def _precision_mode(precision):
+    """"fp64" (default) or "fp32c": the fiber x fiber pair sums in FP32
+    arithmetic with FP64 accumulation (north_star variant, <= 1e-5 of FP64);
+    every other term stays FP64."""
+    from ._native import SF_MODE_FP32C, SF_MODE_FP64
+    modes = {"fp64": SF_MODE_FP64, "fp32c": SF_MODE_FP32C}
+    if precision not in modes:
+        raise ConfigurationError(f"precision must be one of {sorted(modes)}")
+    return modes[precision]
+
+
 class BlockOperator:
     """Linear action of the implicit step system on the stacked unknowns,
     evaluated on the device (solver.py:187-364).  apply/rhs accept and return
     numpy arrays or CUDA tensors."""
 
-    def __init__(self, state, dt, mu=None, backend=None, cache=None, implicit_coupling=True):
+    def __init__(self, state, dt, mu=None, backend=None, cache=None, implicit_coupling=True,
+                 precision="fp64"):
         import torch
         if dt <= 0:
             raise ConfigurationError("time step must be positive")
@@ -129,7 +141,8 @@ class BlockOperator:
         if self.mu <= 0:
             raise ConfigurationError("viscosity must be positive")
         self.layout = StepLayout(state)
-        self.cache = cache if cache is not None else InteractionCache(state, backend=backend)
+        self.cache = cache if cache is not None else \
+            InteractionCache(state, backend=backend, mode=_precision_mode(precision))
         self.implicit_coupling = True
         self.device = self.cache.device
         dev = self.device
@@ -312,9 +325,10 @@ class BlockOperator:
         return A
 
 
-def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implicit_coupling=True):
+def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implicit_coupling=True,
+                           precision="fp64"):
     op = BlockOperator(state, dt, mu=mu, backend=backend, cache=cache,
-                       implicit_coupling=implicit_coupling)
+                       implicit_coupling=implicit_coupling, precision=precision)
     return op, op.rhs_device()
 
 
@@ -559,7 +573,7 @@ def _rotation_is_representable(part, omega, dt):
 
 
 def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=None,
-                        implicit_coupling=True, return_info=False):
+                        implicit_coupling=True, return_info=False, precision="fp64"):
     """Advance the state by one implicit step on the device, halving dt on
     nonconvergence (solver.py:528-592)."""
     from . import fiber as fibers_
@@ -568,7 +582,7 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
     if dt_min is None:
         dt_min = dt / 64.0
     attempt = float(dt)
-    cache = InteractionCache(state, backend=backend)
+    cache = InteractionCache(state, backend=backend, mode=_precision_mode(precision))
     while True:
         op, rhs = assemble_step_operator(state, attempt, mu=mu, backend=backend, cache=cache,
                                          implicit_coupling=implicit_coupling)

@@ -154,3 +154,19 @@ def test_fused_mgs_bitwise_equals_dot_axpy_sequence(cuda, k):
     assert torch.equal(h1, h2)
     assert torch.equal(w1, w2)
     assert torch.equal(V1, V2)
+
+
+def test_fp32c_step_converges_and_tracks_fp64(cuda):
+    """precision="fp32c" (fiber pair sums in FP32 with FP64 accumulation):
+    GMRES still reaches 1e-10 and positions stay within 1e-5 of FP64."""
+    import copy
+    from paper_1602_05650_b200 import configs
+    st0 = configs.cloud_state("c3_scaled", n_fibers=160)
+    out = {}
+    for prec in ("fp64", "fp32c"):
+        st, info = solver.backward_euler_step(copy.deepcopy(st0), 5e-3,
+                                              solver.GmresParams(tolerance=1e-10),
+                                              return_info=True, precision=prec)
+        assert info["history"][-1] <= 1e-10
+        out[prec] = np.stack([f.X for f in st.fibers])
+    assert np.linalg.norm(out["fp32c"] - out["fp64"]) / np.linalg.norm(out["fp64"]) < 1e-5
