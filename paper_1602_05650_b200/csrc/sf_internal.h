@@ -16,7 +16,7 @@ int set_error(int code, const char *fmt, ...);
 // are independent buffers.  Steady-state calls allocate nothing.
 class Workspace {
    public:
-    static constexpr int kSlots = 8;
+    static constexpr int kSlots = 12;
     void *get(int slot, size_t bytes, cudaStream_t st);
     ~Workspace();
 
@@ -67,6 +67,13 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
 int sym_unit_size(int64_t N, int64_t group_size);
+// fiber points (A) x surface nodes (B), both directions per pair (sf_cross.cu)
+int pairs_cross(const double *xa, const double *fa, const double *wa, const double *dcoef,
+                int64_t NA, const double *xb, const double *qb, const double *wb,
+                const double *nb, int64_t NB, double pref_a, double pref_b, double *out_a,
+                int accumulate_a, double *out_b, int accumulate_b, int64_t *bad_a,
+                int64_t *bad_b, cudaStream_t st, Workspace &ws);
+bool use_cross(int64_t NA, int64_t NB);
 int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,

@@ -86,7 +86,35 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
     const double pref = 1.0 / (8.0 * M_PI * L->mu);
     int rc;
     const int64_t off = L->fiber_target_off;
-    if (L->nfs > 0 && off >= 0 && off + L->nfs == L->nt && use_symmetric(L->mode, L->nfs)) {
+    const bool sym = L->nfs > 0 && off >= 0 && off + L->nfs == L->nt &&
+                     use_symmetric(L->mode, L->nfs);
+    // Surface targets are exactly the surface sources (whole system): the
+    // fiber <-> surface pairs then run once per pair (sf_cross.cu).
+    const bool cross = sym && L->nss > 0 && L->nss == off && use_cross(L->nfs, L->nss);
+    if (cross) {
+        // surface targets <- surface sources (writes rows [0, off))
+        rc = pairs_stresslet(L->trg, L->tgrp, off, L->ssrc, L->sgrp, L->nss, L->snrm, q,
+                             -3.0 / (4.0 * M_PI * L->mu), u, bad_s, st, ws, L->sw, 0);
+        if (rc) return rc;
+        // fiber targets <- fiber sources, symmetrically (writes rows [off, nt))
+        int64_t *bad_sym = nullptr;
+        if (bad) {
+            bad_sym = (int64_t *)ws.get(6, sizeof(int64_t), st);
+            if (!bad_sym) return SF_ENOMEM;
+        }
+        rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
+                                 L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws, L->mode);
+        if (rc) return rc;
+        if (bad) {
+            rc = add_counter(bad_f, bad_sym, st);
+            if (rc) return rc;
+        }
+        // fiber targets <- surface sources and surface targets <- fiber sources
+        rc = pairs_cross(L->fsrc, f, L->fw, L->fdcoef, L->nfs, L->ssrc, q, L->sw, L->snrm, L->nss,
+                         -3.0 / (4.0 * M_PI * L->mu), pref, u + 3 * off, 1, u, 1, bad_s, bad_f,
+                         st, ws);
+        if (rc) return rc;
+    } else if (sym) {
         // non-fiber targets against fiber sources, then the fiber block symmetrically
         if (off > 0) {
             rc = pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f, L->fw,
@@ -113,7 +141,7 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
     } else if (cudaMemsetAsync(u, 0, sizeof(double) * 3 * L->nt, st) != cudaSuccess) {
         return check_launch("memset");
     }
-    if (L->nss > 0) {
+    if (L->nss > 0 && !cross) {
         rc = pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss, L->snrm, q,
                              -3.0 / (4.0 * M_PI * L->mu), u, bad_s, st, ws, L->sw, 1);
         if (rc) return rc;

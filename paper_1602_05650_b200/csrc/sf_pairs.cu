@@ -512,6 +512,7 @@ __device__ __forceinline__ void write_out(double *dst, const double *u, double s
 struct __align__(16) TileMeta {
     double lo[3], hi[3];
     int gmin, gmax;
+    int all_grouped;   // every source of the tile has a group id >= 0
 };
 
 template <int TS>
@@ -522,6 +523,7 @@ __global__ void tile_meta_kernel(const Src80 *__restrict__ src, int64_t ns,
     const int64_t j = (int64_t)blockIdx.x * TS + threadIdx.x;
     double v[6];
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    const int ungrouped = __syncthreads_or(j < ns && src[j].g < 0);
     if (j < ns) {
         const Src80 &q = src[j];
         double x, y, z;
@@ -564,6 +566,7 @@ __global__ void tile_meta_kernel(const Src80 *__restrict__ src, int64_t ns,
         }
         m.gmin = gred[0][0];
         m.gmax = gred[1][0];
+        m.all_grouped = !ungrouped;
         for (int k = 1; k < TS / 32; ++k) {
             for (int c = 0; c < 3; ++c) {
                 m.lo[c] = fmin(m.lo[c], red[c][k]);
@@ -596,6 +599,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
     int nb[TB];
     double bx[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    bool tneg = false;   // some target excludes nothing (group < 0)
 #pragma unroll
     for (int k = 0; k < TB; ++k) {
         int64_t i = tbase + k * NT + tid;
@@ -616,8 +620,14 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
         if (g >= 0) {
             gmn = min(gmn, g);
             gmx = max(gmx, g);
+        } else {
+            tneg = true;
         }
     }
+    // a tile whose sources all share the single group of every target of the
+    // CTA is excluded pair by pair: skip it (the reference evaluates and
+    // discards those pairs; the sums are identical)
+    const bool cta_neg = __syncthreads_or(tneg);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -679,6 +689,8 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
             d2 = fma(gap, gap, d2);
         }
         const bool fast = (d2 > kFastTileMinDist2) && (m.gmax < gmn || m.gmin > gmx);
+        const bool excluded = !cta_neg && m.all_grouped && m.gmin == m.gmax && gmn == gmx &&
+                              m.gmin == gmn;
         mbar_wait(&full[s], (uint32_t)((t >> 1) & 1));
         __syncthreads();  // all threads are done with tile t-1 (buffer s^1)
         if (tid == 0 && t + 1 < ntiles) {
@@ -689,7 +701,9 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(PairArgs a,
         }
         const int cnt = (int)imin64(TS, j1 - (j0 + (int64_t)t * TS));
         const Src80 *ts = tile[s];
-        if (fast && cnt == TS) {
+        if (excluded) {
+            // nothing to add
+        } else if (fast && cnt == TS) {
 #pragma unroll UNR
             for (int jj = 0; jj < TS; ++jj) {
                 typename P::SrcR sr;

@@ -681,10 +681,9 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
                                      accumulate, st, ws, mode);
 }
 
-// The unit-pair tasks of rank `rank` of `world`: contiguous equal-count
-// ranges of the G(G+1)/2 tasks.  out receives this rank's contribution to
-// EVERY point (slots of other ranks' tasks are zero); summing `out` over
-// ranks (reduce-scatter) gives the full sum.
+// The unit-pair tasks of rank `rank` of `world`: out receives this rank's
+// contribution to EVERY point; summing `out` over ranks (reduce-scatter)
+// gives the full sum.
 // Contiguous task range of `rank`, balanced by cost: off-diagonal tasks
 // evaluate twice the pairs of a diagonal one.  Tasks run row by row, each row
 // g = {g,g}, {g,g+1}, ..., {g,G-1} starting with its diagonal, so the cost of
