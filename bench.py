@@ -43,11 +43,11 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
-    ap.add_argument("--step-config", default="c2,c5,c5:fp32c",
+    ap.add_argument("--step-config", default="c2,c3,c4,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
     ap.add_argument("--big-step-count", type=int, default=1,
-                    help="timed steps of c3/c5 (about 38 s each on one GPU at c5)")
+                    help="timed steps of c3/c4/c5 (2 s / 8 s / 38 s each on one GPU)")
     return ap.parse_args()
 
 
@@ -172,6 +172,11 @@ def measure_steps(config, count, comm=None, warm=True):
         st = configs.aster(n_fibers=1024)
         dt, tol = 1e-3, 1e-10
         desc = "c2: 1024 fibers x 32 nodes clamped to a sphere (8x8 patches), plus-end force 1"
+    elif config == "c4":
+        st = configs.confined_aster()
+        dt, tol = 1e-3, 1e-8
+        desc = ("c4: 2048 fibers x 32 nodes clamped to a centrosome in a 40,960-node periphery, "
+                "fiber<->boundary and boundary<->boundary double layers")
     else:
         st = configs.cloud_state(config)
         dt, tol = 5e-3, 1e-10
@@ -360,7 +365,7 @@ def run_ours(args, rank, world, local_rank):
         from paper_1602_05650_b200.dsolver import TorchComm
         comm = TorchComm() if world > 1 else None
         for k, cfg in enumerate(c for c in args.step_config.split(",") if c):
-            big = cfg.split(":")[0] in ("c3", "c5")
+            big = cfg.split(":")[0] in ("c3", "c4", "c5")
             try:
                 steps.append(measure_steps(cfg, args.big_step_count if big else args.step_count,
                                            comm, warm=not (big and k > 0)))

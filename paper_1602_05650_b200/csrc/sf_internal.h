@@ -74,6 +74,11 @@ int pairs_cross(const double *xa, const double *fa, const double *wa, const doub
                 int accumulate_a, double *out_b, int accumulate_b, int64_t *bad_a,
                 int64_t *bad_b, cudaStream_t st, Workspace &ws);
 bool use_cross(int64_t NA, int64_t NB);
+// symmetric on-surface subtracted double layer for large meshes (sf_dlsym.cu)
+bool use_dl_symmetric(int64_t n);
+int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const double *w,
+                                  const double *q, int64_t n, double pref, double *out,
+                                  cudaStream_t st, Workspace &ws);
 int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,

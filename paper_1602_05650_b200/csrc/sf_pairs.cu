@@ -1022,6 +1022,8 @@ int pairs_stresslet(const double *trg, const int64_t *tgrp, int64_t nt, const do
 int pairs_dl_subtracted(const double *nodes, const double *nrm, const double *w, const double *q,
                         int64_t n, double pref, double *out, cudaStream_t st, Workspace &ws) {
     if (n == 0) return 0;
+    if (use_dl_symmetric(n))
+        return pairs_dl_subtracted_symmetric(nodes, nrm, w, q, n, pref, out, st, ws);
     Src80 *packed = (Src80 *)ws.get(0, sizeof(Src80) * (size_t)n, st);
     if (!packed) return SF_ENOMEM;
     pack_surface_self<<<pack_grid(n), 256, 0, st>>>(nodes, nrm, w, q, n, packed);
