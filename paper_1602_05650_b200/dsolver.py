@@ -180,9 +180,24 @@ class DistBlockOperator:
         self.cache_fib = (InteractionCache(state, target_range=(lo_f, hi_f), fiber_geometry=geo,
                                            fiber_pairs=not self.symmetric, mode=self.mode)
                           if self.nown else None)
+        # surface targets: rank 0 evaluates the surface/particle sources and the
+        # near maps; the fiber-source sums are split by fiber over the ranks
+        # (each rank: surface targets <- its own fibers) and all-reduced
         self.cache_surf = (InteractionCache(state, target_range=(0, n_surf_t), fiber_geometry=geo,
-                                            mode=self.mode)
+                                            mode=self.mode, fiber_pairs=False)
                            if rank == 0 and n_surf_t else None)
+        self._surf_part = None
+        if n_surf_t and nf:
+            tgt = np.vstack([p.mesh.nodes for p in state.particles]
+                            + ([state.periphery.mesh.nodes] if state.periphery is not None else []))
+            tgr = np.concatenate([np.full(p.mesh.n_nodes, nf + i, dtype=np.int64)
+                                  for i, p in enumerate(state.particles)]
+                                 + ([np.full(state.periphery.mesh.n_nodes, nf + len(state.particles),
+                                             dtype=np.int64)] if state.periphery is not None else []))
+            self._surf_trg = torch.as_tensor(tgt, **f64).contiguous()
+            self._surf_tgrp = torch.as_tensor(tgr, device=dev)
+            self._surf_part = torch.zeros((n_surf_t, 3), **f64)
+            self._surf_bad = torch.zeros(1, dtype=torch.int64, device=dev)
         # frozen fiber operators of the OWN fibers
         o, no = self.f0, self.nown
         self.Dpow = torch.empty((no, 4, n, n), **f64)
@@ -328,9 +343,24 @@ class DistBlockOperator:
                 ub_f = ub_f + self._rs_out[:no * n]
         if no:
             _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(ub_f), int(constants), _ptr(out), st)
+        # surface targets <- own fibers, summed over ranks
+        if self._surf_part is not None:
+            if no:
+                lo, hi = self.f0 * n, (self.f0 + no) * n
+                sw = (self.geo.wnode.reshape(-1)[lo:hi, None] * f_full[lo:hi]).contiguous()
+                _native.call("sf_sbt_pair", _ptr(self._surf_trg), _ptr(self._surf_tgrp),
+                             self.n_surf_t, _ptr(self.geo.X.reshape(-1, 3)[lo:hi]),
+                             _ptr(self.fgrp[lo:hi]), hi - lo, _ptr(sw), _ptr(self.fdcoef[lo:hi]),
+                             1.0 / (8.0 * math.pi * self.mu), self.mode, _ptr(self._surf_part),
+                             _ptr(self._surf_bad), st)
+                if int(self._surf_bad.item()):
+                    raise SingularEvaluationError("a target coincides with another fiber's node")
+            else:
+                self._surf_part.zero_()
+            c.all_reduce_sum(self._surf_part)
         # surfaces (rank 0)
         if self.surf:
-            ub_s = self.cache_surf.apply(f_full, q, wr, check=True)
+            ub_s = self.cache_surf.apply(f_full, q, wr, check=True) + self._surf_part
             pref_dl = -3.0 / (4.0 * math.pi * self.mu)
             for s in self.surf:
                 qs = u[s["sl"]]
