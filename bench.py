@@ -15,7 +15,6 @@ once per step, fixed total work ("strong" scaling).
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess

@@ -23,7 +23,6 @@ laws follow BASELINE.json and SURVEY.md §8(d):
   other fiber's near shell, system.py:564-577).
 """
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

@@ -18,7 +18,7 @@ import numpy as np
 from . import _native, nearfield, spectral
 from ._native import SF_MODE_FP64
 from .fiber import InsideFiberError, end_force_torque
-from .kernels import MIN_SEPARATION, SingularEvaluationError
+from .kernels import SingularEvaluationError
 
 
 class ConfigurationError(ValueError):

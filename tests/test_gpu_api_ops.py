@@ -3,7 +3,6 @@
 against the reference's own outputs (golden api_ops.npz from
 tests/golden/make_golden.py)."""
 
-import numpy as np
 import pytest
 
 from conftest import golden

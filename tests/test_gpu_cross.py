@@ -2,8 +2,6 @@
 separate per-target sweeps (SF_CROSS=0), on the C4 confined aster (65,536
 fiber points, 40,960-node periphery, centrosome) and a C2-sized aster."""
 
-import os
-
 import numpy as np
 import pytest
 

@@ -2,7 +2,6 @@
 device path (test_system.py, test_fiber.py, test_body.py of the reference;
 tolerances as there unless noted)."""
 
-import math
 
 import numpy as np
 import pytest

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from paper_1602_05650_b200 import body, nearfield, spectral
+from paper_1602_05650_b200 import body, nearfield
 from paper_1602_05650_b200.fiber import Fiber, straight_fiber
 
 
