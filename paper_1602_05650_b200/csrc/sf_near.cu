@@ -496,6 +496,20 @@ extern "C" int sf_near_surface_weights(
         return set_error(SF_EINVAL, "null pointer");
     if (!(mu > 0)) return set_error(SF_EINVAL, "viscosity must be positive");
     cudaStream_t st = (cudaStream_t)stream;
+    // pairs ride gridDim.y (<= 65535): launch in chunks
+    constexpr int64_t kChunk = 65535;
+    if (npairs > kChunk) {
+        const int64_t Nc = nt * nph * 16;
+        for (int64_t p0 = 0; p0 < npairs; p0 += kChunk) {
+            const int64_t k = npairs - p0 < kChunk ? npairs - p0 : kChunk;
+            const int rc = sf_near_surface_weights(
+                cnodes, cnrm, cw, nt, nph, fnodes, fnrm, fw, fcoef, f, k, trg + 3 * p0,
+                x0 + 3 * p0, pts + 9 * p0, ell + 4 * p0, jump + p0, r0patch + p0,
+                r0coef + 16 * p0, mu, work, W + p0 * 9 * Nc, stream);
+            if (rc) return rc;
+        }
+        return SF_OK;
+    }
     SurfArgs A;
     A.cnodes = cnodes; A.cnrm = cnrm; A.cw = cw; A.nt = nt; A.nph = nph;
     A.fnodes = fnodes; A.fnrm = fnrm; A.fw = fw; A.fcoef = fcoef; A.f = f;
