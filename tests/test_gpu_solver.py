@@ -170,3 +170,30 @@ def test_fp32c_step_converges_and_tracks_fp64(cuda):
         assert info["history"][-1] <= 1e-10
         out[prec] = np.stack([f.X for f in st.fibers])
     assert np.linalg.norm(out["fp32c"] - out["fp64"]) / np.linalg.norm(out["fp64"]) < 1e-5
+
+
+def test_error_paths_match_reference(cuda):
+    """NonconvergenceError carries the best iterate, iteration count and
+    residual history (solver.py:40-47); backward_euler_step halves dt down to
+    dt_min and re-raises (solver.py:546-556); bad arguments raise
+    ConfigurationError before any state change."""
+    g = golden("step_cloud.npz")
+    st = cloud_from(g)
+    op, rhs = solver.assemble_step_operator(st, float(g["dt"]))
+    prec = solver.Preconditioner(op)
+    with pytest.raises(solver.NonconvergenceError) as err:
+        solver.gmres_solve(op, prec, rhs, solver.GmresParams(tolerance=1e-14, restart=3,
+                                                             max_iterations=4))
+    e = err.value
+    assert e.iterations == 4 and len(e.residuals) == 4 and e.best is not None
+    assert e.best.shape == rhs.shape
+    X0 = np.stack([f.X for f in st.fibers])
+    with pytest.raises(solver.NonconvergenceError):
+        solver.backward_euler_step(st, float(g["dt"]),
+                                   solver.GmresParams(tolerance=1e-14, max_iterations=3),
+                                   dt_min=float(g["dt"]) / 4)
+    assert np.array_equal(np.stack([f.X for f in st.fibers]), X0)    # state untouched
+    with pytest.raises(system.ConfigurationError):
+        solver.backward_euler_step(st, 0.0)
+    with pytest.raises(system.ConfigurationError):
+        solver.backward_euler_step(st, 1e-3, precision="fp16")

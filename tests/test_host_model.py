@@ -126,3 +126,10 @@ def test_spectral_api_matches_reference():
     assert np.array_equal([S.cheb_interp(g["v"], a) for a in (-1.0, -0.37, 0.3, 1.0)], g["interp"])
     with pytest.raises(S.InvalidOrderError):
         S.ChebyshevGrid(3)
+
+
+def test_gmres_params_validation():
+    from paper_1602_05650_b200 import solver, system
+    for kw in (dict(tolerance=0.0), dict(tolerance=1.0), dict(restart=0), dict(max_iterations=0)):
+        with pytest.raises(system.ConfigurationError):
+            solver.GmresParams(**kw)
