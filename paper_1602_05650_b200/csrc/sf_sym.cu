@@ -160,7 +160,7 @@ __device__ __forceinline__ bool boxes_far(const double *blo, const double *bhi, 
     return d2 > 1e-20;
 }
 
-template <int MINB, int TBI>
+template <int MINB, int TBI, bool PF = false>
 __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) {
     constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];           // M x 3 transposed accumulators
@@ -223,7 +223,26 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             const int nxt = (lane + 1) & 31;
             // step s: this lane pairs its i's with j = (lane + s) mod 32 and
             // carries that j's transposed accumulator (rotated by shuffles)
-            if (both && fast) {
+            if (both && fast && PF) {
+                // positions of step s+1 are loaded while step s computes
+                double2 nxy = js_xy[warp][lane], nzf = js_zf[warp][lane];
+#pragma unroll 4
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PData pj;
+                    const double2 ff = js_ff[warp][k], cc = js_cc[warp][k];
+                    pj.x = nxy.x; pj.y = nxy.y; pj.z = nzf.x; pj.fx = nzf.y; pj.fy = ff.x;
+                    pj.fz = ff.y; pj.c = cc.x; pj.c3 = cc.y; pj.g = 0;
+                    const int k1 = (lane + s + 1) & 31;
+                    nxy = js_xy[warp][k1];
+                    nzf = js_zf[warp][k1];
+#pragma unroll
+                    for (int q = 0; q < TBI; ++q) sym_pair<false, true>(pi[q], pj, ui[q], uj, nb);
+                    uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                    uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                    uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                }
+            } else if (both && fast) {
 #pragma unroll 4
                 for (int s = 0; s < 32; ++s) {
                     const int k = (lane + s) & 31;
@@ -753,7 +772,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
         const char *e = getenv("SF_SYM_VARIANT");
-        return e ? atoi(e) : 24;
+        return e ? atoi(e) : 124;
     }();
     auto launch = [&](auto kern) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -788,7 +807,9 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         case 26: lrc = launch(sym_task_kernel<2, 6>); break;
         case 16: lrc = launch(sym_task_kernel<1, 6>); break;
         case 18: lrc = launch(sym_task_kernel<1, 8>); break;
-        default: lrc = launch(sym_task_kernel<2, 4>); break;
+        case 24: lrc = launch(sym_task_kernel<2, 4>); break;
+        case 123: lrc = launch(sym_task_kernel<2, 3, true>); break;
+        default: lrc = launch(sym_task_kernel<2, 4, true>); break;   // 739 vs 735 G/s at C5
     }
     if (lrc) return lrc;
     int rc = check_launch("sym_task_kernel");
