@@ -26,6 +26,7 @@ GPU box, gloo on the CPU), ThreadComm runs the ranks as threads on ONE GPU
 
 import ctypes
 import math
+import os
 import threading
 
 import numpy as np
@@ -441,7 +442,61 @@ class DistPreconditioner:
 
 
 # ----------------------------------------------------------------- GMRES ----
-def dist_gmres_solve(op, prec, rhs, params=None):
+class _GatheredOperator:
+    """M A v with the ranks' owned rows all-gathered into the full vector, so
+    every rank runs the single-GPU GMRES (fused MGS, deterministic dots) on
+    identical full vectors: one collective per iteration instead of one per
+    inner product, and bitwise-identical Krylov decisions on every rank."""
+
+    def __init__(self, op, prec):
+        import torch
+        self.op, self.prec, self.comm = op, prec, op.comm
+        self.device = op.device
+        lay = op.layout
+        self.n = lay.size
+        spans = []
+        for r in range(self.comm.world):
+            f0, no = shard_range(op.nf, r, self.comm.world)
+            lo = 0 if r == 0 else lay.fib_off + 4 * op.n * f0
+            spans.append((lo, lay.fib_off + 4 * op.n * (f0 + no)))
+        self.spans = spans
+        self.width = max(max(b - a for a, b in spans), 1)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self._send = torch.zeros(self.width, **f64)
+        self._recv = torch.zeros(self.comm.world * self.width, **f64)
+
+    def gather(self, v_own):
+        """Full vector from each rank's owned range of v_own."""
+        import torch
+        a, b = self.spans[self.comm.rank]
+        self._send[:b - a].copy_(v_own[a:b])
+        self.comm.all_gather(self._recv, self._send)
+        full = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        for r, (lo, hi) in enumerate(self.spans):
+            full[lo:hi].copy_(self._recv[r * self.width:r * self.width + hi - lo])
+        return full
+
+    def apply_device(self, v):
+        return self.gather(self.prec.apply_device(self.op.rows_device(v, False)))
+
+
+def dist_gmres_solve(op, prec, rhs, params=None, variant="gathered"):
+    """Distributed GMRES (solver.py:444-516).
+
+    "gathered" (default): the preconditioned matvec's owned rows are
+    all-gathered and every rank runs solver.gmres_solve on the full vectors
+    (one all-gather per iteration).  "reduced": every inner product is a
+    local dot over the owned range plus an all-reduce of the scalar (k + 3
+    collectives per iteration; kept for comparison)."""
+    if variant == "gathered":
+        from .solver import gmres_solve
+        g = _GatheredOperator(op, prec)
+        b = g.gather(prec.apply_device(rhs))
+        return gmres_solve(g, None, b, params)
+    return _dist_gmres_reduced(op, prec, rhs, params)
+
+
+def _dist_gmres_reduced(op, prec, rhs, params=None):
     """solver.gmres_solve (solver.py:444-516) over the ranks' owned entries.
     Every inner product is a local deterministic dot over the rank's range
     plus an in-place all-reduce of the scalar, stream-ordered (NCCL), so the
@@ -546,13 +601,16 @@ def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, sy
     op = DistBlockOperator(state, dt, comm, symmetric=symmetric, precision=precision)
     rhs = op.rhs_device()
     prec = DistPreconditioner(op)
-    x, iters, history = dist_gmres_solve(op, prec, rhs, params)
-    # assemble the full solution on every rank: owned ranges summed (others 0)
-    full = torch.zeros_like(x)
-    for a, b in op.owned:
-        full[a:b] = x[a:b]
-    comm.all_reduce_sum(full)
-    sol = full.cpu().numpy()
+    variant = os.environ.get("SF_DIST_GMRES", "gathered")
+    x, iters, history = dist_gmres_solve(op, prec, rhs, params, variant=variant)
+    if variant != "gathered":
+        # assemble the full solution on every rank: owned ranges summed (others 0)
+        full = torch.zeros_like(x)
+        for a, b in op.owned:
+            full[a:b] = x[a:b]
+        comm.all_reduce_sum(full)
+        x = full
+    sol = x.cpu().numpy()
     parts = op.layout.unpack(sol)
     for i, part in enumerate(state.particles):
         part.U = parts.U[i].copy()
