@@ -256,6 +256,12 @@ typedef struct {
     const int64_t *p_uoff;   /* (np) offset of U in the unknown vector (omega at +3) */
     int64_t fib_off;         /* offset of fiber 0's block */
     double dt, mu;
+    /* Mixed Chebyshev orders (one sf_fiber_sys per order class): per-fiber
+     * offset of the unknown block [X T] (else fib_off + 4 n m) and of the
+     * fiber's first point in the point-ordered force / u_bar arrays (else
+     * n m).  Both NULL for a uniform system. */
+    const int64_t *u_off;
+    const int64_t *pt_off;
 } sf_fiber_sys;
 
 /* Ds..Ds4 per fiber (fiber.py:140-143). */
@@ -285,6 +291,10 @@ int sf_block_lu(double *A, int64_t nb, int64_t m, double *r, double *c, int *piv
 int sf_precond_apply(const double *LU, const double *r, const double *c, const int *piv,
                      int64_t nb, int64_t m, int64_t off0, const double *diag, int64_t ndiag,
                      const double *v, double *x, void *stream);
+/* Block solves only, for fibers whose unknown blocks start at boff[b]
+ * (mixed-order systems: one call per order class). */
+int sf_block_solve(const double *LU, const double *r, const double *c, const int *piv, int64_t nb,
+                   int64_t m, const int64_t *boff, const double *v, double *x, void *stream);
 /* Surface rows (solver.py:332-355).  kind 0 (particle): rows hold DL_on +
  * wrench flow on entry; adds u_bar, subtracts U + omega x arm; out_uom gets
  * U - <q>/mu, omega - <arm x q>/mu.  kind 1 (periphery): rows hold DL_on on

@@ -67,6 +67,7 @@ _SIGNATURES = {
     "sf_fiber_rows": [_P, _P, _P, _I, _P, _P],
     "sf_fiber_self_blocks": [_P, _P, _P],
     "sf_block_lu": [_P, _I64, _I64, _P, _P, _P, _P, _P],
+    "sf_block_solve": [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P],
     "sf_precond_apply": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P, _P],
     "sf_surface_rows": [_I, _P, _P, _P, _I64, _P, _D, _P, _P, _P, _D, _P, _P, _P, _P],
     "sf_wrench_flow": [_P, _I64, _P, _P, _D, _P, _P],
@@ -94,7 +95,7 @@ class FiberSys(ctypes.Structure):
         ("tang", _P), ("s_alpha", _P), ("L", _P), ("Ldot", _P), ("E", _P), ("c_log", _P),
         ("c_two", _D), ("K", _P), ("f_ext", _P), ("bc_kind", _P), ("bc_par", _P),
         ("bc_body", _P), ("np", _I64), ("pcenter", _P), ("p_uoff", _P), ("fib_off", _I64),
-        ("dt", _D), ("mu", _D),
+        ("dt", _D), ("mu", _D), ("u_off", _P), ("pt_off", _P),
     ]
 
 

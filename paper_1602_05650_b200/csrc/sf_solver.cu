@@ -3,7 +3,7 @@
 //
 // Unknown / residual vector layout (StepLayout, solver.py:67-110):
 //   [ per particle: U(3) omega(3) q1(3 N_p) | periphery q0 (3 N_0) | per fiber: X(3n) T(n) ]
-// Fiber m's block starts at fib_off + 4 n m.  All per-fiber kernels run one
+// Fiber m's block starts at fib_off + 4 n m (or u_off[m], mixed orders).  All per-fiber kernels run one
 // CTA per fiber with the fiber's small operators staged in shared memory.
 #include <cmath>
 
@@ -93,6 +93,16 @@ __device__ void elastic_force(const FiberCtx &c, double E, const double *X, cons
     }
 }
 
+// Fiber m's unknown block and its point offset in the point-ordered arrays
+// (forces, u_bar): per-fiber tables when the system mixes Chebyshev orders,
+// else the uniform strides.
+__device__ __forceinline__ int64_t ublock(const sf_fiber_sys &S, int m) {
+    return S.u_off ? S.u_off[m] : S.fib_off + (int64_t)4 * S.n * m;
+}
+__device__ __forceinline__ int64_t pt3(const sf_fiber_sys &S, int m) {
+    return 3 * (S.pt_off ? S.pt_off[m] : (int64_t)S.n * m);
+}
+
 // -------------------------------------------------- fiber force densities
 // f (nf,n,3) = elastic force of the candidate (X,T) in u (+ f_ext if constants):
 // the strengths the HI operator needs (solver.py:313-318).
@@ -101,7 +111,7 @@ __global__ void fiber_forces_kernel(sf_fiber_sys S, const double *__restrict__ u
     extern __shared__ double sm[];
     const int n = (int)S.n, m = blockIdx.x;
     double *X = sm, *T = X + 3 * n, *t = T + n;
-    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
+    const double *blk = u + ublock(S, m);
     for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) {
         X[e] = blk[e];
         t[e] = S.tang[(int64_t)3 * n * m + e];
@@ -109,7 +119,7 @@ __global__ void fiber_forces_kernel(sf_fiber_sys S, const double *__restrict__ u
     for (int e = threadIdx.x; e < n; e += blockDim.x) T[e] = blk[3 * n + e];
     __syncthreads();
     FiberCtx c = fiber_ctx(S, m);
-    double *f = fout + (int64_t)3 * n * m;
+    double *f = fout + pt3(S, m);
     const double E = S.E[m];
     for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) {
         const int i = e / 3, a = e - 3 * i;
@@ -141,7 +151,7 @@ __global__ void end_wrench_kernel(sf_fiber_sys S, const double *__restrict__ u,
         return;
     }
     FiberCtx c = fiber_ctx(S, m);
-    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
+    const double *blk = u + ublock(S, m);
     const int k = n - 1;
     double xss[3] = {0, 0, 0}, xsss[3] = {0, 0, 0};
     for (int j = 0; j < n; ++j) {
@@ -208,8 +218,8 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
     const int n = (int)S.n, m = blockIdx.x, n3 = 3 * n;
     double *X = sm, *T = X + n3, *Xc = T + n, *t = Xc + n3, *fel = t + n3, *f = fel + n3,
            *flow = f + n3, *w = flow + n3, *res = w + n3;  // res: 14 BC values
-    const double *blk = u + S.fib_off + (int64_t)4 * n * m;
-    const int64_t o3 = (int64_t)n3 * m;
+    const double *blk = u + ublock(S, m);
+    const int64_t o3 = (int64_t)n3 * m, p3 = pt3(S, m);
     const double dt = S.dt;
     for (int e = threadIdx.x; e < n3; e += blockDim.x) {
         X[e] = blk[e];
@@ -238,13 +248,13 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
             const double fdt = f[3 * i] * t[3 * i] + f[3 * i + 1] * t[3 * i + 1] + f[3 * i + 2] * t[3 * i + 2];
             const double ft = fdt * t[r];
             const double mob = cl * (f[r] + ft) + c2 * (f[r] - ft);
-            flow[r] = (mob + acc) + (ubar ? ubar[o3 + r] : 0.0);
+            flow[r] = (mob + acc) + (ubar ? ubar[p3 + r] : 0.0);
         }
     }
     __syncthreads();
     const double Lm = S.L[m], Ldot = S.Ldot[m];
     const double *sa = S.s_alpha + (int64_t)n * m;
-    double *o = out + S.fib_off + (int64_t)4 * n * m;
+    double *o = out + ublock(S, m);
     // velocity rows and w
     for (int e = threadIdx.x; e < n3; e += blockDim.x) {
         const int i = e / 3;
@@ -362,7 +372,7 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
                             v2[a] = xss[a];
                     }
                     // u_bar at the minus end (solver.py:175-177)
-                    const double *ub = ubar ? ubar + o3 + 3 * (n - 1) : nullptr;
+                    const double *ub = ubar ? ubar + p3 + 3 * (n - 1) : nullptr;
                     double s = 0.0;
                     for (int a = 0; a < 3; ++a)
                         s += (vself[a] + (ub ? ub[a] : 0.0) - U[a] - oxa[a]) * tk[a];
@@ -768,12 +778,13 @@ __global__ void __launch_bounds__(256) block_lu_global_kernel(double *__restrict
 // swaps applied in order (LAPACK getrs).
 __global__ void block_solve_kernel(const double *__restrict__ LU, const double *__restrict__ rsc,
                                    const double *__restrict__ csc, const int *__restrict__ piv,
-                                   int mdim, int64_t off0, const double *__restrict__ v,
-                                   double *__restrict__ x) {
+                                   int mdim, int64_t off0, const int64_t *__restrict__ boff,
+                                   const double *__restrict__ v, double *__restrict__ x) {
     extern __shared__ double y[];
     const int b = blockIdx.x;
     const double *L = LU + (int64_t)mdim * mdim * b;
-    const double *vb = v + off0 + (int64_t)mdim * b;
+    const int64_t ob = boff ? boff[b] : off0 + (int64_t)mdim * b;
+    const double *vb = v + ob;
     const double *r = rsc + (int64_t)mdim * b;
     const int *pv = piv + (int64_t)mdim * b;
     for (int i = threadIdx.x; i < mdim; i += blockDim.x) y[i] = vb[i] / r[i];
@@ -798,7 +809,7 @@ __global__ void block_solve_kernel(const double *__restrict__ LU, const double *
         __syncthreads();
     }
     const double *c = csc + (int64_t)mdim * b;
-    double *xb = x + off0 + (int64_t)mdim * b;
+    double *xb = x + ob;
     for (int i = threadIdx.x; i < mdim; i += blockDim.x) xb[i] = y[i] / c[i];
 }
 
@@ -814,8 +825,8 @@ template <int MT>
 __global__ void __launch_bounds__(32 * kSolveWarps)
 block_solve_warp_kernel(const double *__restrict__ LU, const double *__restrict__ rsc,
                         const double *__restrict__ csc, const int *__restrict__ piv, int mdim,
-                        int64_t nb, int64_t off0, const double *__restrict__ v,
-                        double *__restrict__ x) {
+                        int64_t nb, int64_t off0, const int64_t *__restrict__ boff,
+                        const double *__restrict__ v, double *__restrict__ x) {
     __shared__ double ys_all[kSolveWarps][32 * MT];
     __shared__ int ps_all[kSolveWarps][32 * MT];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -825,7 +836,8 @@ block_solve_warp_kernel(const double *__restrict__ LU, const double *__restrict_
     int *ps = ps_all[wid];
     const int m = mdim;
     const double *L = LU + (int64_t)m * m * b;
-    const double *vb = v + off0 + (int64_t)m * b;
+    const int64_t ob = boff ? boff[b] : off0 + (int64_t)m * b;
+    const double *vb = v + ob;
     const double *r = rsc + (int64_t)m * b;
     const int *pv = piv + (int64_t)m * b;
     for (int i = lane; i < m; i += 32) {
@@ -908,7 +920,7 @@ block_solve_warp_kernel(const double *__restrict__ LU, const double *__restrict_
         }
     }
     const double *c = csc + (int64_t)m * b;
-    double *xb = x + off0 + (int64_t)m * b;
+    double *xb = x + ob;
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
         const int i = 32 * t + lane;
@@ -1288,6 +1300,35 @@ int sf_block_lu(double *A, int64_t nb, int64_t m, double *r, double *c, int *piv
     return check_launch("block_lu_smem_kernel");
 }
 
+static int block_solve_launch(const double *LU, const double *r, const double *c,
+                              const int *piv, int64_t nb, int64_t m, int64_t off0,
+                              const int64_t *boff, const double *v, double *x,
+                              cudaStream_t st) {
+    if (nb <= 0) return SF_OK;
+    static const bool warp_solve = [] {
+        const char *e = getenv("SF_BLOCK_SOLVE");
+        return !(e && e[0] == '0');
+    }();
+    const unsigned g = (unsigned)((nb + kSolveWarps - 1) / kSolveWarps);
+    const int mt = (int)((m + 31) / 32);
+    if (warp_solve && mt <= 8) {
+        switch (mt) {
+#define SF_SOLVE_CASE(T)                                                                          \
+    case T:                                                                                       \
+        block_solve_warp_kernel<T><<<g, 32 * kSolveWarps, 0, st>>>(LU, r, c, piv, (int)m, nb, off0, \
+                                                                   boff, v, x);                   \
+        break;
+            SF_SOLVE_CASE(1) SF_SOLVE_CASE(2) SF_SOLVE_CASE(3) SF_SOLVE_CASE(4)
+            SF_SOLVE_CASE(5) SF_SOLVE_CASE(6) SF_SOLVE_CASE(7) SF_SOLVE_CASE(8)
+#undef SF_SOLVE_CASE
+        }
+        return check_launch("block_solve_warp_kernel");
+    }
+    block_solve_kernel<<<(unsigned)nb, 128, sizeof(double) * m, st>>>(LU, r, c, piv, (int)m, off0,
+                                                                     boff, v, x);
+    return check_launch("block_solve_kernel");
+}
+
 int sf_precond_apply(const double *LU, const double *r, const double *c, const int *piv,
                      int64_t nb, int64_t m, int64_t off0, const double *diag, int64_t ndiag,
                      const double *v, double *x, void *stream) {
@@ -1297,31 +1338,14 @@ int sf_precond_apply(const double *LU, const double *r, const double *c, const i
         int rc = check_launch("diag_div_kernel");
         if (rc) return rc;
     }
-    if (nb > 0) {
-        static const bool warp_solve = [] {
-            const char *e = getenv("SF_BLOCK_SOLVE");
-            return !(e && e[0] == '0');
-        }();
-        const unsigned g = (unsigned)((nb + kSolveWarps - 1) / kSolveWarps);
-        const int mt = (int)((m + 31) / 32);
-        if (warp_solve && mt <= 8) {
-            switch (mt) {
-#define SF_SOLVE_CASE(T)                                                                     \
-    case T:                                                                                  \
-        block_solve_warp_kernel<T><<<g, 32 * kSolveWarps, 0, st>>>(LU, r, c, piv, (int)m, nb, \
-                                                                   off0, v, x);              \
-        break;
-                SF_SOLVE_CASE(1) SF_SOLVE_CASE(2) SF_SOLVE_CASE(3) SF_SOLVE_CASE(4)
-                SF_SOLVE_CASE(5) SF_SOLVE_CASE(6) SF_SOLVE_CASE(7) SF_SOLVE_CASE(8)
-#undef SF_SOLVE_CASE
-            }
-            return check_launch("block_solve_warp_kernel");
-        }
-        block_solve_kernel<<<(unsigned)nb, 128, sizeof(double) * m, st>>>(LU, r, c, piv, (int)m,
-                                                                         off0, v, x);
-        return check_launch("block_solve_kernel");
-    }
-    return SF_OK;
+    return block_solve_launch(LU, r, c, piv, nb, m, off0, nullptr, v, x, st);
+}
+
+int sf_block_solve(const double *LU, const double *r, const double *c, const int *piv, int64_t nb,
+                   int64_t m, const int64_t *boff, const double *v, double *x, void *stream) {
+    if (nb > 0 && (!LU || !r || !c || !piv || !boff || !v || !x))
+        return set_error(SF_EINVAL, "null pointer");
+    return block_solve_launch(LU, r, c, piv, nb, m, 0, boff, v, x, (cudaStream_t)stream);
 }
 
 int sf_surface_rows(int kind, const double *nodes, const double *nrm, const double *w, int64_t n,
