@@ -123,6 +123,70 @@ def _precision_mode(precision):
     return modes[precision]
 
 
+class _FiberBatch:
+    """Fibers of one Chebyshev order: the frozen per-fiber operators and the
+    sf_fiber_sys the per-fiber kernels take.  Unknown blocks and point ranges
+    are addressed through per-fiber offset tables, so batches of different
+    orders interleave freely in the reference's StepLayout."""
+
+    def __init__(self, op, n, idx, g):
+        import torch
+        st = op.state
+        dev = op.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        nb = idx.size
+        self.n, self.idx = n, idx
+        fibs = [st.fibers[m] for m in idx]
+        self.u_off = torch.as_tensor(np.array([op.layout.X[m].start for m in idx], dtype=np.int64),
+                                     device=dev)
+        self.pt_off = torch.as_tensor(op.cache.pt_off[idx].astype(np.int64), device=dev)
+        self.Dpow = torch.empty((nb, 4, n, n), **f64)
+        self.nodes = torch.tensor(spectral.grid(n - 1)[0], **f64)
+        _native.call("sf_fiber_dpow", _ptr(g.D), _ptr(g.s_alpha), nb, n, _ptr(self.Dpow), _stream())
+        self.K = torch.empty((nb, 3 * n, 3 * n), **f64)
+        _native.call("sf_kdelta_build_batched", _ptr(g.X), _ptr(g.s), _ptr(g.s_alpha),
+                     _ptr(g.tang), _ptr(g.wcc), nb, n, _ptr(g.delta),
+                     1.0 / (8.0 * math.pi * op.mu), _ptr(self.K), _stream())
+        eps = np.array([f.eps for f in fibs])
+        self.E = torch.as_tensor(np.array([f.E for f in fibs], dtype=float), **f64)
+        self.c_log = torch.as_tensor(-np.log(eps ** 2 * math.e) / (8.0 * math.pi * op.mu), **f64)
+        self.Ldot = torch.as_tensor(np.array([f.Ldot for f in fibs], dtype=float), **f64)
+        self.f_ext = None
+        if st.force_models:
+            self.f_ext = torch.as_tensor(np.ascontiguousarray(np.stack(
+                [external_force_density(st, f) for f in fibs])), **f64)
+        kinds = np.zeros((nb, 2), dtype=np.int32)
+        par = np.zeros((nb, 2, 12))
+        body = np.full(nb, -1, dtype=np.int32)
+        for k, fib in enumerate(fibs):
+            for e, bc in enumerate((fib.bc_plus, fib.bc_minus)):
+                kinds[k, e] = BC_CODES[bc.kind]
+                if bc.kind == "prescribedForceTorque":
+                    par[k, e, 0:3] = bc.force
+                    par[k, e, 3:6] = bc.torque
+                elif bc.kind == "hingedToSurface":
+                    par[k, e, 6:9] = bc.attachment
+                    par[k, e, 9] = bc.stiffness
+                elif bc.kind == "clampedToBody":
+                    par[k, e, 10] = 0.0 if bc.tangent is None else 1.0
+                    if e == 1:
+                        body[k] = bc.body
+        self.bc_kind = torch.as_tensor(kinds, device=dev)
+        self.bc_par = torch.as_tensor(par, **f64)
+        self.bc_body = torch.as_tensor(body, device=dev)
+        self.geo = g
+        self.sys = _native.FiberSys(
+            nf=nb, n=n, D=_ptr(g.D), nodes=_ptr(self.nodes), Dpow=_ptr(self.Dpow), X=_ptr(g.X),
+            tang=_ptr(g.tang), s_alpha=_ptr(g.s_alpha), L=_ptr(g.L), Ldot=_ptr(self.Ldot),
+            E=_ptr(self.E), c_log=_ptr(self.c_log), c_two=2.0 / (8.0 * math.pi * op.mu),
+            K=_ptr(self.K), f_ext=_ptr(self.f_ext), bc_kind=_ptr(self.bc_kind),
+            bc_par=_ptr(self.bc_par), bc_body=_ptr(self.bc_body), np=op.np,
+            pcenter=_ptr(op.pcenter), p_uoff=_ptr(op.p_uoff), fib_off=op.layout.fib_off,
+            dt=op.dt, mu=op.mu, u_off=_ptr(self.u_off), pt_off=_ptr(self.pt_off))
+        self.blocks = torch.empty((nb, 4 * n, 4 * n), **f64)
+        _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.blocks), _stream())
+
+
 class BlockOperator:
     """Linear action of the implicit step system on the stacked unknowns,
     evaluated on the device (solver.py:187-364).  apply/rhs accept and return
@@ -148,45 +212,8 @@ class BlockOperator:
         dev = self.device
         f64 = dict(dtype=torch.float64, device=dev)
         c = self.cache
-        nf, n = c.nf, c.n_nodes
-        self.nf, self.n = nf, n
-        g = c.geo
-        # frozen fiber operators (refresh_geometry, fiber.py:133-147)
-        self.Dpow = torch.empty((nf, 4, n, n), **f64)
-        self.nodes = torch.tensor(spectral.grid(n - 1)[0], **f64) if nf else None
-        if nf:
-            _native.call("sf_fiber_dpow", _ptr(g.D), _ptr(g.s_alpha), nf, n, _ptr(self.Dpow),
-                         _stream())
-        self.K = torch.empty((nf, 3 * n, 3 * n), **f64)
-        if nf:
-            _native.call("sf_kdelta_build_batched", _ptr(g.X), _ptr(g.s), _ptr(g.s_alpha),
-                         _ptr(g.tang), _ptr(g.wcc), nf, n, _ptr(g.delta),
-                         1.0 / (8.0 * math.pi * self.mu), _ptr(self.K), _stream())
-        eps = np.array([f.eps for f in state.fibers])
-        self.E = torch.as_tensor(np.array([f.E for f in state.fibers], dtype=float), **f64)
-        self.c_log = torch.as_tensor(-np.log(eps ** 2 * math.e) / (8.0 * math.pi * self.mu), **f64)
-        self.c_two = 2.0 / (8.0 * math.pi * self.mu)
-        self.Ldot = torch.as_tensor(np.array([f.Ldot for f in state.fibers], dtype=float), **f64)
-        self.f_ext = self._external_forces()
-        kinds = np.zeros((nf, 2), dtype=np.int32)
-        par = np.zeros((nf, 2, 12))
-        body = np.full(nf, -1, dtype=np.int32)
-        for m, fib in enumerate(state.fibers):
-            for e, bc in enumerate((fib.bc_plus, fib.bc_minus)):
-                kinds[m, e] = BC_CODES[bc.kind]
-                if bc.kind == "prescribedForceTorque":
-                    par[m, e, 0:3] = bc.force
-                    par[m, e, 3:6] = bc.torque
-                elif bc.kind == "hingedToSurface":
-                    par[m, e, 6:9] = bc.attachment
-                    par[m, e, 9] = bc.stiffness
-                elif bc.kind == "clampedToBody":
-                    par[m, e, 10] = 0.0 if bc.tangent is None else 1.0
-                    if e == 1:
-                        body[m] = bc.body
-        self.bc_kind = torch.as_tensor(kinds, device=dev)
-        self.bc_par = torch.as_tensor(par, **f64)
-        self.bc_body = torch.as_tensor(body, device=dev)
+        nf = c.nf
+        self.nf, self.n = nf, c.n_nodes
         np_ = len(state.particles)
         self.np = np_
         self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
@@ -195,13 +222,20 @@ class BlockOperator:
                                       device=dev) if np_ else None
         self.ext = (torch.as_tensor(np.stack([np.concatenate([p.F_ext, p.L_ext])
                                               for p in state.particles]), **f64) if np_ else None)
-        self.sys = _native.FiberSys(
-            nf=nf, n=n, D=_ptr(g.D), nodes=_ptr(self.nodes), Dpow=_ptr(self.Dpow), X=_ptr(g.X),
-            tang=_ptr(g.tang), s_alpha=_ptr(g.s_alpha), L=_ptr(g.L), Ldot=_ptr(self.Ldot),
-            E=_ptr(self.E), c_log=_ptr(self.c_log), c_two=self.c_two, K=_ptr(self.K),
-            f_ext=_ptr(self.f_ext), bc_kind=_ptr(self.bc_kind), bc_par=_ptr(self.bc_par),
-            bc_body=_ptr(self.bc_body), np=np_, pcenter=_ptr(self.pcenter),
-            p_uoff=_ptr(self.p_uoff), fib_off=self.layout.fib_off, dt=self.dt, mu=self.mu)
+        # frozen fiber operators (refresh_geometry, fiber.py:133-147), one
+        # uniform batch per Chebyshev order class
+        self.batches = [_FiberBatch(self, n, idx, g) for n, idx, g in c.classes if idx.size]
+        if len(self.batches) == 1:
+            b = self.batches[0]
+            self.sys, self.Dpow, self.K = b.sys, b.Dpow, b.K
+            self.fiber_blocks = b.blocks
+        else:
+            self.sys = None
+            blocks = [None] * nf
+            for b in self.batches:
+                for k, m in enumerate(b.idx):
+                    blocks[m] = b.blocks[k]
+            self.fiber_blocks = blocks
         # surface data per particle / periphery
         self.surf = []
         for i, part in enumerate(state.particles):
@@ -219,27 +253,13 @@ class BlockOperator:
                                   center=None, sl=self.layout.q0, uom=None,
                                   tsl=c.periphery_slice))
         # scratch
-        self._f = torch.empty((nf * n, 3), **f64)
+        self._f = torch.empty((int(c.node_counts.sum()), 3), **f64)
         self._wf = torch.empty((max(nf, 1), 6), **f64)
         self._wr = torch.empty((max(np_, 1), 6), **f64)
+        self._wr_k = torch.empty((max(np_, 1), 6), **f64) if len(self.batches) > 1 else None
         self._ubar = torch.empty((c.n_targets, 3), **f64)
         self._work = torch.empty(16, **f64)
-        self.fiber_blocks = torch.empty((nf, 4 * n, 4 * n), **f64)
-        if nf:
-            _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.fiber_blocks),
-                         _stream())
         self.matvecs = 0
-
-    def _external_forces(self):
-        import torch
-        st = self.state
-        if not st.force_models or not self.nf:
-            return None
-        f = np.stack([external_force_density(st, fib) for fib in st.fibers]) \
-            if any(m.kind != "uniformBodyForce" for m in st.force_models) else \
-            np.broadcast_to(sum(m.f0 * m.direction for m in st.force_models
-                                if m.kind == "uniformBodyForce"), (self.nf, self.n, 3))
-        return torch.as_tensor(np.ascontiguousarray(f), dtype=torch.float64, device=self.device)
 
     @property
     def shape(self):
@@ -259,12 +279,20 @@ class BlockOperator:
         st = _stream()
         if out is None:
             out = torch.empty_like(u)
-        sysp = ctypes.byref(self.sys)
-        if self.nf:
-            _native.call("sf_fiber_forces", sysp, _ptr(u), int(constants), _ptr(self._f), st)
+        for b in self.batches:
+            _native.call("sf_fiber_forces", ctypes.byref(b.sys), _ptr(u), int(constants),
+                         _ptr(self._f), st)
         if self.np:
-            _native.call("sf_particle_wrenches", sysp, _ptr(u), _ptr(self.ext), int(constants),
-                         _ptr(self._wf), _ptr(self._wr), st)
+            if not self.batches:
+                self._wr.zero_()
+                if constants:
+                    self._wr[:self.np].copy_(self.ext)
+            for k, b in enumerate(self.batches):     # classes summed in a fixed order
+                _native.call("sf_particle_wrenches", ctypes.byref(b.sys), _ptr(u),
+                             _ptr(self.ext) if k == 0 else None, int(constants), _ptr(self._wf),
+                             _ptr(self._wr if k == 0 else self._wr_k), st)
+                if k:
+                    self._wr.add_(self._wr_k)
         q = self._densities(u)
         ubar = c.apply(self._f, q, self._wr[:self.np] if self.np else None, out=self._ubar,
                        check=True)
@@ -287,8 +315,8 @@ class BlockOperator:
                 _native.call("sf_surface_rows", 1, _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
                              s["n"], None, s["area"], _ptr(qs), _ptr(ub), None, self.mu,
                              _ptr(self._work), _ptr(rows), None, st)
-        if self.nf:
-            _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(ubar[c.fiber_slice]),
+        for b in self.batches:
+            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), _ptr(ubar[c.fiber_slice]),
                          int(constants), _ptr(out), st)
         self.matvecs += 1
         return out
@@ -334,51 +362,58 @@ def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implici
 
 class Preconditioner:
     """Block Jacobi: equilibrated exact fiber-block inverses, diagonal on
-    surface rows (solver.py:375-429), factored and applied on the device."""
+    surface rows (solver.py:375-429), factored and applied on the device
+    (one batch of block factors per Chebyshev order class)."""
 
     def __init__(self, op):
         import torch
         self.layout = op.layout
         self.device = op.device
         f64 = dict(dtype=torch.float64, device=op.device)
-        nf, n = op.nf, op.n
-        m = 4 * n
-        self.nb, self.m = nf, m
         self.off0 = op.layout.fib_off
         st = _stream()
-        if nf:
-            A = op.fiber_blocks.clone()
+        self.factors = []       # (LU, r, c, piv, nb, m, u_off) per batch
+        for b in op.batches:
+            nb, m = b.idx.size, 4 * b.n
+            A = b.blocks.clone()
             if not bool(torch.isfinite(A).all()):
                 raise FactorizationError("fiber self-block is not finite")
-            self.r = torch.empty((nf, m), **f64)
-            self.c = torch.empty((nf, m), **f64)
-            self.piv = torch.empty((nf, m), dtype=torch.int32, device=op.device)
-            info = torch.empty(nf, dtype=torch.int32, device=op.device)
             if m <= 256:
                 # shared-memory LU for m <= 160, blocked global-memory LU up to 256
-                _native.call("sf_block_lu", _ptr(A), nf, m, _ptr(self.r), _ptr(self.c),
-                             _ptr(self.piv), _ptr(info), st)
-                self.LU = A
+                r = torch.empty((nb, m), **f64)
+                c = torch.empty((nb, m), **f64)
+                piv = torch.empty((nb, m), dtype=torch.int32, device=op.device)
+                info = torch.empty(nb, dtype=torch.int32, device=op.device)
+                _native.call("sf_block_lu", _ptr(A), nb, m, _ptr(r), _ptr(c), _ptr(piv),
+                             _ptr(info), st)
+                LU = A
             else:
                 # larger blocks: equilibrate on the device and factor with the
                 # batched library getrf (outside every BASELINE config)
-                self.r = A.abs().amax(dim=2)
-                if bool((self.r == 0).any()):
+                r = A.abs().amax(dim=2)
+                if bool((r == 0).any()):
                     raise FactorizationError("fiber self-block is singular")
-                A = A / self.r[:, :, None]
-                self.c = A.abs().amax(dim=1)
-                A = A / self.c[:, None, :]
-                LU, piv, inf = torch.linalg.lu_factor_ex(A)
+                A = A / r[:, :, None]
+                c = A.abs().amax(dim=1)
+                A = A / c[:, None, :]
+                LUt, pv, inf = torch.linalg.lu_factor_ex(A)
                 info = torch.where(inf != 0, 3, 0).to(torch.int32)
-                self.LU = LU.transpose(1, 2).contiguous()
-                self.piv = (piv - 1).to(torch.int32).contiguous()
+                LU = LUt.transpose(1, 2).contiguous()
+                piv = (pv - 1).to(torch.int32).contiguous()
             bad = info.cpu().numpy()
             if np.any(bad == 1):
-                raise FactorizationError(f"fiber {int(np.argmax(bad == 1))} self-block is not finite")
+                raise FactorizationError(
+                    f"fiber {int(b.idx[np.argmax(bad == 1)])} self-block is not finite")
             if np.any(bad == 2) or np.any(bad == 3):
-                raise FactorizationError(f"fiber {int(np.argmax(bad > 1))} self-block is singular")
-        else:
-            self.LU = self.r = self.c = self.piv = None
+                raise FactorizationError(
+                    f"fiber {int(b.idx[np.argmax(bad > 1)])} self-block is singular")
+            self.factors.append((LU, r, c, piv, nb, m, b.u_off))
+        uniform = len(self.factors) == 1 and bool(
+            (self.factors[0][6] == self.off0 + 4 * op.batches[0].n
+             * torch.arange(op.nf, device=op.device)).all()) if op.nf else True
+        self.uniform = uniform
+        if len(self.factors) == 1:
+            self.LU, self.r, self.c, self.piv, self.nb, self.m = self.factors[0][:6]
         diag = torch.ones(self.off0, **f64)
         pref = -3.0 / (4.0 * math.pi * op.mu)
         for s in op.surf:
@@ -398,9 +433,17 @@ class Preconditioner:
         import torch
         if out is None:
             out = torch.empty_like(v)
-        _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c),
-                     _ptr(self.piv), self.nb, self.m, self.off0, _ptr(self.diag), self.off0,
-                     _ptr(v), _ptr(out), _stream())
+        st = _stream()
+        if self.uniform and len(self.factors) == 1:
+            LU, r, c, piv, nb, m, _ = self.factors[0]
+            _native.call("sf_precond_apply", _ptr(LU), _ptr(r), _ptr(c), _ptr(piv), nb, m,
+                         self.off0, _ptr(self.diag), self.off0, _ptr(v), _ptr(out), st)
+            return out
+        _native.call("sf_precond_apply", None, None, None, None, 0, 0, self.off0, _ptr(self.diag),
+                     self.off0, _ptr(v), _ptr(out), st)
+        for LU, r, c, piv, nb, m, uoff in self.factors:
+            _native.call("sf_block_solve", _ptr(LU), _ptr(r), _ptr(c), _ptr(piv), nb, m,
+                         _ptr(uoff), _ptr(v), _ptr(out), st)
         return out
 
     def apply(self, v):

@@ -367,13 +367,23 @@ def _stream():
 
 
 def stack_fibers(fibers):
-    """(nf, n, 3) centrelines; the device layout needs one node count."""
+    """(nf, n, 3) centrelines of fibers that share one node count."""
     if not fibers:
         return np.zeros((0, 5, 3))
     n = fibers[0].n_nodes
     if any(f.n_nodes != n for f in fibers):
-        raise ConfigurationError("the device layout needs every fiber to have the same order p")
+        raise ConfigurationError("stack_fibers needs every fiber to have the same order p")
     return np.stack([f.X for f in fibers])
+
+
+def order_classes(fibers):
+    """[(n, idx)]: the fibers grouped by node count (Chebyshev order), each
+    class a uniform batch for the per-fiber kernels; idx ascending."""
+    ns = np.array([f.n_nodes for f in fibers], dtype=np.int64)
+    out = []
+    for n in dict.fromkeys(ns.tolist()):
+        out.append((int(n), np.nonzero(ns == n)[0]))
+    return out
 
 
 class FiberGeometry:
@@ -458,13 +468,18 @@ class InteractionCache:
             groups.append(np.full(n, nf + np_, dtype=np.int64))
             self.periphery_slice = slice(off, off + n)
             off += n
-        Xf = stack_fibers(state.fibers)
-        self.n_nodes = Xf.shape[1]
-        self.fiber_slice = slice(off, off + nf * self.n_nodes)
-        self.fiber_slices = [slice(off + m * self.n_nodes, off + (m + 1) * self.n_nodes)
+        # fibers in order; node counts may differ (mixed Chebyshev orders)
+        ns = np.array([f.n_nodes for f in state.fibers], dtype=np.int64)
+        self.node_counts = ns
+        self.pt_off = np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64) if nf else ns
+        self.uniform = len(set(ns.tolist())) <= 1
+        self.n_nodes = int(ns[0]) if (nf and self.uniform) else (5 if not nf else 0)
+        npts = int(ns.sum())
+        self.fiber_slice = slice(off, off + npts)
+        self.fiber_slices = [slice(off + int(self.pt_off[m]), off + int(self.pt_off[m] + ns[m]))
                              for m in range(nf)]
-        blocks.append(Xf.reshape(-1, 3))
-        groups.append(np.repeat(np.arange(nf, dtype=np.int64), self.n_nodes))
+        blocks.append(np.concatenate([f.X for f in state.fibers]) if nf else np.zeros((0, 3)))
+        groups.append(np.repeat(np.arange(nf, dtype=np.int64), ns))
         self.targets = np.vstack(blocks) if blocks else np.zeros((0, 3))
         self.target_groups = np.concatenate(groups) if groups else np.zeros(0, np.int64)
         self.target_offset = 0
@@ -492,18 +507,40 @@ class InteractionCache:
         self.fiber_pairs = bool(fiber_pairs) and self.backend is None
 
         _lap("targets")
-        # fibers: geometry, weights, doublet coefficients (device)
-        if fiber_geometry is None:
-            ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in state.fibers]
-            deltas = [0.0 if f.delta_ratio is not None else f.delta for f in state.fibers]
-            fiber_geometry = FiberGeometry(Xf, ratios, deltas, self.device)
-        self.geo = fiber_geometry
+        # fibers: geometry, weights, doublet coefficients (device), one
+        # batched FiberGeometry per order class, flat point arrays in fiber order
         self.eps = torch.as_tensor([f.eps for f in state.fibers], **f64)
-        self.fsrc = self.geo.X.reshape(-1, 3)
-        self.fgrp = torch.as_tensor(np.repeat(np.arange(nf, dtype=np.int64), self.n_nodes), **dev)
-        self.fw = self.geo.wnode.reshape(-1)
-        self.fdcoef = (((self.eps * self.geo.L) ** 2 / 2.0).repeat_interleave(self.n_nodes)
-                       if include_doublet and nf else None)                   # system.py:542
+        if fiber_geometry is not None:
+            self.classes = [(self.n_nodes, np.arange(nf), fiber_geometry)]
+        elif nf == 0:
+            self.classes = [(5, np.arange(0), FiberGeometry(np.zeros((0, 5, 3)), [], [],
+                                                            self.device))]
+        else:
+            self.classes = []
+            for n, idx in order_classes(state.fibers):
+                fibs = [state.fibers[m] for m in idx]
+                ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in fibs]
+                deltas = [0.0 if f.delta_ratio is not None else f.delta for f in fibs]
+                self.classes.append((n, idx, FiberGeometry(stack_fibers(fibs), ratios, deltas,
+                                                           self.device)))
+        self.geo = self.classes[0][2] if (self.uniform and self.classes) else None
+        if self.geo is not None:
+            self.fsrc = self.geo.X.reshape(-1, 3)
+            self.fw = self.geo.wnode.reshape(-1)
+            self.fL = self.geo.L
+        else:
+            self.fsrc = torch.empty((npts, 3), **f64)
+            self.fw = torch.empty(npts, **f64)
+            self.fL = torch.empty(nf, **f64)
+            for n, idx, g in self.classes:
+                pidx = torch.as_tensor((self.pt_off[idx][:, None] + np.arange(n)).reshape(-1),
+                                       **dev)
+                self.fsrc[pidx] = g.X.reshape(-1, 3)
+                self.fw[pidx] = g.wnode.reshape(-1)
+                self.fL[torch.as_tensor(idx, **dev)] = g.L
+        self.fgrp = torch.as_tensor(np.repeat(np.arange(nf, dtype=np.int64), ns), **dev)
+        self.fdcoef = (((self.eps * self.fL) ** 2 / 2.0).repeat_interleave(
+            torch.as_tensor(ns, **dev)) if include_doublet and nf else None)   # system.py:542
 
         # surfaces: particles then periphery (system.py:544-557)
         self.surfaces = [(p.mesh, nf + i, False) for i, p in enumerate(state.particles)]
@@ -540,11 +577,13 @@ class InteractionCache:
                 if near == "host":
                     self.near_fiber = nearfield.find_fiber_pairs(
                         state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
-                else:
+                elif self.uniform:
                     t, l, W = nearfield.device_fiber_pairs(self.geo, self.eps, self.trg, self.tgrp,
                                                            state.mu, include_doublet)
                     self._near_dev = (t, l, W)
                     self.near_fiber = list(zip(t.tolist(), l.tolist(), W))
+                else:
+                    self.near_fiber = self._class_near_pairs(state.mu, include_doublet)
             except InsideFiberError as err:
                 raise OverlapError(f"target node overlaps a fiber: {err}") from err
         _lap("near fiber maps")
@@ -564,6 +603,26 @@ class InteractionCache:
         self.bad = torch.zeros(3, dtype=torch.int64, **dev)
 
     # -- construction helpers ------------------------------------------------
+    def _class_near_pairs(self, mu, include_doublet):
+        """Device near maps of a mixed-order system, one order class at a
+        time (target groups remapped so only a fiber's own nodes are
+        excluded), merged in the reference's order (fiber, then target)."""
+        import torch
+        entries = []
+        nf = self.nf
+        for n, idx, g in self.classes:
+            loc = np.full(nf + self.np + 2, -1, dtype=np.int64)
+            loc[idx] = np.arange(idx.size)
+            tg = loc[np.clip(self.target_groups, -1, nf + self.np + 1)]
+            tg[self.target_groups < 0] = -1
+            t, l, W = nearfield.device_fiber_pairs(
+                g, self.eps[torch.as_tensor(idx, device=self.device)], self.trg,
+                torch.as_tensor(tg, device=self.device), mu, include_doublet)
+            entries.extend(zip(t.tolist(), idx[l].tolist(), W))
+        entries.sort(key=lambda e: (e[1], e[0]))
+        return entries
+
+
     def _check_surface_overlaps(self):
         for mesh, group, is_periphery in self.surfaces:
             others = self.target_groups != group
@@ -581,24 +640,24 @@ class InteractionCache:
         import torch
         self.near_nrows = 0
         self.near_tensors = {}
-        L = 3 * self.n_nodes
-        nfs3 = 3 * self.nf * self.n_nodes
+        nfs3 = 3 * int(self.node_counts.sum())
         nfib = len(self.near_fiber)
         t = np.array([e[0] for e in self.near_fiber] + [e[0] for e in self.near_surface],
                      dtype=np.int64)
         if t.size == 0:
             return
-        xo = np.array([e[1] * L for e in self.near_fiber]
+        xo = np.array([3 * self.pt_off[e[1]] for e in self.near_fiber]
                       + [nfs3 + 3 * self.surface_offsets[e[1]] for e in self.near_surface],
                       dtype=np.int64)
-        xl = np.array([L] * nfib + [3 * self.surfaces[e[1]][0].n_nodes for e in self.near_surface],
+        xl = np.array([3 * self.node_counts[e[1]] for e in self.near_fiber]
+                      + [3 * self.surfaces[e[1]][0].n_nodes for e in self.near_surface],
                       dtype=np.int64)
         order = np.argsort(t, kind="stable")
         dev = dict(device=self.device)
         f64 = dict(dtype=torch.float64, **dev)
         if self._near_dev is not None and not self.near_surface:
             Wall = self._near_dev[2][torch.as_tensor(order, **dev)].reshape(-1)
-            wo = np.arange(t.size, dtype=np.int64) * 3 * L
+            wo = np.arange(t.size, dtype=np.int64) * 9 * self.n_nodes
         else:
             pieces = []
             for i in order:
@@ -634,7 +693,7 @@ class InteractionCache:
             near_x_len=_ptr(nt.get("x_len")), near_nrows=self.near_nrows,
             near_W=_ptr(nt.get("W")), mu=self.mu, mode=self.mode,
             fiber_target_off=self.fiber_slice.start if (self.nf and whole) else -1,
-            fiber_group_size=self.n_nodes)
+            fiber_group_size=self.n_nodes if self.uniform else 0)
 
     # -- application ------------------------------------------------------------
     @property
@@ -642,7 +701,8 @@ class InteractionCache:
         """Non-excluded (target, source) pairs of one application."""
         nfs = self.fsrc.shape[0] if self.fiber_pairs else 0
         ln = lambda sl: sl.stop - sl.start                                 # noqa: E731
-        own = sum(ln(s) for s in self.fiber_slices) * self.n_nodes if self.fiber_pairs else 0
+        own = (sum(ln(s) * int(n) for s, n in zip(self.fiber_slices, self.node_counts))
+               if self.fiber_pairs else 0)
         tsl = list(self.particle_slices) + ([self.periphery_slice]
                                              if self.periphery_slice is not None else [])
         surf = sum(ln(s) * m.n_nodes for s, (m, _, _) in zip(tsl, self.surfaces))

@@ -146,7 +146,9 @@ def surfaces_fixture():
 
 # ---------------------------------------------------------------- implicit steps
 def _step_record(state):
-    return dict(X=np.stack([f.X for f in state.fibers]), T=np.stack([f.T for f in state.fibers]),
+    ragged = len({f.n_nodes for f in state.fibers}) > 1
+    cat = np.concatenate if ragged else np.stack
+    return dict(X=cat([f.X for f in state.fibers]), T=cat([f.T for f in state.fibers]),
                 U=np.stack([p.U for p in state.particles]) if state.particles else np.zeros((0, 3)),
                 omega=(np.stack([p.omega for p in state.particles]) if state.particles
                        else np.zeros((0, 3))),
@@ -205,6 +207,44 @@ def step_fixture(name, state, dt, tol, nsteps, extra=None):
     if extra:
         out.update(extra)
     save(name, **out, **versions())
+
+
+def mixed_cloud_state():
+    """Free fibers of two Chebyshev orders (p = 15 and 23), interleaved."""
+    from slenderflow import system as S
+    a = configs.fiber_cloud(4, 15, eps=5e-3, E=1e-2, region="ball", size=1.2, seed=3,
+                            clear=configs.clean_clear(15), check="node", perturb=1e-2)
+    b = configs.fiber_cloud(4, 23, eps=5e-3, E=1e-2, region="ball", size=1.2, seed=4,
+                            clear=configs.clean_clear(23), check="node", perturb=1e-2)
+    Xs = []
+    for k in range(4):
+        Xs.append(a.X[k])
+        Xs.append(b.X[k] + np.array([3.5, 0.0, 0.0]))
+    fibs = [fiber.Fiber(X, eps=5e-3, E=1e-2) for X in Xs]
+    return S.SystemState(fibs, force_models=[S.UniformBodyForce(1.0, (0.0, 0.0, -1.0))]), Xs
+
+
+def mixed_aster_state(n_fibers=10):
+    """Aster whose clamped fibers alternate between p = 15 and p = 23."""
+    from slenderflow import system as S
+    pnc = body.RigidParticle(body.make_surface(body.sphere_shape(0.5), (4, 4)))
+    pts, dirs = S.aster_attachment_layout(pnc, n_fibers, radius_factor=1.3)
+    fibs = []
+    for k, (x0, d) in enumerate(zip(pts, dirs)):
+        fb = fiber.straight_fiber(15 if k % 2 == 0 else 23, x0, d, 1.0, eps=1e-2, E=1.0)
+        fb.bc_minus = fiber.ClampedToBody(0, x0, d)
+        fb.bc_plus = fiber.PrescribedForceTorque(1.0 * d)
+        fibs.append(fb)
+    return S.SystemState(fibs, [pnc])
+
+
+def steps_mixed():
+    st, Xs = mixed_cloud_state()
+    step_fixture("step_mixed_cloud.npz", st, 5e-3, 1e-10, 2,
+                 extra={f"init_X{k}": X for k, X in enumerate(Xs)})
+    st = mixed_aster_state()
+    step_fixture("step_mixed_aster.npz", st, 1e-3, 1e-10, 2,
+                 extra={f"fiber_p": np.array([f.p for f in st.fibers])})
 
 
 def steps_all():
@@ -396,6 +436,8 @@ if __name__ == "__main__":
         api_ops_fixture()
     if "tree" in which:
         tree_fixture()
+    if "mixed" in which:
+        steps_mixed()
     if "shapes" in which:
         shapes_fixture()
         layouts_fixture()
