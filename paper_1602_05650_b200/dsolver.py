@@ -152,6 +152,9 @@ class DistBlockOperator:
         f64 = dict(dtype=torch.float64, device=dev)
         nf = len(state.fibers)
         n = state.fibers[0].n_nodes if nf else 5
+        if any(f.n_nodes != n for f in state.fibers):
+            raise ConfigurationError("the distributed step needs one Chebyshev order for all "
+                                     "fibers; mixed orders run on one GPU (solver.py)")
         self.nf, self.n = nf, n
         rank, world = comm.rank, comm.world
         self.f0, self.nown = shard_range(nf, rank, world)
