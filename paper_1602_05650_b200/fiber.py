@@ -156,7 +156,8 @@ class Fiber:
 
     @property
     def grid(self):
-        return spectral.grid(self.p)
+        """ChebyshevGrid of this fiber's order (nodes, weights, D), as in the reference."""
+        return spectral.ChebyshevGrid(self.p)
 
     @property
     def delta(self):
@@ -187,6 +188,62 @@ class Fiber:
         Ds = D / self.s_alpha[:, None]
         Ds2 = Ds @ Ds
         return Ds, Ds2, Ds2 @ Ds
+
+    # reference attribute names of the frozen arclength operators (fiber.py:140-143)
+    @property
+    def Ds(self):
+        return self.ds_powers()[0]
+
+    @property
+    def Ds2(self):
+        return self.ds_powers()[1]
+
+    @property
+    def Ds3(self):
+        return self.ds_powers()[2]
+
+    @property
+    def Ds4(self):
+        Ds2 = self.ds_powers()[1]
+        return Ds2 @ Ds2
+
+    def copy_state(self):
+        return dict(X=self.X.copy(), T=self.T.copy(), L=self.L, Ldot=self.Ldot,
+                    growth_state=self.growth_state, tau_cat=self.tau_cat)
+
+    # -- dense per-fiber operators of the reference API (fiber.py:182-222).
+    #    The device step never forms these; they serve API users and checks.
+    def elastic_operators(self):
+        """(FX, FT) with f.ravel() = FX @ X.ravel() + FT @ T."""
+        n = self.n_nodes
+        Ds, Ds2, _ = self.ds_powers()
+        FX = np.zeros((3 * n, 3 * n))
+        FT = np.zeros((3 * n, n))
+        t = self.tangents
+        for c in range(3):
+            FX[c::3, c::3] = -self.E * (Ds2 @ Ds2)
+            FT[c::3, :] = Ds * t[:, c][None, :]
+        return FX, FT
+
+    def mobility_matrix(self, mu):
+        """Dense 3n x 3n local mobility, block diagonal over nodes."""
+        n = self.n_nodes
+        c_log = -math.log(self.eps ** 2 * math.e) / (8.0 * math.pi * mu)
+        c_two = 2.0 / (8.0 * math.pi * mu)
+        tt = self.tangents[:, :, None] * self.tangents[:, None, :]
+        blocks = c_log * (np.eye(3) + tt) + c_two * (np.eye(3) - tt)
+        M = np.zeros((3 * n, 3 * n))
+        for k in range(n):
+            M[3 * k:3 * k + 3, 3 * k:3 * k + 3] = blocks[k]
+        return M
+
+    def kdelta_matrix(self, mu):
+        """Dense 3n x 3n regularized non-local self-mobility, built by the
+        device kernel (bitwise equal to kernels.kdelta_matrix)."""
+        from . import kernels
+        return kernels.kdelta_matrix(self.X, self.s, self.s_alpha, self.tangents,
+                                     spectral.grid(self.p)[1], self.delta,
+                                     1.0 / (8.0 * math.pi * mu))
 
 
 def straight_fiber(p, start, direction, length, eps=0.01, E=10.0, **kwargs):

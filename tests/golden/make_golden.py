@@ -303,6 +303,8 @@ def api_ops_fixture():
          dl_on_p=body.double_layer_onsurface(part.mesh, qp, mu),
          completion=body.completion_flow(part, tgt + 1.0, mu),
          near_eval=body.near_surface_eval(per, q, near_t, mu, interior_jump=True),
+         Ds4=fib.Ds4, FX=fib.elastic_operators()[0], FT=fib.elastic_operators()[1],
+         Mmat=fib.mobility_matrix(mu), Kmat=fib.kdelta_matrix(mu),
          **versions())
 
 

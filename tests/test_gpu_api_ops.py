@@ -3,6 +3,7 @@
 against the reference's own outputs (golden api_ops.npz from
 tests/golden/make_golden.py)."""
 
+import numpy as np
 import pytest
 
 from conftest import golden
@@ -45,3 +46,8 @@ def test_near_shell_is_enforced(cuda, g):
     per = body.make_surface(body.sphere_shape(3.0), (6, 6))
     with pytest.raises(kernels.NearFieldError):
         body.double_layer_offsurface(per, g["q"], g["near_t"][None, :], float(g["mu"]))
+
+
+def test_fiber_kdelta_matrix_method(cuda, g):
+    fib = fiber.Fiber(g["X"], eps=float(g["eps"]), E=float(g["E"]))
+    assert np.array_equal(fib.kdelta_matrix(float(g["mu"])), g["Kmat"])   # bitwise build

@@ -133,3 +133,15 @@ def test_gmres_params_validation():
     for kw in (dict(tolerance=0.0), dict(tolerance=1.0), dict(restart=0), dict(max_iterations=0)):
         with pytest.raises(system.ConfigurationError):
             solver.GmresParams(**kw)
+
+
+def test_fiber_dense_operators_match_reference():
+    """Fiber.Ds..Ds4, elastic_operators, mobility_matrix and the grid object
+    (fiber.py:133-222) equal the reference's bitwise."""
+    g = golden("api_ops.npz")
+    fib = Fiber(g["X"], eps=float(g["eps"]), E=float(g["E"]))
+    assert np.array_equal(fib.Ds4, g["Ds4"])
+    FX, FT = fib.elastic_operators()
+    assert np.array_equal(FX, g["FX"]) and np.array_equal(FT, g["FT"])
+    assert np.array_equal(fib.mobility_matrix(float(g["mu"])), g["Mmat"])
+    assert fib.grid.p == fib.p and fib.grid.D.shape == (fib.n_nodes, fib.n_nodes)
