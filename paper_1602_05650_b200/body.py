@@ -99,6 +99,21 @@ class SurfaceMesh:
     def has_parametrization(self):
         return self.shape is not None and self.patch_grid is not None
 
+    def refined(self, factor):
+        """Same surface with the patch counts multiplied (body.py:108-116)."""
+        if not self.has_parametrization():
+            raise GeometryError("refinement requires a parametrized mesh")
+        nt, nph = self.patch_grid
+        return make_surface(self.shape, (nt * factor, nph * factor), center=self.center)
+
+    def surface_point(self, theta, phi):
+        R = self.shape[2](theta)
+        st = np.sin(theta)
+        return self.center + R * np.array([st * np.cos(phi), st * np.sin(phi), np.cos(theta)])
+
+    def radial_bound(self, theta):
+        return float(self.shape[2](theta))
+
 
 def make_surface(shape, resolution, center=(0.0, 0.0, 0.0)):
     """Patchwise Gauss-Legendre mesh of a polar profile R(theta) (body.py:127-184).
@@ -310,3 +325,113 @@ def mesh_from_text(text):
             raise ValueError("mesh data disagrees with its shape header")
         return mesh
     return SurfaceMesh(data[:, 0:3], data[:, 3:6], data[:, 6])
+
+
+# -- nodal interpolation and nearly singular helpers (body.py:305-519) --------
+
+def _lagrange_coeffs(x, nodes):
+    x = np.atleast_1d(np.asarray(x, dtype=float))
+    c = np.ones((x.size, len(nodes)))
+    for i in range(len(nodes)):
+        for j in range(len(nodes)):
+            if i != j:
+                c[:, i] *= (x - nodes[j]) / (nodes[i] - nodes[j])
+    return c
+
+
+def _patch_coeffs(mesh, theta, phi):
+    nt, nph = mesh.patch_grid
+    dth, dph = np.pi / nt, 2.0 * np.pi / nph
+    it = np.minimum((theta / dth).astype(int), nt - 1)
+    ip = np.minimum((phi / dph).astype(int), nph - 1)
+    return (it * nph + ip, _lagrange_coeffs((theta - it * dth) / dth, GL01_NODES),
+            _lagrange_coeffs((phi - ip * dph) / dph, GL01_NODES))
+
+
+def interpolate_nodal(mesh, values, theta, phi):
+    """Nodal data at (theta, phi) by 4x4 tensor Lagrange interpolation in the
+    containing patch (body.py:316-338)."""
+    if not mesh.has_parametrization():
+        raise GeometryError("interpolation requires a parametrized mesh")
+    scalar_query = np.isscalar(theta)
+    theta = np.atleast_1d(np.asarray(theta, dtype=float))
+    phi = np.atleast_1d(np.asarray(phi, dtype=float)) % (2.0 * np.pi)
+    patch, cu, cv = _patch_coeffs(mesh, theta, phi)
+    vals = np.asarray(values, dtype=float)
+    flat = vals.reshape(vals.shape[0], -1)
+    block = flat[(patch * 16)[:, None] + np.arange(16)].reshape(theta.size, 4, 4, -1)
+    out = np.einsum("mi,mj,mijk->mk", cu, cv, block)
+    if vals.ndim == 1:
+        out = out[:, 0]
+    return (out[0] if vals.ndim > 1 else float(out[0])) if scalar_query else out
+
+
+def interpolation_matrix(mesh, fine):
+    """Sparse nodal map mesh -> fine reproducing interpolate_nodal at the
+    fine nodes (body.py:341-368)."""
+    from scipy import sparse
+    if not mesh.has_parametrization():
+        raise GeometryError("interpolation requires a parametrized mesh")
+    theta = np.asarray(fine.thetas, dtype=float)
+    phi = np.asarray(fine.phis, dtype=float) % (2.0 * np.pi)
+    patch, cu, cv = _patch_coeffs(mesh, theta, phi)
+    vals = np.einsum("mi,mj->mij", cu, cv).reshape(theta.size, 16)
+    cols = (patch * 16)[:, None] + np.arange(16)
+    rows = np.repeat(np.arange(theta.size), 16)
+    return sparse.csr_matrix((vals.ravel(), (rows, cols.ravel())),
+                             shape=(theta.size, mesh.n_nodes))
+
+
+def nearest_surface_point(mesh, target):
+    """(theta, phi, point, signed distance), body.py:371-423."""
+    from . import nearfield
+    return nearfield.nearest_surface_point(mesh, target)
+
+
+def plain_surface_weights(mesh, target, mu):
+    """Stresslet quadrature at one target as a (3, 3N) map (body.py:437-448)."""
+    from . import nearfield
+    return nearfield.plain_surface_weights(mesh, target, mu)
+
+
+def near_surface_weights(mesh, target, mu, interior_jump=True, upsample=6):
+    """Nearly singular (3, 3N) map (body.py:479-519), built on the device
+    (nearfield.device_surface_weights returns W_near - W_plain)."""
+    import torch
+
+    from . import nearfield
+    W = nearfield.device_surface_weights(mesh, np.asarray(target, dtype=float)[None, :], mu,
+                                         torch.device("cuda"), interior_jump=interior_jump,
+                                         upsample=upsample)[0].cpu().numpy()
+    return W + nearfield.plain_surface_weights(mesh, target, mu)
+
+
+def second_kind_matrix(mesh, mu, interior=True, nullspace_scale=None):
+    """Dense one-sided double-layer matrix (body.py:530-566) for small
+    meshes, assembled on the device."""
+    import torch
+    dev = torch.device("cuda")
+    f64 = dict(dtype=torch.float64, device=dev)
+    x = torch.as_tensor(mesh.nodes, **f64)
+    n = torch.as_tensor(mesh.normals, **f64)
+    w = torch.as_tensor(mesh.weights, **f64)
+    N = mesh.n_nodes
+    pref = -3.0 / (4.0 * np.pi * mu)
+    r = x[:, None, :] - x[None, :, :]
+    d2 = (r * r).sum(dim=2)
+    d2.fill_diagonal_(1.0)
+    rhat = r / torch.sqrt(d2)[:, :, None]
+    scal = pref * (rhat * n[None, :, :]).sum(dim=2) / d2 * w[None, :]
+    blocks = scal[:, :, None, None] * rhat[:, :, None, :] * rhat[:, :, :, None]
+    idx = torch.arange(N, device=dev)
+    blocks[idx, idx] = 0.0
+    A = blocks.permute(0, 2, 1, 3).reshape(3 * N, 3 * N).clone()
+    rowsum = blocks.sum(dim=1)
+    for i in range(N):
+        A[3 * i:3 * i + 3, 3 * i:3 * i + 3] -= rowsum[i]
+    if interior:
+        A += torch.eye(3 * N, **f64) / mu
+    if nullspace_scale is not None:
+        nw = (n * w[:, None]).reshape(-1)
+        A += nullspace_scale * torch.outer(n.reshape(-1), nw)
+    return A.cpu().numpy()

@@ -304,6 +304,12 @@ def api_ops_fixture():
          completion=body.completion_flow(part, tgt + 1.0, mu),
          near_eval=body.near_surface_eval(per, q, near_t, mu, interior_jump=True),
          Ds4=fib.Ds4, FX=fib.elastic_operators()[0], FT=fib.elastic_operators()[1],
+         skm=body.second_kind_matrix(body.make_surface(body.sphere_shape(0.5), (2, 2)), mu,
+                                     interior=False),
+         skm_per=body.second_kind_matrix(body.make_surface(body.sphere_shape(3.0), (2, 2)), mu,
+                                         interior=True, nullspace_scale=0.5),
+         interp=body.interpolate_nodal(per, q, np.array([0.3, 1.7, 2.9]), np.array([0.1, 3.0, 6.1])),
+         near_W=body.near_surface_weights(per, near_t, mu, interior_jump=True),
          Mmat=fib.mobility_matrix(mu), Kmat=fib.kdelta_matrix(mu),
          **versions())
 

@@ -51,3 +51,20 @@ def test_near_shell_is_enforced(cuda, g):
 def test_fiber_kdelta_matrix_method(cuda, g):
     fib = fiber.Fiber(g["X"], eps=float(g["eps"]), E=float(g["E"]))
     assert np.array_equal(fib.kdelta_matrix(float(g["mu"])), g["Kmat"])   # bitwise build
+
+
+def test_surface_helpers(cuda, g):
+    """second_kind_matrix (device assembly), interpolate_nodal, and the
+    reference-named near_surface_weights (body.py:316-566)."""
+    mu = float(g["mu"])
+    per = body.make_surface(body.sphere_shape(3.0), (6, 6))
+    A = body.second_kind_matrix(body.make_surface(body.sphere_shape(0.5), (2, 2)), mu,
+                                interior=False)
+    assert np.abs(A - g["skm"]).max() <= 1e-13 * np.abs(g["skm"]).max()
+    A = body.second_kind_matrix(body.make_surface(body.sphere_shape(3.0), (2, 2)), mu,
+                                interior=True, nullspace_scale=0.5)
+    assert np.abs(A - g["skm_per"]).max() <= 1e-13 * np.abs(g["skm_per"]).max()
+    got = body.interpolate_nodal(per, g["q"], np.array([0.3, 1.7, 2.9]), np.array([0.1, 3.0, 6.1]))
+    assert np.array_equal(got, g["interp"])
+    W = body.near_surface_weights(per, g["near_t"], mu, interior_jump=True)
+    assert np.abs(W - g["near_W"]).max() <= 1e-12 * np.abs(g["near_W"]).max()
