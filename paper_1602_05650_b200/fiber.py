@@ -436,3 +436,52 @@ def polymerization_step(fib, dt, rng):
         fib.growth_state = GROWING
         fib.Ldot = (kin.min_length - fib.L) / dt
     return fib.growth_state, fib.Ldot
+
+
+# -- remaining per-fiber API (fiber.py:26-35, 375-600) --------------------------
+
+def shared_grid(p):
+    """ChebyshevGrid of order p (fiber.py:26-31)."""
+    return spectral.ChebyshevGrid(p)
+
+
+def resample_to_fine(values, alphas):
+    """Chebyshev interpolant of nodal values at new points (fiber.py:444-447)."""
+    from numpy.polynomial import chebyshev as C
+    return C.chebval(alphas, spectral.cheb_transform(values))
+
+
+def nearest_centerline_point(fib, target):
+    """(alpha, point, distance) of the closest centreline point (fiber.py:453-481)."""
+    from . import nearfield
+    return nearfield.nearest_centerline_point(fib, target)
+
+
+def plain_fiber_weights(fib, target, mu, include_doublet=False):
+    """Plain collocation map (3, 3n) of one fiber at a target (fiber.py:508-512)."""
+    from . import nearfield
+    return nearfield.plain_fiber_weights(fib, target, mu, include_doublet)
+
+
+def near_fiber_weights(fib, target, mu, include_doublet=False):
+    """Panel-refined, blended near map (3, 3n) (fiber.py:514-565), built on
+    the device by sf_near_fiber_weights (which returns W_near - W_plain)."""
+    import torch
+
+    from . import nearfield
+    from .system import FiberGeometry
+    dev = torch.device("cuda")
+    ratio = [fib.delta_ratio if fib.delta_ratio is not None else -1.0]
+    delta = [0.0 if fib.delta_ratio is not None else fib.delta]
+    geo = FiberGeometry(fib.X[None, :, :], ratio, delta, dev)
+    trg = torch.as_tensor(np.asarray(target, dtype=float)[None, :], dtype=torch.float64,
+                          device=dev)
+    eps = torch.tensor([fib.eps], dtype=torch.float64, device=dev)
+    W = nearfield.device_fiber_weights(geo, eps, trg, [0], [0], mu, include_doublet)[0]
+    return W.cpu().numpy() + nearfield.plain_fiber_weights(fib, target, mu, include_doublet)
+
+
+def near_fiber_eval(fib, f, target, mu, include_doublet=False):
+    """Velocity near (but outside) the fiber: near_fiber_weights @ f (fiber.py:576-587)."""
+    W = near_fiber_weights(fib, target, mu, include_doublet=include_doublet)
+    return W @ np.asarray(f, dtype=float).ravel()

@@ -395,18 +395,37 @@ def device_fiber_pairs(geo, eps, targets, target_groups, mu, include_doublet=Tru
     pl_np, pt_np = (pairs[:found].cpu().numpy().T if found else (np.zeros(0, np.int64),) * 2)
     order = np.lexsort((pt_np, pl_np))
     pl_np, pt_np = pl_np[order], pt_np[order]
-    W = torch.empty((found, 3, 3 * n), dtype=torch.float64, device=dev)
-    if found:
-        from . import spectral
+    W = device_fiber_weights(geo, eps, targets, pt_np, pl_np, mu, include_doublet)
+    return pt_np.astype(np.int64), pl_np.astype(np.int64), W
+
+
+def device_fiber_weights(geo, eps, targets, pt_np, pl_np, mu, include_doublet=True):
+    """W_near - W_plain (3, 3n) for explicit (target, fiber) pairs
+    (sf_near_fiber_weights; fiber.py:453-575), device tensor (k, 3, 3n)."""
+    import ctypes
+
+    import torch
+
+    from . import _native, spectral
+
+    def ptr(t):
+        return t.data_ptr() if t is not None and t.numel() else None
+
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    dev = geo.X.device
+    n, p = geo.n, geo.n - 1
+    k = len(pt_np)
+    W = torch.empty((k, 3, 3 * n), dtype=torch.float64, device=dev)
+    if k:
         nodes, _, _, _ = spectral.grid(p)
         glx, glw = np.polynomial.legendre.leggauss(10)
         consts = dict(Cmat=torch.tensor(spectral.coeff_matrix(p), dtype=torch.float64, device=dev),
                       nodes=torch.tensor(nodes, dtype=torch.float64, device=dev),
                       gl=torch.tensor(np.concatenate([glx, glw]), dtype=torch.float64, device=dev))
-        pt = torch.as_tensor(pt_np, device=dev)
-        pl = torch.as_tensor(pl_np, device=dev)
-        info = torch.empty(found, dtype=torch.int32, device=dev)
-        _native.call("sf_near_fiber_weights", ptr(pt), ptr(pl), found, ptr(targets), ptr(geo.X),
+        pt = torch.as_tensor(np.asarray(pt_np, dtype=np.int64), device=dev)
+        pl = torch.as_tensor(np.asarray(pl_np, dtype=np.int64), device=dev)
+        info = torch.empty(k, dtype=torch.int32, device=dev)
+        _native.call("sf_near_fiber_weights", ptr(pt), ptr(pl), k, ptr(targets), ptr(geo.X),
                      ptr(geo.s_alpha), ptr(geo.wcc), ptr(consts["Cmat"]), ptr(consts["nodes"]),
                      ptr(consts["gl"]), ptr(eps), ptr(geo.L), n, float(mu), int(include_doublet),
                      ptr(W), ptr(info), st)
@@ -415,7 +434,7 @@ def device_fiber_pairs(geo, eps, targets, target_groups, mu, include_doublet=Tru
             raise InsideFiberError("target overlaps the fiber surface")
         if np.any(bad == 2):
             raise RuntimeError("near-field panel refinement overflowed its buffer")
-    return pt_np.astype(np.int64), pl_np.astype(np.int64), W
+    return W
 
 
 _DEV_MESH = {}          # (id(mesh), factor, device) -> (mesh, tensors); small LRU

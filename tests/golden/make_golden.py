@@ -310,6 +310,12 @@ def api_ops_fixture():
                                          interior=True, nullspace_scale=0.5),
          interp=body.interpolate_nodal(per, q, np.array([0.3, 1.7, 2.9]), np.array([0.1, 3.0, 6.1])),
          near_W=body.near_surface_weights(per, near_t, mu, interior_jump=True),
+         fnear_t=cl.X[3].mean(axis=0) + np.array([0.024, 0.018, 0.0]),
+         fnear_W=fiber.near_fiber_weights(fib, cl.X[3].mean(axis=0) + np.array([0.024, 0.018, 0.0]),
+                                          mu, include_doublet=True),
+         fnear_eval=fiber.near_fiber_eval(fib, f, cl.X[3].mean(axis=0)
+                                          + np.array([0.024, 0.018, 0.0]), mu),
+         resampled=fiber.resample_to_fine(f[:, 0], np.linspace(-1, 1, 7)),
          Mmat=fib.mobility_matrix(mu), Kmat=fib.kdelta_matrix(mu),
          **versions())
 

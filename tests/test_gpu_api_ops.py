@@ -68,3 +68,15 @@ def test_surface_helpers(cuda, g):
     assert np.array_equal(got, g["interp"])
     W = body.near_surface_weights(per, g["near_t"], mu, interior_jump=True)
     assert np.abs(W - g["near_W"]).max() <= 1e-12 * np.abs(g["near_W"]).max()
+
+
+def test_fiber_near_field_api(cuda, g):
+    """near_fiber_weights / near_fiber_eval (device-built map) and
+    resample_to_fine against the reference (fiber.py:444-587)."""
+    fib = fiber.Fiber(g["X"], eps=float(g["eps"]), E=float(g["E"]))
+    mu = float(g["mu"])
+    W = fiber.near_fiber_weights(fib, g["fnear_t"], mu, include_doublet=True)
+    assert np.abs(W - g["fnear_W"]).max() <= 1e-11 * np.abs(g["fnear_W"]).max()
+    assert rel_l2(fiber.near_fiber_eval(fib, g["f"], g["fnear_t"], mu), g["fnear_eval"]) < 1e-11
+    assert np.array_equal(fiber.resample_to_fine(g["f"][:, 0], np.linspace(-1, 1, 7)),
+                          g["resampled"])
