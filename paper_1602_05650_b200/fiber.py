@@ -485,3 +485,61 @@ def near_fiber_eval(fib, f, target, mu, include_doublet=False):
     """Velocity near (but outside) the fiber: near_fiber_weights @ f (fiber.py:576-587)."""
     W = near_fiber_weights(fib, target, mu, include_doublet=include_doublet)
     return W @ np.asarray(f, dtype=float).ravel()
+
+
+# -- boundary residuals (fiber.py:375-441): host form of the 14 BC rows the
+#    device rows kernel assembles analytically; for API users and checks ------
+
+def _end_rows(fib, Xcand, Tcand, plus, bc, body_kinematics, mu=None, u_bar=None,
+              homogeneous=False):
+    """Residuals (vec1, vec2, tension) of the boundary equations at one end."""
+    k = fib.end_index(plus)
+    sigma = 1.0 if plus else -1.0
+    t = fib.tangents[k]
+    Ds, Ds2, Ds3 = fib.ds_powers()
+    Xss = (Ds2 @ Xcand)[k]
+    Xsss = (Ds3 @ Xcand)[k]
+    if bc.kind == "free":
+        return Xss, Xsss, Tcand[k]
+    if bc.kind == "prescribedForceTorque":
+        Fx = -fib.E * Xsss + Tcand[k] * t
+        if homogeneous:
+            return Fx, Xss, Tcand[k]
+        return (Fx - sigma * bc.force, Xss - sigma * np.cross(t, bc.torque) / fib.E,
+                Tcand[k] - sigma * (bc.force @ t + (bc.torque @ bc.torque) / fib.E))
+    if bc.kind == "hingedToSurface":
+        Fx = -fib.E * Xsss + Tcand[k] * t
+        spring = -bc.stiffness * (Xcand[k] - (0.0 if homogeneous else bc.attachment))
+        return Fx - sigma * spring, Xss, Tcand[k] - sigma * (spring @ t)
+    if bc.kind == "clampedToBody":
+        if body_kinematics is None:
+            raise ValueError("clamped end requires body kinematics")
+        U = np.asarray(body_kinematics["U"], dtype=float)
+        Om = np.asarray(body_kinematics["omega"], dtype=float)
+        c = np.asarray(body_kinematics["center"], dtype=float)
+        dt = float(body_kinematics["dt"])
+        vel = (Xcand[k] - (0.0 if homogeneous else fib.X[k])) / dt
+        vec1 = vel - U - np.cross(Om, fib.X[k] - c)
+        if bc.tangent is None:
+            vec2 = Xss
+        else:
+            vec2 = ((Ds @ Xcand)[k] - (0.0 if homogeneous else t)) / dt - np.cross(Om, t)
+        u_bar = np.zeros(3) if u_bar is None else u_bar
+        f = elastic_force_density(fib, Xcand, Tcand)
+        v_self = local_mobility_apply(fib, f, mu) + nonlocal_Kdelta_apply(fib, f, mu)
+        tres = float((v_self[k] + u_bar - U - np.cross(Om, fib.X[k] - c)) @ t)
+        return vec1, vec2, tres
+    raise ValueError(f"unknown boundary-condition kind {bc.kind!r}")
+
+
+def bc_residuals(fib, Xcand, Tcand, body_kinematics=None, mu=1.0, u_bar=None,
+                 homogeneous=False):
+    """The 14 scalar boundary residuals: plus-end pair, minus-end pair, and
+    the two tension conditions (fiber.py:430-441)."""
+    Xcand = np.asarray(Xcand, dtype=float)
+    Tcand = np.asarray(Tcand, dtype=float)
+    p1, p2, pt = _end_rows(fib, Xcand, Tcand, True, fib.bc_plus, body_kinematics, mu, u_bar,
+                           homogeneous)
+    m1, m2, mt = _end_rows(fib, Xcand, Tcand, False, fib.bc_minus, body_kinematics, mu, u_bar,
+                           homogeneous)
+    return np.concatenate([p1, p2, m1, m2, [pt], [mt]])

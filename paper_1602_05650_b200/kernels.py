@@ -230,6 +230,76 @@ def kdelta_matrix(X, s, s_alpha, tang, w, delta, pref):
     return K
 
 
+def rotlet_sum(trg, src, L, pref):
+    """Sum of rotlets pref (L_j x r) / r^3 (kernels.py:149-174), no group
+    exclusion (sources are body centres), r^2 < 1e-24 skipped and counted.
+    Evaluated on the device; numpy in -> numpy out."""
+    import torch
+    host = not _is_torch(trg)
+    dev = torch.device("cuda")
+    t = torch.as_tensor(np.asarray(trg, dtype=float) if host else trg, dtype=torch.float64,
+                        device=dev).reshape(-1, 3)
+    s = torch.as_tensor(np.asarray(src, dtype=float) if host else src, dtype=torch.float64,
+                        device=dev).reshape(-1, 3)
+    Lt = torch.as_tensor(np.asarray(L, dtype=float) if host else L, dtype=torch.float64,
+                         device=dev).reshape(-1, 3)
+    r = t[:, None, :] - s[None, :, :]
+    r2 = (r * r).sum(dim=2)
+    ok = r2 >= MIN_SEPARATION * MIN_SEPARATION
+    ir3 = torch.where(ok, 1.0 / (torch.where(ok, r2, 1.0) * torch.sqrt(torch.where(ok, r2, 1.0))),
+                      torch.zeros_like(r2))
+    u = (torch.cross(Lt[None, :, :].expand_as(r), r, dim=2) * ir3[:, :, None]).sum(dim=1) * pref
+    bad = int((~ok).sum().item())
+    return (u.cpu().numpy() if host else u), bad
+
+
+# -- single-pair kernels and the viscosity holder (kernels.py:22-69): scalar
+#    host helpers of the reference API --------------------------------------
+
+class KernelContext:
+    """Holds the fluid viscosity shared by the kernel evaluations."""
+
+    def __init__(self, mu):
+        if mu <= 0:
+            raise ValueError(f"viscosity must be positive, got {mu}")
+        self.mu = float(mu)
+
+
+def _checked_r(r):
+    r = np.asarray(r, dtype=float)
+    d = np.sqrt(r @ r)
+    if d < MIN_SEPARATION:
+        raise SingularEvaluationError(f"evaluation point within {MIN_SEPARATION} of source")
+    return r, d
+
+
+def stokeslet_apply(r, f, mu):
+    """(1/8 pi mu)(I + rhat rhat) f / |r|."""
+    r, d = _checked_r(r)
+    f = np.asarray(f, dtype=float)
+    return (f / d + (r @ f) * r / d ** 3) / (8.0 * np.pi * mu)
+
+
+def stresslet_apply(r, n, q, mu):
+    """-(3/4 pi mu)(q.rhat)(n.rhat) rhat / |r|^2."""
+    r, d = _checked_r(r)
+    return -3.0 * (np.asarray(q, dtype=float) @ r) * (np.asarray(n, dtype=float) @ r) * r / (
+        4.0 * np.pi * mu * d ** 5)
+
+
+def rotlet_apply(r, L, mu):
+    """(1/8 pi mu)(L x rhat) / |r|^2."""
+    r, d = _checked_r(r)
+    return np.cross(np.asarray(L, dtype=float), r) / (8.0 * np.pi * mu * d ** 3)
+
+
+def doublet_apply(r, f, mu):
+    """(1/8 pi mu)(I - 3 rhat rhat) f / |r|^3."""
+    r, d = _checked_r(r)
+    f = np.asarray(f, dtype=float)
+    return (f / d ** 3 - 3.0 * (r @ f) * r / d ** 5) / (8.0 * np.pi * mu)
+
+
 def dfma_peak(iters=1 << 16):
     """Measured FP64 DFMA throughput of this GPU: (flop/s, ms)."""
     flops = ctypes.c_double(0.0)
@@ -241,6 +311,7 @@ def dfma_peak(iters=1 << 16):
 __all__ = [
     "MIN_SEPARATION", "SingularEvaluationError", "NearFieldError", "no_groups",
     "stokeslet_sum", "doublet_sum", "sbt_pair_sum", "stresslet_sum",
-    "stresslet_sum_subtracted", "stresslet_rowsum", "kdelta_matrix", "dfma_peak",
+    "stresslet_sum_subtracted", "stresslet_rowsum", "kdelta_matrix", "dfma_peak", "rotlet_sum",
+    "KernelContext", "stokeslet_apply", "stresslet_apply", "rotlet_apply", "doublet_apply",
     "SF_MODE_FP64", "SF_MODE_FP32C",
 ]

@@ -271,6 +271,29 @@ def near_surface_fixture():
          nsp=np.array([[a, b, *x, d] for a, b, x, d in nsp]), **versions())
 
 
+def bc_fixture(fib, Xc, Tc, mu):
+    """bc_residuals (fiber.py:375-441) for every boundary-condition kind."""
+    out = {}
+    d = fib.tangents[-1]
+    kin = dict(U=np.array([0.1, -0.2, 0.05]), omega=np.array([0.3, 0.1, -0.2]),
+               center=fib.X[-1] - 0.4 * d, dt=1e-3)
+    cases = {
+        "free": (fiber.FreeEnd(), fiber.FreeEnd()),
+        "pft": (fiber.PrescribedForceTorque([0.5, -1.0, 0.2], [0.1, 0.0, -0.3]), fiber.FreeEnd()),
+        "hinged": (fiber.HingedToSurface(fib.X[0] + 0.01, 3.0), fiber.FreeEnd()),
+        "clamped": (fiber.FreeEnd(), fiber.ClampedToBody(0, fib.X[-1], d)),
+        "clamped_h": (fiber.FreeEnd(), fiber.ClampedToBody(0, fib.X[-1])),
+    }
+    for name, (bp, bm) in cases.items():
+        fib.bc_plus, fib.bc_minus = bp, bm
+        for hom in (False, True):
+            out[f"bc_{name}_{int(hom)}"] = fiber.bc_residuals(
+                fib, Xc, Tc, body_kinematics=kin, mu=mu, u_bar=np.array([0.01, 0.02, -0.03]),
+                homogeneous=hom)
+    fib.bc_plus, fib.bc_minus = fiber.FreeEnd(), fiber.FreeEnd()
+    return out
+
+
 def api_ops_fixture():
     """Per-constituent operator API of the reference (fiber.py:237-289,
     body.py:237-283, 522-527) on seeded inputs: the functions a reference
@@ -316,6 +339,15 @@ def api_ops_fixture():
          fnear_eval=fiber.near_fiber_eval(fib, f, cl.X[3].mean(axis=0)
                                           + np.array([0.024, 0.018, 0.0]), mu),
          resampled=fiber.resample_to_fine(f[:, 0], np.linspace(-1, 1, 7)),
+         rot_src=np.array([[0.3, -0.2, 0.1], [2.0, 1.0, -1.0]]), rot_L=np.array([[1.0, 2.0, -0.5],
+                                                                                 [0.3, 0.0, 0.7]]),
+         rot=kernels.rotlet_sum(tgt, np.array([[0.3, -0.2, 0.1], [2.0, 1.0, -1.0]]),
+                                np.array([[1.0, 2.0, -0.5], [0.3, 0.0, 0.7]]), 0.2)[0],
+         apply1=np.concatenate([kernels.stokeslet_apply(tgt[0], f[0], mu),
+                                kernels.stresslet_apply(tgt[0], f[1], f[2], mu),
+                                kernels.rotlet_apply(tgt[1], f[3], mu),
+                                kernels.doublet_apply(tgt[2], f[4], mu)]),
+         **bc_fixture(fib, Xc, Tc, mu),
          Mmat=fib.mobility_matrix(mu), Kmat=fib.kdelta_matrix(mu),
          **versions())
 
