@@ -602,6 +602,36 @@ class InteractionCache:
         self._layout()
         self.bad = torch.zeros(3, dtype=torch.int64, **dev)
 
+    # -- the reference's host-side attributes (system.py:536-557), read back
+    #    from the device layout on demand --------------------------------------
+    @property
+    def fiber_sources(self):
+        return self.fsrc.cpu().numpy()
+
+    @property
+    def fiber_groups(self):
+        return self.fgrp.cpu().numpy()
+
+    @property
+    def fiber_weights(self):
+        return np.split(self.fw.cpu().numpy(), np.cumsum(self.node_counts)[:-1])
+
+    @property
+    def doublet_coeffs(self):
+        return list(((self.eps * self.fL) ** 2 / 2.0).cpu().numpy())
+
+    @property
+    def surface_sources(self):
+        return self.ssrc.cpu().numpy() if self.ssrc is not None else np.zeros((0, 3))
+
+    @property
+    def surface_normals(self):
+        return self.snrm.cpu().numpy() if self.snrm is not None else np.zeros((0, 3))
+
+    @property
+    def surface_groups(self):
+        return self.sgrp.cpu().numpy() if self.sgrp is not None else np.zeros(0, dtype=np.int64)
+
     # -- construction helpers ------------------------------------------------
     def _class_near_pairs(self, mu, include_doublet):
         """Device near maps of a mixed-order system, one order class at a

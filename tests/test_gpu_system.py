@@ -106,3 +106,20 @@ def test_near_fiber_pair_routes_through_near_evaluation(cuda):
                                            cache=system.InteractionCache(st, near="host"))
     assert len(system.InteractionCache(st).near_fiber) > 0
     assert rel_l2(dev.fibers[1], host.fibers[1]) < 1e-12
+
+
+def test_cache_reference_attributes(cuda):
+    """InteractionCache exposes the reference's host attributes
+    (system.py:536-557): sources, groups, per-fiber weights, doublet
+    coefficients, surface arrays."""
+    from paper_1602_05650_b200 import configs
+    st = configs.aster(n_fibers=16)
+    c = system.InteractionCache(st)
+    assert c.fiber_sources.shape == (16 * 32, 3)
+    assert np.array_equal(c.fiber_groups, np.repeat(np.arange(16), 32))
+    assert len(c.fiber_weights) == 16
+    for f, w in zip(st.fibers, c.fiber_weights):
+        assert np.allclose(w, f.node_weights(), rtol=1e-11, atol=1e-15)   # device geometry
+        assert abs(c.doublet_coeffs[st.fibers.index(f)] - (f.eps * f.L) ** 2 / 2) < 1e-15
+    assert np.array_equal(c.surface_sources, st.particles[0].mesh.nodes)
+    assert np.array_equal(c.surface_groups, np.full(st.particles[0].mesh.n_nodes, 16))
