@@ -122,6 +122,67 @@ __device__ __forceinline__ void sym_pair(const PData &pi, const PData &pj, doubl
     }
 }
 
+// The TBI pairs of one step (fast path, both directions) evaluated phase by
+// phase so that consecutive DFMAs share the j operand (c_j, f_j) in one
+// slot and can take it from the operand reuse cache: DFMAs with three
+// distinct register sources issue at 2/3 rate on sm_100a.
+template <int TBI>
+__device__ __forceinline__ void sym_step_grouped(const PData (&pi)[TBI], const PData &pj,
+                                                 double (&ui)[TBI][3], double *uj) {
+    double rx[TBI], ry[TBI], rz[TBI], ir[TBI], ir3[TBI], ir5[TBI];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        rx[q] = pi[q].x - pj.x;
+        ry[q] = pi[q].y - pj.y;
+        rz[q] = pi[q].z - pj.z;
+    }
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        const double r2 = fma(rx[q], rx[q], fma(ry[q], ry[q], rz[q] * rz[q]));
+        ir[q] = rsq_refine(r2, rsq_seed(r2));
+        const double ir2 = ir[q] * ir[q];
+        ir3[q] = ir[q] * ir2;
+        ir5[q] = ir3[q] * ir2;
+    }
+    double a[TBI], b[TBI];
+    // owner direction: coefficients of source j (c_j, 3c_j, f_j shared across q)
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) a[q] = fma(pj.c, ir3[q], ir[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = rx[q] * pj.fx;
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = fma(ry[q], pj.fy, b[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = fma(rz[q], pj.fz, b[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] *= fma(-pj.c3, ir5[q], ir3[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][0] = fma(a[q], pj.fx, ui[q][0]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][1] = fma(a[q], pj.fy, ui[q][1]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][2] = fma(a[q], pj.fz, ui[q][2]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        ui[q][0] = fma(b[q], rx[q], ui[q][0]);
+        ui[q][1] = fma(b[q], ry[q], ui[q][1]);
+        ui[q][2] = fma(b[q], rz[q], ui[q][2]);
+    }
+    // transposed direction: coefficients of the i points
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        const double ai = fma(pi[q].c, ir3[q], ir[q]);
+        const double bi = fma(rz[q], pi[q].fz, fma(ry[q], pi[q].fy, rx[q] * pi[q].fx)) *
+                          fma(-pi[q].c3, ir5[q], ir3[q]);
+        uj[0] = fma(ai, pi[q].fx, uj[0]);
+        uj[1] = fma(ai, pi[q].fy, uj[1]);
+        uj[2] = fma(ai, pi[q].fz, uj[2]);
+        uj[0] = fma(bi, rx[q], uj[0]);
+        uj[1] = fma(bi, ry[q], uj[1]);
+        uj[2] = fma(bi, rz[q], uj[2]);
+    }
+}
+
 __device__ __forceinline__ PData shfl_next(const PData &p, int src_lane) {
     PData q;
     q.x = __shfl_sync(0xffffffffu, p.x, src_lane);
@@ -160,7 +221,7 @@ __device__ __forceinline__ bool boxes_far(const double *blo, const double *bhi, 
     return d2 > 1e-20;
 }
 
-template <int MINB, int TBI, bool PF = false>
+template <int MINB, int TBI, bool PF = false, bool GRP = false>
 __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) {
     constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];           // M x 3 transposed accumulators
@@ -236,8 +297,12 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
                     const int k1 = (lane + s + 1) & 31;
                     nxy = js_xy[warp][k1];
                     nzf = js_zf[warp][k1];
+                    if (GRP) {
+                        sym_step_grouped<TBI>(pi, pj, ui, uj);
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < TBI; ++q) sym_pair<false, true>(pi[q], pj, ui[q], uj, nb);
+                        for (int q = 0; q < TBI; ++q) sym_pair<false, true>(pi[q], pj, ui[q], uj, nb);
+                    }
                     uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
                     uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
                     uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
@@ -772,7 +837,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
         const char *e = getenv("SF_SYM_VARIANT");
-        return e ? atoi(e) : 124;
+        return e ? atoi(e) : 224;
     }();
     auto launch = [&](auto kern) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -809,7 +874,8 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         case 18: lrc = launch(sym_task_kernel<1, 8>); break;
         case 24: lrc = launch(sym_task_kernel<2, 4>); break;
         case 123: lrc = launch(sym_task_kernel<2, 3, true>); break;
-        default: lrc = launch(sym_task_kernel<2, 4, true>); break;   // 739 vs 735 G/s at C5
+        case 124: lrc = launch(sym_task_kernel<2, 4, true>); break;
+        default: lrc = launch(sym_task_kernel<2, 4, true, true>); break;   // 749 G/s at C5
     }
     if (lrc) return lrc;
     int rc = check_launch("sym_task_kernel");
