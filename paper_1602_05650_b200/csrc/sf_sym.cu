@@ -486,7 +486,53 @@ __device__ __forceinline__ void sym_pair_f(const PDataF &pi, const PDataF &pj, f
     }
 }
 
-template <int MINB, int TBI>
+// FP32 form of sym_step_grouped (fast path, both directions).
+template <int TBI>
+__device__ __forceinline__ void sym_step_grouped_f(const PDataF (&pi)[TBI], const PDataF &pj,
+                                                   float (&ui)[TBI][3], float *uj) {
+    float rx[TBI], ry[TBI], rz[TBI], ir[TBI], ir3[TBI], ir5[TBI];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        rx[q] = (pi[q].xh - pj.xh) + (pi[q].xl - pj.xl);
+        ry[q] = (pi[q].yh - pj.yh) + (pi[q].yl - pj.yl);
+        rz[q] = (pi[q].zh - pj.zh) + (pi[q].zl - pj.zl);
+    }
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        ir[q] = rsqrtf(fmaf(rx[q], rx[q], fmaf(ry[q], ry[q], rz[q] * rz[q])));
+        const float ir2 = ir[q] * ir[q];
+        ir3[q] = ir[q] * ir2;
+        ir5[q] = ir3[q] * ir2;
+    }
+    float a[TBI], b[TBI];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) a[q] = fmaf(pj.c, ir3[q], ir[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = rx[q] * pj.fx;
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = fmaf(ry[q], pj.fy, b[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] = fmaf(rz[q], pj.fz, b[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) b[q] *= fmaf(-pj.c3, ir5[q], ir3[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][0] = fmaf(a[q], pj.fx, fmaf(b[q], rx[q], ui[q][0]));
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][1] = fmaf(a[q], pj.fy, fmaf(b[q], ry[q], ui[q][1]));
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ui[q][2] = fmaf(a[q], pj.fz, fmaf(b[q], rz[q], ui[q][2]));
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        const float ai = fmaf(pi[q].c, ir3[q], ir[q]);
+        const float bi = fmaf(rz[q], pi[q].fz, fmaf(ry[q], pi[q].fy, rx[q] * pi[q].fx)) *
+                         fmaf(-pi[q].c3, ir5[q], ir3[q]);
+        uj[0] = fmaf(ai, pi[q].fx, fmaf(bi, rx[q], uj[0]));
+        uj[1] = fmaf(ai, pi[q].fy, fmaf(bi, ry[q], uj[1]));
+        uj[2] = fmaf(ai, pi[q].fz, fmaf(bi, rz[q], uj[2]));
+    }
+}
+
+template <int MINB, int TBI, bool GRP = false>
 __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs a) {
     constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];
@@ -559,7 +605,9 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
                 pj.fz = js_c[warp][k][0]; pj.c = js_c[warp][k][1]; pj.c3 = js_c[warp][k][2];
                 pj.g = js_g[warp][k];
                 int nbi = 0;
-                if (fast) {
+                if (fast && both && GRP) {
+                    sym_step_grouped_f<TBI>(pi, pj, uf, uj);
+                } else if (fast) {
 #pragma unroll
                     for (int q = 0; q < TBI; ++q) {
                         if (both) sym_pair_f<false, true>(pi[q], pj, uf[q], uj, nbi);
@@ -850,7 +898,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     if (f32) {
         static const int fvariant = [] {
             const char *e = getenv("SF_SYM_F32_VARIANT");
-            return e ? atoi(e) : 34;
+            return e ? atoi(e) : 134;
         }();
         switch (fvariant) {
             case 32: lrc = launch(sym_task_kernel_f32<3, 2>); break;
@@ -859,7 +907,15 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
             case 26: lrc = launch(sym_task_kernel_f32<2, 6>); break;
             case 28: lrc = launch(sym_task_kernel_f32<2, 8>); break;
             case 44: lrc = launch(sym_task_kernel_f32<4, 4>); break;
-            default: lrc = launch(sym_task_kernel_f32<3, 4>); break;
+            case 134: lrc = launch(sym_task_kernel_f32<3, 4, true>); break;
+            case 124: lrc = launch(sym_task_kernel_f32<2, 4, true>); break;
+            case 144: lrc = launch(sym_task_kernel_f32<4, 4, true>); break;
+            case 133: lrc = launch(sym_task_kernel_f32<3, 3, true>); break;
+            case 136: lrc = launch(sym_task_kernel_f32<3, 6, true>); break;
+            case 126: lrc = launch(sym_task_kernel_f32<2, 6, true>); break;
+            case 128: lrc = launch(sym_task_kernel_f32<2, 8, true>); break;
+            case 34: lrc = launch(sym_task_kernel_f32<3, 4>); break;
+            default: lrc = launch(sym_task_kernel_f32<3, 4, true>); break;   // 1067 G/s at C5
         }
     } else switch (variant) {
         case 41: lrc = launch(sym_task_kernel<4, 1>); break;
