@@ -931,6 +931,10 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         case 24: lrc = launch(sym_task_kernel<2, 4>); break;
         case 123: lrc = launch(sym_task_kernel<2, 3, true>); break;
         case 124: lrc = launch(sym_task_kernel<2, 4, true>); break;
+        case 233: lrc = launch(sym_task_kernel<3, 3, true, true>); break;
+        case 223: lrc = launch(sym_task_kernel<2, 3, true, true>); break;
+        case 225: lrc = launch(sym_task_kernel<2, 5, true, true>); break;
+        case 232: lrc = launch(sym_task_kernel<3, 2, true, true>); break;
         default: lrc = launch(sym_task_kernel<2, 4, true, true>); break;   // 749 G/s at C5
     }
     if (lrc) return lrc;
