@@ -95,6 +95,13 @@ int sf_stresslet_sum(const double *trg, const int64_t *tgrp, int64_t nt,
 int sf_stresslet_sum_subtracted(const double *nodes, const double *nrm,
                                 const double *w, const double *q, int64_t n,
                                 double pref, double *out, void *stream);
+/* Rank `rank` of `world`'s share of the symmetric subtracted double layer
+ * (unit-pair tasks split by cost, as sf_sbt_symmetric_partial): out (n,3)
+ * receives this rank's contribution to every node; summing over ranks gives
+ * sf_stresslet_sum_subtracted. */
+int sf_stresslet_sum_subtracted_partial(const double *nodes, const double *nrm, const double *w,
+                                        const double *q, int64_t n, double pref, int rank,
+                                        int world, double *out, void *stream);
 
 /* Replaces kernels.stresslet_rowsum (kernels.py:252-281); out is (n,3,3). */
 int sf_stresslet_rowsum(const double *nodes, const double *nrm, const double *w,

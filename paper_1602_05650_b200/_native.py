@@ -41,6 +41,7 @@ _SIGNATURES = {
     "sf_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P, _P],
     "sf_stresslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _P, _P, _P],
     "sf_stresslet_sum_subtracted": [_P, _P, _P, _P, _I64, _D, _P, _P],
+    "sf_stresslet_sum_subtracted_partial": [_P, _P, _P, _P, _I64, _D, _I, _I, _P, _P],
     "sf_stresslet_rowsum": [_P, _P, _P, _I64, _D, _P, _P],
     "sf_kdelta_build_batched": [_P, _P, _P, _P, _P, _I64, _I64, _P, _D, _P, _P],
     "sf_self_apply_batched": [_P, _P, _P, _D, _P, _I64, _I64, _I, _P, _P],

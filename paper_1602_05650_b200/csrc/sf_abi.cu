@@ -158,6 +158,16 @@ int sf_stresslet_sum_subtracted(const double *nodes, const double *nrm, const do
     return pairs_dl_subtracted(nodes, nrm, w, q, n, pref, out, st, workspace_for(st));
 }
 
+int sf_stresslet_sum_subtracted_partial(const double *nodes, const double *nrm, const double *w,
+                                        const double *q, int64_t n, double pref, int rank,
+                                        int world, double *out, void *stream) {
+    SF_REQUIRE(n >= 0 && world >= 1 && rank >= 0 && rank < world, "bad sizes");
+    SF_REQUIRE(n == 0 || (nodes && nrm && w && q && out), "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    return pairs_dl_subtracted_symmetric(nodes, nrm, w, q, n, pref, out, st, workspace_for(st),
+                                         rank, world);
+}
+
 int sf_stresslet_rowsum(const double *nodes, const double *nrm, const double *w, int64_t n,
                         double pref, double *out, void *stream) {
     SF_REQUIRE(n >= 0, "negative size");

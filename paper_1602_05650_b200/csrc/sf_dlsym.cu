@@ -28,6 +28,7 @@ struct DlArgs {
     const DlNode *p;
     int64_t N;
     int M, G;
+    int64_t task0;  // first task of this launch (a rank's share)
     double *part;   // (G, N, 3)
 };
 
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
     __shared__ double ui_s[4][kI][3];
     __shared__ DlNode js[4][32];
     int g, h;
-    dl_task_units(blockIdx.x, A.G, g, h);
+    dl_task_units(A.task0 + blockIdx.x, A.G, g, h);
     const bool both = g != h;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t g0 = (int64_t)g * A.M, h0 = (int64_t)h * A.M;
@@ -175,12 +176,20 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
     }
 }
 
-__global__ void dl_reduce_kernel(const double *__restrict__ part, int G, int64_t N, double pref,
-                                 double *__restrict__ out) {
+// Slot k of a point in unit u was written by task {min(u,k), max(u,k)};
+// slots of tasks outside [t0, t1) (another rank's share) are skipped.
+__global__ void dl_reduce_kernel(const double *__restrict__ part, int G, int64_t N, int M,
+                                 int64_t t0, int64_t t1, double pref, double *__restrict__ out) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= 3 * N) return;
+    const int64_t u = (e / 3) / M;
     double s = 0.0;
-    for (int k = 0; k < G; ++k) s += part[(int64_t)k * 3 * N + e];
+    for (int k = 0; k < G; ++k) {
+        const int64_t g = k < u ? k : u, h = k < u ? u : k;
+        const int64_t t = g * G - g * (g - 1) / 2 + (h - g);
+        if (t < t0 || t >= t1) continue;
+        s += part[(int64_t)k * 3 * N + e];
+    }
     out[e] = pref * s;
 }
 
@@ -194,9 +203,10 @@ bool use_dl_symmetric(int64_t n) {
 
 int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const double *w,
                                   const double *q, int64_t n, double pref, double *out,
-                                  cudaStream_t st, Workspace &ws) {
+                                  cudaStream_t st, Workspace &ws, int rank, int world) {
     if (n == 0) return SF_OK;
     int64_t M = n / 128;   // >= 8256 unit-pair tasks, as sym_unit_size
+    // (tasks split by cost over ranks as in sf_sym.cu: sym_task_range)
     M = M < 256 ? 256 : (M > 2048 ? 2048 : M);
     M = (M / 128) * 128;
     const int G = (int)((n + M - 1) / M);
@@ -207,14 +217,17 @@ int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const 
     dl_pack<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(nodes, nrm, w, q, n, packed);
     DlArgs a;
     a.p = packed; a.N = n; a.M = (int)M; a.G = G; a.part = part;
+    int64_t ntasks = 0;
+    a.task0 = sym_task_range(G, rank, world, &ntasks);
     const size_t smem = sizeof(double) * 3 * (size_t)M;
     if (cudaFuncSetAttribute(dl_task_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute");
-    dl_task_kernel<4><<<(unsigned)((int64_t)G * (G + 1) / 2), kDlThreads, smem, st>>>(a);
+    if (ntasks > 0) dl_task_kernel<4><<<(unsigned)ntasks, kDlThreads, smem, st>>>(a);
     int rc = check_launch("dl_task_kernel");
     if (rc) return rc;
-    dl_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(part, G, n, pref, out);
+    dl_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(part, G, n, (int)M, a.task0,
+                                                                     a.task0 + ntasks, pref, out);
     return check_launch("dl_reduce_kernel");
 }
 

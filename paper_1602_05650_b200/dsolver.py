@@ -166,7 +166,6 @@ class DistBlockOperator:
         self.n_surf_t = n_surf_t
         N = nf * n
         if symmetric is None:
-            import os
             symmetric = N >= 8192 and os.environ.get("SF_SYMMETRIC", "1") != "0"
         self.symmetric = bool(symmetric) and nf > 0
         lo_f = n_surf_t + self.f0 * n
@@ -258,6 +257,20 @@ class DistBlockOperator:
             bc_par=_ptr(self.bc_par), bc_body=_ptr(self.bc_body), np=np_, pcenter=_ptr(self.pcenter),
             p_uoff=_ptr(self.p_uoff), fib_off=fo + 4 * n * o, dt=self.dt, mu=self.mu)
         # surfaces (rank 0 rows)
+        # large meshes: the on-surface double layer is split over the ranks
+        # (symmetric unit-pair tasks, sf_stresslet_sum_subtracted_partial)
+        # and all-reduced; rank 0 consumes the sum in its surface rows
+        self.dl_split = {}
+        meshes = [(lay.q1[i], p.mesh) for i, p in enumerate(state.particles)]
+        if state.periphery is not None:
+            meshes.append((lay.q0, state.periphery.mesh))
+        if os.environ.get("SF_SYMMETRIC", "1") != "0":
+            for sl, m in meshes:
+                if m.n_nodes >= 8192:
+                    self.dl_split[sl.start] = dict(
+                        sl=sl, n=m.n_nodes, nodes=torch.as_tensor(m.nodes, **f64),
+                        nrm=torch.as_tensor(m.normals, **f64), w=torch.as_tensor(m.weights, **f64),
+                        out=torch.empty((m.n_nodes, 3), **f64))
         self.surf = []
         if rank == 0:
             for i, part in enumerate(state.particles):
@@ -362,15 +375,23 @@ class DistBlockOperator:
             else:
                 self._surf_part.zero_()
             c.all_reduce_sum(self._surf_part)
+        pref_dl = -3.0 / (4.0 * math.pi * self.mu)
+        for d in self.dl_split.values():
+            _native.call("sf_stresslet_sum_subtracted_partial", _ptr(d["nodes"]), _ptr(d["nrm"]),
+                         _ptr(d["w"]), _ptr(u[d["sl"]]), d["n"], pref_dl, c.rank, c.world,
+                         _ptr(d["out"]), st)
+            c.all_reduce_sum(d["out"])
         # surfaces (rank 0)
         if self.surf:
             ub_s = self.cache_surf.apply(f_full, q, wr, check=True) + self._surf_part
-            pref_dl = -3.0 / (4.0 * math.pi * self.mu)
             for s in self.surf:
                 qs = u[s["sl"]]
                 rows = out[s["sl"]]
-                _native.call("sf_stresslet_sum_subtracted", _ptr(s["nodes"]), _ptr(s["nrm"]),
-                             _ptr(s["w"]), _ptr(qs), s["n"], pref_dl, _ptr(rows), st)
+                if s["sl"].start in self.dl_split:
+                    rows.copy_(self.dl_split[s["sl"].start]["out"].reshape(-1))
+                else:
+                    _native.call("sf_stresslet_sum_subtracted", _ptr(s["nodes"]), _ptr(s["nrm"]),
+                                 _ptr(s["w"]), _ptr(qs), s["n"], pref_dl, _ptr(rows), st)
                 ub = ub_s[s["tsl"]]
                 if s["kind"] == 0:
                     _native.call("sf_wrench_flow", _ptr(s["nodes"]), s["n"], _ptr(s["center"]),

@@ -120,11 +120,11 @@ def test_dist_kinetics_steps_match_reference(cuda):
 
 def test_dist_rows_mid_size_confined(cuda):
     """A confined aster large enough for the symmetric, cross and symmetric
-    double-layer kernels on one GPU (16,384 fiber points, 4,096-node
+    double-layer kernels on one GPU (16,384 fiber points, 9,216-node
     periphery): rows of 2 emulated ranks equal the single-GPU rows."""
     import torch
     from paper_1602_05650_b200 import configs
-    st = configs.confined_aster(n_fibers=512, periphery_res=(16, 16), periphery_radius=2.5)
+    st = configs.confined_aster(n_fibers=512, periphery_res=(24, 24), periphery_radius=2.5)
     op1 = solver.BlockOperator(st, 1e-3)
     u = np.random.default_rng(2).standard_normal(op1.layout.size)
     ref = op1.apply(u)
