@@ -71,6 +71,47 @@ __device__ __forceinline__ void dl_pair(const DlNode &pi, const DlNode &pj, doub
     }
 }
 
+// The TBI pairs of one step, phase by phase (shared j operands in one slot).
+template <int TBI>
+__device__ __forceinline__ void dl_step_grouped(const DlNode (&pi)[TBI], const DlNode &pj,
+                                                double (&ui)[TBI][3], double *uj) {
+    double rx[TBI], ry[TBI], rz[TBI], qr5[TBI];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        rx[q] = pi[q].x - pj.x;
+        ry[q] = pi[q].y - pj.y;
+        rz[q] = pi[q].z - pj.z;
+    }
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        const double r2 = fma(rx[q], rx[q], fma(ry[q], ry[q], rz[q] * rz[q]));
+        const double ir = rsq_refine(r2, rsq_seed(r2));
+        const double ir2 = ir * ir;
+        const double dqx = pj.qx - pi[q].qx, dqy = pj.qy - pi[q].qy, dqz = pj.qz - pi[q].qz;
+        qr5[q] = fma(dqx, rx[q], fma(dqy, ry[q], dqz * rz[q])) * (ir * ir2 * ir2);
+    }
+    double c[TBI];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) c[q] = rx[q] * pj.nx;
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) c[q] = fma(ry[q], pj.ny, c[q]);
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) c[q] = fma(rz[q], pj.nz, c[q]) * qr5[q];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        ui[q][0] = fma(c[q], rx[q], ui[q][0]);
+        ui[q][1] = fma(c[q], ry[q], ui[q][1]);
+        ui[q][2] = fma(c[q], rz[q], ui[q][2]);
+    }
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) {
+        const double cj = fma(pi[q].nx, rx[q], fma(pi[q].ny, ry[q], pi[q].nz * rz[q])) * qr5[q];
+        uj[0] = fma(cj, rx[q], uj[0]);
+        uj[1] = fma(cj, ry[q], uj[1]);
+        uj[2] = fma(cj, rz[q], uj[2]);
+    }
+}
+
 __device__ __forceinline__ void dl_task_units(int64_t t, int G, int &g, int &h) {
     double Gd = (double)G;
     double disc = (2.0 * Gd + 1.0) * (2.0 * Gd + 1.0) - 8.0 * (double)t;
@@ -83,7 +124,7 @@ __device__ __forceinline__ void dl_task_units(int64_t t, int G, int &g, int &h) 
     h = r + (int)(t - start(r));
 }
 
-template <int TBI>
+template <int TBI, bool GRP>
 __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
     constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];
@@ -131,8 +172,12 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
 #pragma unroll 2
                 for (int s = 0; s < 32; ++s) {
                     const DlNode pj = js[warp][(lane + s) & 31];
+                    if (GRP) {
+                        dl_step_grouped<TBI>(pi, pj, ui, uj);
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < TBI; ++q) dl_pair<true>(pi[q], pj, ui[q], uj);
+                        for (int q = 0; q < TBI; ++q) dl_pair<true>(pi[q], pj, ui[q], uj);
+                    }
                     uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
                     uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
                     uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
@@ -220,10 +265,15 @@ int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const 
     int64_t ntasks = 0;
     a.task0 = sym_task_range(G, rank, world, &ntasks);
     const size_t smem = sizeof(double) * 3 * (size_t)M;
-    if (cudaFuncSetAttribute(dl_task_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    static const bool grouped = [] {
+        const char *e = getenv("SF_DL_GROUPED");
+        return !(e && e[0] == '0');
+    }();
+    auto kern = grouped ? dl_task_kernel<4, true> : dl_task_kernel<4, false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
         return check_launch("cudaFuncSetAttribute");
-    if (ntasks > 0) dl_task_kernel<4><<<(unsigned)ntasks, kDlThreads, smem, st>>>(a);
+    if (ntasks > 0) kern<<<(unsigned)ntasks, kDlThreads, smem, st>>>(a);
     int rc = check_launch("dl_task_kernel");
     if (rc) return rc;
     dl_reduce_kernel<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(part, G, n, (int)M, a.task0,
