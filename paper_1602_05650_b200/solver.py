@@ -104,14 +104,6 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def host_elastic_force_density(fib, Xcand, Tcand):
-    """f = -E Ds^4 X + Ds (T X_s) (fiber.py:237-241); host helper for API defaults."""
-    Ds, Ds2, _ = fib.ds_powers()
-    Ds4 = Ds2 @ Ds2
-    return (-fib.E * (Ds4 @ np.asarray(Xcand, dtype=float))
-            + Ds @ (np.asarray(Tcand, dtype=float)[:, None] * fib.tangents))
-
-
 def _precision_mode(precision):
     """"fp64" (default) or "fp32c": the fiber x fiber pair sums in FP32
     arithmetic with FP64 accumulation (north_star variant, <= 1e-5 of FP64);

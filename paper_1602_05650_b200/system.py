@@ -809,8 +809,8 @@ def complementary_velocities(state, periphery_density=None, particle_densities=N
     if cache is None:
         cache = InteractionCache(state, include_doublet=include_doublet, backend=backend)
     if fiber_forces is None:
-        from .solver import host_elastic_force_density
-        fiber_forces = [host_elastic_force_density(f, f.X, f.T) + external_force_density(state, f)
+        from .fiber import elastic_force_density
+        fiber_forces = [elastic_force_density(f, f.X, f.T) + external_force_density(state, f)
                         for f in state.fibers]
     if particle_densities is None:
         particle_densities = [p.q for p in state.particles]
