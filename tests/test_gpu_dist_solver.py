@@ -135,3 +135,31 @@ def test_dist_rows_mid_size_confined(cuda):
     for owned, a in run_ranks(2, fn):
         for lo, hi in owned:
             assert rel_l2(a[lo:hi], ref[lo:hi]) < 1e-12
+
+
+def test_torch_comm_nccl_single_rank_step(cuda):
+    """The NCCL code path of TorchComm (all_gather_into_tensor,
+    reduce_scatter_tensor, broadcast, all_reduce) in a world-size-1 process
+    group on the box: the distributed step reproduces the golden step."""
+    import socket
+
+    import torch.distributed as dist
+    g = golden("step_confined.npz")
+    st = CASES["step_confined.npz"](g)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=cuda)
+    try:
+        comm = dsolver.TorchComm()
+        assert comm.nccl
+        params = solver.GmresParams(tolerance=float(g["tol"]))
+        st, info = dsolver.dist_backward_euler_step(st, float(g["dt"]), comm, params,
+                                                    return_info=True, symmetric=True)
+    finally:
+        dist.destroy_process_group()
+    X = np.stack([f.X for f in st.fibers])
+    assert np.linalg.norm(X - g["step0_X"]) / np.linalg.norm(g["step0_X"]) < 1e-8
+    assert abs(info["iterations"] - int(g["iters_0"])) <= 1
