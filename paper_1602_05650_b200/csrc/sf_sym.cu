@@ -54,6 +54,7 @@ struct SymArgs {
     int64_t task0;    // first task (rank share of the G(G+1)/2 unit pairs)
     double *part;  // (G, N, 3)
     unsigned long long *bad;
+    const double *x;  // (N, 3) FP64 positions: the FP32 variant's coincidence test
 };
 
 constexpr int kSymThreads = 128;
@@ -425,45 +426,70 @@ __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
 
 
 // ------------------------------------------------ FP32-compute variant ----
-// Same task structure; pair arithmetic in FP32 with positions split into
-// float hi + lo parts (r = (x_hi - y_hi) + (x_lo - y_lo) keeps FP32 relative
-// accuracy in r), FP32 sums over one 32-point slab, FP64 accumulation across
-// slabs (owner sums in registers, transposed sums in shared memory).
-// Record floats: xh yh zh xl yl zl fx fy fz c c3, int g at the record's end.
+// Same task structure; pair arithmetic in FP32, FP32 sums over one 32-point
+// slab, FP64 accumulation across slabs (owner sums in registers, transposed
+// sums in shared memory).
+//
+// Positions are slab-relative: every 32-point slab has an FP64 origin o_s
+// (its bounding-box centre) and a record stores float(y - o_s).  For a j
+// slab the i points are re-expressed once, in FP64, relative to that slab's
+// origin: xr_i = float((x_i - o_i) + (o_i - o_j)), so each pair costs a single
+// FP32 subtraction per component, r = xr_i - yl_j.  Both operands are small
+// whenever r is small (|xr_i| <= r + slab extent), so the rounding error of
+// r stays at FP32 precision relative to r itself -- the property the earlier
+// hi+lo split bought with three subtractions per component.
+// Record floats: ylx yly ylz fx fy fz c c3 (32 bytes), int g at the record's end.
 struct PDataF {
-    float xh, yh, zh, xl, yl, zl, fx, fy, fz, c, c3;
+    float x, y, z, fx, fy, fz, c, c3;
     int g;
 };
+
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    // every fast-path r^2 is >= 1e-20 > FLT_MIN; checked pairs select 0 for r^2 < 1e-24
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 __device__ __forceinline__ PDataF load_point_f(const SymSrc *src, int64_t k, bool valid) {
     PDataF p;
     if (valid) {
         const float4 *q = reinterpret_cast<const float4 *>(src + k);
-        const float4 a0 = q[0], a1 = q[1], a2 = q[2];
-        p.xh = a0.x; p.yh = a0.y; p.zh = a0.z; p.xl = a0.w;
-        p.yl = a1.x; p.zl = a1.y; p.fx = a1.z; p.fy = a1.w;
-        p.fz = a2.x; p.c = a2.y; p.c3 = a2.z;
+        const float4 a0 = q[0], a1 = q[1];
+        p.x = a0.x; p.y = a0.y; p.z = a0.z; p.fx = a0.w;
+        p.fy = a1.x; p.fz = a1.y; p.c = a1.z; p.c3 = a1.w;
         p.g = src[k].g;
-    } else {
-        p.xh = p.yh = p.zh = 1e30f;
-        p.xl = p.yl = p.zl = 0.f;
+    } else {  // strengthless and far away (padding i lanes sit at +1e18 instead,
+              // so no two padding points coincide; r^2 stays finite in FP32)
+        p.x = p.y = p.z = -1e18f;
         p.fx = p.fy = p.fz = p.c = p.c3 = 0.f;
         p.g = -3;
     }
     return p;
 }
 
+__device__ __forceinline__ void slab_origin(const SlabMeta &m, double *o) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[c] = 0.5 * (m.lo[c] + m.hi[c]);
+}
+
+// CHECK: group exclusion, and the r^2 < 1e-24 skip decided on the FP64
+// positions (slab-relative FP32 coordinates of coincident points in
+// different slabs round differently, so FP32 r would not be exactly 0).
 template <bool CHECK, bool BOTH>
 __device__ __forceinline__ void sym_pair_f(const PDataF &pi, const PDataF &pj, float *ui,
-                                           float *uj, int &nb) {
-    const float rx = (pi.xh - pj.xh) + (pi.xl - pj.xl);
-    const float ry = (pi.yh - pj.yh) + (pi.yl - pj.yl);
-    const float rz = (pi.zh - pj.zh) + (pi.zl - pj.zl);
+                                           float *uj, int &nb, const double *xi = nullptr,
+                                           const double *xj = nullptr) {
+    const float rx = pi.x - pj.x, ry = pi.y - pj.y, rz = pi.z - pj.z;
     const float r2 = fmaf(rx, rx, fmaf(ry, ry, rz * rz));
-    float ir = rsqrtf(r2);
+    float ir = rsqrt_ftz(r2);
     if (CHECK) {
         const bool excl = (pi.g == pj.g) && pi.g >= 0;
-        const bool small = r2 < 1e-24f;
+        bool small = false;
+        if (xi && xj && !excl) {
+            const double dx = xi[0] - xj[0], dy = xi[1] - xj[1], dz = xi[2] - xj[2];
+            small = below_min_sep(fma(dx, dx, fma(dy, dy, dz * dz)));
+        }
         nb += (small && !excl) ? (BOTH ? 2 : 1) : 0;
         ir = (excl || small) ? 0.f : ir;
     }
@@ -486,20 +512,21 @@ __device__ __forceinline__ void sym_pair_f(const PDataF &pi, const PDataF &pj, f
     }
 }
 
-// FP32 form of sym_step_grouped (fast path, both directions).
+// FP32 form of sym_step_grouped (fast path, both directions), phase by phase
+// so the shared j operands come from the operand reuse cache.
 template <int TBI>
 __device__ __forceinline__ void sym_step_grouped_f(const PDataF (&pi)[TBI], const PDataF &pj,
                                                    float (&ui)[TBI][3], float *uj) {
     float rx[TBI], ry[TBI], rz[TBI], ir[TBI], ir3[TBI], ir5[TBI];
 #pragma unroll
     for (int q = 0; q < TBI; ++q) {
-        rx[q] = (pi[q].xh - pj.xh) + (pi[q].xl - pj.xl);
-        ry[q] = (pi[q].yh - pj.yh) + (pi[q].yl - pj.yl);
-        rz[q] = (pi[q].zh - pj.zh) + (pi[q].zl - pj.zl);
+        rx[q] = pi[q].x - pj.x;
+        ry[q] = pi[q].y - pj.y;
+        rz[q] = pi[q].z - pj.z;
     }
 #pragma unroll
     for (int q = 0; q < TBI; ++q) {
-        ir[q] = rsqrtf(fmaf(rx[q], rx[q], fmaf(ry[q], ry[q], rz[q] * rz[q])));
+        ir[q] = rsqrt_ftz(fmaf(rx[q], rx[q], fmaf(ry[q], ry[q], rz[q] * rz[q])));
         const float ir2 = ir[q] * ir[q];
         ir3[q] = ir[q] * ir2;
         ir5[q] = ir3[q] * ir2;
@@ -532,13 +559,12 @@ __device__ __forceinline__ void sym_step_grouped_f(const PDataF (&pi)[TBI], cons
     }
 }
 
-template <int MINB, int TBI, bool GRP = false>
+template <int MINB, int TBI>
 __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs a) {
     constexpr int kI = 32 * TBI;
     extern __shared__ double jacc_s[];
     __shared__ double ui_s[4][kI][3];
     __shared__ float4 js_a[4][32], js_b[4][32];
-    __shared__ float js_c[4][32][4];
     __shared__ int js_g[4][32];
     if ((int64_t)blockIdx.x >= a.ntasks) return;
     const int64_t t = a.task0 + blockIdx.x;
@@ -554,10 +580,17 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     int nb = 0;
     for (int ib = 0; ib < ng; ib += kI) {
         PDataF pi[TBI];
+        float xl[TBI][3];    // own-slab-relative positions
+        double oi[TBI][3];   // own slab origins
+        bool vi[TBI];
         double ud[TBI][3];
 #pragma unroll
         for (int k = 0; k < TBI; ++k) {
-            pi[k] = load_point_f(a.src, g0 + ib + 32 * k + lane, ib + 32 * k + lane < ng);
+            vi[k] = ib + 32 * k + lane < ng;
+            pi[k] = load_point_f(a.src, g0 + ib + 32 * k + lane, vi[k]);
+            xl[k][0] = pi[k].x; xl[k][1] = pi[k].y; xl[k][2] = pi[k].z;
+            const int64_t sk = (g0 + ib) / 32 + (vi[k] ? k : 0);
+            slab_origin(a.slab[sk], oi[k]);
             ud[k][0] = ud[k][1] = ud[k][2] = 0.0;
         }
         double blo[3], bhi[3];
@@ -581,50 +614,70 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
             const int jl = sl * 32 + lane;
             {
                 const PDataF q = load_point_f(a.src, h0 + jl, jl < nh);
-                js_a[warp][lane] = make_float4(q.xh, q.yh, q.zh, q.xl);
-                js_b[warp][lane] = make_float4(q.yl, q.zl, q.fx, q.fy);
-                js_c[warp][lane][0] = q.fz;
-                js_c[warp][lane][1] = q.c;
-                js_c[warp][lane][2] = q.c3;
+                js_a[warp][lane] = make_float4(q.x, q.y, q.z, q.fx);
+                js_b[warp][lane] = make_float4(q.fy, q.fz, q.c, q.c3);
                 js_g[warp][lane] = q.g;
+            }
+            const SlabMeta &mj = a.slab[h0 / 32 + sl];
+            {   // i points relative to this j slab's origin (FP64, once per slab);
+                // padding i lanes sit 1e18 away and carry no strength
+                double oj[3];
+                slab_origin(mj, oj);
+#pragma unroll
+                for (int k = 0; k < TBI; ++k) {
+                    pi[k].x = vi[k] ? (float)(((double)xl[k][0] + (oi[k][0] - oj[0]))) : 1e18f;
+                    pi[k].y = vi[k] ? (float)(((double)xl[k][1] + (oi[k][1] - oj[1]))) : 1e18f;
+                    pi[k].z = vi[k] ? (float)(((double)xl[k][2] + (oi[k][2] - oj[2]))) : 1e18f;
+                }
             }
             __syncwarp();
             float uf[TBI][3];
 #pragma unroll
             for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
             float uj[3] = {0.f, 0.f, 0.f};
-            const SlabMeta &mj = a.slab[h0 / 32 + sl];
             const bool fast = boxes_far(blo, bhi, mj) && (mj.gmax < gmn || mj.gmin > gmx);
             const int nxt = (lane + 1) & 31;
-            for (int s = 0; s < 32; ++s) {
-                const int k = (lane + s) & 31;
-                PDataF pj;
-                const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
-                pj.xh = A0.x; pj.yh = A0.y; pj.zh = A0.z; pj.xl = A0.w;
-                pj.yl = B0.x; pj.zl = B0.y; pj.fx = B0.z; pj.fy = B0.w;
-                pj.fz = js_c[warp][k][0]; pj.c = js_c[warp][k][1]; pj.c3 = js_c[warp][k][2];
-                pj.g = js_g[warp][k];
-                int nbi = 0;
-                if (fast && both && GRP) {
+            if (fast && both) {
+#pragma unroll 2
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PDataF pj;
+                    const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
+                    pj.x = A0.x; pj.y = A0.y; pj.z = A0.z; pj.fx = A0.w;
+                    pj.fy = B0.x; pj.fz = B0.y; pj.c = B0.z; pj.c3 = B0.w;
+                    pj.g = 0;
                     sym_step_grouped_f<TBI>(pi, pj, uf, uj);
-                } else if (fast) {
-#pragma unroll
-                    for (int q = 0; q < TBI; ++q) {
-                        if (both) sym_pair_f<false, true>(pi[q], pj, uf[q], uj, nbi);
-                        else sym_pair_f<false, false>(pi[q], pj, uf[q], uj, nbi);
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < TBI; ++q) {
-                        if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi);
-                        else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi);
-                    }
-                }
-                if (pj.g != -3) nb += nbi;
-                if (both) {
                     uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
                     uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
                     uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                }
+            } else {
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PDataF pj;
+                    const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
+                    pj.x = A0.x; pj.y = A0.y; pj.z = A0.z; pj.fx = A0.w;
+                    pj.fy = B0.x; pj.fz = B0.y; pj.c = B0.z; pj.c3 = B0.w;
+                    pj.g = js_g[warp][k];
+                    int nbi = 0;
+                    if (fast) {
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) sym_pair_f<false, false>(pi[q], pj, uf[q], uj, nbi);
+                    } else {
+                        const double *xj = pj.g != -3 ? a.x + 3 * (h0 + sl * 32 + k) : nullptr;
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) {
+                            const double *xi = vi[q] ? a.x + 3 * (g0 + ib + 32 * q + lane) : nullptr;
+                            if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                            else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                        }
+                    }
+                    if (pj.g != -3) nb += nbi;
+                    if (both) {
+                        uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                        uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                        uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                    }
                 }
             }
             __syncwarp();
@@ -668,36 +721,10 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     }
 }
 
-// FP32 record packing: float hi/lo positions, weighted strengths, c, 3c.
-__global__ void sym_pack_f32_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
-                                    const double *__restrict__ f, const double *__restrict__ w,
-                                    const double *__restrict__ dcoef, int64_t N,
-                                    SymSrc *__restrict__ out) {
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        SymSrc s;
-        float *pf = reinterpret_cast<float *>(&s);
-        const double wj = w ? w[j] : 1.0;
-        for (int c = 0; c < 3; ++c) {
-            const double v = x[3 * j + c];
-            const float hf = __double2float_rn(v);
-            pf[c] = hf;
-            pf[3 + c] = __double2float_rn(v - (double)hf);
-            pf[6 + c] = __double2float_rn(wj * f[3 * j + c]);
-        }
-        const double c = dcoef ? dcoef[j] : 0.0;
-        pf[9] = __double2float_rn(c);
-        pf[10] = __double2float_rn(3.0 * c);
-        for (int k = 11; k < 18; ++k) pf[k] = 0.f;
-        s.g = grp ? pack_source_group(grp[j]) : -1;
-        s.pad = 0;
-        out[j] = s;
-    }
-}
-
-// Slab bounds from FP32 records (coordinate = hi + lo).
-__global__ void slab_meta_f32_kernel(const SymSrc *__restrict__ src, int64_t N,
-                                     SlabMeta *__restrict__ meta) {
+// Slab bounds straight from the FP64 positions (the FP32 records are packed
+// relative to these boxes' centres afterwards).
+__global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
+                                   int64_t N, SlabMeta *__restrict__ meta) {
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (s * 32 >= N) return;
@@ -705,9 +732,9 @@ __global__ void slab_meta_f32_kernel(const SymSrc *__restrict__ src, int64_t N,
     double v[6];
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
     if (j < N) {
-        const float *pf = reinterpret_cast<const float *>(src + j);
-        for (int c = 0; c < 3; ++c) v[c] = v[3 + c] = (double)pf[c] + (double)pf[3 + c];
-        if (src[j].g >= 0) { gmn = src[j].g; gmx = src[j].g; }
+        for (int c = 0; c < 3; ++c) v[c] = v[3 + c] = x[3 * j + c];
+        const int gj = grp ? pack_source_group(grp[j]) : -1;
+        if (gj >= 0) { gmn = gj; gmx = gj; }
     } else {
         v[0] = v[1] = v[2] = 1e300;
         v[3] = v[4] = v[5] = -1e300;
@@ -728,6 +755,33 @@ __global__ void slab_meta_f32_kernel(const SymSrc *__restrict__ src, int64_t N,
         m.gmin = gmn;
         m.gmax = gmx;
         meta[s] = m;
+    }
+}
+
+// FP32 record packing: float positions relative to the slab origin, weighted
+// strengths, c, 3c.
+__global__ void sym_pack_f32_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
+                                    const double *__restrict__ f, const double *__restrict__ w,
+                                    const double *__restrict__ dcoef, int64_t N,
+                                    const SlabMeta *__restrict__ meta, SymSrc *__restrict__ out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        SymSrc s;
+        float *pf = reinterpret_cast<float *>(&s);
+        double o[3];
+        slab_origin(meta[j / 32], o);
+        const double wj = w ? w[j] : 1.0;
+        for (int c = 0; c < 3; ++c) {
+            pf[c] = __double2float_rn(x[3 * j + c] - o[c]);
+            pf[3 + c] = __double2float_rn(wj * f[3 * j + c]);
+        }
+        const double c = dcoef ? dcoef[j] : 0.0;
+        pf[6] = __double2float_rn(c);
+        pf[7] = __double2float_rn(3.0 * c);
+        for (int k = 8; k < 18; ++k) pf[k] = 0.f;
+        s.g = grp ? pack_source_group(grp[j]) : -1;
+        s.pad = 0;
+        out[j] = s;
     }
 }
 
@@ -865,9 +919,9 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     int64_t pg = (N + 255) / 256;
     const int64_t nslab = (N + 31) / 32;
     if (f32) {
+        slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, N, meta);
         sym_pack_f32_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef,
-                                                                             N, packed);
-        slab_meta_f32_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
+                                                                             N, meta, packed);
     } else {
         sym_pack_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef, N,
                                                                          packed);
@@ -882,6 +936,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     a.task0 = sym_task_range(G, rank, world, &a.ntasks);
     a.part = part;
     a.bad = (unsigned long long *)bad;
+    a.x = x;
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
         const char *e = getenv("SF_SYM_VARIANT");
@@ -898,24 +953,14 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     if (f32) {
         static const int fvariant = [] {
             const char *e = getenv("SF_SYM_F32_VARIANT");
-            return e ? atoi(e) : 134;
+            return e ? atoi(e) : 34;
         }();
         switch (fvariant) {
-            case 32: lrc = launch(sym_task_kernel_f32<3, 2>); break;
-            case 33: lrc = launch(sym_task_kernel_f32<3, 3>); break;
             case 24: lrc = launch(sym_task_kernel_f32<2, 4>); break;
+            case 33: lrc = launch(sym_task_kernel_f32<3, 3>); break;
             case 26: lrc = launch(sym_task_kernel_f32<2, 6>); break;
-            case 28: lrc = launch(sym_task_kernel_f32<2, 8>); break;
             case 44: lrc = launch(sym_task_kernel_f32<4, 4>); break;
-            case 134: lrc = launch(sym_task_kernel_f32<3, 4, true>); break;
-            case 124: lrc = launch(sym_task_kernel_f32<2, 4, true>); break;
-            case 144: lrc = launch(sym_task_kernel_f32<4, 4, true>); break;
-            case 133: lrc = launch(sym_task_kernel_f32<3, 3, true>); break;
-            case 136: lrc = launch(sym_task_kernel_f32<3, 6, true>); break;
-            case 126: lrc = launch(sym_task_kernel_f32<2, 6, true>); break;
-            case 128: lrc = launch(sym_task_kernel_f32<2, 8, true>); break;
-            case 34: lrc = launch(sym_task_kernel_f32<3, 4>); break;
-            default: lrc = launch(sym_task_kernel_f32<3, 4, true>); break;   // 1067 G/s at C5
+            default: lrc = launch(sym_task_kernel_f32<3, 4>); break;
         }
     } else switch (variant) {
         case 41: lrc = launch(sym_task_kernel<4, 1>); break;

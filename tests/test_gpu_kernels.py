@@ -223,10 +223,13 @@ def test_symmetric_task_shards_sum_to_single_gpu(cuda, world):
     assert rel(total.cpu().numpy(), one.cpu().numpy()) < 1e-14
 
 
-def test_symmetric_fp32c_variant(cuda):
-    """FP32-compute / FP64-accumulate symmetric evaluation within 1e-5 of FP64."""
+@pytest.mark.parametrize("nf,n", [(200, 64), (333, 32), (401, 24)])
+def test_symmetric_fp32c_variant(cuda, nf, n):
+    """FP32-compute / FP64-accumulate symmetric evaluation within 1e-5 of FP64
+    (slab-relative FP32 positions); the sizes give partial units, padding i
+    lanes and j slabs, and fibers that straddle slabs."""
     from paper_1602_05650_b200._native import SF_MODE_FP32C, SF_MODE_FP64
-    cl, F = _cloud_operator_inputs(200, 64)
+    cl, F = _cloud_operator_inputs(nf, n)
     a, _ = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP64).apply(F, self_terms=False)
     op32 = FiberHIOperator(cl.X, cl.eps, mode=SF_MODE_FP32C)
     assert op32.symmetric
@@ -235,6 +238,17 @@ def test_symmetric_fp32c_variant(cuda):
     assert torch_equal(b, c)
     e = rel(b.cpu().numpy(), a.cpu().numpy())
     assert e < 1e-5, e
+
+
+def test_symmetric_fp32c_counts_coincident_pairs(cuda):
+    from paper_1602_05650_b200._native import SF_MODE_FP32C
+    cl, F = _cloud_operator_inputs(160, 64)
+    X = cl.X.copy()
+    X[7, 10] = X[90, 33]
+    op = FiberHIOperator(X, cl.eps, mode=SF_MODE_FP32C)
+    u, _ = op.apply(F, self_terms=False)
+    assert int(op.bad.item()) == 2
+    assert np.isfinite(u.cpu().numpy()).all()
 
 
 def torch_equal(x, y):
