@@ -42,8 +42,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
-    ap.add_argument("--step-config", default="c2,c3,c4,c5,c5:fp32c",
-                    help="implicit-step workloads, comma separated ('' to skip)")
+    ap.add_argument("--step-config", default="c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
+                    help="implicit-step workloads, comma separated, each with optional "
+                         "':fp32c' / ':body' ('+'-joined) options ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
     ap.add_argument("--big-step-count", type=int, default=1,
                     help="timed steps of c3/c4/c5 (2 s / 8 s / 38 s each on one GPU)")
@@ -175,8 +176,10 @@ def measure_steps(config, count, comm=None, warm=True):
     import torch
 
     from paper_1602_05650_b200 import configs, solver
-    config, _, precision = config.partition(":")
-    precision = precision or "fp64"
+    config, _, opts = config.partition(":")
+    opts = set(opts.split("+")) if opts else set()
+    precision = "fp32c" if "fp32c" in opts else "fp64"
+    body = "body" in opts          # body-coupled preconditioner (not in the reference)
     if config == "c2":
         st = configs.aster(n_fibers=1024)
         dt, tol = 1e-3, 1e-10
@@ -194,9 +197,12 @@ def measure_steps(config, count, comm=None, warm=True):
     if comm is None:
         def one(st):
             return solver.backward_euler_step(st, dt, params, return_info=True,
-                                              precision=precision)
+                                              precision=precision, body_coupling=body)
     else:
         from paper_1602_05650_b200 import dsolver
+
+        if body:
+            raise ValueError("the body-coupled preconditioner is single-GPU only")
 
         def one(st):
             return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True,
@@ -221,7 +227,10 @@ def measure_steps(config, count, comm=None, warm=True):
         t = torch.tensor(times, dtype=torch.float64, device="cuda")
         comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
         times = t.tolist()
-    return {"config": desc, "precision": precision, "dt": dt, "gmres_tol": tol, "steps": count,
+    return {"config": desc, "precision": precision,
+            "preconditioner": ("body-coupled (not in the reference)" if body
+                               else "block Jacobi (reference)"),
+            "dt": dt, "gmres_tol": tol, "steps": count,
             "ranks": 1 if comm is None else comm.world,
             "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
             "gmres_iterations": iters,
@@ -373,7 +382,10 @@ def run_ours(args, rank, world, local_rank):
     if args.step_config:
         from paper_1602_05650_b200.dsolver import TorchComm
         comm = TorchComm() if world > 1 else None
-        for k, cfg in enumerate(c for c in args.step_config.split(",") if c):
+        cfgs = [c for c in args.step_config.split(",") if c]
+        if comm is not None:           # the body-coupled preconditioner is single-GPU only
+            cfgs = [c for c in cfgs if "body" not in c.partition(":")[2]]
+        for k, cfg in enumerate(cfgs):
             big = cfg.split(":")[0] in ("c3", "c4", "c5")
             try:
                 steps.append(measure_steps(cfg, args.big_step_count if big else args.step_count,

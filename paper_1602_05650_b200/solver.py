@@ -251,6 +251,7 @@ class BlockOperator:
         self._wr_k = torch.empty((max(np_, 1), 6), **f64) if len(self.batches) > 1 else None
         self._ubar = torch.empty((c.n_targets, 3), **f64)
         self._work = torch.empty(16, **f64)
+        self._pcache = None
         self.matvecs = 0
 
     @property
@@ -313,6 +314,84 @@ class BlockOperator:
         self.matvecs += 1
         return out
 
+    def particle_rows_device(self, u, out=None):
+        """Rows of the particle blocks [U omega q1 per particle] driven by the
+        FIBER unknowns of u alone (its surface entries are ignored): the
+        fibers' attachment wrenches, their wrench flow and the fibers'
+        velocity at the particle nodes (pair sums, near corrections,
+        completion flows).  This is A[particle rows, fiber columns] @ u, the
+        coupling block of the body-coupled preconditioner; it evaluates only
+        the particle targets (a target-ranged InteractionCache), not the
+        fiber x fiber sum."""
+        import torch
+        st = _stream()
+        pend = self.layout.q1[-1].stop
+        if out is None:
+            out = torch.empty(pend, dtype=torch.float64, device=self.device)
+        if self._pcache is None:
+            npn = sum(s["n"] for s in self.surf if s["kind"] == 0)
+            self._pcache = InteractionCache(self.state, mode=self.cache.mode,
+                                            target_range=(0, npn))
+            nss = sum(s["n"] for s in self.surf)
+            self._pzero_q = torch.zeros((max(nss, 1), 3), dtype=torch.float64, device=self.device)
+            self._pzero_u = torch.zeros(6, dtype=torch.float64, device=self.device)
+            self._pubar = torch.empty((npn, 3), dtype=torch.float64, device=self.device)
+        pc = self._pcache
+        for b in self.batches:
+            _native.call("sf_fiber_forces", ctypes.byref(b.sys), _ptr(u), 0, _ptr(self._f), st)
+        for k, b in enumerate(self.batches):
+            _native.call("sf_particle_wrenches", ctypes.byref(b.sys), _ptr(u), None, 0,
+                         _ptr(self._wf), _ptr(self._wr if k == 0 else self._wr_k), st)
+            if k:
+                self._wr.add_(self._wr_k)
+        q = self._pzero_q[:sum(s["n"] for s in self.surf)] if self.surf else None
+        ubar = pc.apply(self._f, q, self._wr[:self.np], out=self._pubar, check=False)
+        out.zero_()
+        for s in self.surf:
+            if s["kind"] != 0:
+                continue
+            rows = out[s["sl"]]
+            _native.call("sf_wrench_flow", _ptr(s["nodes"]), s["n"], _ptr(s["center"]),
+                         _ptr(self._wr[s["pi"]]), self.mu, _ptr(rows), st)
+            _native.call("sf_surface_rows", 0, _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                         s["n"], _ptr(s["center"]), s["area"], _ptr(self._pzero_q[:s["n"]]),
+                         _ptr(ubar[pc.particle_slices[s["pi"]]]), _ptr(self._pzero_u), self.mu,
+                         _ptr(self._work), _ptr(rows), _ptr(out[s["uom"]:s["uom"] + 6]), st)
+        return out
+
+    def particle_block_matrix(self):
+        """Dense A[particle rows, particle columns] (own-particle terms; the
+        particles' mutual coupling through the fluid is left out), assembled
+        on the device from the row definitions (solver.py:332-346):
+        U - <q>/mu, omega - <arm x q>/mu, and the on-surface double layer of
+        q1 (body.second_kind_matrix without the jump) - (U + omega x arm)."""
+        import torch
+        pend = self.layout.q1[-1].stop
+        f64 = dict(dtype=torch.float64, device=self.device)
+        B = torch.zeros((pend, pend), **f64)
+        eye = torch.eye(3, **f64)
+        for s in self.surf:
+            if s["kind"] != 0:
+                continue
+            a, n = s["uom"], s["n"]
+            q0 = a + 6
+            arm = s["nodes"] - s["center"]
+            cross = torch.zeros((n, 3, 3), **f64)          # [arm]_x v = arm x v
+            cross[:, 0, 1], cross[:, 0, 2] = -arm[:, 2], arm[:, 1]
+            cross[:, 1, 0], cross[:, 1, 2] = arm[:, 2], -arm[:, 0]
+            cross[:, 2, 0], cross[:, 2, 1] = -arm[:, 1], arm[:, 0]
+            wj = s["w"] / (s["area"] * self.mu)
+            B[a:a + 3, a:a + 3] = eye
+            B[a + 3:a + 6, a + 3:a + 6] = eye
+            B[a:a + 3, q0:q0 + 3 * n] = -(wj[:, None, None] * eye).permute(1, 0, 2).reshape(3, 3 * n)
+            B[a + 3:a + 6, q0:q0 + 3 * n] = -(wj[:, None, None] * cross).permute(1, 0, 2).reshape(
+                3, 3 * n)
+            B[q0:q0 + 3 * n, a:a + 3] = -eye.repeat(n, 1)
+            B[q0:q0 + 3 * n, a + 3:a + 6] = cross.reshape(3 * n, 3)
+            B[q0:q0 + 3 * n, q0:q0 + 3 * n] = _double_layer_matrix(s["nodes"], s["nrm"], s["w"],
+                                                                   self.mu)
+        return B
+
     def _to_dev(self, u):
         import torch
         return torch.as_tensor(u, dtype=torch.float64, device=self.device).contiguous()
@@ -345,6 +424,26 @@ class BlockOperator:
         return A
 
 
+def _double_layer_matrix(x, n, w, mu):
+    """Dense matrix of double_layer_onsurface (body.py:254-262: the
+    subtracted stresslet sum, kernels.py:216-249): off-diagonal 3x3 blocks
+    pref w_j (n_j . r) r r^T / r^5, diagonal blocks minus their row sums
+    (body.second_kind_matrix with interior=False)."""
+    import torch
+    N = x.shape[0]
+    pref = -3.0 / (4.0 * math.pi * mu)
+    r = x[:, None, :] - x[None, :, :]
+    d2 = (r * r).sum(dim=2)
+    d2.fill_diagonal_(1.0)
+    scal = pref * (r * n[None, :, :]).sum(dim=2) / (d2 * d2 * torch.sqrt(d2)) * w[None, :]
+    idx = torch.arange(N, device=x.device)
+    scal[idx, idx] = 0.0
+    blocks = scal[:, :, None, None] * r[:, :, :, None] * r[:, :, None, :]
+    rowsum = blocks.sum(dim=1)
+    blocks[idx, idx] = -rowsum
+    return blocks.permute(0, 2, 1, 3).reshape(3 * N, 3 * N)
+
+
 def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implicit_coupling=True,
                            precision="fp64"):
     op = BlockOperator(state, dt, mu=mu, backend=backend, cache=cache,
@@ -355,9 +454,23 @@ def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implici
 class Preconditioner:
     """Block Jacobi: equilibrated exact fiber-block inverses, diagonal on
     surface rows (solver.py:375-429), factored and applied on the device
-    (one batch of block factors per Chebyshev order class)."""
+    (one batch of block factors per Chebyshev order class).
 
-    def __init__(self, op):
+    body_coupling=True (not in the reference; off by default) additionally
+    inverts, exactly, the rigid particles' own blocks [U omega q1] together
+    with their coupling to the fibers: the particle rows' dependence on every
+    fiber unknown (attachment wrenches, wrench flow, fiber velocity at the
+    particle nodes) and the fiber rows' dependence on U and omega (clamped
+    ends).  Only the fiber <-> fiber and periphery couplings stay outside.
+    Solved by a Schur complement on the particle unknowns:
+        W = D^-1 A[f, U omega],  S = A[p, p] - A[p, f] W,
+        z_p = S^-1 (v_p - A[p, f] D^-1 v_f),  z_f = D^-1 v_f - W z_(U omega).
+    Per apply: the block solves, one particle-rows evaluation
+    (BlockOperator.particle_rows_device) and one dense triangular solve.  It
+    targets asters, where GMRES with block Jacobi needs 175 (C2) to 480 (C4)
+    iterations; the solution is the same to the GMRES tolerance."""
+
+    def __init__(self, op, body_coupling=False):
         import torch
         self.layout = op.layout
         self.device = op.device
@@ -420,8 +533,52 @@ class Preconditioner:
         if bool((diag == 0).any()):
             raise FactorizationError("zero diagonal entry in a surface block")
         self.diag = diag
+        self.coupled = None
+        if body_coupling and op.np and op.nf:
+            self._setup_body_coupling(op)
+
+    def _setup_body_coupling(self, op):
+        import torch
+        lay = op.layout
+        n, fo = lay.size, lay.fib_off
+        pend = lay.q1[-1].stop
+        f64 = dict(dtype=torch.float64, device=self.device)
+        cols = [k for i in range(op.np) for k in range(lay.U[i].start, lay.U[i].start + 6)]
+        e = torch.zeros(n, **f64)
+        W = torch.empty((n - fo, len(cols)), **f64)
+        v = torch.zeros(n, **f64)
+        for k, j in enumerate(cols):
+            e[j] = 1.0
+            col = op.rows_device(e, False)       # fiber rows of the U / omega columns
+            e[j] = 0.0
+            v[fo:] = col[fo:]
+            W[:, k] = self._block_jacobi(v)[fo:]
+        S = op.particle_block_matrix()
+        t = torch.zeros(n, **f64)
+        for k, j in enumerate(cols):
+            t[fo:] = W[:, k]
+            S[:, j] -= op.particle_rows_device(t)
+        if not bool(torch.isfinite(S).all()):
+            raise FactorizationError("particle Schur complement is not finite")
+        LU, piv, info = torch.linalg.lu_factor_ex(S)
+        if int(info.item()) != 0:
+            raise FactorizationError("particle Schur complement is singular")
+        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, LU=LU, piv=piv,
+                            cols=torch.as_tensor(cols, device=self.device))
 
     def apply_device(self, v, out=None):
+        out = self._block_jacobi(v, out)
+        cp = self.coupled
+        if cp is not None:
+            import torch
+            pend, fo = cp["pend"], cp["fo"]
+            r = v[:pend] - cp["op"].particle_rows_device(out)
+            zb = torch.linalg.lu_solve(cp["LU"], cp["piv"], r[:, None])[:, 0]
+            out[:pend] = zb
+            out[fo:] -= cp["W"] @ zb[cp["cols"]]
+        return out
+
+    def _block_jacobi(self, v, out=None):
         import torch
         if out is None:
             out = torch.empty_like(v)
@@ -608,9 +765,11 @@ def _rotation_is_representable(part, omega, dt):
 
 
 def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=None,
-                        implicit_coupling=True, return_info=False, precision="fp64"):
+                        implicit_coupling=True, return_info=False, precision="fp64",
+                        body_coupling=False):
     """Advance the state by one implicit step on the device, halving dt on
-    nonconvergence (solver.py:528-592)."""
+    nonconvergence (solver.py:528-592).  body_coupling=True selects the
+    body-coupled preconditioner (see Preconditioner; not in the reference)."""
     from . import fiber as fibers_
     if dt <= 0:
         raise ConfigurationError("time step must be positive")
@@ -621,7 +780,7 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
     while True:
         op, rhs = assemble_step_operator(state, attempt, mu=mu, backend=backend, cache=cache,
                                          implicit_coupling=implicit_coupling)
-        prec = Preconditioner(op)
+        prec = Preconditioner(op, body_coupling=body_coupling)
         try:
             sol, iters, history = gmres_solve(op, prec, rhs, params)
             break
