@@ -314,6 +314,22 @@ class BlockOperator:
         self.matvecs += 1
         return out
 
+    def fiber_rows_local_device(self, u, out):
+        """Fiber rows of A u without the complementary velocity (ubar = 0):
+        each fiber's self terms, elastic operators and boundary rows,
+        including the clamped ends' dependence on the particle's U, omega.
+        Writes the fiber entries of out."""
+        import torch
+        c = self.cache
+        npts = c.fiber_slice.stop - c.fiber_slice.start
+        if getattr(self, "_zero_ubar", None) is None or self._zero_ubar.shape[0] != npts:
+            self._zero_ubar = torch.zeros((max(npts, 1), 3), dtype=torch.float64,
+                                          device=self.device)
+        for b in self.batches:
+            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), _ptr(self._zero_ubar), 0,
+                         _ptr(out), _stream())
+        return out
+
     def particle_rows_device(self, u, out=None):
         """Rows of the particle blocks [U omega q1 per particle] driven by the
         FIBER unknowns of u alone (its surface entries are ignored): the
@@ -466,7 +482,7 @@ class Preconditioner:
         W = D^-1 A[f, U omega],  S = A[p, p] - A[p, f] W,
         z_p = S^-1 (v_p - A[p, f] D^-1 v_f),  z_f = D^-1 v_f - W z_(U omega).
     Per apply: the block solves, one particle-rows evaluation
-    (BlockOperator.particle_rows_device) and one dense triangular solve.  It
+    (BlockOperator.particle_rows_device) and one GEMV with S^-1.  It
     targets asters, where GMRES with block Jacobi needs 175 (C2) to 480 (C4)
     iterations; the solution is the same to the GMRES tolerance."""
 
@@ -548,10 +564,11 @@ class Preconditioner:
         W = torch.empty((n - fo, len(cols)), **f64)
         v = torch.zeros(n, **f64)
         for k, j in enumerate(cols):
+            # fiber rows of the U / omega columns: only the clamped ends see
+            # them, and U, omega are no flow sources, so ubar = 0 is exact
             e[j] = 1.0
-            col = op.rows_device(e, False)       # fiber rows of the U / omega columns
+            op.fiber_rows_local_device(e, v)
             e[j] = 0.0
-            v[fo:] = col[fo:]
             W[:, k] = self._block_jacobi(v)[fo:]
         S = op.particle_block_matrix()
         t = torch.zeros(n, **f64)
@@ -560,10 +577,12 @@ class Preconditioner:
             S[:, j] -= op.particle_rows_device(t)
         if not bool(torch.isfinite(S).all()):
             raise FactorizationError("particle Schur complement is not finite")
-        LU, piv, info = torch.linalg.lu_factor_ex(S)
-        if int(info.item()) != 0:
+        # explicit inverse: one GEMV per apply (a single-RHS library
+        # triangular solve of this size measured ~0.8 ms, the GEMV ~20 us)
+        Sinv, info = torch.linalg.inv_ex(S)
+        if int(info.item()) != 0 or not bool(torch.isfinite(Sinv).all()):
             raise FactorizationError("particle Schur complement is singular")
-        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, LU=LU, piv=piv,
+        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, Sinv=Sinv,
                             cols=torch.as_tensor(cols, device=self.device))
 
     def apply_device(self, v, out=None):
@@ -573,7 +592,7 @@ class Preconditioner:
             import torch
             pend, fo = cp["pend"], cp["fo"]
             r = v[:pend] - cp["op"].particle_rows_device(out)
-            zb = torch.linalg.lu_solve(cp["LU"], cp["piv"], r[:, None])[:, 0]
+            zb = cp["Sinv"] @ r
             out[:pend] = zb
             out[fo:] -= cp["W"] @ zb[cp["cols"]]
         return out
