@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kCrossThreads, 2) cross_task_kernel(CrossArgs 
     const int ng = (int)min((int64_t)A.MA, A.NA - g0), nh = (int)min((int64_t)A.MB, A.NB - h0);
     const int nslab = (nh + 31) / 32;
     for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();   // zero-fill (any warp) before the owning warp's first +=
     int nb_a = 0, nb_b = 0;
     for (int ib = 0; ib < ng; ib += kI) {
         CrossA pi[TBI];

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
     const int nslab = (nh + 31) / 32;
     if (both)
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();   // zero-fill (any warp) before the owning warp's first +=
     for (int ib = 0; ib < ng; ib += kI) {
         DlNode pi[TBI];
         double ui[TBI][3];

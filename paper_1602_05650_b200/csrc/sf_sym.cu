@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     const int nslab = (nh + 31) / 32;
     if (both)
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();   // zero-fill (any warp) before the owning warp's first +=
     int nb = 0;
     for (int ib = 0; ib < ng; ib += kI) {
         PData pi[TBI];
@@ -577,6 +578,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     const int nslab = (nh + 31) / 32;
     if (both)
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();   // zero-fill (any warp) before the owning warp's first +=
     int nb = 0;
     for (int ib = 0; ib < ng; ib += kI) {
         PDataF pi[TBI];
