@@ -570,20 +570,20 @@ class InteractionCache:
         self._check_surface_overlaps()
         _lap("overlap checks")
         # near maps: fibers on the device (default) or the host restatement
-        self.near_fiber = []
+        self._near_fiber_list = []
         self._near_dev = None
         if near and nf:
             try:
                 if near == "host":
-                    self.near_fiber = nearfield.find_fiber_pairs(
+                    self._near_fiber_list = nearfield.find_fiber_pairs(
                         state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
                 elif self.uniform:
                     t, l, W = nearfield.device_fiber_pairs(self.geo, self.eps, self.trg, self.tgrp,
                                                            state.mu, include_doublet)
                     self._near_dev = (t, l, W)
-                    self.near_fiber = list(zip(t.tolist(), l.tolist(), W))
+                    self._near_fiber_list = None      # built on first access (near_fiber)
                 else:
-                    self.near_fiber = self._class_near_pairs(state.mu, include_doublet)
+                    self._near_fiber_list = self._class_near_pairs(state.mu, include_doublet)
             except InsideFiberError as err:
                 raise OverlapError(f"target node overlaps a fiber: {err}") from err
         _lap("near fiber maps")
@@ -604,6 +604,16 @@ class InteractionCache:
 
     # -- the reference's host-side attributes (system.py:536-557), read back
     #    from the device layout on demand --------------------------------------
+    @property
+    def near_fiber(self):
+        """[(target, fiber, W (3, 3n))] in the reference's order
+        (system.py:564-599); device-built maps are listed on first access
+        (the step itself uses the device arrays directly)."""
+        if self._near_fiber_list is None:
+            t, l, W = self._near_dev
+            self._near_fiber_list = list(zip(t.tolist(), l.tolist(), W))
+        return self._near_fiber_list
+
     @property
     def fiber_sources(self):
         return self.fsrc.cpu().numpy()
@@ -666,45 +676,61 @@ class InteractionCache:
     def _build_near_map(self):
         """CSR by target of every correction map, fiber entries before surface
         entries for a target (the reference applies the fiber list first,
-        system.py:702-707).  x = [fiber forces | surface densities], flattened."""
+        system.py:702-707).  x = [fiber forces | surface densities], flattened.
+        Map matrices stay where they were built (fiber maps in one device
+        block, then the surface maps); entries address them by offset."""
         import torch
         self.near_nrows = 0
         self.near_tensors = {}
         nfs3 = 3 * int(self.node_counts.sum())
-        nfib = len(self.near_fiber)
-        t = np.array([e[0] for e in self.near_fiber] + [e[0] for e in self.near_surface],
-                     dtype=np.int64)
-        if t.size == 0:
-            return
-        xo = np.array([3 * self.pt_off[e[1]] for e in self.near_fiber]
-                      + [nfs3 + 3 * self.surface_offsets[e[1]] for e in self.near_surface],
-                      dtype=np.int64)
-        xl = np.array([3 * self.node_counts[e[1]] for e in self.near_fiber]
-                      + [3 * self.surfaces[e[1]][0].n_nodes for e in self.near_surface],
-                      dtype=np.int64)
-        order = np.argsort(t, kind="stable")
         dev = dict(device=self.device)
         f64 = dict(dtype=torch.float64, **dev)
-        if self._near_dev is not None and not self.near_surface:
-            Wall = self._near_dev[2][torch.as_tensor(order, **dev)].reshape(-1)
-            wo = np.arange(t.size, dtype=np.int64) * 9 * self.n_nodes
+        blocks, wo_parts = [], []
+        if self._near_dev is not None:
+            t_d, l_d, W_d = self._near_dev
+            tf = np.asarray(t_d.cpu().numpy() if torch.is_tensor(t_d) else t_d, dtype=np.int64)
+            lf = np.asarray(l_d.cpu().numpy() if torch.is_tensor(l_d) else l_d, dtype=np.int64)
+            if tf.size:
+                per = int(W_d[0].numel())
+                blocks.append(W_d.reshape(-1))
+                wo_parts.append(np.arange(tf.size, dtype=np.int64) * per)
         else:
-            pieces = []
-            for i in order:
-                W = (self.near_fiber[i][2] if i < nfib else self.near_surface[i - nfib][2])
-                pieces.append(torch.as_tensor(W, **f64).reshape(-1))
+            nearf = self._near_fiber_list
+            tf = np.array([e[0] for e in nearf], dtype=np.int64)
+            lf = np.array([e[1] for e in nearf], dtype=np.int64)
+            pieces = [torch.as_tensor(e[2], **f64).reshape(-1) for e in nearf]
+            if pieces:
+                sizes = np.array([x.numel() for x in pieces], dtype=np.int64)
+                wo_parts.append(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64))
+                blocks.append(torch.cat(pieces))
+        base = int(sum(b.numel() for b in blocks))
+        ns = self.near_surface
+        ts = np.array([e[0] for e in ns], dtype=np.int64)
+        ls = np.array([e[1] for e in ns], dtype=np.int64)
+        if ns:
+            pieces = [torch.as_tensor(e[2], **f64).reshape(-1) for e in ns]
             sizes = np.array([x.numel() for x in pieces], dtype=np.int64)
-            wo = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
-            Wall = torch.cat(pieces)
+            wo_parts.append(base + np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64))
+            blocks.append(torch.cat(pieces))
+        t = np.concatenate([tf, ts])
+        if t.size == 0:
+            return
+        s_off = np.asarray(self.surface_offsets, dtype=np.int64) if ns else np.zeros(0, np.int64)
+        s_n = (np.array([m.n_nodes for m, _, _ in self.surfaces], dtype=np.int64) if ns
+               else np.zeros(0, np.int64))
+        xo = np.concatenate([3 * self.pt_off[lf], nfs3 + 3 * s_off[ls] if ns else ls])
+        xl = np.concatenate([3 * self.node_counts[lf], 3 * s_n[ls] if ns else ls])
+        wo = np.concatenate(wo_parts)
+        order = np.argsort(t, kind="stable")
         t = t[order]
         rows, starts = np.unique(t, return_index=True)
         self.near_tensors = dict(
             row_ptr=torch.as_tensor(np.append(starts, t.size).astype(np.int64), **dev),
             rows=torch.as_tensor(rows, **dev),
-            w_off=torch.as_tensor(wo, **dev),
-            x_off=torch.as_tensor(xo[order], **dev),
-            x_len=torch.as_tensor(xl[order], **dev),
-            W=Wall.contiguous())
+            w_off=torch.as_tensor(wo[order], **dev),
+            x_off=torch.as_tensor(xo[order].astype(np.int64), **dev),
+            x_len=torch.as_tensor(xl[order].astype(np.int64), **dev),
+            W=(torch.cat(blocks) if len(blocks) > 1 else blocks[0]).contiguous())
         self.near_nrows = rows.size
 
     def _layout(self):
