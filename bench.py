@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
     ap.add_argument("--step-config", default="c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated, each with optional "
-                         "':fp32c' / ':body' ('+'-joined) options ('' to skip)")
+                         "':fp32c' / ':body' / ':warm' ('+'-joined) options ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
     ap.add_argument("--big-step-count", type=int, default=1,
                     help="timed steps of c3/c4/c5 (2 s / 8 s / 38 s each on one GPU)")
@@ -180,6 +180,7 @@ def measure_steps(config, count, comm=None, warm=True):
     opts = set(opts.split("+")) if opts else set()
     precision = "fp32c" if "fp32c" in opts else "fp64"
     body = "body" in opts          # body-coupled preconditioner (not in the reference)
+    warm = "warm" in opts          # GMRES warm start from the current state (not in the reference)
     if config == "c2":
         st = configs.aster(n_fibers=1024)
         dt, tol = 1e-3, 1e-10
@@ -197,12 +198,13 @@ def measure_steps(config, count, comm=None, warm=True):
     if comm is None:
         def one(st):
             return solver.backward_euler_step(st, dt, params, return_info=True,
-                                              precision=precision, body_coupling=body)
+                                              precision=precision, body_coupling=body,
+                                              warm_start=warm)
     else:
         from paper_1602_05650_b200 import dsolver
 
-        if body:
-            raise ValueError("the body-coupled preconditioner is single-GPU only")
+        if body or warm:
+            raise ValueError("body coupling and warm start are single-GPU options")
 
         def one(st):
             return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True,
@@ -230,6 +232,8 @@ def measure_steps(config, count, comm=None, warm=True):
     return {"config": desc, "precision": precision,
             "preconditioner": ("body-coupled (not in the reference)" if body
                                else "block Jacobi (reference)"),
+            "initial_guess": ("current state (not in the reference)" if warm
+                              else "zero (reference)"),
             "dt": dt, "gmres_tol": tol, "steps": count,
             "ranks": 1 if comm is None else comm.world,
             "steps_per_s": count / sum(times), "ms_per_step": 1e3 * sum(times) / count,
@@ -384,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
         comm = TorchComm() if world > 1 else None
         cfgs = [c for c in args.step_config.split(",") if c]
         if comm is not None:           # the body-coupled preconditioner is single-GPU only
-            cfgs = [c for c in cfgs if "body" not in c.partition(":")[2]]
+            cfgs = [c for c in cfgs if not ({"body", "warm"} & set(c.partition(":")[2].split("+")))]
         for k, cfg in enumerate(cfgs):
             big = cfg.split(":")[0] in ("c3", "c4", "c5")
             try:
