@@ -259,7 +259,16 @@ def run_ours(args, rank, world, local_rank):
     mode = _native.SF_MODE_FP64 if args.mode == "fp64" else _native.SF_MODE_FP32C
     cloud = configs.make(args.config, seed=args.seed)
     f_all = configs.forces(cloud, seed=args.seed + 1)
-    op = FiberHIOperator(cloud.X, cloud.eps, device=dev, mode=mode, shard=(rank, world))
+    # the reference's state and interaction cache for this cloud: its near-field
+    # maps (system.py:564-599; C5 has 2 targets inside another fiber's near
+    # shell) complete the operator, and it serves the reference-API e2e below
+    from paper_1602_05650_b200 import system as sysm
+    from paper_1602_05650_b200.fiber import Fiber
+    st_api = sysm.SystemState([Fiber(X, eps=cloud.eps, E=cloud.E) for X in cloud.X])
+    cache = sysm.InteractionCache(st_api, device=dev)
+    near = cache.near_fiber
+    op = FiberHIOperator(cloud.X, cloud.eps, device=dev, mode=mode, shard=(rank, world),
+                         near=near)
     sop = ShardedHIOperator(op)
     f_local = torch.as_tensor(f_all[op.f0:op.f0 + op.nown], device=dev).contiguous()
     u_nl = torch.empty((op.Nown, 3), dtype=torch.float64, device=dev)
@@ -354,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
     variant = None
     if args.mode == "fp64" and not args.no_variant:
         op32 = FiberHIOperator(cloud.X, cloud.eps, device=dev, mode=_native.SF_MODE_FP32C,
-                               shard=(rank, world))
+                               shard=(rank, world), near=near)
         sop32 = ShardedHIOperator(op32)
         u32 = torch.empty_like(u_nl)
         for _ in range(2):
@@ -381,6 +390,32 @@ def run_ours(args, rank, world, local_rank):
                    "rel_l2_vs_fp64": float((err[0] / err[1]).sqrt().item()),
                    "tolerance": 1e-5}
         del op32, sop32, u32
+
+    # ---- e2e through the reference's own operator signature (world 1):
+    # system.complementary_velocities(state, fiber_forces=[per-fiber numpy
+    # arrays], cache=cache) -> per-fiber numpy velocities (system.py:623-709)
+    ref_api = None
+    if world == 1 and args.mode == "fp64":
+        f_list = [f_all[m] for m in range(cloud.n_fibers)]
+        res = sysm.complementary_velocities(st_api, fiber_forces=f_list, cache=cache)
+        u_api = np.concatenate(res.fibers)
+        api_rel = float(np.linalg.norm(u_api - u_nl.cpu().numpy()) / np.linalg.norm(u_api))
+        t_api = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sysm.complementary_velocities(st_api, fiber_forces=f_list, cache=cache)
+            t_api.append(time.perf_counter() - t0)
+        ms_api = 1e3 * sum(t_api) / len(t_api)
+        ref_api = {"value": total_pairs / (ms_api * 1e-3), "unit": "pair-interactions/s",
+                   "ms_per_step": ms_api,
+                   "call": "system.complementary_velocities(state, fiber_forces=[16384 (64,3) "
+                           "numpy arrays], cache=InteractionCache(state)) -> per-fiber numpy "
+                           "velocities; the non-local part only (no self terms), host wall clock",
+                   "h2d_bytes_per_step": int(cloud.n_points * 3 * 8),
+                   "d2h_bytes_per_step": int(cloud.n_points * 3 * 8),
+                   "rel_diff_vs_operator_nonlocal": api_rel}
+    del cache, st_api
 
     steps = []
     if args.step_config:
@@ -414,7 +449,8 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if args.mode == "fp64" else "f32-compute/f64-accumulate",
             "data": "synthetic (seeded rejection-sampled perturbed fiber cloud, N(0,1) forces)",
-            "config": dict(workload_config(args, cloud, world), steps_per_s=1e3 / ms_step),
+            "config": dict(workload_config(args, cloud, world), steps_per_s=1e3 / ms_step,
+                           near_maps=len(near)),
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_flops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_flops, "traffic": traffic,
@@ -435,6 +471,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": args.steps * op.launches_per_apply,
             "clocks": clocks,
             "variant_fp32c": variant,
+            "e2e_reference_api": ref_api,
             "implicit_steps": steps,
         }
         print(json.dumps(lines), flush=True)

@@ -48,7 +48,8 @@ class NearMap:
             return
         t = np.array([e[0] for e in entries], dtype=np.int64)
         l = np.array([e[1] for e in entries], dtype=np.int64)
-        W = np.stack([np.asarray(e[2], dtype=float).reshape(3, -1) for e in entries])
+        W = np.stack([np.asarray(e[2].cpu() if torch.is_tensor(e[2]) else e[2],
+                                 dtype=float).reshape(3, -1) for e in entries])
         order = np.argsort(t, kind="stable")
         t, l, W = t[order], l[order], W[order]
         rows, starts = np.unique(t, return_index=True)

@@ -59,3 +59,27 @@ def test_full_size_operator_parity(cuda, big):
     lin = op.apply(Fd + 2.0 * G, self_terms=False)[0].cpu().numpy()
     ag = op.apply(G, self_terms=False)[0].cpu().numpy()
     assert rel(lin, a + 2.0 * ag) < 1e-12
+
+
+def test_full_size_reference_api_with_near_maps(cuda, big):
+    """complementary_velocities (the reference's signature, host arrays in and
+    out) at full size equals the batched operator given the same near maps;
+    rows with near maps are the oracle's pair sum plus W . f of the source
+    fiber (system.py:702-707)."""
+    import torch
+    from paper_1602_05650_b200 import system
+    from paper_1602_05650_b200.fiber import Fiber
+    name, cl, F = big
+    st = system.SystemState([Fiber(X, eps=cl.eps, E=cl.E) for X in cl.X])
+    cache = system.InteractionCache(st)
+    ua = np.concatenate(system.complementary_velocities(st, fiber_forces=list(F), cache=cache).fibers)
+    op = FiberHIOperator(cl.X, cl.eps, near=cache.near_fiber)
+    ub = op.apply(torch.as_tensor(F, device=cuda), self_terms=False)[0].cpu().numpy()
+    assert rel(ua, ub) < 1e-14
+    if cache.near_fiber:                      # C5: 2 targets inside a near shell
+        rows = np.array(sorted({t for t, _, _ in cache.near_fiber}))
+        corr = np.zeros((rows.size, 3))
+        for t, l, W in cache.near_fiber:
+            W = W.cpu().numpy() if torch.is_tensor(W) else np.asarray(W)
+            corr[np.searchsorted(rows, t)] += W.reshape(3, -1) @ F[l].reshape(-1)
+        assert rel(ua[rows], oracle_rows(cl, op, F, rows) + corr) < 1e-12
