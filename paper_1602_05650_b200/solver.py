@@ -467,6 +467,48 @@ def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implici
     return op, op.rhs_device()
 
 
+_PARTICLE_INV_CACHE = []      # [(key arrays, mu, device, inverse)], most recent first
+
+
+def _particle_block_inverse(op):
+    """A_pp^-1 (BlockOperator.particle_block_matrix, own-particle blocks) as
+    an explicit matrix: one GEMV per preconditioner apply (a single-RHS
+    library triangular solve of this size measured ~0.8 ms, the GEMV ~20 us).
+    A_pp depends only on each particle's nodes relative to its centre,
+    normals and weights, so the inverse is reused while the particles
+    translate (relative geometry equal to 1e-13 of its size)."""
+    import torch
+    key = [(np.asarray(p.mesh.nodes) - np.asarray(p.center), np.asarray(p.mesh.normals),
+            np.asarray(p.mesh.weights)) for p in op.state.particles]
+
+    def same(a, b):
+        if len(a) != len(b):
+            return False
+        for (r1, n1, w1), (r2, n2, w2) in zip(a, b):
+            if r1.shape != r2.shape:
+                return False
+            scale = max(1.0, float(np.abs(r1).max()))
+            if (np.abs(r1 - r2).max() > 1e-13 * scale or np.abs(n1 - n2).max() > 1e-13
+                    or np.abs(w1 - w2).max() > 1e-13 * float(np.abs(w1).max())):
+                return False
+        return True
+    for entry in _PARTICLE_INV_CACHE:
+        k, mu, dev, inv = entry
+        if mu == op.mu and dev == op.device and same(k, key):
+            _PARTICLE_INV_CACHE.remove(entry)
+            _PARTICLE_INV_CACHE.insert(0, entry)
+            return inv
+    A = op.particle_block_matrix()
+    if not bool(torch.isfinite(A).all()):
+        raise FactorizationError("particle block is not finite")
+    inv, info = torch.linalg.inv_ex(A)
+    if int(info.item()) != 0 or not bool(torch.isfinite(inv).all()):
+        raise FactorizationError("particle block is singular")
+    _PARTICLE_INV_CACHE.insert(0, (key, op.mu, op.device, inv))
+    del _PARTICLE_INV_CACHE[4:]
+    return inv
+
+
 class Preconditioner:
     """Block Jacobi: equilibrated exact fiber-block inverses, diagonal on
     surface rows (solver.py:375-429), factored and applied on the device
@@ -481,7 +523,10 @@ class Preconditioner:
     Solved by a Schur complement on the particle unknowns:
         W = D^-1 A[f, U omega],  S = A[p, p] - A[p, f] W,
         z_p = S^-1 (v_p - A[p, f] D^-1 v_f),  z_f = D^-1 v_f - W z_(U omega).
-    Per apply: the block solves, one particle-rows evaluation
+    S^-1 by Sherman-Morrison-Woodbury around A[p, p]^-1 (S differs from it
+    in the 6 U/omega columns per particle; A[p, p] is translation invariant,
+    so its inverse is cached across steps; S^-1 is then a rank-6 update of
+    it).  Per apply: the block solves, one particle-rows evaluation
     (BlockOperator.particle_rows_device) and one GEMV with S^-1.  It
     targets asters, where GMRES with block Jacobi needs 175 (C2) to 480 (C4)
     iterations; the solution is the same to the GMRES tolerance."""
@@ -570,20 +615,25 @@ class Preconditioner:
             op.fiber_rows_local_device(e, v)
             e[j] = 0.0
             W[:, k] = self._block_jacobi(v)[fo:]
-        S = op.particle_block_matrix()
+        # S = A_pp - Z E^T with Z = A_pf W and E the U/omega columns, inverted
+        # by Sherman-Morrison-Woodbury around A_pp^-1, which depends only on
+        # the particles' geometry relative to their centres (translation
+        # invariant), so it is computed once and reused while they translate
+        Ainv = _particle_block_inverse(op)
         t = torch.zeros(n, **f64)
-        for k, j in enumerate(cols):
+        Z = torch.empty((pend, len(cols)), **f64)
+        for k in range(len(cols)):
             t[fo:] = W[:, k]
-            S[:, j] -= op.particle_rows_device(t)
-        if not bool(torch.isfinite(S).all()):
-            raise FactorizationError("particle Schur complement is not finite")
-        # explicit inverse: one GEMV per apply (a single-RHS library
-        # triangular solve of this size measured ~0.8 ms, the GEMV ~20 us)
-        Sinv, info = torch.linalg.inv_ex(S)
-        if int(info.item()) != 0 or not bool(torch.isfinite(Sinv).all()):
+            Z[:, k] = op.particle_rows_device(t)
+        colt = torch.as_tensor(cols, device=self.device)
+        AZ = Ainv @ Z
+        C = torch.eye(len(cols), **f64) - AZ[colt]
+        Cinv, info = torch.linalg.inv_ex(C)
+        if int(info.item()) != 0 or not bool(torch.isfinite(Cinv).all()) or \
+                not bool(torch.isfinite(AZ).all()):
             raise FactorizationError("particle Schur complement is singular")
-        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, Sinv=Sinv,
-                            cols=torch.as_tensor(cols, device=self.device))
+        Sinv = torch.addmm(Ainv, AZ, Cinv @ Ainv[colt])      # rank-6np update
+        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, Sinv=Sinv, cols=colt)
 
     def apply_device(self, v, out=None):
         out = self._block_jacobi(v, out)

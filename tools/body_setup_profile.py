@@ -1,4 +1,4 @@
-"""Where does the body-coupled preconditioner's setup go? (C2 / C4)"""
+"""Where does the body-coupled preconditioner's setup and apply go? (C2 / C4)"""
 import os
 import sys
 import time
@@ -11,38 +11,27 @@ from paper_1602_05650_b200 import configs, solver  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 st = configs.aster(n_fibers=1024) if cfg == "c2" else configs.confined_aster()
 op, rhs = solver.assemble_step_operator(st, 1e-3)
-for rep in range(2):
+
+
+def timed(label, fn, reps=1):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    op._pcache = None
-    p0 = solver.Preconditioner(op)
+    for _ in range(reps):
+        r = fn()
     torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    p1 = solver.Preconditioner(op, body_coupling=True)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    B = op.particle_block_matrix()
-    torch.cuda.synchronize()
-    t3 = time.perf_counter()
-    op._pcache = None
-    y = torch.zeros(op.layout.size, dtype=torch.float64, device=op.device)
-    op.particle_rows_device(y)
-    torch.cuda.synchronize()
-    t4 = time.perf_counter()
-    op.particle_rows_device(y)
-    torch.cuda.synchronize()
-    t5 = time.perf_counter()
-    LU = torch.linalg.inv_ex(B)
-    torch.cuda.synchronize()
-    t6 = time.perf_counter()
-    v = torch.randn(op.layout.size, dtype=torch.float64, device=op.device)
-    p1.apply_device(v)
-    torch.cuda.synchronize()
-    t7 = time.perf_counter()
-    p0.apply_device(v)
-    torch.cuda.synchronize()
-    t8 = time.perf_counter()
-    print(f"{cfg} rep {rep}: block-Jacobi setup {1e3*(t1-t0):.1f} ms, coupled setup {1e3*(t2-t1):.1f} ms "
-          f"[particle block {1e3*(t3-t2):.1f}, particle cache+rows {1e3*(t4-t3):.1f}, rows {1e3*(t5-t4):.2f}, "
-          f"LU {1e3*(t6-t5):.1f}]; apply coupled {1e3*(t7-t6):.2f} ms vs bj {1e3*(t8-t7):.2f} ms",
-          flush=True)
+    print(f"{cfg} {label:44s} {1e3 * (time.perf_counter() - t0) / reps:8.2f} ms", flush=True)
+    return r
+
+
+p0 = timed("block-Jacobi setup", lambda: solver.Preconditioner(op))
+p1 = timed("coupled setup (cold particle inverse)", lambda: solver.Preconditioner(op, body_coupling=True))
+p1 = timed("coupled setup (cached particle inverse)", lambda: solver.Preconditioner(op, body_coupling=True), 3)
+v = torch.randn(op.layout.size, dtype=torch.float64, device=op.device)
+timed("apply block-Jacobi", lambda: p0.apply_device(v), 20)
+timed("apply coupled", lambda: p1.apply_device(v), 20)
+y = torch.zeros(op.layout.size, dtype=torch.float64, device=op.device)
+timed("particle_rows_device", lambda: op.particle_rows_device(y), 20)
+timed("matvec", lambda: op.rows_device(v, False), 10)
+x, it, _ = timed("gmres (coupled)", lambda: solver.gmres_solve(op, p1, rhs, solver.GmresParams(tolerance=1e-10)))
+print("iterations", it)
+timed("full step (coupled)", lambda: solver.backward_euler_step(st, 1e-3, solver.GmresParams(tolerance=1e-10), body_coupling=True), 3)
