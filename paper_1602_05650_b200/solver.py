@@ -342,8 +342,10 @@ class BlockOperator:
         import torch
         st = _stream()
         pend = self.layout.q1[-1].stop
-        if out is None:
-            out = torch.empty(pend, dtype=torch.float64, device=self.device)
+        if out is None:     # a reused buffer: callers consume it before the next call
+            if getattr(self, "_prow", None) is None:
+                self._prow = torch.empty(pend, dtype=torch.float64, device=self.device)
+            out = self._prow
         if self._pcache is None:
             npn = sum(s["n"] for s in self.surf if s["kind"] == 0)
             self._pcache = InteractionCache(self.state, mode=self.cache.mode,
@@ -633,7 +635,9 @@ class Preconditioner:
                 not bool(torch.isfinite(AZ).all()):
             raise FactorizationError("particle Schur complement is singular")
         Sinv = torch.addmm(Ainv, AZ, Cinv @ Ainv[colt])      # rank-6np update
-        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, Sinv=Sinv, cols=colt)
+        contiguous = cols == list(range(cols[0], cols[0] + len(cols)))
+        self.coupled = dict(op=op, pend=pend, fo=fo, W=W, Sinv=Sinv, cols=colt,
+                            cslice=slice(cols[0], cols[0] + len(cols)) if contiguous else None)
 
     def apply_device(self, v, out=None):
         out = self._block_jacobi(v, out)
@@ -641,10 +645,10 @@ class Preconditioner:
         if cp is not None:
             import torch
             pend, fo = cp["pend"], cp["fo"]
-            r = v[:pend] - cp["op"].particle_rows_device(out)
-            zb = cp["Sinv"] @ r
-            out[:pend] = zb
-            out[fo:] -= cp["W"] @ zb[cp["cols"]]
+            r = torch.sub(v[:pend], cp["op"].particle_rows_device(out))
+            zb = torch.mv(cp["Sinv"], r, out=out[:pend])
+            zc = zb[cp["cols"]] if cp["cslice"] is None else zb[cp["cslice"]]
+            out[fo:].addmv_(cp["W"], zc, alpha=-1.0)
         return out
 
     def _block_jacobi(self, v, out=None):

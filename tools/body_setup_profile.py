@@ -35,3 +35,11 @@ timed("matvec", lambda: op.rows_device(v, False), 10)
 x, it, _ = timed("gmres (coupled)", lambda: solver.gmres_solve(op, p1, rhs, solver.GmresParams(tolerance=1e-10)))
 print("iterations", it)
 timed("full step (coupled)", lambda: solver.backward_euler_step(st, 1e-3, solver.GmresParams(tolerance=1e-10), body_coupling=True), 3)
+cp = p1.coupled
+if cp is not None:
+    r = torch.randn(cp["pend"], dtype=torch.float64, device=op.device)
+    timed("  GEMV S^-1 (pend x pend)", lambda: torch.mv(cp["Sinv"], r), 50)
+    zc = torch.randn(cp["W"].shape[1], dtype=torch.float64, device=op.device)
+    tgt = torch.zeros(cp["W"].shape[0], dtype=torch.float64, device=op.device)
+    timed("  addmv W (fiber unknowns x 6)", lambda: tgt.addmv_(cp["W"], zc, alpha=-1.0), 50)
+    timed("  block-Jacobi only", lambda: p1._block_jacobi(v), 50)
