@@ -180,7 +180,7 @@ def measure_steps(config, count, comm=None, warm=True):
     opts = set(opts.split("+")) if opts else set()
     precision = "fp32c" if "fp32c" in opts else "fp64"
     body = "body" in opts          # body-coupled preconditioner (not in the reference)
-    warm = "warm" in opts          # GMRES warm start from the current state (not in the reference)
+    warm_start = "warm" in opts    # GMRES warm start from the current state (not in the reference)
     if config == "c2":
         st = configs.aster(n_fibers=1024)
         dt, tol = 1e-3, 1e-10
@@ -199,11 +199,11 @@ def measure_steps(config, count, comm=None, warm=True):
         def one(st):
             return solver.backward_euler_step(st, dt, params, return_info=True,
                                               precision=precision, body_coupling=body,
-                                              warm_start=warm)
+                                              warm_start=warm_start)
     else:
         from paper_1602_05650_b200 import dsolver
 
-        if body or warm:
+        if body or warm_start:
             raise ValueError("body coupling and warm start are single-GPU options")
 
         def one(st):
@@ -232,7 +232,7 @@ def measure_steps(config, count, comm=None, warm=True):
     return {"config": desc, "precision": precision,
             "preconditioner": ("body-coupled (not in the reference)" if body
                                else "block Jacobi (reference)"),
-            "initial_guess": ("current state (not in the reference)" if warm
+            "initial_guess": ("current state (not in the reference)" if warm_start
                               else "zero (reference)"),
             "dt": dt, "gmres_tol": tol, "steps": count,
             "ranks": 1 if comm is None else comm.world,
