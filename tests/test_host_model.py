@@ -145,3 +145,22 @@ def test_fiber_dense_operators_match_reference():
     assert np.array_equal(FX, g["FX"]) and np.array_equal(FT, g["FT"])
     assert np.array_equal(fib.mobility_matrix(float(g["mu"])), g["Mmat"])
     assert fib.grid.p == fib.p and fib.grid.D.shape == (fib.n_nodes, fib.n_nodes)
+
+
+def test_warm_start_vector_round_trips_through_the_layout():
+    """solver.warm_start_vector packs the state in StepLayout order
+    (solver.py:67-110): unpack returns the state's own arrays."""
+    from paper_1602_05650_b200 import configs, solver
+    st = configs.aster(n_fibers=6, p=15, mesh_res=(4, 4))
+    rng = np.random.default_rng(0)
+    part = st.particles[0]
+    part.U, part.omega = rng.standard_normal(3), rng.standard_normal(3)
+    part.q = rng.standard_normal(part.q.shape)
+    for f in st.fibers:
+        f.T = rng.standard_normal(f.T.shape)
+    lay = solver.StepLayout(st)
+    parts = lay.unpack(solver.warm_start_vector(st, lay))
+    assert np.array_equal(parts.U[0], part.U) and np.array_equal(parts.omega[0], part.omega)
+    assert np.array_equal(parts.q1[0], part.q)
+    for m, f in enumerate(st.fibers):
+        assert np.array_equal(parts.X[m], f.X) and np.array_equal(parts.T[m], f.T)
