@@ -965,22 +965,12 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
             default: lrc = launch(sym_task_kernel_f32<3, 4>); break;
         }
     } else switch (variant) {
-        case 41: lrc = launch(sym_task_kernel<4, 1>); break;
-        case 42: lrc = launch(sym_task_kernel<4, 2>); break;
-        case 22: lrc = launch(sym_task_kernel<2, 2>); break;
-        case 23: lrc = launch(sym_task_kernel<2, 3>); break;
-        case 33: lrc = launch(sym_task_kernel<3, 3>); break;
-        case 32: lrc = launch(sym_task_kernel<3, 2>); break;
-        case 25: lrc = launch(sym_task_kernel<2, 5>); break;
-        case 26: lrc = launch(sym_task_kernel<2, 6>); break;
-        case 16: lrc = launch(sym_task_kernel<1, 6>); break;
-        case 18: lrc = launch(sym_task_kernel<1, 8>); break;
+        // launch-shape sweep (tools/gpu_sym_sweep.sh, tools/gpu_sym_aster_sweep.sh):
+        // MINB*10 + i-per-lane (+100 prefetch, +200 prefetch + grouped pairs)
         case 24: lrc = launch(sym_task_kernel<2, 4>); break;
-        case 123: lrc = launch(sym_task_kernel<2, 3, true>); break;
         case 124: lrc = launch(sym_task_kernel<2, 4, true>); break;
         case 233: lrc = launch(sym_task_kernel<3, 3, true, true>); break;
         case 223: lrc = launch(sym_task_kernel<2, 3, true, true>); break;
-        case 225: lrc = launch(sym_task_kernel<2, 5, true, true>); break;
         case 232: lrc = launch(sym_task_kernel<3, 2, true, true>); break;
         default: lrc = launch(sym_task_kernel<2, 4, true, true>); break;   // 749 G/s at C5
     }
