@@ -96,8 +96,8 @@ int fiber_kdelta_build(const double *X, const double *s, const double *s_alpha,
     return check_launch("kdelta_build_kernel");
 }
 
-// u = M f + K f (fiber.py:244-258).  One CTA per fiber, warp per K row,
-// lanes stride the row (coalesced 256-byte reads), shuffle reduction.
+// u = M f + K f (fiber.py:244-258).  One CTA per fiber, a warp per 4 K rows,
+// lanes stride the rows (coalesced 256-byte reads), shuffle reductions.
 __global__ void self_apply_kernel(const double *__restrict__ K, const double *__restrict__ tang,
                                   const double *__restrict__ c_log, double c_two,
                                   const double *__restrict__ f, int n, int accumulate,
@@ -112,14 +112,25 @@ __global__ void self_apply_kernel(const double *__restrict__ K, const double *__
     const double *Tm = tang + (int64_t)ld * m;
     const double cl = c_log[m];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int r = warp; r < ld; r += nw) {
-        const double *row = Km ? Km + (int64_t)r * ld : nullptr;
-        double acc = 0.0;
+    // 4 rows per warp pass: 4 independent coalesced K loads per lane in flight
+    constexpr int RB = 4;
+    for (int r0 = warp * RB; r0 < ld; r0 += nw * RB) {
+        double accs[RB] = {0.0, 0.0, 0.0, 0.0};
         if (K) {   // K == nullptr: local mobility only
-            for (int c = lane; c < ld; c += 32) acc = fma(row[c], fs[c], acc);
-            acc = warp_sum(acc);
+            for (int c = lane; c < ld; c += 32) {
+                const double fc = fs[c];
+#pragma unroll
+                for (int q = 0; q < RB; ++q)
+                    if (r0 + q < ld) accs[q] = fma(Km[(int64_t)(r0 + q) * ld + c], fc, accs[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < RB; ++q) accs[q] = warp_sum(accs[q]);
         }
-        if (lane == 0) {
+        if (lane < RB && r0 + lane < ld) {
+            const int r = r0 + lane;
+            double acc = accs[0];
+#pragma unroll
+            for (int q = 1; q < RB; ++q) acc = lane == q ? accs[q] : acc;
             const int i = r / 3, a = r - 3 * (r / 3);
             const double tx = Tm[3 * i], ty = Tm[3 * i + 1], tz = Tm[3 * i + 2];
             const double fdt = fs[3 * i] * tx + fs[3 * i + 1] * ty + fs[3 * i + 2] * tz;
