@@ -262,14 +262,14 @@ __global__ void __launch_bounds__(kCrossThreads, 2) cross_task_kernel(CrossArgs 
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                A.partA[((int64_t)h * A.NA + g0 + ib + il) * 3 + c] = s;
+                __stcs(&A.partA[((int64_t)h * A.NA + g0 + ib + il) * 3 + c], s);
             }
         }
         __syncthreads();
     }
     __syncthreads();
     for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-        A.partB[((int64_t)g * A.NB + h0) * 3 + e] = jacc_s[e];
+        __stcs(&A.partB[((int64_t)g * A.NB + h0) * 3 + e], jacc_s[e]);
     if (A.bad_a) {
         nb_a = warp_sum_int(nb_a);
         nb_b = warp_sum_int(nb_b);

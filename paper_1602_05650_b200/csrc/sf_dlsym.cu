@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                A.part[((int64_t)h * A.N + g0 + ib + il) * 3 + c] = s;
+                __stcs(&A.part[((int64_t)h * A.N + g0 + ib + il) * 3 + c], s);
             }
         }
         __syncthreads();
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kDlThreads, 2) dl_task_kernel(DlArgs A) {
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            A.part[((int64_t)g * A.N + h0) * 3 + e] = jacc_s[e];
+            __stcs(&A.part[((int64_t)g * A.N + h0) * 3 + e], jacc_s[e]);
     }
 }
 

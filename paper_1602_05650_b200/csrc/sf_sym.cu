@@ -7,6 +7,10 @@
 // 14 + 2 x 12 = 38 FP64 instructions per unordered pair (19 per pair
 // interaction) instead of 2 x 26.
 //
+// Partial slots are written with streaming stores (st.global.cs): they are
+// read once, by the ordered reduce, and must not evict the source records
+// that every CTA re-reads from L2.
+//
 // Determinism without atomics: points are split into G units of M points
 // (M a multiple of the fiber size, so units align to fibers).  A task is an
 // unordered unit pair {g,h}; the CTA computes every (i in g, j in h) pair in
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c] = s;
+                __stcs(&a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c], s);
             }
         }
         __syncthreads();
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            a.part[((int64_t)g * a.N + h0) * 3 + e] = jacc_s[e];
+            __stcs(&a.part[((int64_t)g * a.N + h0) * 3 + e], jacc_s[e]);
     }
     // invalid i lanes never count (their g is -3 and they sit at 1e30)
     if (a.bad) {
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c] = sv;
+                __stcs(&a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c], sv);
             }
         }
         __syncthreads();
@@ -715,7 +719,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            a.part[((int64_t)g * a.N + h0) * 3 + e] = jacc_s[e];
+            __stcs(&a.part[((int64_t)g * a.N + h0) * 3 + e], jacc_s[e]);
     }
     if (a.bad) {
         nb = warp_sum_int(nb);
