@@ -454,10 +454,12 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_flops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_flops, "traffic": traffic,
-                         "traffic_note": "DRAM bytes per launch of the symmetric kernel from "
-                                         "profiles/r01_ncu_sym_kernel_notes.md: the unit-pair "
-                                         "partial buffer (written once, read once); algorithmic "
-                                         "inputs are 80 MB",
+                         "traffic_note": "DRAM bytes per launch of the symmetric kernel "
+                                         "(profiles/r01_ncu_sym_c5_metrics.json, ncu): mostly "
+                                         "the deterministic unit-pair partial buffer, written "
+                                         "once with streaming stores and read once by the "
+                                         "ordered reduce; algorithmic inputs are 80 MB; the "
+                                         "kernel is FP64-pipe bound, not HBM bound",
                          "kernel": "pack + slab meta + sym_task_kernel (symmetric fiber-fiber "
                                    "pairs) + ordered partial reduce",
                          "flops_per_pair": FLOPS_PER_PAIR,

@@ -181,8 +181,9 @@ int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
 int sf_pair_split(int64_t nt, int64_t ns);
 
 /* Non-excluded ordered pair interactions evaluated by rank `rank` of `world`
- * in sf_sbt_symmetric_partial for N points in groups of group_size (the
- * algorithmic work of that launch; host function, no device access). */
+ * in sf_sbt_symmetric_partial (FP64 mode; the FP32c task split uses smaller
+ * units) for N points in groups of group_size (the algorithmic work of that
+ * launch; host function, no device access). */
 int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world);
 
 /* ---------------------------------------------------------------------------

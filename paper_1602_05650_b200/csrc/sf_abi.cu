@@ -273,7 +273,7 @@ extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt,
 
 extern "C" int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world) {
     if (N <= 0 || world < 1 || rank < 0 || rank >= world) return 0;
-    const int64_t M = sf::sym_unit_size(N, group_size);
+    const int64_t M = sf::sym_unit_size(N, group_size, SF_MODE_FP64);   // the FP64 task split
     const int64_t G = (N + M - 1) / M;
     int64_t count = 0;
     const int64_t t0 = sf::sym_task_range(G, rank, world, &count);

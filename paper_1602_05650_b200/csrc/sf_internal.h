@@ -66,7 +66,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               int rank, int world, double *out, int64_t *bad, int accumulate,
                               cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
-int sym_unit_size(int64_t N, int64_t group_size);
+int sym_unit_size(int64_t N, int64_t group_size, int mode);
 // fiber points (A) x surface nodes (B), both directions per pair (sf_cross.cu)
 int pairs_cross(const double *xa, const double *fa, const double *wa, const double *dcoef,
                 int64_t NA, const double *xb, const double *qb, const double *wb,

@@ -830,14 +830,17 @@ __global__ void sym_pack_kernel(const double *__restrict__ x, const int64_t *__r
     }
 }
 
-int sym_unit_size(int64_t N, int64_t group_size) {
+int sym_unit_size(int64_t N, int64_t group_size, int mode) {
     // units: a multiple of the 32-point slab (and of the fiber size when that
-    // keeps them near the target, so units align to fibers), at most 2048
-    // points, and small enough that the G(G+1)/2 unit-pair tasks fill the GPU
-    // many times over (G >= 128 -> >= 8256 tasks) for mid-size systems; the
-    // sweep (tools/gpu_unit_sweep.sh) peaks at N/128..N/85 for N = 32k-64k
+    // keeps them near the target, so units align to fibers), at most 3072
+    // points in FP64 (2048 for FP32c, whose 3 CTAs/SM need the smaller
+    // M x 3 shared accumulator), and small enough that the G(G+1)/2 unit-pair
+    // tasks fill the GPU many times over (G >= 128 -> >= 8256 tasks) for
+    // mid-size systems; the sweeps (tools/gpu_unit_sweep.sh) peak at
+    // N/128..N/85 for N = 32k-64k, and at C5 M = 3072 matches 2048 (750 vs
+    // 748 G/s) with a third fewer partial slots (8.6 instead of 12.9 GB)
     const char *e = getenv("SF_SYM_UNIT");
-    int64_t target = e ? atoi(e) : 2048;
+    int64_t target = e ? atoi(e) : (mode == SF_MODE_FP32C ? 2048 : 3072);
     if (!e) {
         const int64_t fill = N / 128;
         if (fill < target) target = fill;
@@ -916,7 +919,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
-    const int M = sym_unit_size(N, group_size);
+    const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
     SymSrc *packed = (SymSrc *)ws.get(3, sizeof(SymSrc) * (size_t)N, st);
     SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)((N + 31) / 32 + 1), st);
