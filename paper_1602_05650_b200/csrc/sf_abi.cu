@@ -276,7 +276,7 @@ extern "C" int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, i
     const int64_t M = sf::sym_unit_size(N, group_size, SF_MODE_FP64);   // the FP64 task split
     const int64_t G = (N + M - 1) / M;
     int64_t count = 0;
-    const int64_t t0 = sf::sym_task_range(G, rank, world, &count);
+    const int64_t t0 = sf::sym_task_range(G, N, M, rank, world, &count);
     auto units = [&](int64_t t, int64_t &g, int64_t &h) {   // row-major {g <= h}
         int64_t r = 0, start = 0;
         while (start + (G - r) <= t) { start += G - r; ++r; }

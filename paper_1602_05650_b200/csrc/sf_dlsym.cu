@@ -264,7 +264,7 @@ int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const 
     DlArgs a;
     a.p = packed; a.N = n; a.M = (int)M; a.G = G; a.part = part;
     int64_t ntasks = 0;
-    a.task0 = sym_task_range(G, rank, world, &ntasks);
+    a.task0 = sym_task_range(G, n, M, rank, world, &ntasks);
     const size_t smem = sizeof(double) * 3 * (size_t)M;
     static const bool grouped = [] {
         const char *e = getenv("SF_DL_GROUPED");

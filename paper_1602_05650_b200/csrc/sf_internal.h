@@ -79,7 +79,7 @@ bool use_dl_symmetric(int64_t n);
 int pairs_dl_subtracted_symmetric(const double *nodes, const double *nrm, const double *w,
                                   const double *q, int64_t n, double pref, double *out,
                                   cudaStream_t st, Workspace &ws, int rank = 0, int world = 1);
-int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count);
+int64_t sym_task_range(int64_t G, int64_t N, int64_t M, int rank, int world, int64_t *count);
 int near_apply(const int64_t *row_ptr, const int64_t *rows, int64_t nrows, const int64_t *w_off,
                const int64_t *x_off, const int64_t *x_len, const double *W, const double *x,
                double *u, cudaStream_t st);

@@ -29,7 +29,9 @@
 // j's transposed sum stays in registers; after 32 rotations it is added to
 // the task's shared-memory accumulator for that j (always by the same warp,
 // in i-sub-block order).
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "sf_common.cuh"
 #include "sf_internal.h"
@@ -879,32 +881,35 @@ int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t 
 // The unit-pair tasks of rank `rank` of `world`: out receives this rank's
 // contribution to EVERY point; summing `out` over ranks (reduce-scatter)
 // gives the full sum.
-// Contiguous task range of `rank`, balanced by cost: off-diagonal tasks
-// evaluate twice the pairs of a diagonal one.  Tasks run row by row, each row
-// g = {g,g}, {g,g+1}, ..., {g,G-1} starting with its diagonal, so the cost of
-// the first t tasks is 2t - (rows started before t).
-int64_t sym_task_range(int64_t G, int rank, int world, int64_t *count) {
+// Contiguous task range of `rank`, balanced by pair count: task {g,h}
+// evaluates n_g n_h pair geometries in both directions (cost 2 n_g n_h), a
+// diagonal task n_g^2 ordered pairs; unit sizes n_g = min(M, N - g M) (the
+// last unit may be ragged).  Tasks run row by row, each row
+// g = {g,g}, {g,g+1}, ..., {g,G-1} starting with its diagonal.
+int64_t sym_task_range(int64_t G, int64_t N, int64_t M, int rank, int world, int64_t *count) {
     const int64_t ntasks = G * (G + 1) / 2;
+    auto nu = [&](int64_t g) { return std::min(M, N - g * M); };
+    // suffix sums of unit sizes and prefix costs of whole rows
+    std::vector<int64_t> suffix(G + 1, 0), rowpre(G + 1, 0);
+    for (int64_t g = G - 1; g >= 0; --g) suffix[g] = suffix[g + 1] + nu(g);
+    for (int64_t g = 0; g < G; ++g)
+        rowpre[g + 1] = rowpre[g] + nu(g) * nu(g) + 2 * nu(g) * suffix[g + 1];
     auto start = [&](int64_t row) { return row * G - row * (row - 1) / 2; };
-    auto cost = [&](int64_t t) {   // cost of tasks [0, t)
-        int64_t lo = 0, hi = G;    // rows with start(row) < t
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) / 2;
-            if (start(mid) < t) lo = mid + 1; else hi = mid;
-        }
-        return 2 * t - lo;
-    };
-    const int64_t total = 2 * ntasks - G;
     auto boundary = [&](int r) {   // first task whose prefix cost reaches r/world of the total
         if (r <= 0) return (int64_t)0;
         if (r >= world) return ntasks;
-        const int64_t want = (total * r + world - 1) / world;
-        int64_t lo = 0, hi = ntasks;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) / 2;
-            if (cost(mid) < want) lo = mid + 1; else hi = mid;
-        }
-        return lo;
+        const int64_t total = rowpre[G];
+        const int64_t want = total / world * r + (total % world) * r / world;
+        // row holding the boundary: rowpre[g] < want <= rowpre[g + 1]
+        int64_t g = std::upper_bound(rowpre.begin(), rowpre.end(), want - 1) - rowpre.begin() - 1;
+        if (g < 0) g = 0;
+        if (g >= G) return ntasks;
+        int64_t c = rowpre[g], t = start(g);
+        if (c >= want) return t;
+        c += nu(g) * nu(g);                 // the diagonal task
+        ++t;
+        for (int64_t h = g + 1; h < G && c < want; ++h, ++t) c += 2 * nu(g) * nu(h);
+        return t;
     };
     const int64_t b = boundary(rank), e = boundary(rank + 1);
     *count = e - b;
@@ -942,7 +947,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     a.N = N;
     a.M = M;
     a.G = G;
-    a.task0 = sym_task_range(G, rank, world, &a.ntasks);
+    a.task0 = sym_task_range(G, N, M, rank, world, &a.ntasks);
     a.part = part;
     a.bad = (unsigned long long *)bad;
     a.x = x;
