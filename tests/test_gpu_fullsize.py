@@ -83,3 +83,63 @@ def test_full_size_reference_api_with_near_maps(cuda, big):
             W = W.cpu().numpy() if torch.is_tensor(W) else np.asarray(W)
             corr[np.searchsorted(rows, t)] += W.reshape(3, -1) @ F[l].reshape(-1)
         assert rel(ua[rows], oracle_rows(cl, op, F, rows) + corr) < 1e-12
+
+
+def test_confined_aster_full_size_rows_match_oracle(cuda):
+    """BASELINE config 4 at full size (2,048 fibers x 32, 40,960-node periphery,
+    centrosome, ~116k near maps): complementary_velocities on sampled target
+    rows against the reference's composition (system.py:653-707) restated
+    with the oracle's pair sums, the completion flow and the cache's
+    near-field maps.  Rows of every kind (centrosome, periphery, fibers,
+    near-map targets) are sampled."""
+    import torch
+    from paper_1602_05650_b200 import system
+    st = configs.confined_aster()
+    cache = system.InteractionCache(st)
+    rng = np.random.default_rng(11)
+    f_list = [rng.standard_normal((fb.n_nodes, 3)) for fb in st.fibers]
+    q1 = rng.standard_normal((st.particles[0].mesh.n_nodes, 3))
+    q0 = rng.standard_normal((st.periphery.mesh.n_nodes, 3))
+    F, L = rng.standard_normal(3), rng.standard_normal(3)
+    res = system.complementary_velocities(st, periphery_density=q0, particle_densities=[q1],
+                                          fiber_forces=f_list, particle_wrenches=[(F, L)],
+                                          cache=cache)
+    u = np.concatenate([res.particles[0], res.periphery] + list(res.fibers))
+    trg, tgrp = cache.targets, cache.target_groups
+    near_t = np.array(sorted({t for t, _, _ in cache.near_fiber}))
+    rows = np.unique(np.concatenate([
+        rng.choice(cache.particle_slices[0].stop, 24, replace=False),
+        cache.periphery_slice.start + rng.choice(st.periphery.mesh.n_nodes, 48, replace=False),
+        cache.fiber_slice.start + rng.choice(cache.fiber_slice.stop - cache.fiber_slice.start, 96,
+                                             replace=False),
+        rng.choice(near_t, 48, replace=False)]))
+    mu = st.mu
+    src = np.concatenate([fb.X for fb in st.fibers])
+    sgrp = np.repeat(np.arange(len(st.fibers), dtype=np.int64), [fb.n_nodes for fb in st.fibers])
+    w = np.concatenate(cache.fiber_weights)
+    f = np.concatenate(f_list)
+    c = np.repeat(cache.doublet_coeffs, [fb.n_nodes for fb in st.fibers])
+    pref = 1.0 / (8.0 * np.pi * mu)
+    ref, _ = pairs.stokeslet_sum(trg[rows], tgrp[rows], src, sgrp, w[:, None] * f, pref)
+    ref += pairs.doublet_sum(trg[rows], tgrp[rows], src, sgrp, (c * w)[:, None] * f, pref)[0]
+    meshes = [m for m, _, _ in cache.surfaces]
+    qs = [q0 if isp else q1 for _, _, isp in cache.surfaces]
+    qw = np.concatenate([q * m.weights[:, None] for q, m in zip(qs, meshes)])
+    ref += pairs.stresslet_sum(trg[rows], tgrp[rows], cache.surface_sources, cache.surface_groups,
+                               cache.surface_normals, qw, -3.0 / (4.0 * np.pi * mu))[0]
+    part = st.particles[0]
+    mask = tgrp[rows] != len(st.fibers)
+    r = trg[rows][mask] - part.center
+    d = np.linalg.norm(r, axis=1)
+    ref[mask] += pref * (F[None, :] / d[:, None] + ((r @ F) / d ** 3)[:, None] * r)
+    ref[mask] += pref * np.cross(L[None, :], r) / (d ** 3)[:, None]
+    pos = {t: k for k, t in enumerate(rows)}
+    for t, l, W in cache.near_fiber:
+        if t in pos:
+            W = W.cpu().numpy() if torch.is_tensor(W) else np.asarray(W)
+            ref[pos[t]] += W.reshape(3, -1) @ f_list[l].ravel()
+    for t, si, W in cache.near_surface:
+        if t in pos:
+            W = W.cpu().numpy() if torch.is_tensor(W) else np.asarray(W)
+            ref[pos[t]] += W.reshape(3, -1) @ qs[si].ravel()
+    assert rel(u[rows], ref) < 1e-12
