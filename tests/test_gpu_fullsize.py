@@ -85,34 +85,41 @@ def test_full_size_reference_api_with_near_maps(cuda, big):
         assert rel(ua[rows], oracle_rows(cl, op, F, rows) + corr) < 1e-12
 
 
-def test_confined_aster_full_size_rows_match_oracle(cuda):
-    """BASELINE config 4 at full size (2,048 fibers x 32, 40,960-node periphery,
-    centrosome, ~116k near maps): complementary_velocities on sampled target
-    rows against the reference's composition (system.py:653-707) restated
-    with the oracle's pair sums, the completion flow and the cache's
-    near-field maps.  Rows of every kind (centrosome, periphery, fibers,
-    near-map targets) are sampled."""
+@pytest.mark.parametrize("name", ["c4", "c2"])
+def test_aster_full_size_rows_match_oracle(cuda, name):
+    """BASELINE configs 4 (2,048 fibers x 32, 40,960-node periphery,
+    centrosome, ~116k near maps) and 2 (1,024-fiber aster on an (8,8)
+    particle) at full size: complementary_velocities on sampled target rows
+    against the reference's composition (system.py:653-707) restated with
+    the oracle's pair sums, the completion flow and the cache's near-field
+    maps.  Rows of every kind (particle, periphery, fibers, near-map
+    targets) are sampled."""
     import torch
     from paper_1602_05650_b200 import system
-    st = configs.confined_aster()
+    st = configs.confined_aster() if name == "c4" else configs.aster(n_fibers=1024)
     cache = system.InteractionCache(st)
     rng = np.random.default_rng(11)
     f_list = [rng.standard_normal((fb.n_nodes, 3)) for fb in st.fibers]
     q1 = rng.standard_normal((st.particles[0].mesh.n_nodes, 3))
-    q0 = rng.standard_normal((st.periphery.mesh.n_nodes, 3))
+    q0 = (rng.standard_normal((st.periphery.mesh.n_nodes, 3)) if st.periphery is not None
+          else None)
     F, L = rng.standard_normal(3), rng.standard_normal(3)
     res = system.complementary_velocities(st, periphery_density=q0, particle_densities=[q1],
                                           fiber_forces=f_list, particle_wrenches=[(F, L)],
                                           cache=cache)
-    u = np.concatenate([res.particles[0], res.periphery] + list(res.fibers))
+    u = np.concatenate([res.particles[0]] + ([res.periphery] if q0 is not None else [])
+                       + list(res.fibers))
     trg, tgrp = cache.targets, cache.target_groups
-    near_t = np.array(sorted({t for t, _, _ in cache.near_fiber}))
-    rows = np.unique(np.concatenate([
-        rng.choice(cache.particle_slices[0].stop, 24, replace=False),
-        cache.periphery_slice.start + rng.choice(st.periphery.mesh.n_nodes, 48, replace=False),
-        cache.fiber_slice.start + rng.choice(cache.fiber_slice.stop - cache.fiber_slice.start, 96,
-                                             replace=False),
-        rng.choice(near_t, 48, replace=False)]))
+    near_t = np.array(sorted({t for t, _, _ in cache.near_fiber}), dtype=np.int64)
+    picks = [rng.choice(cache.particle_slices[0].stop, 24, replace=False),
+             cache.fiber_slice.start + rng.choice(cache.fiber_slice.stop - cache.fiber_slice.start,
+                                                  96, replace=False)]
+    if q0 is not None:
+        picks.append(cache.periphery_slice.start +
+                     rng.choice(st.periphery.mesh.n_nodes, 48, replace=False))
+    if near_t.size:
+        picks.append(rng.choice(near_t, min(48, near_t.size), replace=False))
+    rows = np.unique(np.concatenate(picks))
     mu = st.mu
     src = np.concatenate([fb.X for fb in st.fibers])
     sgrp = np.repeat(np.arange(len(st.fibers), dtype=np.int64), [fb.n_nodes for fb in st.fibers])
