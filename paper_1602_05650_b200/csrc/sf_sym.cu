@@ -623,8 +623,14 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
         }
         const SlabMeta *mi = a.slab + (g0 + ib) / 32;
         const int kvalid = min(TBI, (ng - ib + 31) / 32);
+        double blo[3], bhi[3];
         int gmn = mi[0].gmin, gmx = mi[0].gmax;
+        for (int c = 0; c < 3; ++c) { blo[c] = mi[0].lo[c]; bhi[c] = mi[0].hi[c]; }
         for (int k = 1; k < kvalid; ++k) {
+            for (int c = 0; c < 3; ++c) {
+                blo[c] = fmin(blo[c], mi[k].lo[c]);
+                bhi[c] = fmax(bhi[c], mi[k].hi[c]);
+            }
             gmn = min(gmn, mi[k].gmin);
             gmx = max(gmx, mi[k].gmax);
         }
@@ -653,7 +659,8 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
 #pragma unroll
             for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
             float uj[3] = {0.f, 0.f, 0.f};
-            const bool fast = (mj.gmax < gmn || mj.gmin > gmx) && islabs_far<TBI>(mi, kvalid, mj);
+            const bool fast = (mj.gmax < gmn || mj.gmin > gmx) &&
+                              (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
             const int nxt = (lane + 1) & 31;
             if (fast && both) {
 #pragma unroll 2
