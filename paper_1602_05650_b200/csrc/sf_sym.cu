@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             if (both && fast && PF) {
                 // positions of step s+1 are loaded while step s computes
                 double2 nxy = js_xy[warp][lane], nzf = js_zf[warp][lane];
-#pragma unroll 4
+#pragma unroll 8
                 for (int s = 0; s < 32; ++s) {
                     const int k = (lane + s) & 31;
                     PData pj;
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
                               (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
             const int nxt = (lane + 1) & 31;
             if (fast && both) {
-#pragma unroll 2
+#pragma unroll 4
                 for (int s = 0; s < 32; ++s) {
                     const int k = (lane + s) & 31;
                     PDataF pj;
