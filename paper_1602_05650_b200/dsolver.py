@@ -345,7 +345,12 @@ class DistBlockOperator:
         q = (torch.cat([u[sl] for sl in self.dens_sl]).reshape(-1, 3) if self.dens_sl else None)
         wr = self._wr[:self.np] if self.np else None
         # fiber targets: the other families (and the fiber pairs when direct)
-        ub_f = self.cache_fib.apply(f_full, q, wr, check=True) if no else None
+        # skipped-pair counts are geometric: checked on the first application only
+        ub_f = (self.cache_fib.apply(f_full, q, wr,
+                                     check=not getattr(self.cache_fib, "_bad_checked", False))
+                if no else None)
+        if no:
+            self.cache_fib._bad_checked = True
         if self.symmetric:
             g = self.geo
             _native.call("sf_sbt_symmetric_partial", _ptr(g.X), _ptr(self.fgrp), N, n,
@@ -383,7 +388,10 @@ class DistBlockOperator:
             c.all_reduce_sum(d["out"])
         # surfaces (rank 0)
         if self.surf:
-            ub_s = self.cache_surf.apply(f_full, q, wr, check=True) + self._surf_part
+            ub_s = self.cache_surf.apply(
+                f_full, q, wr, check=not getattr(self.cache_surf, "_bad_checked", False)) \
+                + self._surf_part
+            self.cache_surf._bad_checked = True
             for s in self.surf:
                 qs = u[s["sl"]]
                 rows = out[s["sl"]]

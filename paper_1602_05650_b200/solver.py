@@ -287,8 +287,13 @@ class BlockOperator:
                 if k:
                     self._wr.add_(self._wr_k)
         q = self._densities(u)
+        # the skipped-pair counts depend only on the frozen geometry (which
+        # pairs are cross-group and closer than 1e-12), not on u: check them
+        # on the cache's first application and never sync on them again
+        check = not getattr(c, "_bad_checked", False)
         ubar = c.apply(self._f, q, self._wr[:self.np] if self.np else None, out=self._ubar,
-                       check=True)
+                       check=check)
+        c._bad_checked = True
         pref_dl = -3.0 / (4.0 * math.pi * self.mu)
         for s in self.surf:
             qs = u[s["sl"]]
