@@ -55,6 +55,16 @@ __global__ void completion_kernel(const double *__restrict__ trg, const int64_t 
     if ((threadIdx.x & 31) == 0 && nbad && bad) atomicAdd(bad, (unsigned long long)nbad);
 }
 
+// u += pref * t, contracted to one FMA per entry exactly as the pair
+// kernels' accumulating epilogue (write_out) is, so a sum computed with
+// scale 1 into t and added here equals the in-kernel accumulation bit for bit.
+__global__ void fma_add_kernel(double *__restrict__ u, const double *__restrict__ t, double pref,
+                               int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        u[i] = fma(pref, t[i], u[i]);
+}
+
 __global__ void add_counter_kernel(int64_t *dst, const int64_t *src) { dst[0] += src[0]; }
 
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st) {
@@ -121,6 +131,7 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
     const double pref = 1.0 / (8.0 * M_PI * L->mu);
     int rc;
     const int64_t off = L->fiber_target_off;
+    double *stress_tmp = nullptr;  // surface-source sum computed on the side stream
     const bool sym = L->nfs > 0 && off >= 0 && off + L->nfs == L->nt &&
                      use_symmetric(L->mode, L->nfs);
     // Surface targets are exactly the surface sources (whole system): the
@@ -158,10 +169,11 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
             bad_sym = (int64_t *)ws.get(6, sizeof(int64_t), st);
             if (!bad_sym) return SF_ENOMEM;
         }
-        // non-fiber targets against fiber sources (on the side stream when
-        // there is one), concurrently with the fiber block done symmetrically
-        SideStream *side = off > 0 ? side_for(st) : nullptr;
-        if (off > 0) {
+        // non-fiber targets against fiber sources and every target against
+        // the surface sources (on the side stream when there is one),
+        // concurrently with the fiber block done symmetrically
+        SideStream *side = (off > 0 || L->nss > 0) ? side_for(st) : nullptr;
+        if (off > 0 || side) {
             cudaStream_t rs = st;
             if (side) {
                 if (cudaEventRecord(side->fork, st) != cudaSuccess ||
@@ -169,9 +181,19 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
                     return check_launch("side stream fork");
                 rs = side->s;
             }
-            rc = pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f, L->fw,
-                                    L->fdcoef, pref, SF_MODE_FP64, u, bad_f, rs,
-                                    side ? workspace_for(rs) : ws, 0);
+            Workspace &rws = side ? workspace_for(rs) : ws;
+            rc = off > 0 ? pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f,
+                                              L->fw, L->fdcoef, pref, SF_MODE_FP64, u, bad_f, rs,
+                                              rws, 0)
+                         : SF_OK;
+            if (!rc && side && L->nss > 0) {
+                // the stresslet sum unscaled into a side buffer, added after the join
+                stress_tmp = (double *)rws.get(11, sizeof(double) * 3 * (size_t)L->nt, rs);
+                rc = stress_tmp ? pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss,
+                                                  L->snrm, q, 1.0, stress_tmp, bad_s, rs, rws,
+                                                  L->sw, 0)
+                                : SF_ENOMEM;
+            }
             if (side && cudaEventRecord(side->join, side->s) != cudaSuccess && !rc)
                 rc = check_launch("side stream join");
             if (rc) {
@@ -197,7 +219,14 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
     } else if (cudaMemsetAsync(u, 0, sizeof(double) * 3 * L->nt, st) != cudaSuccess) {
         return check_launch("memset");
     }
-    if (L->nss > 0 && !cross) {
+    if (stress_tmp) {
+        const double pref_dl = -3.0 / (4.0 * M_PI * L->mu);
+        int64_t n = 3 * L->nt, blocks = (n + 255) / 256;
+        if (blocks > 4096) blocks = 4096;
+        fma_add_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, stress_tmp, pref_dl, n);
+        rc = check_launch("fma_add_kernel");
+        if (rc) return rc;
+    } else if (L->nss > 0 && !cross) {
         rc = pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss, L->snrm, q,
                              -3.0 / (4.0 * M_PI * L->mu), u, bad_s, st, ws, L->sw, 1);
         if (rc) return rc;
