@@ -28,6 +28,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOPS_PER_PAIR = 35          # fused Stokeslet + doublet, minimal formula
+# the symmetric kernel evaluates each unordered pair's geometry once: its own
+# minimal work is 29 flops per directed interaction: per unordered pair the
+# shared geometry r 3 + r^2 5 + rsqrt 1 + powers 3 = 12, per direction
+# r.f 5 + a 2 + b 4 + accumulate 12 = 23; (12 + 2 x 23) / 2 = 29
+FLOPS_PER_PAIR_SYM = 29
+# FP64 hardware flops executed per interaction, from the ncu instruction
+# counts of the symmetric kernel (DFMA x2 + DMUL + DADD per interaction,
+# profiles/r01_ncu_counters.md: 12.52 x 2 + 5.01 + 1.54)
+HW_FLOPS_PER_PAIR = 2 * 12.52 + 5.01 + 1.54
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
@@ -42,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="start the ranks (gloo), print one JSON line per rank, do no work")
     ap.add_argument("--step-config", default="c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated, each with optional "
                          "':fp32c' / ':body' / ':warm' ('+'-joined) options ('' to skip)")
@@ -132,10 +143,38 @@ def workload_config(args, cloud, world):
             "l2": "flushed between timed steps (256 MB write); K_delta 4.8 GB > L2"}
 
 
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+REFERENCE_STEPS = os.path.join(ROOT, "profiles", "r02_reference_cpu_steps.json")
+
+
+def reference_cpu_steps():
+    """Implicit steps/s of the reference's own Python path (slenderflow,
+    backward_euler_step) measured in the build container on the BASELINE
+    configs (tools/reference_cpu_steps.py); the reference is not importable
+    on the GPU box, so this is a recorded figure, labelled as such."""
+    if not os.path.exists(REFERENCE_STEPS):
+        return None
+    with open(REFERENCE_STEPS) as fh:
+        return json.load(fh)
+
+
 def run_reference(args, rank, world):
+    """The reference's pair sums on the host cores: the oracle C port of the
+    numba kernels (kernels.py:72-145), OpenMP over every host thread.  A step
+    is a bounded row sample of the config's matvec (each target row costs the
+    same Ns pairs), timed as it runs: ms_per_step is that
+    sample's wall time, value its pair-interactions/s."""
     if rank != 0:
         return
+    from oracle import pairs
     from paper_1602_05650_b200 import configs
+    pairs.set_num_threads(host_threads())
     cloud = configs.make(args.config, seed=args.seed)
     f = configs.forces(cloud, seed=args.seed + 1)
     N = cloud.n_points
@@ -149,21 +188,22 @@ def run_reference(args, rank, world):
         rates.append(r)
         times.append(dt)
     value = statistics.median(rates)
-    full_pairs = N * N - cloud.n_fibers * cloud.n_nodes ** 2
     line = {
         "impl": "reference", "metric": "stokes_pair_interactions_per_s", "value": value,
         "unit": "pair-interactions/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * full_pairs / value,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded rejection-sampled fiber cloud, N(0,1) forces)",
+        "data": "synthetic (seeded rejection-sampled perturbed fiber cloud, N(0,1) forces)",
         "config": workload_config(args, cloud, world),
         "cpu_baseline": {"value": value, "unit": "pair-interactions/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{rows} target rows x {N} sources, Stokeslet + doublet passes "
-                                   f"(oracle/oracle_pairs.c, OpenMP); ms_per_step extrapolated "
-                                   f"linearly in rows to the full {N}-row matvec"},
+                         "sample": f"each step: {rows} target rows x {N} sources, Stokeslet + "
+                                   f"doublet passes (oracle/oracle_pairs.c, OpenMP on {threads} "
+                                   f"host threads); ms_per_step is the sample's own wall time "
+                                   f"(a full matvec is {N / rows:.0f}x the sample)"},
         "e2e": {"value": value, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_implicit_steps": reference_cpu_steps(),
     }
     print(json.dumps(line), flush=True)
 
@@ -436,6 +476,9 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
+            pairs_mod_threads = host_threads()
+            from oracle import pairs as _pairs
+            _pairs.set_num_threads(pairs_mod_threads)
             rows = max(64, int(round(2e10 / cloud.n_points)))     # ~13 s on 16 host cores
             rate, dt, npairs, threads = cpu_pair_rate(cloud.X, f_all, cloud.eps, rows)
             cpu = {"value": rate, "unit": "pair-interactions/s", "cores": threads, "kind": "port",
@@ -449,11 +492,19 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if args.mode == "fp64" else "f32-compute/f64-accumulate",
             "data": "synthetic (seeded rejection-sampled perturbed fiber cloud, N(0,1) forces)",
-            "config": dict(workload_config(args, cloud, world), steps_per_s=1e3 / ms_step,
-                           near_maps=len(near)),
+            "config": workload_config(args, cloud, world),
+            "matvecs_per_s": 1e3 / ms_step, "near_maps": len(near),
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_flops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_flops, "traffic": traffic,
+                         "frac_alg_sym": rank_pairs * FLOPS_PER_PAIR_SYM / (pair_ms * 1e-3)
+                         / peak_flops,
+                         "frac_hw": rank_pairs * HW_FLOPS_PER_PAIR / (pair_ms * 1e-3) / peak_flops,
+                         "frac_note": "frac: 35-flop one-sided convention (SURVEY §8d); "
+                                      "frac_alg_sym: 29 flops per directed interaction, the "
+                                      "symmetric kernel's own minimal work; frac_hw: FP64 "
+                                      "hardware flops executed per interaction (ncu "
+                                      "instruction counts)",
                          "traffic_note": "DRAM bytes per launch of the symmetric kernel "
                                          "(profiles/r01_ncu_sym_c5_metrics.json, ncu): mostly "
                                          "the deterministic unit-pair partial buffer, written "
@@ -480,28 +531,71 @@ def run_ours(args, rank, world, local_rank):
     barrier()
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: launch the
+    N ranks here, one process per GPU, exactly as the driver's torchrun
+    command would (127.0.0.1 rendezvous), and return their exit code.  Never
+    silently measures fewer ranks than asked for."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def init_ranks(args, rank, world, local_rank):
+    """Process group for world > 1; checks that the world matches --gpus and
+    that every rank has its own GPU (NCCL), failing loudly otherwise."""
+    import torch
+    import torch.distributed as dist
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # SF_DIST_BACKEND=gloo: functional check of the multi-rank code path with
+    # host-side collectives (never a scaling number); ranks may share a GPU
+    backend = os.environ.get("SF_DIST_BACKEND", "nccl")
+    if args.launch_check:
+        backend = "gloo"
+    elif backend == "nccl" and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, "
+                         f"found {torch.cuda.device_count()}")
+    if backend == "nccl":
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        if torch.cuda.is_available():
+            local_rank = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend)
+    return local_rank
+
+
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
         run_reference(args, rank, world)
         return
     if world > 1:
-        import torch
-        import torch.distributed as dist
-        # SF_DIST_BACKEND=gloo: functional check of the multi-rank code path
-        # with host-side collectives (never a scaling number)
-        backend = os.environ.get("SF_DIST_BACKEND", "nccl")
-        if backend != "nccl":
-            local_rank = local_rank % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local_rank)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        else:
-            dist.init_process_group(backend)
+        local_rank = init_ranks(args, rank, world, local_rank)
     try:
+        if args.launch_check:          # launcher test: report the rank layout, no work
+            print(json.dumps({"launch_check": True, "rank": rank, "world": world,
+                              "local_rank": local_rank}), flush=True)
+            return
         run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:

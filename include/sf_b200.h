@@ -186,6 +186,21 @@ int sf_pair_split(int64_t nt, int64_t ns);
  * launch; host function, no device access). */
 int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world);
 
+/* Kernels one symmetric fiber-pair evaluation launches for rank `rank` of
+ * `world` (pack, slab metas, one task kernel and one ordered reduce per wave
+ * of task rows, final scale); host function, no device access. */
+int64_t sf_sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int world);
+
+/* Tuning: partial-sum budget (bytes) of one wave of the symmetric fiber-pair
+ * evaluation and the number of wave buffers / streams (<= 3); 0 restores the
+ * defaults (SF_SYM_WAVE_MB, SF_SYM_STREAMS, else 192 MB and 2).  The results
+ * are bitwise independent of both.  Not thread safe against running calls. */
+int sf_sym_set_waves(int64_t bytes, int streams);
+
+/* Device scratch currently held by the library's per-stream workspaces, in
+ * bytes (all devices and streams of this process). */
+int64_t sf_workspace_bytes(void);
+
 /* ---------------------------------------------------------------------------
  * complementary_velocities (system.py:623-709) on one frozen layout.
  * ------------------------------------------------------------------------- */

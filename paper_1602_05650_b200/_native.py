@@ -55,6 +55,9 @@ _SIGNATURES = {
                           _D, _D, _D, _P, _P, _P],
     "sf_tree_work_doubles": [_I64],
     "sf_sym_shard_pairs": [_I64, _I64, _I, _I],
+    "sf_sym_launch_count": [_I64, _I64, _I, _I, _I],
+    "sf_sym_set_waves": [_I64, _I],
+    "sf_workspace_bytes": [],
     "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
@@ -130,6 +133,8 @@ def load(require_device=False):
             fn.argtypes = argtypes
             fn.restype = _I
         lib.sf_sym_shard_pairs.restype = ctypes.c_int64
+        lib.sf_sym_launch_count.restype = ctypes.c_int64
+        lib.sf_workspace_bytes.restype = ctypes.c_int64
         lib.sf_tree_work_doubles.restype = ctypes.c_int64
         lib.sf_last_error.argtypes = []
         lib.sf_last_error.restype = ctypes.c_char_p

@@ -252,26 +252,17 @@ def forces(cloud, seed=1):
     return np.random.default_rng(seed).standard_normal(cloud.X.shape)
 
 
-def aster(n_fibers=1024, p=31, radius=0.5, standoff=1.3, center=(0.0, 0.0, 0.0), eps=1e-2,
-          E=1.0, length=1.0, mesh_res=(8, 8), min_sep=0.05, motor_force=1.0, seed=0,
-          layout="random"):
-    """BASELINE config 2 (and 4's centrosome): fibers clamped radially to a
-    rigid sphere, plus-end force of magnitude `motor_force` along the initial
-    tangent (a fixed vector, as PrescribedForceTorque stores it, fiber.py:58-63).
+def aster_layout(n_fibers=1024, radius=0.5, standoff=1.3, center=(0.0, 0.0, 0.0),
+                 min_sep=0.05, seed=0, layout="random"):
+    """Attachment points (n_fibers, 3) and unit directions (n_fibers, 3) of a
+    radial aster (BASELINE config 2, config 4's centrosome).
 
     layout "random": uniform directions (normalised Gaussians) with rejection
     of attachment points closer than `min_sep` (uniform draws overlap,
-    SURVEY.md fact 6); "fibonacci": the reference's aster_attachment_layout
-    spiral (system.py:428-443).  Attachment at standoff * radius (the
-    reference default 1.3).  Returns a SystemState of this package.
-    """
-    from . import body
-    from .fiber import ClampedToBody, PrescribedForceTorque, straight_fiber
-    from .system import SystemState
-
+    SURVEY.md fact 6); "fibonacci": a Fibonacci spiral over the sphere (the
+    law of the reference's aster_attachment_layout, system.py:428-443).
+    Attachment at standoff * radius (the reference default 1.3)."""
     center = np.asarray(center, dtype=float)
-    part = body.RigidParticle(body.make_surface(body.sphere_shape(radius), mesh_res,
-                                                center=tuple(center)))
     rng = np.random.default_rng(seed)
     r_att = standoff * radius
     if layout == "fibonacci":
@@ -296,9 +287,26 @@ def aster(n_fibers=1024, p=31, radius=0.5, standoff=1.3, center=(0.0, 0.0, 0.0),
             dirs.append(d)
             pts.append(x)
         dirs = np.asarray(dirs)
+    return center[None, :] + r_att * dirs, dirs
+
+
+def aster(n_fibers=1024, p=31, radius=0.5, standoff=1.3, center=(0.0, 0.0, 0.0), eps=1e-2,
+          E=1.0, length=1.0, mesh_res=(8, 8), min_sep=0.05, motor_force=1.0, seed=0,
+          layout="random"):
+    """BASELINE config 2 (and 4's centrosome): fibers clamped radially to a
+    rigid sphere (attachment from aster_layout), plus-end force of magnitude
+    `motor_force` along the initial tangent (a fixed vector, as
+    PrescribedForceTorque stores it, fiber.py:58-63).  Returns a SystemState
+    of this package."""
+    from . import body
+    from .fiber import ClampedToBody, PrescribedForceTorque, straight_fiber
+    from .system import SystemState
+
+    part = body.RigidParticle(body.make_surface(body.sphere_shape(radius), mesh_res,
+                                                center=tuple(float(c) for c in center)))
+    pts, dirs = aster_layout(n_fibers, radius, standoff, center, min_sep, seed, layout)
     fibs = []
-    for d in dirs:
-        x0 = center + r_att * d
+    for x0, d in zip(pts, dirs):
         fibs.append(straight_fiber(p, x0, d, length, eps=eps, E=E,
                                    bc_minus=ClampedToBody(0, x0, d),
                                    bc_plus=PrescribedForceTorque(motor_force * d)))

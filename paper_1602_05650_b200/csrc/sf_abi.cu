@@ -34,6 +34,14 @@ void *Workspace::get(int slot, size_t bytes, cudaStream_t st) {
     if (slot < 0 || slot >= kSlots) return nullptr;
     if (bytes == 0) bytes = 16;
     if (cap_[slot] >= bytes) return ptr_[slot];
+    // growing inside a stream capture would cache a graph-owned pointer:
+    // callers warm the path up (one uncaptured call) before capturing it
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        set_error(SF_ENOMEM, "workspace slot %d must grow to %zu bytes during stream capture; "
+                  "run the call once before capturing it", slot, bytes);
+        return nullptr;
+    }
     if (ptr_[slot]) cudaFreeAsync(ptr_[slot], st);
     size_t cap = bytes + bytes / 4;
     void *p = nullptr;
@@ -51,17 +59,63 @@ void *Workspace::get(int slot, size_t bytes, cudaStream_t st) {
 
 Workspace::~Workspace() {}
 
+// Per-stream state is keyed by (device, stream): the legacy default stream
+// handle 0 (and per-thread default streams) is the same value on every
+// device, so a stream handle alone does not identify one device's queue.
+static uint64_t stream_key(cudaStream_t st) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return ((uint64_t)(uintptr_t)st << 8) ^ (uint64_t)(unsigned)dev;
+}
+
 static std::mutex g_ws_mu;
-static std::unordered_map<cudaStream_t, Workspace *> *g_ws = nullptr;
+static std::unordered_map<uint64_t, Workspace *> *g_ws = nullptr;
 
 Workspace &workspace_for(cudaStream_t st) {
+    const uint64_t key = stream_key(st);
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    if (!g_ws) g_ws = new std::unordered_map<cudaStream_t, Workspace *>();
-    auto it = g_ws->find(st);
+    if (!g_ws) g_ws = new std::unordered_map<uint64_t, Workspace *>();
+    auto it = g_ws->find(key);
     if (it != g_ws->end()) return *it->second;
     Workspace *w = new Workspace();
-    (*g_ws)[st] = w;
+    (*g_ws)[key] = w;
     return *w;
+}
+
+size_t workspace_bytes_total() {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    size_t b = 0;
+    if (g_ws)
+        for (auto &kv : *g_ws) b += kv.second->bytes();
+    return b;
+}
+
+static std::mutex g_side_mu;
+static std::unordered_map<uint64_t, SidePool *> *g_side = nullptr;
+
+SidePool *side_pool_for(cudaStream_t st) {
+    const uint64_t key = stream_key(st);
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    if (!g_side) g_side = new std::unordered_map<uint64_t, SidePool *>();
+    auto it = g_side->find(key);
+    if (it != g_side->end()) return it->second;
+    SidePool *p = new SidePool();
+    bool ok = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&p->done[0], cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; ok && k < SidePool::kStreams; ++k) {
+        ok = cudaStreamCreateWithFlags(&p->s[k], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&p->done[k + 1], cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        delete p;
+        return nullptr;  // no side streams: callers run in order on st
+    }
+    (*g_side)[key] = p;
+    return p;
 }
 
 // ---- host-buffer staging (drop-in path): grow-only device + pinned buffers
@@ -270,6 +324,19 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
 }
 
 extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt, ns); }
+
+extern "C" int64_t sf_workspace_bytes(void) { return (int64_t)sf::workspace_bytes_total(); }
+
+extern "C" int sf_sym_set_waves(int64_t bytes, int streams) {
+    sf::sym_set_waves(bytes, streams);
+    return SF_OK;
+}
+
+extern "C" int64_t sf_sym_launch_count(int64_t N, int64_t group_size, int mode, int rank,
+                                       int world) {
+    if (N <= 0 || world < 1 || rank < 0 || rank >= world) return 0;
+    return sf::sym_launch_count(N, group_size, mode, rank, world);
+}
 
 extern "C" int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world) {
     if (N <= 0 || world < 1 || rank < 0 || rank >= world) return 0;

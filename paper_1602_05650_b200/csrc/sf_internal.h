@@ -18,6 +18,11 @@ class Workspace {
    public:
     static constexpr int kSlots = 12;
     void *get(int slot, size_t bytes, cudaStream_t st);
+    size_t bytes() const {
+        size_t b = 0;
+        for (int k = 0; k < kSlots; ++k) b += cap_[k];
+        return b;
+    }
     ~Workspace();
 
    private:
@@ -25,6 +30,20 @@ class Workspace {
     size_t cap_[kSlots] = {};
 };
 Workspace &workspace_for(cudaStream_t st);
+size_t workspace_bytes_total();
+
+// Side streams of one caller stream (keyed by device and stream), forked from
+// and joined back into it with events; created once per process.  done[0]
+// belongs to the caller stream, done[k + 1] to s[k].  Used under stream
+// capture too: every side stream first waits on `fork`, recorded on the
+// capturing stream, and the caller stream waits on the side work it needs.
+struct SidePool {
+    static constexpr int kStreams = 3;
+    cudaStream_t s[kStreams] = {};
+    cudaEvent_t fork = nullptr;
+    cudaEvent_t done[kStreams + 1] = {};
+};
+SidePool *side_pool_for(cudaStream_t st);
 
 int pairs_sbt(const double *trg, const int64_t *tgrp, int64_t nt, const double *src,
               const int64_t *sgrp, int64_t ns, const double *f, const double *dcoef, double pref,
@@ -67,6 +86,8 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
 int sym_unit_size(int64_t N, int64_t group_size, int mode);
+int64_t sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int world);
+void sym_set_waves(int64_t bytes, int streams);
 // fiber points (A) x surface nodes (B), both directions per pair (sf_cross.cu)
 int pairs_cross(const double *xa, const double *fa, const double *wa, const double *dcoef,
                 int64_t NA, const double *xb, const double *qb, const double *wb,

@@ -72,36 +72,29 @@ int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st) {
     return check_launch("add_counter_kernel");
 }
 
-// A side stream per caller stream, forked from and joined back into it with
-// events, so the small non-fiber-target x fiber-source sum (rows [0, off))
-// overlaps the symmetric fiber block (rows [off, nt)): the two write
-// disjoint rows, so the result is bit-identical to running them in order.
-// Keyed by caller stream like the workspaces; events and the stream live for
-// the process.  Works under stream capture (the fork is an event recorded on
-// the capturing stream).  SF_OVERLAP=0 serialises (A/B measurements).
+// A side stream per caller stream (the last stream of the caller's SidePool;
+// the symmetric fiber kernel's waves use the others), forked from and joined
+// back into it with events, so the small non-fiber-target x fiber-source sum
+// (rows [0, off)) overlaps the symmetric fiber block (rows [off, nt)): the two
+// write disjoint rows, so the result is bit-identical to running them in
+// order.  SF_OVERLAP=0 serialises (A/B measurements; read once).
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 
-static std::mutex g_side_mu;
-static std::unordered_map<cudaStream_t, SideStream> *g_side = nullptr;
-
-static SideStream *side_for(cudaStream_t st) {
-    const char *e = getenv("SF_OVERLAP");
-    if (e && atoi(e) == 0) return nullptr;
-    std::lock_guard<std::mutex> lk(g_side_mu);
-    if (!g_side) g_side = new std::unordered_map<cudaStream_t, SideStream>();
-    auto it = g_side->find(st);
-    if (it != g_side->end()) return &it->second;
-    SideStream ss;
-    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;  // no side stream: run in order on the caller's stream
-    }
-    return &((*g_side)[st] = ss);
+static bool side_for(cudaStream_t st, SideStream *out) {
+    static const bool enabled = [] {
+        const char *e = getenv("SF_OVERLAP");
+        return !(e && atoi(e) == 0);
+    }();
+    if (!enabled) return false;
+    SidePool *p = side_pool_for(st);
+    if (!p) return false;
+    out->s = p->s[SidePool::kStreams - 1];
+    out->fork = p->fork;
+    out->join = p->done[SidePool::kStreams];
+    return true;
 }
 
 }  // namespace sf
@@ -172,7 +165,8 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
         // non-fiber targets against fiber sources and every target against
         // the surface sources (on the side stream when there is one),
         // concurrently with the fiber block done symmetrically
-        SideStream *side = (off > 0 || L->nss > 0) ? side_for(st) : nullptr;
+        SideStream side_s;
+        SideStream *side = ((off > 0 || L->nss > 0) && side_for(st, &side_s)) ? &side_s : nullptr;
         if (off > 0 || side) {
             cudaStream_t rs = st;
             if (side) {

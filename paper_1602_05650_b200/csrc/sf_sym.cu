@@ -14,12 +14,24 @@
 // Determinism without atomics: points are split into G units of M points
 // (M a multiple of the fiber size, so units align to fibers).  A task is an
 // unordered unit pair {g,h}; the CTA computes every (i in g, j in h) pair in
-// both directions and writes two partial sums:
-//     part[h][points of g] = sum over j in h   (owner direction)
-//     part[g][points of h] = sum over i in g   (transposed direction)
-// Diagonal tasks {g,g} write only the owner direction.  A final pass sums the
-// G partials of every point in slot order.  Every partial is produced by one
-// CTA in a fixed loop order, so results are bitwise reproducible.
+// both directions and produces two partial sums, the slot-h partial of the
+// points of g (sum over j in h, owner direction) and the slot-g partial of
+// the points of h (sum over i in g, transposed direction).  Diagonal tasks
+// {g,g} produce only the owner direction.  Every point's G partials are
+// summed in slot order.  Every partial is produced by one CTA in a fixed
+// loop order, so results are bitwise reproducible.
+//
+// Bounded partial storage: the tasks run in waves, each a contiguous range
+// of task rows [ga, gl] (row g = tasks {g, h >= g}).  A wave's partials live
+// in a compact buffer: owner partials A[g - ga][h - ga][M points][3] and
+// transposed partials B[g - ga][points >= ga M][3]; after the wave, an
+// ordered pass adds them to the running per-point sum in slot order.  Along
+// one point's slot order the task index increases, so consecutive waves add
+// consecutive runs of its slots: the sum is the same sequence of additions
+// as one pass over all G slots, bit for bit, for any wave size.  Waves
+// alternate over the caller's stream and side streams with one buffer each,
+// so one wave's tail overlaps the next wave (SF_SYM_WAVE_MB per buffer,
+// SF_SYM_STREAMS buffers/streams).
 //
 // Inside a task: 4 warps share an i-sub-block of 64 points (2 per lane, in
 // registers with their owner accumulators); j runs in 32-point slabs, slab
@@ -56,14 +68,27 @@ struct SymArgs {
     int64_t N;
     int M;
     int G;
-    int64_t ntasks;   // tasks of this launch
-    int64_t task0;    // first task (rank share of the G(G+1)/2 unit pairs)
-    double *part;  // (G, N, 3)
+    int64_t ntasks;   // tasks of this launch (one wave)
+    int64_t task0;    // first task of the wave
+    double *partA;    // owner partials (rows, Acols, M, 3) of the wave's rows
+    double *partB;    // transposed partials (rows, Bstride, 3)
+    int64_t ga;       // first task row of the wave
+    int64_t Acols;    // G - ga
+    int64_t Bstride;  // N - ga M
     unsigned long long *bad;
     const double *x;  // (N, 3) FP64 positions: the FP32 variant's coincidence test
 };
 
 constexpr int kSymThreads = 128;
+
+// slot-h partial of point g0 + local (owner direction of task {g,h})
+__device__ __forceinline__ double *owner_slot(const SymArgs &a, int g, int h, int64_t local) {
+    return a.partA + ((((int64_t)g - a.ga) * a.Acols + ((int64_t)h - a.ga)) * a.M + local) * 3;
+}
+// slot-g partial of point p >= g M (transposed direction of task {g,h})
+__device__ __forceinline__ double *trans_slot(const SymArgs &a, int g, int64_t p) {
+    return a.partB + ((((int64_t)g - a.ga) * a.Bstride) + (p - a.ga * a.M)) * 3;
+}
 
 struct PData {
     double x, y, z, fx, fy, fz, c, c3;
@@ -397,7 +422,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                __stcs(&a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c], s);
+                __stcs(owner_slot(a, g, h, ib + il) + c, s);
             }
         }
         __syncthreads();
@@ -405,7 +430,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            __stcs(&a.part[((int64_t)g * a.N + h0) * 3 + e], jacc_s[e]);
+            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
     }
     // invalid i lanes never count (their g is -3 and they sit at 1e30)
     if (a.bad) {
@@ -730,7 +755,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                __stcs(&a.part[((int64_t)h * a.N + g0 + ib + il) * 3 + c], sv);
+                __stcs(owner_slot(a, g, h, ib + il) + c, sv);
             }
         }
         __syncthreads();
@@ -738,7 +763,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            __stcs(&a.part[((int64_t)g * a.N + h0) * 3 + e], jacc_s[e]);
+            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
     }
     if (a.bad) {
         nb = warp_sum_int(nb);
@@ -810,24 +835,46 @@ __global__ void sym_pack_f32_kernel(const double *__restrict__ x, const int64_t 
     }
 }
 
-// out[i] (+)= pref * sum_{s < G} part[s][i], slots in order.  Slot s of a
-// point in unit u was written by task {min(u,s), max(u,s)}; slots whose task
-// is outside this launch's range [t0, t1) (another rank's share) are skipped
-// instead of being zero-filled and read back -- the sum is unchanged.
-__global__ void sym_reduce_kernel(const double *__restrict__ part, int G, int64_t N, int M,
-                                  int64_t t0, int64_t t1, double pref, double *__restrict__ out,
-                                  int accumulate) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ int64_t task_index(int64_t g, int64_t h, int64_t G) {
+    return g * G - g * (g - 1) / 2 + (h - g);
+}
+
+// acc[i] += this wave's partials of point i, in slot order: the transposed
+// slots k in [ga, min(gl, u - 1)] (tasks {k, u}), then, when u is one of the
+// wave's rows, the owner slots h >= u (tasks {u, h}); only tasks inside the
+// wave's range [tb, te) (a partial first or last row, a rank's share) count.
+__global__ void sym_wave_reduce_kernel(const double *__restrict__ A, const double *__restrict__ B,
+                                       int G, int64_t N, int M, int64_t ga, int64_t gl,
+                                       int64_t tb, int64_t te, int64_t Acols, int64_t Bstride,
+                                       double *__restrict__ acc) {
+    const int64_t e = 3 * ga * M + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= 3 * N) return;
-    const int64_t u = (e / 3) / M;
-    double s = 0.0;
-    for (int k = 0; k < G; ++k) {
-        const int64_t g = k < u ? k : u, h = k < u ? u : k;
-        const int64_t t = g * G - g * (g - 1) / 2 + (h - g);
-        if (t < t0 || t >= t1) continue;
-        s += part[(int64_t)k * 3 * N + e];
+    const int64_t p = e / 3, c = e - 3 * p;
+    const int64_t u = p / M;
+    double s = acc[e];
+    const int64_t kmax = min(gl, u - 1);
+    for (int64_t k = ga; k <= kmax; ++k) {
+        const int64_t t = task_index(k, u, G);
+        if (t >= te) break;
+        if (t >= tb) s += B[((k - ga) * Bstride + (p - ga * M)) * 3 + c];
     }
-    out[e] = accumulate ? out[e] + pref * s : pref * s;
+    if (u >= ga && u <= gl) {
+        const int64_t loc = p - u * M;
+        for (int64_t h = u; h < G; ++h) {
+            const int64_t t = task_index(u, h, G);
+            if (t >= te) break;
+            if (t >= tb) s += A[(((u - ga) * Acols + (h - ga)) * M + loc) * 3 + c];
+        }
+    }
+    acc[e] = s;
+}
+
+// out[i] (+)= pref * acc[i]
+__global__ void sym_scale_kernel(const double *__restrict__ acc, int64_t n, double pref,
+                                 double *__restrict__ out, int accumulate) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    out[e] = accumulate ? out[e] + pref * acc[e] : pref * acc[e];
 }
 
 // Packing identical to the pair engine's (x y z, w f, c, 3c, group).
@@ -933,6 +980,61 @@ int64_t sym_task_range(int64_t G, int64_t N, int64_t M, int rank, int world, int
     return b;
 }
 
+struct SymWave {
+    int64_t tb, te, ga, gl;
+};
+
+// partial-buffer budget per wave and number of wave buffers/streams:
+// SF_SYM_WAVE_MB / SF_SYM_STREAMS at first use, or sf_sym_set_waves()
+static int64_t g_wave_bytes = -1;
+static int g_wave_streams = -1;
+
+size_t sym_wave_bytes() {
+    if (g_wave_bytes < 0) {
+        const char *e = getenv("SF_SYM_WAVE_MB");
+        g_wave_bytes = (int64_t)((e ? atof(e) : 192.0) * (double)(1 << 20));
+    }
+    return (size_t)g_wave_bytes;
+}
+
+int sym_wave_streams() {
+    if (g_wave_streams < 0) {
+        const char *e = getenv("SF_SYM_STREAMS");
+        g_wave_streams = e ? atoi(e) : 2;
+    }
+    return std::max(1, std::min(g_wave_streams, SidePool::kStreams));
+}
+
+void sym_set_waves(int64_t bytes, int streams) {
+    g_wave_bytes = bytes > 0 ? bytes : -1;
+    g_wave_streams = streams > 0 ? streams : -1;
+}
+
+// Waves over the task range [t0, t1): whole task rows from the first row of
+// the wave, as many as fit `budget` bytes of partials (at least one row).
+// Row g needs (G - ga) M + (N - ga M) points x 3 doubles, so a wave holds a
+// roughly constant number of tasks (budget / (2 M x 24 bytes)).
+static std::vector<SymWave> sym_waves(int64_t G, int64_t N, int64_t M, int64_t t0, int64_t t1,
+                                      size_t budget, size_t *max_bytes) {
+    std::vector<SymWave> out;
+    *max_bytes = 0;
+    auto start = [&](int64_t row) { return row * G - row * (row - 1) / 2; };
+    int64_t t = t0, row = 0;
+    while (t < t1) {
+        while (row + 1 < G && start(row + 1) <= t) ++row;
+        const int64_t ga = row;
+        const size_t per_row = (size_t)((G - ga) * M + (N - ga * M)) * 3 * sizeof(double);
+        int64_t rows = (int64_t)(budget / per_row);
+        if (rows < 1) rows = 1;
+        const int64_t gl = std::min(G - 1, ga + rows - 1);
+        const int64_t te = std::min(t1, start(gl + 1));
+        out.push_back({t, te, ga, gl});
+        *max_bytes = std::max(*max_bytes, (size_t)(gl - ga + 1) * per_row);
+        t = te;
+    }
+    return out;
+}
+
 int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
@@ -943,10 +1045,23 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     if (N == 0) return SF_OK;
     const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
+    const size_t wave_bytes = sym_wave_bytes();
+    const int nbuf_env = sym_wave_streams();
+    int64_t ntasks = 0;
+    const int64_t t0 = sym_task_range(G, N, M, rank, world, &ntasks);
+    size_t buf_bytes = 0;
+    const std::vector<SymWave> waves = sym_waves(G, N, M, t0, t0 + ntasks, wave_bytes, &buf_bytes);
+    SidePool *pool = (waves.size() > 1 && nbuf_env > 1) ? side_pool_for(st) : nullptr;
+    const int nbuf = pool ? (int)std::min<size_t>(nbuf_env, waves.size()) : 1;
+    buf_bytes = (buf_bytes + 255) / 256 * 256;
+
     SymSrc *packed = (SymSrc *)ws.get(3, sizeof(SymSrc) * (size_t)N, st);
     SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)((N + 31) / 32 + 1), st);
-    double *part = (double *)ws.get(5, sizeof(double) * 3 * (size_t)N * G, st);
-    if (!packed || !meta || !part) return SF_ENOMEM;
+    double *acc = (double *)ws.get(5, sizeof(double) * 3 * (size_t)N, st);
+    char *bufs = (char *)ws.get(6, buf_bytes * nbuf, st);
+    if (!packed || !meta || !acc || (!bufs && !waves.empty())) return SF_ENOMEM;
+    if (cudaMemsetAsync(acc, 0, sizeof(double) * 3 * (size_t)N, st) != cudaSuccess)
+        return check_launch("memset");
     int64_t pg = (N + 255) / 256;
     const int64_t nslab = (N + 31) / 32;
     if (f32) {
@@ -958,14 +1073,14 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                                                                          packed);
         slab_meta_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(packed, N, meta);
     }
+    int rc = check_launch("sym_pack");
+    if (rc) return rc;
     SymArgs a;
     a.src = packed;
     a.slab = meta;
     a.N = N;
     a.M = M;
     a.G = G;
-    a.task0 = sym_task_range(G, N, M, rank, world, &a.ntasks);
-    a.part = part;
     a.bad = (unsigned long long *)bad;
     a.x = x;
     const size_t smem = sizeof(double) * 3 * M;
@@ -973,43 +1088,90 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         const char *e = getenv("SF_SYM_VARIANT");
         return e ? atoi(e) : 224;
     }();
-    auto launch = [&](auto kern) -> int {
+    static const int fvariant = [] {
+        const char *e = getenv("SF_SYM_F32_VARIANT");
+        return e ? atoi(e) : 34;
+    }();
+    auto launch = [&](auto kern, cudaStream_t s) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        if (a.ntasks > 0) kern<<<(unsigned)a.ntasks, kSymThreads, smem, st>>>(a);
-        return SF_OK;
+        if (a.ntasks > 0) kern<<<(unsigned)a.ntasks, kSymThreads, smem, s>>>(a);
+        return check_launch("sym_task_kernel");
     };
-    int lrc;
-    if (f32) {
-        static const int fvariant = [] {
-            const char *e = getenv("SF_SYM_F32_VARIANT");
-            return e ? atoi(e) : 34;
-        }();
-        switch (fvariant) {
-            case 24: lrc = launch(sym_task_kernel_f32<2, 4>); break;
-            case 33: lrc = launch(sym_task_kernel_f32<3, 3>); break;
-            case 26: lrc = launch(sym_task_kernel_f32<2, 6>); break;
-            case 44: lrc = launch(sym_task_kernel_f32<4, 4>); break;
-            default: lrc = launch(sym_task_kernel_f32<3, 4>); break;
+    auto run = [&](cudaStream_t s) -> int {
+        if (f32) {
+            switch (fvariant) {
+                case 24: return launch(sym_task_kernel_f32<2, 4>, s);
+                case 33: return launch(sym_task_kernel_f32<3, 3>, s);
+                case 26: return launch(sym_task_kernel_f32<2, 6>, s);
+                case 44: return launch(sym_task_kernel_f32<4, 4>, s);
+                default: return launch(sym_task_kernel_f32<3, 4>, s);
+            }
         }
-    } else switch (variant) {
-        // launch-shape sweep (tools/gpu_sym_sweep.sh, tools/gpu_sym_aster_sweep.sh):
-        // MINB*10 + i-per-lane (+100 prefetch, +200 prefetch + grouped pairs)
-        case 24: lrc = launch(sym_task_kernel<2, 4>); break;
-        case 124: lrc = launch(sym_task_kernel<2, 4, true>); break;
-        case 233: lrc = launch(sym_task_kernel<3, 3, true, true>); break;
-        case 223: lrc = launch(sym_task_kernel<2, 3, true, true>); break;
-        case 232: lrc = launch(sym_task_kernel<3, 2, true, true>); break;
-        default: lrc = launch(sym_task_kernel<2, 4, true, true>); break;   // 749 G/s at C5
+        switch (variant) {
+            // launch-shape sweep (tools/gpu_sym_sweep.sh, tools/gpu_sym_aster_sweep.sh):
+            // MINB*10 + i-per-lane (+100 prefetch, +200 prefetch + grouped pairs)
+            case 24: return launch(sym_task_kernel<2, 4>, s);
+            case 124: return launch(sym_task_kernel<2, 4, true>, s);
+            case 233: return launch(sym_task_kernel<3, 3, true, true>, s);
+            case 223: return launch(sym_task_kernel<2, 3, true, true>, s);
+            case 232: return launch(sym_task_kernel<3, 2, true, true>, s);
+            default: return launch(sym_task_kernel<2, 4, true, true>, s);   // 749 G/s at C5
+        }
+    };
+    // fork the side streams off the caller's stream (packed sources, slab
+    // metas and the zeroed sums are ready)
+    if (pool) {
+        if (cudaEventRecord(pool->fork, st) != cudaSuccess) return check_launch("event record");
+        for (int b = 1; b < nbuf; ++b)
+            if (cudaStreamWaitEvent(pool->s[b - 1], pool->fork, 0) != cudaSuccess)
+                return check_launch("stream wait");
     }
-    if (lrc) return lrc;
-    int rc = check_launch("sym_task_kernel");
-    if (a.ntasks == 0 && world == 1) return rc;
-    if (rc) return rc;
-    sym_reduce_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(
-        part, G, N, M, a.task0, a.task0 + a.ntasks, pref, out, accumulate);
-    return check_launch("sym_reduce_kernel");
+    int prev = -1;   // buffer (stream) of the previous wave's ordered reduce
+    for (size_t wv = 0; wv < waves.size(); ++wv) {
+        const SymWave &W = waves[wv];
+        const int b = (int)(wv % nbuf);
+        cudaStream_t s = b == 0 ? st : pool->s[b - 1];
+        double *A = (double *)(bufs + (size_t)b * buf_bytes);
+        const int64_t rows = W.gl - W.ga + 1;
+        a.task0 = W.tb;
+        a.ntasks = W.te - W.tb;
+        a.ga = W.ga;
+        a.Acols = G - W.ga;
+        a.Bstride = N - W.ga * M;
+        a.partA = A;
+        a.partB = A + (size_t)rows * a.Acols * M * 3;
+        if ((rc = run(s))) return rc;
+        // the running sums are added to in wave order
+        if (prev >= 0 && prev != b && cudaStreamWaitEvent(s, pool->done[prev], 0) != cudaSuccess)
+            return check_launch("stream wait");
+        const int64_t nel = 3 * (N - W.ga * M);
+        sym_wave_reduce_kernel<<<(unsigned)((nel + 255) / 256), 256, 0, s>>>(
+            a.partA, a.partB, G, N, M, W.ga, W.gl, W.tb, W.te, a.Acols, a.Bstride, acc);
+        if ((rc = check_launch("sym_wave_reduce_kernel"))) return rc;
+        if (pool && cudaEventRecord(pool->done[b], s) != cudaSuccess)
+            return check_launch("event record");
+        prev = b;
+    }
+    // join: the last reduce waited on every earlier one
+    if (pool && prev > 0 && cudaStreamWaitEvent(st, pool->done[prev], 0) != cudaSuccess)
+        return check_launch("stream wait");
+    sym_scale_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(acc, 3 * N, pref, out,
+                                                                     accumulate);
+    return check_launch("sym_scale_kernel");
+}
+
+// kernels launched by one pairs_sbt_symmetric_shard call (gpu_launches accounting)
+int64_t sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int world) {
+    if (N == 0) return 0;
+    const int M = sym_unit_size(N, group_size, mode);
+    const int64_t G = (N + M - 1) / M;
+    int64_t ntasks = 0;
+    const int64_t t0 = sym_task_range(G, N, M, rank, world, &ntasks);
+    size_t mx = 0;
+    const auto w = sym_waves(G, N, M, t0, t0 + ntasks, sym_wave_bytes(), &mx);
+    return 3 + 2 * (int64_t)w.size();   // pack + meta + per wave (tasks + reduce) + scale
 }
 
 }  // namespace sf

@@ -197,11 +197,13 @@ class FiberHIOperator:
 
     @property
     def launches_per_apply(self):
-        """Kernels one apply launches: symmetric path = pack, slab meta, task
-        kernel, ordered reduce; direct path = pack, tile meta, pair kernel
+        """Kernels one apply launches: symmetric path = pack, slab meta, a
+        task kernel and an ordered reduce per wave, final scale
+        (sf_sym_launch_count); direct path = pack, tile meta, pair kernel
         (+ ordered split reduce); then near (if any) and self terms."""
         if self.symmetric or self.symmetric_shard:
-            pair = 4
+            rank, world = (self.rank, self.world) if self.symmetric_shard else (0, 1)
+            pair = _native.load().sf_sym_launch_count(self.N, self.n, self.mode, rank, world)
         else:
             split = _native.load().sf_pair_split(self.Nown, self.N)
             pair = 3 + (1 if split > 1 else 0)
