@@ -593,8 +593,11 @@ def main():
         local_rank = init_ranks(args, rank, world, local_rank)
     try:
         if args.launch_check:          # launcher test: report the rank layout, no work
-            print(json.dumps({"launch_check": True, "rank": rank, "world": world,
-                              "local_rank": local_rank}), flush=True)
+            # one write(2) per rank so the lines of concurrent ranks never interleave
+            line = json.dumps({"launch_check": True, "rank": rank, "world": world,
+                               "local_rank": local_rank}) + "\n"
+            sys.stdout.flush()
+            os.write(sys.stdout.fileno(), line.encode())
             return
         run_ours(args, rank, world, local_rank)
     finally:

@@ -201,6 +201,11 @@ int sf_sym_set_waves(int64_t bytes, int streams);
  * bytes (all devices and streams of this process). */
 int64_t sf_workspace_bytes(void);
 
+/* Synchronise every device the library used and free all its per-stream
+ * workspaces (they regrow on the next call).  Not safe against running calls
+ * on other host threads. */
+int sf_workspace_release(void);
+
 /* ---------------------------------------------------------------------------
  * complementary_velocities (system.py:623-709) on one frozen layout.
  * ------------------------------------------------------------------------- */
@@ -345,6 +350,27 @@ int sf_combine(const double *V, int64_t ld, int k, const double *coef, double *x
  * k+1 <= R); work >= 4*296 doubles. */
 int sf_gmres_mgs(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol, int R,
                  double *work, void *stream);
+
+/* GMRES Hessenberg / Givens bookkeeping on the device (solver.py:444-516),
+ * so the host needs one small status record per Arnoldi step instead of the
+ * Hessenberg column.  gs: sf_gmres_state_doubles(R, I) doubles of device
+ * state (H, cs, sn, g, y, scalars, residual history; see sf_gmres.cu).
+ * sf_gmres_reset: start a solve (iterations = 0).  sf_gmres_cycle: start a
+ * cycle, g = beta e_0 and V0 = r / beta (beta a device scalar).
+ * sf_gmres_givens: step k of the cycle from hcol (sf_gmres_mgs output):
+ * previous rotations, new rotation, g, relative residual |g_{k+1}|/beta0
+ * into the history, done = converged | breakdown (|w_orth| <= 1e-12 |w|) |
+ * cycle full | iteration cap; a no-op once done (speculative steps);
+ * status (optional, 4 doubles) = [done, iterations, rel, k].
+ * sf_gmres_update: x += V_k^T triu(H_k)^-1 g_k for the k steps taken. */
+int64_t sf_gmres_state_doubles(int R, int max_iterations);
+int sf_gmres_reset(double *gs, int R, int max_iterations, double beta0, double tol,
+                   void *stream);
+int sf_gmres_cycle(double *gs, int R, const double *beta, const double *r, double *V0, int64_t n,
+                   void *stream);
+int sf_gmres_givens(const double *hcol, double *gs, int R, int k, double *status, void *stream);
+int sf_gmres_update(const double *V, int64_t ld, double *gs, int R, double *x, int64_t n,
+                    void *stream);
 
 /* Near-field map construction on the device.
  * sf_near_search: (fiber, target) pairs whose minimum node distance is below

@@ -58,6 +58,7 @@ _SIGNATURES = {
     "sf_sym_launch_count": [_I64, _I64, _I, _I, _I],
     "sf_sym_set_waves": [_I64, _I],
     "sf_workspace_bytes": [],
+    "sf_workspace_release": [],
     "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
@@ -79,6 +80,11 @@ _SIGNATURES = {
     "sf_axpy_dev": [_P, _D, _I, _P, _P, _I64, _P],
     "sf_combine": [_P, _I64, _I, _P, _P, _I64, _P],
     "sf_gmres_mgs": [_P, _I64, _I, _P, _I64, _P, _I, _P, _P],
+    "sf_gmres_state_doubles": [_I, _I],
+    "sf_gmres_reset": [_P, _I, _I, _D, _D, _P],
+    "sf_gmres_cycle": [_P, _I, _P, _P, _P, _I64, _P],
+    "sf_gmres_givens": [_P, _P, _I, _I, _P, _P],
+    "sf_gmres_update": [_P, _I64, _P, _I, _P, _I64, _P],
     "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_sbt_pair": [_P, _P, _I64, _P, _P, _I64, _P, _P, _D, _I, _P, _P],
@@ -90,6 +96,7 @@ _SIGNATURES = {
 }
 
 _lib = None
+_device_ok = False
 
 
 class FiberSys(ctypes.Structure):
@@ -122,7 +129,7 @@ def exported_symbols():
 
 def load(require_device=False):
     """Load the library (cached).  require_device also checks for a GPU."""
-    global _lib
+    global _lib, _device_ok
     if _lib is None:
         if not os.path.exists(LIB):
             raise NativeUnavailable(
@@ -135,12 +142,15 @@ def load(require_device=False):
         lib.sf_sym_shard_pairs.restype = ctypes.c_int64
         lib.sf_sym_launch_count.restype = ctypes.c_int64
         lib.sf_workspace_bytes.restype = ctypes.c_int64
+        lib.sf_gmres_state_doubles.restype = ctypes.c_int64
         lib.sf_tree_work_doubles.restype = ctypes.c_int64
         lib.sf_last_error.argtypes = []
         lib.sf_last_error.restype = ctypes.c_char_p
         _lib = lib
-    if require_device and _lib.sf_device_sm_count() <= 0:
-        raise NativeUnavailable("no CUDA device visible to libsf_b200")
+    if require_device and not _device_ok:
+        if _lib.sf_device_sm_count() <= 0:
+            raise NativeUnavailable("no CUDA device visible to libsf_b200")
+        _device_ok = True
     return _lib
 
 

@@ -158,6 +158,7 @@ class RigidParticle:
     """Closed rigid surface with its double-layer density and wrenches (body.py:197-215)."""
 
     def __init__(self, mesh, center=None):
+        self._dev = None        # devstate.DeviceState holding the step unknowns
         self.mesh = mesh
         self.center = np.asarray(center if center is not None else mesh.center, dtype=float)
         self.q = np.zeros((mesh.n_nodes, 3))
@@ -165,6 +166,30 @@ class RigidParticle:
         self.omega = np.zeros(3)
         self.F_ext = np.zeros(3)
         self.L_ext = np.zeros(3)
+
+    # mesh (its nodes), center, q, U and omega live on the device between
+    # implicit steps (devstate.DeviceState): reading brings the state back,
+    # writing hands it back to the host
+    def _get(self, name):
+        if self._dev is not None:
+            self._dev.pull()
+        return self.__dict__["_" + name]
+
+    def _set(self, name, value):
+        if self.__dict__.get("_dev") is not None:
+            self._dev.release()
+        self.__dict__["_" + name] = value
+
+    mesh = property(lambda self: self._get("mesh"), lambda self, v: self._set("mesh", v))
+    center = property(lambda self: self._get("center"), lambda self, v: self._set("center", v))
+    q = property(lambda self: self._get("q"), lambda self, v: self._set("q", v))
+    U = property(lambda self: self._get("U"), lambda self, v: self._set("U", v))
+    omega = property(lambda self: self._get("omega"), lambda self, v: self._set("omega", v))
+
+    @property
+    def n_nodes(self):
+        """Mesh node count (static; never reads the state back)."""
+        return self.__dict__["_mesh"].n_nodes
 
     def translate(self, displacement):
         d = np.asarray(displacement, dtype=float)
@@ -180,8 +205,21 @@ class Periphery:
     def __init__(self, mesh):
         if not mesh.has_parametrization():
             raise GeometryError("periphery requires a parametrized mesh")
+        self._dev = None        # devstate.DeviceState holding the density
         self.mesh = mesh
         self.q = np.zeros((mesh.n_nodes, 3))
+
+    @property
+    def q(self):
+        if self._dev is not None:
+            self._dev.pull()
+        return self._q
+
+    @q.setter
+    def q(self, value):
+        if self.__dict__.get("_dev") is not None:
+            self._dev.release()
+        self._q = value
 
     def contains(self, points, margin=0.0):
         pts = np.atleast_2d(np.asarray(points, dtype=float)) - self.mesh.center

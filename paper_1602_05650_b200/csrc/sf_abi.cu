@@ -59,6 +59,14 @@ void *Workspace::get(int slot, size_t bytes, cudaStream_t st) {
 
 Workspace::~Workspace() {}
 
+void Workspace::release() {
+    for (int k = 0; k < kSlots; ++k) {
+        if (ptr_[k]) cudaFree(ptr_[k]);
+        ptr_[k] = nullptr;
+        cap_[k] = 0;
+    }
+}
+
 // Per-stream state is keyed by (device, stream): the legacy default stream
 // handle 0 (and per-thread default streams) is the same value on every
 // device, so a stream handle alone does not identify one device's queue.
@@ -91,6 +99,20 @@ size_t workspace_bytes_total() {
     if (g_ws)
         for (auto &kv : *g_ws) b += kv.second->bytes();
     return b;
+}
+
+void workspace_release_all() {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (!g_ws) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : *g_ws) {
+        const int dev = (int)(kv.first & 0xff);
+        if (cudaSetDevice(dev) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess)
+            kv.second->release();
+        cudaGetLastError();
+    }
+    cudaSetDevice(cur);
 }
 
 static std::mutex g_side_mu;
@@ -326,6 +348,11 @@ extern "C" int sf_fiber_hi_apply(const double *X, const int64_t *grp, int64_t nf
 extern "C" int sf_pair_split(int64_t nt, int64_t ns) { return sf::pair_split(nt, ns); }
 
 extern "C" int64_t sf_workspace_bytes(void) { return (int64_t)sf::workspace_bytes_total(); }
+
+extern "C" int sf_workspace_release(void) {
+    sf::workspace_release_all();
+    return SF_OK;
+}
 
 extern "C" int sf_sym_set_waves(int64_t bytes, int streams) {
     sf::sym_set_waves(bytes, streams);

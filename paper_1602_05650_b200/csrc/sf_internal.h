@@ -16,8 +16,11 @@ int set_error(int code, const char *fmt, ...);
 // are independent buffers.  Steady-state calls allocate nothing.
 class Workspace {
    public:
-    static constexpr int kSlots = 12;
+    // slots: 0-2 pair engine, 3-5 symmetric kernels, 6 skipped-pair scratch,
+    // 7-10 cross kernel, 11 side-stream stresslet sum, 12 symmetric waves
+    static constexpr int kSlots = 14;
     void *get(int slot, size_t bytes, cudaStream_t st);
+    void release();   // frees every slot (the caller synchronised the device)
     size_t bytes() const {
         size_t b = 0;
         for (int k = 0; k < kSlots; ++k) b += cap_[k];
@@ -31,6 +34,7 @@ class Workspace {
 };
 Workspace &workspace_for(cudaStream_t st);
 size_t workspace_bytes_total();
+void workspace_release_all();   // synchronises each device, frees every workspace slot
 
 // Side streams of one caller stream (keyed by device and stream), forked from
 // and joined back into it with events; created once per process.  done[0]

@@ -1058,7 +1058,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     SymSrc *packed = (SymSrc *)ws.get(3, sizeof(SymSrc) * (size_t)N, st);
     SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)((N + 31) / 32 + 1), st);
     double *acc = (double *)ws.get(5, sizeof(double) * 3 * (size_t)N, st);
-    char *bufs = (char *)ws.get(6, buf_bytes * nbuf, st);
+    char *bufs = (char *)ws.get(12, buf_bytes * nbuf, st);
     if (!packed || !meta || !acc || (!bufs && !waves.empty())) return SF_ENOMEM;
     if (cudaMemsetAsync(acc, 0, sizeof(double) * 3 * (size_t)N, st) != cudaSuccess)
         return check_launch("memset");

@@ -96,8 +96,9 @@ class Fiber:
             raise ValueError(f"aspect ratio must lie in (0, 0.1], got {eps}")
         if E <= 0:
             raise ValueError("flexural modulus must be positive")
+        self._dev = None        # devstate.DeviceState holding this fiber's step unknowns
         self._X = X.copy()
-        self.T = np.zeros(X.shape[0]) if tension is None else np.asarray(tension, dtype=float).copy()
+        self._T = np.zeros(X.shape[0]) if tension is None else np.asarray(tension, dtype=float).copy()
         self.eps = float(eps)
         self.E = float(E)
         self.growth_state = growth_state
@@ -112,17 +113,36 @@ class Fiber:
         self._geo = None
 
     # -- geometry (lazy, host) ------------------------------------------------
+    # X and T live on the device between implicit steps (devstate.DeviceState):
+    # reading them brings the whole state back once, writing them hands the
+    # state back to the host (the next step re-uploads it)
     @property
     def X(self):
+        if self._dev is not None:
+            self._dev.pull()
         return self._X
 
     @X.setter
     def X(self, value):
+        if self._dev is not None:
+            self._dev.release()
         self._X = np.asarray(value, dtype=float).copy()
         self._geo = None
 
+    @property
+    def T(self):
+        if self._dev is not None:
+            self._dev.pull()
+        return self._T
+
+    @T.setter
+    def T(self, value):
+        if self._dev is not None:
+            self._dev.release()
+        self._T = np.asarray(value, dtype=float).copy()
+
     def refresh_geometry(self):
-        s, s_alpha, L, t = spectral.fiber_geometry(self._X, self.p)
+        s, s_alpha, L, t = spectral.fiber_geometry(self.X, self.p)
         self._geo = dict(s=s, s_alpha=s_alpha, L=L, tangents=t)
 
     def _g(self, key):

@@ -553,26 +553,40 @@ def device_surface_weights(mesh, targets, mu, device, interior_jump=True, upsamp
     return W_all
 
 
-def device_surface_pairs(surfaces, targets, target_groups, mu, device, upsample=6):
-    """find_surface_pairs with the maps built on the device
-    (device_surface_weights).  Returns [(t, si, W)] in the reference's order
-    (system.py:588-613) with W (3, 3N) device rows."""
+def device_surface_pairs(surfaces, trg, tgrp, mu, device, upsample=6, surface_arrays=None):
+    """find_surface_pairs with the search and the maps on the device
+    (device_surface_weights).  trg (nt, 3) and tgrp (nt,) are device
+    tensors.  Candidates: other constituents' targets in the radial band of
+    the mesh, then the nearest node closer than 1.5 h (system.py:588-613),
+    both on the device; only the near targets' coordinates come back to the
+    host for the per-target nearest-point preparation.  Returns
+    [(t, si, W)] in the reference's order with W (3, 3N) device rows."""
+    import torch
+    f64 = dict(dtype=torch.float64, device=device)
     out = []
     for si, (mesh, group, is_periphery) in enumerate(surfaces):
-        others = target_groups != group
+        if surface_arrays is not None:
+            nodes = surface_arrays[si][0]
+        else:
+            nodes = torch.as_tensor(mesh.nodes, **f64)
+        center = getattr(mesh, "center_dev", None)
+        if center is None:
+            center = torch.as_tensor(mesh.center, **f64)
         shell = 1.5 * mesh.h
-        rel = np.linalg.norm(targets - mesh.center, axis=1)
-        rho_nodes = np.linalg.norm(mesh.nodes - mesh.center, axis=1)
-        band = others & (rel >= rho_nodes.min() - shell) & (rel <= rho_nodes.max() + shell)
-        cand = np.nonzero(band)[0]
-        if cand.size == 0:
+        rel = torch.linalg.vector_norm(trg - center, dim=1)
+        rho_nodes = torch.linalg.vector_norm(nodes - center, dim=1)
+        band = (tgrp != group) & (rel >= rho_nodes.min() - shell) & (rel <= rho_nodes.max() + shell)
+        cand = torch.nonzero(band).reshape(-1)
+        if cand.numel() == 0:
             continue
-        from scipy.spatial import cKDTree
-        d, _ = cKDTree(mesh.nodes).query(targets[cand], k=1)
-        near = cand[d * d < shell * shell]
+        d2 = torch.empty(cand.numel(), **f64)
+        for a in range(0, cand.numel(), 128):          # nearest node, brute force in chunks
+            c = trg[cand[a:a + 128]]
+            d2[a:a + 128] = ((c[:, None, :] - nodes[None, :, :]) ** 2).sum(dim=2).min(dim=1).values
+        near = cand[d2 < shell * shell].cpu().numpy()
         if near.size == 0:
             continue
-        W = device_surface_weights(mesh, targets[near], mu, device,
-                                   interior_jump=is_periphery, upsample=upsample)
+        W = device_surface_weights(mesh, trg[torch.as_tensor(near, device=device)].cpu().numpy(),
+                                   mu, device, interior_jump=is_periphery, upsample=upsample)
         out.extend((int(t), si, W[j]) for j, t in enumerate(near))
     return out

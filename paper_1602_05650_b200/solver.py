@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 from . import _native, spectral
-from .system import ConfigurationError, InteractionCache, external_force_density
+from .system import ConfigurationError, InteractionCache
 
 LOG = logging.getLogger("paper_1602_05650_b200.solver")
 
@@ -63,7 +63,7 @@ class StepLayout:
         for part in state.particles:
             self.U.append(slice(off, off + 3))
             self.omega.append(slice(off + 3, off + 6))
-            n = part.mesh.n_nodes
+            n = part.n_nodes
             self.q1.append(slice(off + 6, off + 6 + 3 * n))
             off += 6 + 3 * n
         self.q0 = None
@@ -115,6 +115,20 @@ def _precision_mode(precision):
     return modes[precision]
 
 
+def _external_force_density_device(state, g, nb, n):
+    """external_force_density (system.py:297-305) for one order class on the
+    device, from the class's device tangents: the same elementwise sums in
+    the same model order."""
+    import torch
+    f = torch.zeros((nb, n, 3), dtype=torch.float64, device=g.tang.device)
+    for m in state.force_models:
+        if m.kind == "uniformBodyForce":
+            f += torch.as_tensor(m.f0 * m.direction, dtype=torch.float64, device=f.device)
+        elif m.kind == "cytoplasmicPulling":
+            f += (m.motor_force * m.motor_density) * g.tang
+    return f
+
+
 class _FiberBatch:
     """Fibers of one Chebyshev order: the frozen per-fiber operators and the
     sf_fiber_sys the per-fiber kernels take.  Unknown blocks and point ranges
@@ -145,8 +159,7 @@ class _FiberBatch:
         self.Ldot = torch.as_tensor(np.array([f.Ldot for f in fibs], dtype=float), **f64)
         self.f_ext = None
         if st.force_models:
-            self.f_ext = torch.as_tensor(np.ascontiguousarray(np.stack(
-                [external_force_density(st, f) for f in fibs])), **f64)
+            self.f_ext = _external_force_density_device(st, g, nb, n)
         kinds = np.zeros((nb, 2), dtype=np.int32)
         par = np.zeros((nb, 2, 12))
         body = np.full(nb, -1, dtype=np.int32)
@@ -208,8 +221,7 @@ class BlockOperator:
         self.nf, self.n = nf, c.n_nodes
         np_ = len(state.particles)
         self.np = np_
-        self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
-                        if np_ else None)
+        self.pcenter = self.cache.pcenter if np_ else None
         self.p_uoff = torch.as_tensor(np.array([s.start for s in self.layout.U], dtype=np.int64),
                                       device=dev) if np_ else None
         self.ext = (torch.as_tensor(np.stack([np.concatenate([p.F_ext, p.L_ext])
@@ -228,20 +240,18 @@ class BlockOperator:
                 for k, m in enumerate(b.idx):
                     blocks[m] = b.blocks[k]
             self.fiber_blocks = blocks
-        # surface data per particle / periphery
+        # surface data per particle / periphery, the cache's device arrays
         self.surf = []
         for i, part in enumerate(state.particles):
-            m = part.mesh
-            self.surf.append(dict(kind=0, pi=i, nodes=torch.as_tensor(m.nodes, **f64),
-                                  nrm=torch.as_tensor(m.normals, **f64),
-                                  w=torch.as_tensor(m.weights, **f64), n=m.n_nodes, area=m.area,
+            m = c.surfaces[i][0]
+            nodes, nrm, w = c.surface_arrays[i]
+            self.surf.append(dict(kind=0, pi=i, nodes=nodes, nrm=nrm, w=w, n=m.n_nodes, area=m.area,
                                   center=self.pcenter[i], sl=self.layout.q1[i],
                                   uom=self.layout.U[i].start, tsl=c.particle_slices[i]))
         if state.periphery is not None:
-            m = state.periphery.mesh
-            self.surf.append(dict(kind=1, nodes=torch.as_tensor(m.nodes, **f64),
-                                  nrm=torch.as_tensor(m.normals, **f64),
-                                  w=torch.as_tensor(m.weights, **f64), n=m.n_nodes, area=m.area,
+            m = c.surfaces[-1][0]
+            nodes, nrm, w = c.surface_arrays[-1]
+            self.surf.append(dict(kind=1, nodes=nodes, nrm=nrm, w=w, n=m.n_nodes, area=m.area,
                                   center=None, sl=self.layout.q0, uom=None,
                                   tsl=c.periphery_slice))
         # scratch
@@ -485,20 +495,20 @@ def _particle_block_inverse(op):
     normals and weights, so the inverse is reused while the particles
     translate (relative geometry equal to 1e-13 of its size)."""
     import torch
-    key = [(np.asarray(p.mesh.nodes) - np.asarray(p.center), np.asarray(p.mesh.normals),
-            np.asarray(p.mesh.weights)) for p in op.state.particles]
+    key = [(s["nodes"] - s["center"], s["nrm"], s["w"]) for s in op.surf if s["kind"] == 0]
 
     def same(a, b):
+        """Relative geometry equal to 1e-13 (one flag read on the device)."""
         if len(a) != len(b):
             return False
+        flags = []
         for (r1, n1, w1), (r2, n2, w2) in zip(a, b):
-            if r1.shape != r2.shape:
+            if r1.shape != r2.shape or r1.device != r2.device:
                 return False
-            scale = max(1.0, float(np.abs(r1).max()))
-            if (np.abs(r1 - r2).max() > 1e-13 * scale or np.abs(n1 - n2).max() > 1e-13
-                    or np.abs(w1 - w2).max() > 1e-13 * float(np.abs(w1).max())):
-                return False
-        return True
+            scale = torch.clamp(r1.abs().max(), min=1.0)
+            flags.append(((r1 - r2).abs().max() <= 1e-13 * scale) & ((n1 - n2).abs().max() <= 1e-13)
+                         & ((w1 - w2).abs().max() <= 1e-13 * w1.abs().max()))
+        return bool(torch.stack(flags).all())
     for entry in _PARTICLE_INV_CACHE:
         k, mu, dev, inv = entry
         if mu == op.mu and dev == op.device and same(k, key):
@@ -716,10 +726,35 @@ def _as_apply(obj, device):
     return wrapped
 
 
-def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
-    """Left-preconditioned restarted GMRES (solver.py:444-516) with the Krylov
-    basis on the device.  Returns (solution, iterations, residual history);
-    the solution has the type of `rhs` (numpy or CUDA tensor)."""
+_GMRES_STATUS_RING = 8
+
+
+def _status_lag(operator):
+    """Arnoldi steps queued ahead of the convergence read.  With lag 1 the
+    host enqueues step k+1 before it waits for step k's status, so the GPU
+    never idles on the host; the price is one speculative matvec when the
+    solve converges, which only pays off while a matvec is cheap next to
+    the host's per-step launch work.  SF_GMRES_LAG overrides."""
+    env = os.environ.get("SF_GMRES_LAG")
+    if env is not None:
+        return max(0, int(env))
+    cache = getattr(operator, "cache", None)
+    pairs = getattr(cache, "pairs_per_apply", None) if cache is not None else None
+    if pairs is None:
+        return 1
+    return 1 if pairs < 2e10 else 0
+
+
+def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
+    """Left-preconditioned restarted GMRES (solver.py:444-516), entirely on
+    the device: Krylov basis, fused modified Gram-Schmidt (sf_gmres_mgs),
+    Hessenberg rotations, residual estimate and the restart update
+    (sf_gmres_givens / sf_gmres_update).  Per Arnoldi step the host reads one
+    4-double status record, copied asynchronously into pinned memory and
+    consumed `lag` steps late (see _status_lag); once per cycle it reads the
+    scalars and the residual history.  Returns (solution, iterations,
+    residual history); the solution has the type of `rhs` (numpy or CUDA
+    tensor)."""
     import torch
     if params is None:
         params = GmresParams()
@@ -732,6 +767,8 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
     st = _stream()
     n = rhs_d.numel()
     fused = os.environ.get("SF_GMRES_FUSED", "1") != "0"
+    if lag is None:
+        lag = _status_lag(operator)
 
     def ret(x):
         return x.cpu().numpy() if host_io else x
@@ -745,9 +782,17 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
     warm = x0 is not None
     x = (torch.as_tensor(x0, dtype=torch.float64, device=device).clone() if warm
          else torch.zeros(n, dtype=torch.float64, device=device))
-    R = params.restart
+    R, maxit = params.restart, params.max_iterations
     V = torch.empty((R + 1, n), dtype=torch.float64, device=device)
     hcol = torch.empty(R + 2, dtype=torch.float64, device=device)
+    lib = _native.load(require_device=True)
+    ns = int(lib.sf_gmres_state_doubles(R, maxit))
+    gs = torch.zeros(ns, dtype=torch.float64, device=device)
+    status = torch.zeros(4, dtype=torch.float64, device=device)
+    ring = torch.zeros((_GMRES_STATUS_RING, 4), dtype=torch.float64).pin_memory()
+    events = [torch.cuda.Event() for _ in range(_GMRES_STATUS_RING)]
+    hist_off = ns - maxit
+    _native.call("sf_gmres_reset", _ptr(gs), R, maxit, beta0, params.tolerance, st)
     history = []
     iters = 0
     while True:
@@ -756,14 +801,10 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
         beta = float(scal[0].item())
         if beta / beta0 <= params.tolerance:
             return ret(x), iters, history or [beta / beta0]
-        V[0].copy_(r / beta)
-        H = np.zeros((R + 1, R))
-        cs = np.zeros(R)
-        sn = np.zeros(R)
-        g = np.zeros(R + 1)
-        g[0] = beta
+        _native.call("sf_gmres_cycle", _ptr(gs), R, _ptr(scal[0:1]), _ptr(r), _ptr(V[0]), n, st)
         k = 0
-        while k < R and iters < params.max_iterations:
+        pending = []
+        while k < R and iters + k < maxit:
             w = apply_m(apply_a(V[k])).contiguous()
             if fused:
                 # wnorm, modified Gram-Schmidt, |w| and V[k+1] = w/|w| in one launch
@@ -776,37 +817,32 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None):
                     _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w),
                                  n, st)
                 vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
-            hh = hcol.cpu().numpy()
-            wnorm = float(hh[R + 1])
-            H[:k + 2, k] = hh[:k + 2]
-            for j in range(k):
-                tmp = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
-                H[j + 1, k] = -sn[j] * H[j, k] + cs[j] * H[j + 1, k]
-                H[j, k] = tmp
-            denom = math.hypot(H[k, k], H[k + 1, k])
-            cs[k] = H[k, k] / denom if denom else 1.0
-            sn[k] = H[k + 1, k] / denom if denom else 0.0
-            H[k, k] = denom
-            g[k + 1] = -sn[k] * g[k]
-            g[k] = cs[k] * g[k]
-            iters += 1
-            rel = abs(g[k + 1]) / beta0
-            history.append(rel)
-            breakdown = H[k + 1, k] <= 1e-12 * max(wnorm, 1e-300)
-            if not breakdown and not fused:
                 _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]),
                              n, st)
+            _native.call("sf_gmres_givens", _ptr(hcol), _ptr(gs), R, k, _ptr(status), st)
+            slot = k % _GMRES_STATUS_RING
+            ring[slot].copy_(status, non_blocking=True)
+            events[slot].record()
+            pending.append(slot)
             k += 1
-            if rel <= params.tolerance or breakdown:
+            done = False
+            while len(pending) > lag:
+                s0 = pending.pop(0)
+                events[s0].synchronize()
+                if ring[s0, 0] != 0.0:
+                    done = True
+                    break
+            if done:
                 break
-        if k:
-            y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
-            coef = torch.as_tensor(y, dtype=torch.float64, device=device)
-            _native.call("sf_combine", _ptr(V), n, k, _ptr(coef), _ptr(x), n, st)
+        _native.call("sf_gmres_update", _ptr(V), n, _ptr(gs), R, _ptr(x), n, st)
+        sc = gs[hist_off - 8:].cpu().numpy()            # scalars + history (one read per cycle)
+        new_iters = int(sc[1])
+        history.extend(float(h) for h in sc[8 + iters:8 + new_iters])
+        iters = new_iters
         rel = history[-1] if history else 0.0
         if rel <= params.tolerance:
             return ret(x), iters, history
-        if iters >= params.max_iterations:
+        if iters >= maxit:
             raise NonconvergenceError(
                 f"GMRES did not reach {params.tolerance:g} within "
                 f"{params.max_iterations} iterations (residual {rel:.3e})",
@@ -847,7 +883,12 @@ def warm_start_vector(state, layout):
     positions X^n for the candidate X^(n+1), the previous step's tensions,
     rigid velocities and densities.  Its residual is O(dt |velocity|), so
     GMRES started there reaches the same relative tolerance (measured
-    against the preconditioned rhs, solver.py:459-462) in fewer iterations."""
+    against the preconditioned rhs, solver.py:459-462) in fewer iterations.
+    A device tensor when the state lives on the device (devstate)."""
+    from . import devstate
+    mirror = devstate.mirror_of(state)
+    if mirror is not None:
+        return mirror.unknowns_vector(layout)
     x0 = np.zeros(layout.size)
     for i, part in enumerate(state.particles):
         x0[layout.U[i]] = part.U
@@ -865,17 +906,33 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
                         implicit_coupling=True, return_info=False, precision="fp64",
                         body_coupling=False, warm_start=False):
     """Advance the state by one implicit step on the device, halving dt on
-    nonconvergence (solver.py:528-592).  Two options beyond the reference
-    (off by default, same solution to the GMRES tolerance):
-    body_coupling=True selects the body-coupled preconditioner (see
-    Preconditioner); warm_start=True starts GMRES from the current state
-    (warm_start_vector) instead of zero."""
+    nonconvergence (solver.py:528-592).
+
+    The state stays on the device (devstate.DeviceState): the step reads the
+    centrelines, tensions, particle meshes and densities from device
+    tensors, and writes the solution back into new device tensors (X, T, q,
+    U, omega; the particles translate by dt U); the host objects read them
+    back only when user code touches them.  Polymerization kinetics and the
+    contact models (per-fiber host logic with the reference's RNG draws)
+    run only when a fiber is not STALLED or a contact model is configured,
+    as in the reference (solver.py:574-588); none of the BASELINE configs
+    has either.
+
+    Two options beyond the reference (off by default, same solution to the
+    GMRES tolerance): body_coupling=True selects the body-coupled
+    preconditioner (see Preconditioner); warm_start=True starts GMRES from
+    the current state (warm_start_vector) instead of zero."""
+    import torch
+
+    from . import devstate
     from . import fiber as fibers_
     if dt <= 0:
         raise ConfigurationError("time step must be positive")
     if dt_min is None:
         dt_min = dt / 64.0
     attempt = float(dt)
+    _native.load(require_device=True)
+    mirror = devstate.for_state(state, torch.device("cuda", torch.cuda.current_device()))
     cache = InteractionCache(state, backend=backend, mode=_precision_mode(precision))
     while True:
         op, rhs = assemble_step_operator(state, attempt, mu=mu, backend=backend, cache=cache,
@@ -891,23 +948,21 @@ def backward_euler_step(state, dt, params=None, mu=None, backend=None, dt_min=No
             if attempt / 2.0 < dt_min:
                 raise
             attempt /= 2.0
-    sol = sol.cpu().numpy()
-    parts = op.layout.unpack(sol)
-    from .system import ConfigurationError as _CE
+    lay = op.layout
+    # non-spherical particles cannot rotate (their polar parametrisation
+    # would break): the reference's check, before any state changes
     for i, part in enumerate(state.particles):
-        if not _rotation_is_representable(part, parts.omega[i], attempt):
-            raise _CE("rotation of a non-spherical particle is not supported")
-        part.U = parts.U[i].copy()
-        part.omega = parts.omega[i].copy()
-        part.q = parts.q1[i].copy()
-        part.translate(attempt * part.U)
-    if state.periphery is not None:
-        state.periphery.q = parts.q0.copy()
-    for m, fib in enumerate(state.fibers):
-        fib.X = parts.X[m].copy()
-        fib.T = parts.T[m].copy()
+        shape = part.__dict__["_mesh"].shape
+        if shape is None or shape[0] != "sphere":
+            omega = sol[lay.omega[i]].cpu().numpy()
+            if float(np.linalg.norm(omega)) * attempt >= 1e-14:     # _rotation_is_representable
+                raise ConfigurationError("rotation of a non-spherical particle is not supported")
+    mirror.write_solution(sol, lay, attempt)
     state.time += attempt
-    _kinetics_and_contacts(state, attempt)
+    if state.force_models and any(m.kind in ("corticalPushing", "cytoplasmicPulling")
+                                  for m in state.force_models) or \
+            any(f.growth_state != fibers_.STALLED for f in state.fibers):
+        _kinetics_and_contacts(state, attempt)
     LOG.info("step time=%.9g dt=%.3e gmres_iterations=%d residual=%.3e",
              state.time, attempt, iters, history[-1] if history else 0.0)
     if return_info:

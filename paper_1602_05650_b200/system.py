@@ -418,6 +418,40 @@ class FiberGeometry:
             self.delta = torch.where(ratio > 0, ratio * self.L, self.delta)
 
 
+class _DeviceMesh:
+    """A moving rigid particle's mesh while its nodes live on the device:
+    the static attributes (normals, weights, parametrisation, shape) of the
+    host mesh, the current nodes and centre as device tensors, host copies
+    of those read back on demand."""
+
+    def __init__(self, base, nodes_dev, center_dev):
+        self.base = base
+        self.nodes_dev = nodes_dev
+        self.center_dev = center_dev
+        for a in ("normals", "weights", "thetas", "phis", "patch_grid", "shape", "area", "h"):
+            setattr(self, a, getattr(base, a))
+        self._nodes = self._center = None
+
+    @property
+    def n_nodes(self):
+        return self.base.n_nodes
+
+    def has_parametrization(self):
+        return self.base.has_parametrization()
+
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            self._nodes = self.nodes_dev.cpu().numpy()
+        return self._nodes
+
+    @property
+    def center(self):
+        if self._center is None:
+            self._center = self.center_dev.cpu().numpy()
+        return self._center
+
+
 class InteractionCache:
     """Frozen-geometry layout of complementary_velocities, resident on the B200
     (system.py:492-620).  Rebuild whenever any constituent moves."""
@@ -443,7 +477,15 @@ class InteractionCache:
                 now = time.perf_counter()
                 print(f"  cache {label:28s} {1e3 * (now - _t[0]):9.2f} ms", flush=True)
                 _t[0] = now
-        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        from . import devstate
+        # the step's state on the device (devstate.DeviceState): targets,
+        # fiber geometry and surfaces come from its tensors, not the host
+        mirror = devstate.mirror_of(state) if fiber_geometry is None else None
+        self.mirror = mirror
+        if mirror is not None:
+            self.device = mirror.device
+        else:
+            self.device = torch.device(device) if device is not None else torch.device("cuda")
         dev = dict(device=self.device)
         f64 = dict(dtype=torch.float64, **dev)
         self.include_doublet = include_doublet
@@ -452,19 +494,39 @@ class InteractionCache:
         np_ = len(state.particles)
         self.nf, self.np = nf, np_
 
-        blocks, groups = [], []
+        # surfaces: particles then periphery (system.py:544-557); moving
+        # particle meshes are device-backed views while a mirror is live
+        self.surfaces = []
+        surf_dev = []
+        for i, part in enumerate(state.particles):
+            if mirror is not None:
+                mesh = _DeviceMesh(part.__dict__["_mesh"], mirror.pnodes[i], mirror.pmesh_center[i])
+                surf_dev.append((mesh.nodes_dev, mirror.pnrm[i], mirror.pw[i]))
+            else:
+                mesh = part.mesh
+                surf_dev.append(None)
+            self.surfaces.append((mesh, nf + i, False))
+        if state.periphery is not None:
+            self.surfaces.append((state.periphery.mesh, nf + np_, True))
+            surf_dev.append((mirror.per_nodes, mirror.per_nrm, mirror.per_w)
+                            if mirror is not None else None)
+        self.surface_arrays = [
+            sd if sd is not None else (torch.as_tensor(m.nodes, **f64),
+                                       torch.as_tensor(m.normals, **f64),
+                                       torch.as_tensor(m.weights, **f64))
+            for sd, (m, _, _) in zip(surf_dev, self.surfaces)]
+
+        groups = []
         self.particle_slices = []
         off = 0
         for i, part in enumerate(state.particles):
-            n = part.mesh.n_nodes
-            blocks.append(part.mesh.nodes)
+            n = self.surfaces[i][0].n_nodes
             groups.append(np.full(n, nf + i, dtype=np.int64))
             self.particle_slices.append(slice(off, off + n))
             off += n
         self.periphery_slice = None
         if state.periphery is not None:
             n = state.periphery.mesh.n_nodes
-            blocks.append(state.periphery.mesh.nodes)
             groups.append(np.full(n, nf + np_, dtype=np.int64))
             self.periphery_slice = slice(off, off + n)
             off += n
@@ -478,14 +540,25 @@ class InteractionCache:
         self.fiber_slice = slice(off, off + npts)
         self.fiber_slices = [slice(off + int(self.pt_off[m]), off + int(self.pt_off[m] + ns[m]))
                              for m in range(nf)]
-        blocks.append(np.concatenate([f.X for f in state.fibers]) if nf else np.zeros((0, 3)))
         groups.append(np.repeat(np.arange(nf, dtype=np.int64), ns))
-        self.targets = np.vstack(blocks) if blocks else np.zeros((0, 3))
         self.target_groups = np.concatenate(groups) if groups else np.zeros(0, np.int64)
+        # target positions [particles | periphery | fibers], on the device
+        tblocks = [a[0] for a in self.surface_arrays]
+        if mirror is not None:
+            fx = torch.empty((npts, 3), **f64)
+            for n, idx, X in mirror.fiber_X():
+                pidx = torch.as_tensor((self.pt_off[idx][:, None] + np.arange(n)).reshape(-1), **dev)
+                fx[pidx] = X.reshape(-1, 3)
+            tblocks.append(fx)
+        else:
+            tblocks.append(torch.as_tensor(np.concatenate([f.X for f in state.fibers]) if nf
+                                           else np.zeros((0, 3)), **f64))
+        trg = torch.cat(tblocks) if len(tblocks) > 1 else tblocks[0]
+        self._targets_host = None
         self.target_offset = 0
         if target_range is not None:
             lo, hi = target_range
-            self.targets = self.targets[lo:hi]
+            trg = trg[lo:hi]
             self.target_groups = self.target_groups[lo:hi]
             self.target_offset = lo
 
@@ -497,7 +570,8 @@ class InteractionCache:
                 self.periphery_slice = clip(self.periphery_slice)
             self.fiber_slice = clip(self.fiber_slice)
             self.fiber_slices = [clip(x) for x in self.fiber_slices]
-        self.n_targets = self.targets.shape[0]
+        self.trg = trg.contiguous()
+        self.n_targets = self.trg.shape[0]
         kind = getattr(backend, "kind", "direct") if backend is not None else "direct"
         if kind not in ("direct", "treeAccelerated"):
             raise ConfigurationError(f"backend {kind!r} is not available on the device")
@@ -517,12 +591,13 @@ class InteractionCache:
                                                             self.device))]
         else:
             self.classes = []
+            Xdev = {n: X for n, _, X in mirror.fiber_X()} if mirror is not None else None
             for n, idx in order_classes(state.fibers):
                 fibs = [state.fibers[m] for m in idx]
                 ratios = [f.delta_ratio if f.delta_ratio is not None else -1.0 for f in fibs]
                 deltas = [0.0 if f.delta_ratio is not None else f.delta for f in fibs]
-                self.classes.append((n, idx, FiberGeometry(stack_fibers(fibs), ratios, deltas,
-                                                           self.device)))
+                X = Xdev[n] if Xdev is not None else stack_fibers(fibs)
+                self.classes.append((n, idx, FiberGeometry(X, ratios, deltas, self.device)))
         self.geo = self.classes[0][2] if (self.uniform and self.classes) else None
         if self.geo is not None:
             self.fsrc = self.geo.X.reshape(-1, 3)
@@ -542,10 +617,6 @@ class InteractionCache:
         self.fdcoef = (((self.eps * self.fL) ** 2 / 2.0).repeat_interleave(
             torch.as_tensor(ns, **dev)) if include_doublet and nf else None)   # system.py:542
 
-        # surfaces: particles then periphery (system.py:544-557)
-        self.surfaces = [(p.mesh, nf + i, False) for i, p in enumerate(state.particles)]
-        if state.periphery is not None:
-            self.surfaces.append((state.periphery.mesh, nf + np_, True))
         self.surface_offsets = []
         o = 0
         for m, _, _ in self.surfaces:
@@ -553,16 +624,18 @@ class InteractionCache:
             o += m.n_nodes
         self.nss = o
         if self.surfaces:
-            self.ssrc = torch.as_tensor(np.vstack([m.nodes for m, _, _ in self.surfaces]), **f64)
-            self.snrm = torch.as_tensor(np.vstack([m.normals for m, _, _ in self.surfaces]), **f64)
-            self.sw = torch.as_tensor(np.concatenate([m.weights for m, _, _ in self.surfaces]), **f64)
+            self.ssrc = torch.cat([a[0] for a in self.surface_arrays]).contiguous()
+            self.snrm = torch.cat([a[1] for a in self.surface_arrays]).contiguous()
+            self.sw = torch.cat([a[2] for a in self.surface_arrays]).contiguous()
             self.sgrp = torch.as_tensor(np.concatenate(
                 [np.full(m.n_nodes, g, dtype=np.int64) for m, g, _ in self.surfaces]), **dev)
         else:
             self.ssrc = self.snrm = self.sw = self.sgrp = None
-        self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
-                        if np_ else None)
-        self.trg = torch.as_tensor(self.targets, **f64).contiguous()
+        if mirror is not None:
+            self.pcenter = mirror.pcenter if np_ else None
+        else:
+            self.pcenter = (torch.as_tensor(np.stack([p.center for p in state.particles]), **f64)
+                            if np_ else None)
         self.tgrp = torch.as_tensor(self.target_groups, **dev)
         self.pgrp = torch.as_tensor(np.arange(nf, nf + np_, dtype=np.int64), **dev) if np_ else None
 
@@ -594,7 +667,8 @@ class InteractionCache:
                     self.surfaces, self.targets, self.target_groups, state.mu)
             else:
                 self.near_surface = nearfield.device_surface_pairs(
-                    self.surfaces, self.targets, self.target_groups, state.mu, self.device)
+                    self.surfaces, self.trg, self.tgrp, state.mu, self.device,
+                    surface_arrays=self.surface_arrays)
         _lap("near surface maps")
         self._build_near_map()
         _lap("near CSR")
@@ -663,15 +737,45 @@ class InteractionCache:
         return entries
 
 
+    @property
+    def targets(self):
+        """Target positions (n_targets, 3) on the host (read back on demand;
+        the device path uses trg)."""
+        if self._targets_host is None:
+            self._targets_host = self.trg.cpu().numpy()
+        return self._targets_host
+
     def _check_surface_overlaps(self):
-        for mesh, group, is_periphery in self.surfaces:
+        """Targets of other constituents inside a rigid particle or outside
+        the periphery raise OverlapError (system.py:581-583, 591-598).  Sphere
+        meshes are tested on the device (rho < R, one flag read for all
+        surfaces); other star-shaped profiles on the host."""
+        import torch
+        flags = []
+        for si, (mesh, group, is_periphery) in enumerate(self.surfaces):
+            if mesh.shape is None:
+                continue
+            if mesh.shape[0] == "sphere":
+                center = getattr(mesh, "center_dev", None)
+                if center is None:
+                    center = torch.as_tensor(mesh.center, dtype=torch.float64, device=self.device)
+                rho = torch.linalg.vector_norm(self.trg - center, dim=1)
+                inside = rho < float(mesh.shape[1])
+                bad = (self.tgrp != group) & (~inside if is_periphery else inside)
+                flags.append(bad.any())
+                continue
             others = self.target_groups != group
-            if mesh.shape is not None:
-                inside = _inside_star_surface(mesh, self.targets)
-                if is_periphery and np.any(others & ~inside):
-                    raise OverlapError("a target lies outside the confining periphery")
-                if not is_periphery and np.any(others & inside):
-                    raise OverlapError("a target lies inside a rigid particle")
+            inside = _inside_star_surface(mesh, self.targets)
+            flags.append(torch.tensor(bool(np.any(others & ~inside) if is_periphery
+                                           else np.any(others & inside)), device=self.device))
+        if not flags:
+            return
+        hit = torch.stack(flags).cpu().numpy()
+        for f, (mesh, group, is_periphery) in zip(hit, [x for x in self.surfaces
+                                                        if x[0].shape is not None]):
+            if f:
+                raise OverlapError("a target lies outside the confining periphery" if is_periphery
+                                   else "a target lies inside a rigid particle")
 
     def _build_near_map(self):
         """CSR by target of every correction map, fiber entries before surface

@@ -73,9 +73,12 @@ def test_c5_scratch_is_bounded(cuda, waves_reset):
     """C5 (1,048,576 points): the library's scratch after one evaluation stays
     near 2 x 192 MB of wave buffers plus the packed sources and sums (the
     unbounded G x N x 3 slot buffer was 8.6 GB)."""
+    lib = _native.load()
     cl = configs.make("c5", seed=0)
     f = configs.forces(cl, seed=1)
     op = FiberHIOperator(cl.X, cl.eps, device=cuda)
+    lib.sf_workspace_release()             # scratch other tests' calls left behind
+    assert lib.sf_workspace_bytes() == 0
     _apply(op, f)
-    held = _native.load().sf_workspace_bytes()
+    held = lib.sf_workspace_bytes()
     assert held < 1.0e9, held
