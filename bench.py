@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
     ap.add_argument("--launch-check", action="store_true",
                     help="start the ranks (gloo), print one JSON line per rank, do no work")
-    ap.add_argument("--step-config", default="c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
+    ap.add_argument("--step-config", default="c1,c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated, each with optional "
                          "':fp32c' / ':body' / ':warm' ('+'-joined) options ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
@@ -150,18 +150,95 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-REFERENCE_STEPS = os.path.join(ROOT, "profiles", "r02_reference_cpu_steps.json")
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
 
 
-def reference_cpu_steps():
-    """Implicit steps/s of the reference's own Python path (slenderflow,
-    backward_euler_step) measured in the build container on the BASELINE
-    configs (tools/reference_cpu_steps.py); the reference is not importable
-    on the GPU box, so this is a recorded figure, labelled as such."""
-    if not os.path.exists(REFERENCE_STEPS):
-        return None
-    with open(REFERENCE_STEPS) as fh:
-        return json.load(fh)
+def c1_step_state(pkg):
+    """C1 as implicit steps (the golden bstep_c1 case): 64 fibers, p = 31,
+    centres in [-2,2]^3 with 2 eps L segment clearance (near pairs present,
+    maps rebuilt every step), uniform force density (0,0,-1); built with
+    `pkg`'s own constructors (this package's or slenderflow's)."""
+    from paper_1602_05650_b200 import configs
+    cl = configs.fiber_cloud(64, 31, eps=1e-2, E=1.0, region="cube", size=2.0, seed=0,
+                             clear=2e-2, check="segment")
+    fibs = [pkg["fiber"].Fiber(X, eps=1e-2, E=1.0) for X in cl.X]
+    return pkg["system"].SystemState(
+        fibs, force_models=[pkg["system"].UniformBodyForce(1.0, (0.0, 0.0, -1.0))])
+
+
+def c2_step_state(pkg):
+    """C2 (the golden bstep_c2 case): 1,024 fibers p = 31 clamped radially to
+    an (8,8) sphere of radius 0.5, plus-end force 1 along the tangent."""
+    from paper_1602_05650_b200 import configs
+    pts, dirs = configs.aster_layout(1024, 0.5, 1.3, (0.0, 0.0, 0.0), 0.05, 0, "random")
+    F, B = pkg["fiber"], pkg["body"]
+    part = B.RigidParticle(B.make_surface(B.sphere_shape(0.5), (8, 8)))
+    fibs = [F.straight_fiber(31, x0, d, 1.0, eps=1e-2, E=1.0,
+                             bc_minus=F.ClampedToBody(0, x0, d),
+                             bc_plus=F.PrescribedForceTorque(1.0 * d)) for x0, d in zip(pts, dirs)]
+    return pkg["system"].SystemState(fibs, [part])
+
+
+def reference_implicit_steps(threads, c2_iterations=None):
+    """Implicit steps/s of the reference's OWN Python path -- slenderflow's
+    backward_euler_step, unmodified, staged in baseline/_ref by build() --
+    on the host cores (numba prange over `threads` threads, BLAS single
+    threaded as SURVEY §6 prescribes, JIT compilation excluded).
+    C1: one warm-up step, then two timed steps.  C2: a full step is ~7.5 min
+    on 8 cores, so one step is timed in parts -- InteractionCache +
+    assemble_step_operator + Preconditioner once, two matvecs
+    (BlockOperator.apply + Preconditioner.apply) -- and the step is
+    setup + (iterations + 2) matvecs with the reference's own iteration count
+    (tests/golden/bstep_c2.npz), labelled as extrapolated."""
+    if not os.path.isdir(os.path.join(REF_PKG, "slenderflow")):
+        return {"unavailable": "reference not staged in baseline/_ref"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    os.environ["NUMBA_NUM_THREADS"] = str(threads)
+    import importlib
+
+    from threadpoolctl import threadpool_limits
+    sys.path.insert(0, REF_PKG)
+    try:
+        pkg = {m: importlib.import_module(f"slenderflow.{m}")
+               for m in ("fiber", "body", "system", "solver")}
+    finally:
+        sys.path.remove(REF_PKG)
+    sv = pkg["solver"]
+    out = []
+    with threadpool_limits(1, user_api="blas"):
+        st = c1_step_state(pkg)
+        params = sv.GmresParams(tolerance=1e-10)
+        sv.backward_euler_step(st, 5e-3, params)              # JIT warm-up
+        times = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            sv.backward_euler_step(st, 5e-3, params)
+            times.append(time.perf_counter() - t0)
+        out.append({"config": "c1: 64 fibers x 32 nodes cube cloud (near pairs), gravity",
+                    "steps": 2, "ms_per_step": 1e3 * sum(times) / 2,
+                    "steps_per_s": 2 / sum(times), "timing": "measured, full steps"})
+        st = c2_step_state(pkg)
+        t0 = time.perf_counter()
+        cache = pkg["system"].InteractionCache(st)
+        op, rhs = sv.assemble_step_operator(st, 1e-3, cache=cache)
+        prec = sv.Preconditioner(op)
+        setup = time.perf_counter() - t0
+        u = np.random.default_rng(0).standard_normal(op.layout.size)
+        mv = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            prec.apply(op.apply(u))
+            mv.append(time.perf_counter() - t0)
+        its = c2_iterations
+        if its is None:
+            g = os.path.join(ROOT, "tests", "golden", "bstep_c2.npz")
+            its = int(np.load(g)["iters_0"]) if os.path.exists(g) else 175
+        step = setup + (its + 2) * min(mv)
+        out.append({"config": "c2: 1024 fibers x 32 nodes clamped to a sphere (8x8 patches)",
+                    "ms_per_step": 1e3 * step, "steps_per_s": 1.0 / step,
+                    "setup_s": setup, "matvec_s": min(mv), "gmres_iterations": its,
+                    "timing": "extrapolated: setup + (iterations + 2) x measured matvec"})
+    return {"threads": threads, "steps": out}
 
 
 def run_reference(args, rank, world):
@@ -203,7 +280,8 @@ def run_reference(args, rank, world):
                                    f"(a full matvec is {N / rows:.0f}x the sample)"},
         "e2e": {"value": value, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "reference_implicit_steps": reference_cpu_steps(),
+        "implicit_steps": (reference_implicit_steps(threads)
+                           if args.step_config else None),
     }
     print(json.dumps(line), flush=True)
 
@@ -221,8 +299,14 @@ def measure_steps(config, count, comm=None, warm=True):
     precision = "fp32c" if "fp32c" in opts else "fp64"
     body = "body" in opts          # body-coupled preconditioner (not in the reference)
     warm_start = "warm" in opts    # GMRES warm start from the current state (not in the reference)
-    if config == "c2":
-        st = configs.aster(n_fibers=1024)
+    from paper_1602_05650_b200 import body as body_, fiber as fiber_, system as system_
+    ours = {"fiber": fiber_, "body": body_, "system": system_}
+    if config == "c1":
+        st = c1_step_state(ours)
+        dt, tol = 5e-3, 1e-10
+        desc = "c1: 64 fibers x 32 nodes cube cloud (near pairs), gravity"
+    elif config == "c2":
+        st = c2_step_state(ours)
         dt, tol = 1e-3, 1e-10
         desc = "c2: 1024 fibers x 32 nodes clamped to a sphere (8x8 patches), plus-end force 1"
     elif config == "c4":
