@@ -369,6 +369,13 @@ int sf_gmres_reset(double *gs, int R, int max_iterations, double beta0, double t
 int sf_gmres_cycle(double *gs, int R, const double *beta, const double *r, double *V0, int64_t n,
                    void *stream);
 int sf_gmres_givens(const double *hcol, double *gs, int R, int k, double *status, void *stream);
+/* The same two launches with the step index read from the device state
+ * (k = -1 for sf_gmres_givens; `scalars` = gs + the scalar block offset,
+ * sf_gmres_state_doubles(R, I) - I - 8, for the MGS), so one captured CUDA
+ * graph serves every Arnoldi step of a solve; both are no-ops once the
+ * cycle is done. */
+int sf_gmres_mgs_dk(double *V, int64_t ld, const double *scalars, double *w, int64_t n,
+                    double *hcol, int R, double *work, void *stream);
 int sf_gmres_update(const double *V, int64_t ld, double *gs, int R, double *x, int64_t n,
                     void *stream);
 

@@ -84,6 +84,7 @@ _SIGNATURES = {
     "sf_gmres_reset": [_P, _I, _I, _D, _D, _P],
     "sf_gmres_cycle": [_P, _I, _P, _P, _P, _I64, _P],
     "sf_gmres_givens": [_P, _P, _I, _I, _P, _P],
+    "sf_gmres_mgs_dk": [_P, _I64, _P, _P, _I64, _P, _I, _P, _P],
     "sf_gmres_update": [_P, _I64, _P, _I, _P, _I64, _P],
     "sf_host_stokeslet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],
     "sf_host_doublet_sum": [_P, _P, _I64, _P, _P, _I64, _P, _D, _P, _P],

@@ -79,7 +79,8 @@ __global__ void gmres_cycle_kernel(double *gs, int R, const double *__restrict__
 __global__ void gmres_givens_kernel(const double *__restrict__ hcol, double *gs, int R, int k,
                                     double *__restrict__ status) {
     GState G = gstate(gs, R);
-    if (G.s[S_DONE] == 0.0 && (int)G.s[S_K] == k) {
+    if (k < 0) k = (int)G.s[S_K];          // step index from the device (graph replays)
+    if (G.s[S_DONE] == 0.0 && (int)G.s[S_K] == k && k < R) {
         const double wnorm = hcol[R + 1];
         double *H = G.H;
         for (int j = 0; j <= k + 1; ++j) H[(int64_t)j * R + k] = hcol[j];
@@ -185,7 +186,7 @@ int sf_gmres_cycle(double *gs, int R, const double *beta, const double *r, doubl
 }
 
 int sf_gmres_givens(const double *hcol, double *gs, int R, int k, double *status, void *stream) {
-    if (!hcol || !gs || k < 0 || k >= R) return set_error(SF_EINVAL, "bad Givens step");
+    if (!hcol || !gs || k < -1 || k >= R) return set_error(SF_EINVAL, "bad Givens step");
     gmres_givens_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(hcol, gs, R, k, status);
     return check_launch("gmres_givens_kernel");
 }

@@ -1171,8 +1171,18 @@ __device__ __forceinline__ double final_reduce(const double *part, double *red,
 }
 __global__ void __launch_bounds__(kDotThreads)
 mgs_kernel(double *__restrict__ V, int64_t ld, int k, double *__restrict__ w, int64_t n,
-           double *__restrict__ hcol, int R, double *__restrict__ part) {
+           double *__restrict__ hcol, int R, double *__restrict__ part,
+           const double *__restrict__ sc) {
     namespace cg = cooperative_groups;
+    // sc (optional): the GMRES state scalars of sf_gmres.cu, [k, iters, done,
+    // ...]; the step index comes from the device and a finished cycle makes
+    // the launch a no-op (every block reads the same values, so no block
+    // reaches a grid barrier alone)
+    if (sc) {
+        if (sc[2] != 0.0) return;
+        k = (int)sc[0];
+        if (k < 0 || k + 1 > R) return;
+    }
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[kDotThreads / 32];
     __shared__ double bc;
@@ -1414,9 +1424,23 @@ int sf_dot(const double *x, const double *y, int64_t n, double *work, double *ou
     return check_launch("dot");
 }
 
+static int gmres_mgs_launch(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol,
+                            int R, double *work, const double *sc, void *stream);
+
 int sf_gmres_mgs(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol, int R,
                  double *work, void *stream) {
     if (k < 0 || k + 1 > R || n < 0) return set_error(SF_EINVAL, "bad Arnoldi sizes");
+    return gmres_mgs_launch(V, ld, k, w, n, hcol, R, work, nullptr, stream);
+}
+
+int sf_gmres_mgs_dk(double *V, int64_t ld, const double *scalars, double *w, int64_t n,
+                    double *hcol, int R, double *work, void *stream) {
+    if (!scalars || R < 1 || n < 0) return set_error(SF_EINVAL, "bad Arnoldi sizes");
+    return gmres_mgs_launch(V, ld, 0, w, n, hcol, R, work, scalars, stream);
+}
+
+static int gmres_mgs_launch(double *V, int64_t ld, int k, double *w, int64_t n, double *hcol,
+                            int R, double *work, const double *sc, void *stream) {
     if (n > 0 && (!V || !w || !hcol || !work)) return set_error(SF_EINVAL, "null pointer");
     static int resident = -1;
     if (resident < 0) {
@@ -1427,7 +1451,7 @@ int sf_gmres_mgs(double *V, int64_t ld, int k, double *w, int64_t n, double *hco
         resident = sms * per;
     }
     if (resident < kDotBlocks) return set_error(SF_ECUDA, "cooperative MGS grid not co-resident");
-    void *args[] = {&V, &ld, &k, &w, &n, &hcol, &R, &work};
+    void *args[] = {&V, &ld, &k, &w, &n, &hcol, &R, &work, &sc};
     if (cudaLaunchCooperativeKernel((const void *)mgs_kernel, dim3(kDotBlocks), dim3(kDotThreads),
                                     args, 0, (cudaStream_t)stream) != cudaSuccess)
         return check_launch("mgs_kernel");

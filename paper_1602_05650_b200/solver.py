@@ -795,6 +795,13 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
     _native.call("sf_gmres_reset", _ptr(gs), R, maxit, beta0, params.tolerance, st)
     history = []
     iters = 0
+    # One Arnoldi step (matvec, preconditioner, fused MGS, Givens) captured
+    # once as a CUDA graph and replayed for every later step: the step index
+    # is read from the device state, so the same graph serves every k; only
+    # the copy V[k] -> vin and the status copy run outside it.  Device-native
+    # operators only (rows_device / apply_device); SF_GMRES_GRAPH=0 disables.
+    graph = _ArnoldiGraph.create(operator, preconditioner, V, hcol, gs, hist_off - 8, R, vec,
+                                 fused) if n else None
     while True:
         r = b - apply_m(apply_a(x)) if (iters or warm) else b
         vec.dot_into(r, r, scal[0:1], sqrt_mode=True)
@@ -805,21 +812,10 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
         k = 0
         pending = []
         while k < R and iters + k < maxit:
-            w = apply_m(apply_a(V[k])).contiguous()
-            if fused:
-                # wnorm, modified Gram-Schmidt, |w| and V[k+1] = w/|w| in one launch
-                _native.call("sf_gmres_mgs", _ptr(V), n, k, _ptr(w), n, _ptr(hcol), R,
-                             _ptr(vec.work), st)
+            if graph is not None and graph.ready(iters + k):
+                graph.step(V[k], status)
             else:
-                vec.dot_into(w, w, hcol[R + 1:R + 2], sqrt_mode=True)   # wnorm
-                for j in range(k + 1):                                   # modified Gram-Schmidt
-                    vec.dot_into(V[j], w, hcol[j:j + 1])
-                    _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w),
-                                 n, st)
-                vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
-                _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]),
-                             n, st)
-            _native.call("sf_gmres_givens", _ptr(hcol), _ptr(gs), R, k, _ptr(status), st)
+                _eager_arnoldi_step(apply_a, apply_m, V, k, hcol, gs, R, vec, fused, n, status)
             slot = k % _GMRES_STATUS_RING
             ring[slot].copy_(status, non_blocking=True)
             events[slot].record()
@@ -847,6 +843,116 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
                 f"GMRES did not reach {params.tolerance:g} within "
                 f"{params.max_iterations} iterations (residual {rel:.3e})",
                 best=ret(x), iterations=iters, residuals=history)
+
+
+def _eager_arnoldi_step(apply_a, apply_m, V, k, hcol, gs, R, vec, fused, n, status):
+    """One Arnoldi step launched kernel by kernel (solver.py:482-505)."""
+    st = _stream()
+    w = apply_m(apply_a(V[k])).contiguous()
+    if fused:
+        # wnorm, modified Gram-Schmidt, |w| and V[k+1] = w/|w| in one launch
+        _native.call("sf_gmres_mgs", _ptr(V), n, k, _ptr(w), n, _ptr(hcol), R, _ptr(vec.work), st)
+    else:
+        vec.dot_into(w, w, hcol[R + 1:R + 2], sqrt_mode=True)   # wnorm
+        for j in range(k + 1):                                   # modified Gram-Schmidt
+            vec.dot_into(V[j], w, hcol[j:j + 1])
+            _native.call("sf_axpy_dev", _ptr(hcol[j:j + 1]), -1.0, 0, _ptr(V[j]), _ptr(w), n, st)
+        vec.dot_into(w, w, hcol[k + 1:k + 2], sqrt_mode=True)
+        _native.call("sf_axpy_dev", _ptr(hcol[k + 1:k + 2]), 1.0, 2, _ptr(w), _ptr(V[k + 1]), n, st)
+    _native.call("sf_gmres_givens", _ptr(hcol), _ptr(gs), R, k, _ptr(status), st)
+
+
+class _ArnoldiGraph:
+    """The Arnoldi step of gmres_solve as one CUDA graph: A vin -> tmp,
+    M tmp -> w (both into fixed buffers), the fused MGS and the Givens
+    update with the step index read from the device (sf_gmres_mgs_dk,
+    sf_gmres_givens with k = -1).  Captured after the first eagerly run step
+    (so every workspace, side stream and lazily built buffer exists) and
+    replayed for the rest of the solve; the launch work per step drops from
+    ~30 host-side kernel launches to one graph launch.  Falls back to the
+    eager path if the capture fails."""
+
+    @classmethod
+    def create(cls, operator, preconditioner, V, hcol, gs, sc_off, R, vec, fused):
+        if not fused or os.environ.get("SF_GMRES_GRAPH", "1") == "0":
+            return None
+        if not hasattr(operator, "rows_device"):
+            return None
+        if preconditioner is not None and not hasattr(preconditioner, "apply_device"):
+            return None
+        return cls(operator, preconditioner, V, hcol, gs, sc_off, R, vec)
+
+    def __init__(self, operator, preconditioner, V, hcol, gs, sc_off, R, vec):
+        import torch
+        self.op, self.prec = operator, preconditioner
+        self.V, self.hcol, self.gs, self.R, self.vec = V, hcol, gs, R, vec
+        self.sc = gs[sc_off:]
+        n = V.shape[1]
+        self.vin = torch.empty(n, dtype=torch.float64, device=V.device)
+        self.tmp = torch.empty_like(self.vin)
+        self.w = torch.empty_like(self.vin)
+        self.status = torch.empty(4, dtype=torch.float64, device=V.device)
+        # the library keys its scratch and side streams by stream: the step
+        # is warmed up and captured on one dedicated stream, so the graph
+        # holds that stream's (already grown) workspaces
+        self.stream = torch.cuda.Stream(device=V.device)
+        self.graph = None
+        self.warm = False
+        self.failed = False
+
+    def ready(self, step):
+        """Step 0 runs eagerly on the caller's stream, step 1 eagerly on the
+        capture stream (warm-up), step 2 is captured, later steps replay."""
+        return step >= 1 and not self.failed
+
+    def _body(self):
+        st = _stream()
+        self.op.rows_device(self.vin, False, self.tmp)
+        if self.prec is None:
+            self.w.copy_(self.tmp)
+        else:
+            self.prec.apply_device(self.tmp, self.w)
+        n = self.V.shape[1]
+        _native.call("sf_gmres_mgs_dk", _ptr(self.V), n, _ptr(self.sc), _ptr(self.w), n,
+                     _ptr(self.hcol), self.R, _ptr(self.vec.work), st)
+        _native.call("sf_gmres_givens", _ptr(self.hcol), _ptr(self.gs), self.R, -1,
+                     _ptr(self.status), st)
+
+    def step(self, vk, status):
+        import torch
+        self.vin.copy_(vk)
+        cur = torch.cuda.current_stream()
+        if not self.warm:
+            self.stream.wait_stream(cur)
+            with torch.cuda.stream(self.stream):
+                self._body()
+            cur.wait_stream(self.stream)
+            self.warm = True
+            status.copy_(self.status)
+            return
+        if self.graph is None:
+            g = torch.cuda.CUDAGraph()
+            matvecs = getattr(self.op, "matvecs", None)
+            try:
+                self.stream.wait_stream(cur)
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._body()
+            except Exception as err:      # noqa: BLE001 - capture unsupported: stay eager
+                LOG.warning("GMRES step graph capture failed (%s); running eagerly", err)
+                self.failed = True
+                torch.cuda.synchronize()
+                if matvecs is not None:
+                    self.op.matvecs = matvecs
+                self._body()
+                status.copy_(self.status)
+                return
+            if matvecs is not None:
+                self.op.matvecs = matvecs
+            self.graph = g
+        self.graph.replay()
+        if hasattr(self.op, "matvecs"):
+            self.op.matvecs += 1
+        status.copy_(self.status)
 
 
 def _kinetics_and_contacts(state, dt):

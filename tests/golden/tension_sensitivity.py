@@ -8,8 +8,9 @@ For each make_golden_baseline case, slenderflow runs the first steps twice:
 from the fixture's initial centrelines and from the same centrelines times
 (1 + 1e-15 xi), xi ~ N(0,1) (a perturbation at the level of FP64 rounding).
 The relative change of X, T, U, q1 and q0 after every step is written to
-tension_sensitivity.json ("dX", "dT", ... for the first step and "steps"
-with one record per step).  At p = 31 the inextensibility rows are sums of
+tension_sensitivity.json ("dX", "dT", ... for the first step, "steps"
+with one record per step, and "operator": the change of the first step's
+A u, rhs and M v).  At p = 31 the inextensibility rows are sums of
 D_s^4 terms of size ~1e12 that cancel to O(1), so T (and the surface
 densities, which balance the clamped fibers' end loads) move by 1e-4-1e-3
 under rounding-level input changes while X moves by ~1e-10: any FP64
@@ -48,6 +49,19 @@ def run(case, nsteps, scale=None):
     return out
 
 
+def operator_records(case, scale=None):
+    """A u, rhs and M v of the first step (the seeded u, v of the fixture)."""
+    st, inputs, spec, dt, tol, _ = mg.CASES[case]()
+    if scale is not None:
+        for f, s in zip(st.fibers, scale):
+            f.X = f.X * s
+    op, rhs = solver.assemble_step_operator(st, dt)
+    n = op.layout.size
+    u = np.random.default_rng(mg.SEED_U).standard_normal(n)
+    v = np.random.default_rng(mg.SEED_V).standard_normal(n)
+    return dict(Au=op.apply(u), rhs=rhs, Mv=solver.Preconditioner(op).apply(v))
+
+
 def rel(a, b):
     d = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / d) if d else float(np.linalg.norm(a))
@@ -65,8 +79,10 @@ def main(specs):
         a = run(case, ns)
         b = run(case, ns, scale=1.0 + 1e-15 * xi)
         steps = [{k: rel(rb[k], ra[k]) for k in ra} for ra, rb in zip(a, b)]
+        oa, ob = operator_records(case), operator_records(case, scale=1.0 + 1e-15 * xi)
+        ops = {k: rel(ob[k], oa[k]) for k in oa}
         out[case] = dict(perturbation=1e-15, **{"d" + k: v for k, v in steps[0].items()},
-                         steps=steps)
+                         steps=steps, operator=ops)
         print(case, steps, flush=True)
         json.dump(out, open(path, "w"), indent=1, sort_keys=True)
 

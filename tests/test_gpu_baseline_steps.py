@@ -6,7 +6,8 @@ step), a 256-fiber C2 aster for 10 steps, the full 1,024-fiber C2 aster for
 40,960-node periphery for 5 steps.
 
 Tolerances (north_star): operator A u and rhs <= 1e-10 relative L2;
-preconditioner M v <= 1e-7 (equilibrated block LU, cond ~1e8 at p = 31);
+preconditioner M v <= 1e-7 (equilibrated block LU, cond ~1e8 at p = 31;
+at p = 63 20x the reference's own first-step M v sensitivity);
 positions <= 1e-8 relative after every step; GMRES iteration counts within
 one of the reference's.  Where the reference's OWN trajectory is not fixed
 to that level by FP64, the bound is 20x its measured rounding sensitivity
@@ -17,7 +18,8 @@ of size ~1e12 cancelling to O(1): T moves 2e-4-8e-4, q1 1e-7-1e-5) and
 for the positions of the C1 near-pair cloud after its first step (1e-7 at
 step 1 growing to 5e-6 by step 6: the near-field quadrature's adaptive panel
 splits and nearest-point searches are discrete decisions that rounding can
-flip)."""
+flip), and for everything at p = 63: there the reference's own positions
+move by 8e-7 after the first step and its tensions by 20-100 %."""
 
 import glob
 import json
@@ -48,6 +50,15 @@ def sens_tol(name, step, key, base):
         return max(base, 20.0 * steps[step][key])
     vals = [s[key] for s in steps if key in s] or ([rec["d" + key]] if "d" + key in rec else [])
     return max(base, 20.0 * max(vals)) if vals else base
+
+
+def op_tol(name, key, base):
+    """max(base, 20x the change of the reference's first-step A u / rhs / M v
+    under the 1e-15 input perturbation).  At p = 63 the equilibrated fiber
+    blocks are so ill-conditioned that the reference's own M v moves at the
+    1e-6-1e-5 level."""
+    rec = SENS.get(name[:-4], {}).get("operator", {})
+    return max(base, 20.0 * rec[key]) if key in rec else base
 
 
 def state_from(g):
@@ -87,11 +98,11 @@ def test_operator_rhs_preconditioner_at_baseline_orders(cuda, name):
     assert n == int(g["layout_size"])
     u = np.random.default_rng(int(g["seed_u"])).standard_normal(n)
     v = np.random.default_rng(int(g["seed_v"])).standard_normal(n)
-    assert rel_l2(op.apply(u), g["apply_Au"]) < 1e-10
-    assert rel_l2(rhs.cpu().numpy(), g["rhs"]) < 1e-10
+    assert rel_l2(op.apply(u), g["apply_Au"]) < op_tol(name, "Au", 1e-10)
+    assert rel_l2(rhs.cpu().numpy(), g["rhs"]) < op_tol(name, "rhs", 1e-10)
     assert len(op.cache.near_fiber) == int(g["n_near_fiber"])
     assert len(op.cache.near_surface) == int(g["n_near_surface"])
-    assert rel_l2(solver.Preconditioner(op).apply(v), g["prec_Mv"]) < 1e-7
+    assert rel_l2(solver.Preconditioner(op).apply(v), g["prec_Mv"]) < op_tol(name, "Mv", 1e-7)
 
 
 @pytest.mark.parametrize("name", CASES)
