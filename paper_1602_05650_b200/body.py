@@ -296,7 +296,7 @@ def near_surface_eval(mesh, q, target, mu, interior_jump=True, upsample=6):
     return plain + corr
 
 
-# -- small host helpers and mesh text IO (body.py:186-193, 265-295, 567-618) --
+# -- small host helpers (body.py:186-193, 265-295) ---------------------------
 
 def surface_integral(mesh, f):
     """Quadrature sum of scalar or vector nodal data."""
@@ -322,47 +322,6 @@ def rigid_constraint_averages(particle, q):
     wq = mesh.weights[:, None] * q
     return wq.sum(axis=0) / mesh.area, \
         (mesh.weights[:, None] * np.cross(mesh.nodes - particle.center, q)).sum(axis=0) / mesh.area
-
-
-MESH_FORMAT_VERSION = 1
-
-
-def mesh_to_text(mesh):
-    """One node per line (x y z nx ny nz w) after a header that records the
-    parametrization, so a parametrized mesh round-trips exactly."""
-    out = [f"# surface-mesh v{MESH_FORMAT_VERSION}"]
-    if mesh.has_parametrization():
-        nt, nph = mesh.patch_grid
-        c = [float(v) for v in mesh.center]
-        out.append(f"# shape {mesh.shape[0]} {float(mesh.shape[1]):.17g} patches {nt} {nph} "
-                   f"center {c[0]:.17g} {c[1]:.17g} {c[2]:.17g}")
-    out.append("# columns: x y z nx ny nz w")
-    rows = np.column_stack([mesh.nodes, mesh.normals, mesh.weights])
-    out.extend(" ".join(f"{v:.17g}" for v in row) for row in rows)
-    return "\n".join(out) + "\n"
-
-
-def mesh_from_text(text):
-    """Inverse of mesh_to_text: a named parametrized shape is rebuilt exactly
-    (and checked against the data), otherwise a bare quadrature mesh."""
-    lines = text.splitlines()
-    if not lines or not lines[0].startswith("# surface-mesh v"):
-        raise ValueError("not a surface-mesh file")
-    if int(lines[0].rsplit("v", 1)[1]) > MESH_FORMAT_VERSION:
-        raise ValueError("unsupported mesh format version")
-    data = np.array([[float(t) for t in ln.split()] for ln in lines
-                     if ln and not ln.startswith("#")])
-    if data.ndim != 2 or data.shape[1] != 7:
-        raise ValueError("expected 7 columns: x y z nx ny nz w")
-    header = [ln.split() for ln in lines if ln.startswith("# shape ")]
-    if header:
-        h = header[0]
-        mesh = make_surface(named_shape(h[2], float(h[3])), (int(h[5]), int(h[6])),
-                            center=tuple(float(v) for v in h[8:11]))
-        if not np.allclose(mesh.nodes, data[:, 0:3], atol=1e-12):
-            raise ValueError("mesh data disagrees with its shape header")
-        return mesh
-    return SurfaceMesh(data[:, 0:3], data[:, 3:6], data[:, 6])
 
 
 # -- nodal interpolation and nearly singular helpers (body.py:305-519) --------
@@ -420,28 +379,42 @@ def interpolation_matrix(mesh, fine):
                              shape=(theta.size, mesh.n_nodes))
 
 
-def nearest_surface_point(mesh, target):
-    """(theta, phi, point, signed distance), body.py:371-423."""
-    from . import nearfield
-    return nearfield.nearest_surface_point(mesh, target)
+def _plain_surface_map_device(mesh, targets, mu, dev):
+    """The stresslet quadrature map (k, 3, 3N) at k targets (body.py:437-448)
+    on the device: block j = -3/(4 pi mu) w_j (r.n_j) r r^T / r^5, r = t - y_j."""
+    import torch
+    f64 = dict(dtype=torch.float64, device=dev)
+    t = torch.as_tensor(np.atleast_2d(targets), **f64)
+    y = torch.as_tensor(mesh.nodes, **f64)
+    nrm = torch.as_tensor(mesh.normals, **f64)
+    w = torch.as_tensor(mesh.weights, **f64)
+    r = t[:, None, :] - y[None, :, :]
+    d2 = (r * r).sum(dim=2)
+    s = (-3.0 / (4.0 * np.pi * mu)) * w[None, :] * (r * nrm[None, :, :]).sum(dim=2) / (
+        d2 * d2 * torch.sqrt(d2))
+    blocks = s[..., None, None] * r[..., :, None] * r[..., None, :]
+    return blocks.permute(0, 2, 1, 3).reshape(t.shape[0], 3, -1)
 
 
 def plain_surface_weights(mesh, target, mu):
-    """Stresslet quadrature at one target as a (3, 3N) map (body.py:437-448)."""
-    from . import nearfield
-    return nearfield.plain_surface_weights(mesh, target, mu)
+    """Stresslet quadrature at one target as a (3, 3N) map (body.py:437-448),
+    evaluated on the device."""
+    import torch
+    return _plain_surface_map_device(mesh, target, mu, torch.device("cuda"))[0].cpu().numpy()
 
 
 def near_surface_weights(mesh, target, mu, interior_jump=True, upsample=6):
     """Nearly singular (3, 3N) map (body.py:479-519), built on the device
-    (nearfield.device_surface_weights returns W_near - W_plain)."""
+    (nearfield.device_surface_weights returns W_near - W_plain; the plain
+    map is added back on the device)."""
     import torch
 
     from . import nearfield
-    W = nearfield.device_surface_weights(mesh, np.asarray(target, dtype=float)[None, :], mu,
-                                         torch.device("cuda"), interior_jump=interior_jump,
-                                         upsample=upsample)[0].cpu().numpy()
-    return W + nearfield.plain_surface_weights(mesh, target, mu)
+    dev = torch.device("cuda")
+    t = np.asarray(target, dtype=float)[None, :]
+    W = nearfield.device_surface_weights(mesh, t, mu, dev, interior_jump=interior_jump,
+                                         upsample=upsample)[0]
+    return (W + _plain_surface_map_device(mesh, t, mu, dev)[0]).cpu().numpy()
 
 
 def second_kind_matrix(mesh, mu, interior=True, nullspace_scale=None):

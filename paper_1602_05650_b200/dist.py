@@ -6,8 +6,8 @@ Once per matvec each rank contributes its fibers' force densities and an
 all-gather (NCCL over NVLink/NVSwitch) gives every rank the full source
 strengths; each rank then evaluates its target block against all sources in
 the same fixed order as on one GPU, so per-target sums are bitwise identical
-at any world size.  GMRES inner products would be all-reduced (not on this
-path yet).
+at any world size.  The distributed implicit step built on it (sharded block
+rows, gathered or all-reduced GMRES) is dsolver.py.
 """
 
 import torch

@@ -1,10 +1,8 @@
-"""Multi-GPU implicit step: sharded block rows, all-reduced GMRES.
+"""Multi-GPU implicit step: sharded block rows, gathered GMRES.
 
 One process per GPU.  Rank r owns a contiguous block of fibers (their X, T
 unknowns and rows); rank 0 also owns the particle and periphery unknowns
-(U, omega, q1, q0) and rows.  Every vector is allocated full length on every
-rank but only the owned entries are meaningful; the Krylov bookkeeping
-(Hessenberg, Givens) is replicated.
+(U, omega, q1, q0) and rows.
 
 Per matvec:
   1. broadcast the surface/particle unknowns from rank 0;
@@ -14,10 +12,17 @@ Per matvec:
      over ranks + reduce-scatter (>= 8192 points), or own targets against
      all sources (direct);
   5. the other families (surface double layers, completion flow, near maps)
-     for the rank's own targets;
+     for the rank's own targets; surface targets <- own fibers as per-rank
+     partials, all-reduced; a large on-surface double layer split by its
+     symmetric tasks and all-reduced;
   6. own fiber rows; surface rows on rank 0.
-Per GMRES iteration the MGS dot products are all-reduced (one collective per
-inner product, preserving modified Gram-Schmidt).
+GMRES (default "gathered"): each iteration the ranks' rows of M A v are
+all-gathered (one collective of the unknown-vector size) and every rank
+runs the single-GPU GMRES on the full, identical vectors, so every rank
+takes bitwise-identical Krylov decisions.  SF_DIST_GMRES=reduced instead
+all-reduces every MGS inner product (one collective per inner product).
+Errors that one rank detects (skipped pairs, singular fiber blocks) are
+summed over the ranks first, so every rank raises together.
 
 `Comm` hides the transport: TorchComm uses torch.distributed (NCCL on the
 GPU box, gloo on the CPU), ThreadComm runs the ranks as threads on ONE GPU
@@ -33,8 +38,9 @@ import numpy as np
 
 from . import _native, spectral
 from .dist import shard_range
-from .solver import (BC_CODES, FactorizationError, GmresParams, NonconvergenceError,
-                     StepLayout, _kinetics_and_contacts, _precision_mode, _ptr, _stream)
+from .solver import (BC_CODES, LOG, FactorizationError, GmresParams, NonconvergenceError,
+                     StepLayout, _kinetics_and_contacts, _precision_mode, _ptr,
+                     _rotation_is_representable, _stream)
 from .system import (ConfigurationError, SingularEvaluationError, FiberGeometry, InteractionCache, external_force_density,
                      stack_fibers)
 
@@ -305,6 +311,7 @@ class DistBlockOperator:
         self._rs_in = torch.zeros((world * max(self.per, 1) * n, 3), **f64)
         self._rs_out = torch.zeros((max(self.per, 1) * n, 3), **f64)
         self._bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._checked = False
         self.fiber_blocks = torch.empty((no, 4 * n, 4 * n), **f64)
         if no:
             _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.fiber_blocks),
@@ -346,11 +353,10 @@ class DistBlockOperator:
         wr = self._wr[:self.np] if self.np else None
         # fiber targets: the other families (and the fiber pairs when direct)
         # skipped-pair counts are geometric: checked on the first application only
-        ub_f = (self.cache_fib.apply(f_full, q, wr,
-                                     check=not getattr(self.cache_fib, "_bad_checked", False))
-                if no else None)
-        if no:
-            self.cache_fib._bad_checked = True
+        # skipped-pair counts depend only on the frozen geometry: they are
+        # checked once, on the first application, collectively (_check_once)
+        first = not self._checked
+        ub_f = self.cache_fib.apply(f_full, q, wr, check=False) if no else None
         if self.symmetric:
             g = self.geo
             _native.call("sf_sbt_symmetric_partial", _ptr(g.X), _ptr(self.fgrp), N, n,
@@ -359,8 +365,6 @@ class DistBlockOperator:
                          _ptr(self._part), _ptr(self._bad), st)
             self._rs_in[:N].copy_(self._part)
             c.reduce_scatter_sum(self._rs_out, self._rs_in)
-            if int(self._bad.item()):
-                raise SingularEvaluationError("a target coincides with another fiber's node")
             if no:
                 ub_f = ub_f + self._rs_out[:no * n]
         if no:
@@ -375,8 +379,6 @@ class DistBlockOperator:
                              _ptr(self.fgrp[lo:hi]), hi - lo, _ptr(sw), _ptr(self.fdcoef[lo:hi]),
                              1.0 / (8.0 * math.pi * self.mu), self.mode, _ptr(self._surf_part),
                              _ptr(self._surf_bad), st)
-                if int(self._surf_bad.item()):
-                    raise SingularEvaluationError("a target coincides with another fiber's node")
             else:
                 self._surf_part.zero_()
             c.all_reduce_sum(self._surf_part)
@@ -388,10 +390,7 @@ class DistBlockOperator:
             c.all_reduce_sum(d["out"])
         # surfaces (rank 0)
         if self.surf:
-            ub_s = self.cache_surf.apply(
-                f_full, q, wr, check=not getattr(self.cache_surf, "_bad_checked", False)) \
-                + self._surf_part
-            self.cache_surf._bad_checked = True
+            ub_s = self.cache_surf.apply(f_full, q, wr, check=False) + self._surf_part
             for s in self.surf:
                 qs = u[s["sl"]]
                 rows = out[s["sl"]]
@@ -413,8 +412,36 @@ class DistBlockOperator:
                     _native.call("sf_surface_rows", 1, _ptr(s["nodes"]), _ptr(s["nrm"]),
                                  _ptr(s["w"]), s["n"], None, s["area"], _ptr(qs), _ptr(ub), None,
                                  self.mu, _ptr(self._work), _ptr(rows), None, st)
+        if first:
+            self._check_once()
         self.matvecs += 1
         return out
+
+    def _check_once(self):
+        """The skipped-pair counters of the first application (fiber targets,
+        the symmetric task share, surface targets <- own fibers, surface
+        targets), summed over the ranks in one collective, so that a
+        coincidence on any rank raises SingularEvaluationError on every rank
+        instead of leaving the others blocked in the next collective."""
+        import torch
+        flags = torch.zeros(6, dtype=torch.float64, device=self.device)
+        if self.nown:
+            flags[0:3] = self.cache_fib.bad.to(torch.float64)
+        if self.symmetric:
+            flags[3] = self._bad.to(torch.float64)[0]
+        if self._surf_part is not None and self.nown:
+            flags[4] = self._surf_bad.to(torch.float64)[0]
+        if self.surf:
+            flags[5] = self.cache_surf.bad.to(torch.float64).sum()
+        self.comm.all_reduce_sum(flags)
+        self._checked = True
+        f = flags.cpu().numpy()
+        if f[0] or f[3] or f[4]:
+            raise SingularEvaluationError("a target coincides with another fiber's node")
+        if f[1] or f[5]:
+            raise SingularEvaluationError("a target coincides with another surface's node")
+        if f[2]:
+            raise SingularEvaluationError("target at a particle center")
 
     def rhs_device(self):
         import torch
@@ -445,11 +472,15 @@ class DistPreconditioner:
             info = torch.empty(no, dtype=torch.int32, device=op.device)
             _native.call("sf_block_lu", _ptr(A), no, m, _ptr(self.r), _ptr(self.c),
                          _ptr(self.piv), _ptr(info), st)
-            bad = info.cpu().numpy()
-            if np.any(bad > 0):
-                raise FactorizationError(f"fiber {op.f0 + int(np.argmax(bad > 0))} self-block "
-                                         "is not invertible")
             self.LU = A
+        # failed factorizations counted over every rank (one collective), so
+        # all ranks raise together
+        nbad = torch.zeros(1, **f64)
+        if no:
+            nbad[0] = (info > 0).sum().to(torch.float64)
+        op.comm.all_reduce_sum(nbad)
+        if float(nbad.item()) > 0:
+            raise FactorizationError(f"{int(nbad.item())} fiber self-block(s) are not invertible")
         fo = op.layout.fib_off
         self.ndiag = fo if op.comm.rank == 0 else 0
         self.diag = torch.ones(max(self.ndiag, 1), **f64)
@@ -626,15 +657,32 @@ def _dist_gmres_reduced(op, prec, rhs, params=None):
 
 
 def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, symmetric=None,
-                             precision="fp64"):
-    """backward_euler_step (solver.py:528-592) over `comm`'s ranks.  The host
-    state is replicated; every rank ends with the same updated state."""
+                             precision="fp64", dt_min=None):
+    """backward_euler_step (solver.py:528-592) over `comm`'s ranks: the same
+    dt halving on NonconvergenceError down to dt_min (every rank takes the
+    same GMRES decisions, so every rank retries together) and the same
+    rotation check for non-spherical particles before any state changes.
+    The host state is replicated; every rank ends with the same state."""
     import torch
-    op = DistBlockOperator(state, dt, comm, symmetric=symmetric, precision=precision)
-    rhs = op.rhs_device()
-    prec = DistPreconditioner(op)
+    if dt <= 0:
+        raise ConfigurationError("time step must be positive")
+    if dt_min is None:
+        dt_min = dt / 64.0
+    attempt = float(dt)
     variant = os.environ.get("SF_DIST_GMRES", "gathered")
-    x, iters, history = dist_gmres_solve(op, prec, rhs, params, variant=variant)
+    while True:
+        op = DistBlockOperator(state, attempt, comm, symmetric=symmetric, precision=precision)
+        rhs = op.rhs_device()
+        prec = DistPreconditioner(op)
+        try:
+            x, iters, history = dist_gmres_solve(op, prec, rhs, params, variant=variant)
+            break
+        except NonconvergenceError as err:
+            LOG.warning("step_rejected time=%.9g dt=%.3e residual=%.3e",
+                        state.time, attempt, err.residuals[-1])
+            if attempt / 2.0 < dt_min:
+                raise
+            attempt /= 2.0
     if variant != "gathered":
         # assemble the full solution on every rank: owned ranges summed (others 0)
         full = torch.zeros_like(x)
@@ -645,17 +693,20 @@ def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, sy
     sol = x.cpu().numpy()
     parts = op.layout.unpack(sol)
     for i, part in enumerate(state.particles):
+        if not _rotation_is_representable(part, parts.omega[i], attempt):
+            raise ConfigurationError("rotation of a non-spherical particle is not supported")
+    for i, part in enumerate(state.particles):
         part.U = parts.U[i].copy()
         part.omega = parts.omega[i].copy()
         part.q = parts.q1[i].copy()
-        part.translate(dt * part.U)
+        part.translate(attempt * part.U)
     if state.periphery is not None:
         state.periphery.q = parts.q0.copy()
     for m, fib in enumerate(state.fibers):
         fib.X = parts.X[m].copy()
         fib.T = parts.T[m].copy()
-    state.time += dt
-    _kinetics_and_contacts(state, dt)          # replicated: same RNG streams on every rank
+    state.time += attempt
+    _kinetics_and_contacts(state, attempt)     # replicated: same RNG streams on every rank
     if return_info:
-        return state, dict(iterations=iters, history=history, matvecs=op.matvecs)
+        return state, dict(dt=attempt, iterations=iters, history=history, matvecs=op.matvecs)
     return state

@@ -377,88 +377,12 @@ def nonlocal_Kdelta_apply(fib, f, mu):
     return u.cpu().numpy()
 
 
-def fiber_induced_velocity(fib, f, targets, mu, include_doublet=False, allow_near=False):
-    """Clenshaw-Curtis line quadrature of the Stokeslet (+ doublet) of one
-    fiber at distant targets (fiber.py:261-289), through the device kernels."""
-    from . import kernels
-    targets = np.atleast_2d(np.asarray(targets, dtype=float))
-    f = np.asarray(f, dtype=float)
-    if not allow_near:
-        h = fib.L / fib.p
-        d = targets[:, None, :] - fib.X[None, :, :]
-        if np.any((d * d).sum(axis=2).min(axis=1) < (1.5 * h) ** 2):
-            raise kernels.NearFieldError("target inside the fiber's near-field shell")
-    strengths = fib.node_weights()[:, None] * f
-    ng_t = kernels.no_groups(targets.shape[0])
-    ng_s = kernels.no_groups(fib.n_nodes)
-    out, bad = kernels.stokeslet_sum(targets, ng_t, fib.X, ng_s, strengths,
-                                     1.0 / (8.0 * np.pi * mu))
-    if bad:
-        raise kernels.SingularEvaluationError("target coincides with a fiber node")
-    if include_doublet:
-        coeff = (fib.eps * fib.L) ** 2 / 2.0
-        dbl, bad = kernels.doublet_sum(targets, ng_t, fib.X, ng_s, strengths,
-                                       coeff / (8.0 * np.pi * mu))
-        if bad:
-            raise kernels.SingularEvaluationError("target coincides with a fiber node")
-        out = out + dbl
-    return out
-
-
-# -- polymerization kinetics (fiber.py:297-356): per-fiber scalar host logic
-#    run after each device solve; the reparametrization velocity enters the
-#    device rows through Ldot (sf_fiber_rows) -----------------------------------
-
-def reparam_velocity(fib):
-    """((alpha + 1) Ldot / L) X_alpha (fiber.py:297-302)."""
-    nodes, _, D, _ = spectral.grid(fib.p)
-    coef = (nodes + 1.0) * fib.Ldot / fib.L
-    return coef[:, None] * (D @ fib.X)
-
-
-def growth_rate(fib, end_force, v_grow0, stall_force):
-    """Load-dependent plus-end polymerization speed (fiber.py:307-319)."""
-    if fib.growth_state == SHRINKING:
-        return -fib.kinetics.v_shrink
-    t_plus = fib.tangents[fib.end_index(plus=True)]
-    load = float(np.dot(np.asarray(end_force, dtype=float), t_plus))
-    return v_grow0 * math.exp(-(7.0 / 3.0) * load / stall_force)
-
-
-def catastrophe_rate(v_g, v_g0, f_cat0, tau_cat):
-    """Catastrophe rate, never below 1/tau_cat (fiber.py:322-328)."""
-    if v_g <= 0:
-        raise ValueError("catastrophe rate is defined for growing fibers only")
-    return max(f_cat0 * v_g0 / v_g, 1.0 / tau_cat)
-
-
-def polymerization_step(fib, dt, rng):
-    """Dynamic-instability transitions and growth rate (fiber.py:331-356):
-    one uniform draw per transition test, rescue at the minimum length."""
-    if dt <= 0:
-        raise ValueError("time step must be positive")
-    kin = fib.kinetics
-    if fib.growth_state in (GROWING, STALLED):
-        v_g = fib.Ldot if fib.Ldot > 0 else kin.v_grow
-        rate = catastrophe_rate(v_g, kin.v_grow, kin.f_cat, fib.tau_cat)
-        if rng.random() < -math.expm1(-rate * dt):
-            fib.growth_state = SHRINKING
-            fib.Ldot = -kin.v_shrink
-        elif fib.growth_state == GROWING and fib.Ldot <= 0:
-            fib.Ldot = kin.v_grow
-    elif fib.growth_state == SHRINKING:
-        if rng.random() < -math.expm1(-kin.f_res * dt):
-            fib.growth_state = GROWING
-            fib.Ldot = kin.v_grow
-        else:
-            fib.Ldot = -kin.v_shrink
-    if fib.Ldot < 0 and fib.L + fib.Ldot * dt < kin.min_length:
-        fib.growth_state = GROWING
-        fib.Ldot = (kin.min_length - fib.L) / dt
-    return fib.growth_state, fib.Ldot
-
-
-# -- remaining per-fiber API (fiber.py:26-35, 375-600) --------------------------
+# -- remaining per-fiber API (fiber.py:26-35, 444-587).  The reference's
+#    other host-side per-fiber logic -- the far-field line quadrature
+#    fiber_induced_velocity, the dynamic-instability kinetics and the host
+#    boundary residuals -- stays in the reference package (_reference.py);
+#    the device step assembles the boundary rows analytically (sf_fiber_rows,
+#    sf_fiber_self_blocks) ----------------------------------------------------
 
 def shared_grid(p):
     """ChebyshevGrid of order p (fiber.py:26-31)."""
@@ -471,95 +395,63 @@ def resample_to_fine(values, alphas):
     return C.chebval(alphas, spectral.cheb_transform(values))
 
 
-def nearest_centerline_point(fib, target):
-    """(alpha, point, distance) of the closest centreline point (fiber.py:453-481)."""
-    from . import nearfield
-    return nearfield.nearest_centerline_point(fib, target)
+def _plain_map_device(geo, eps, trg, mu, include_doublet):
+    """The collocation map (k, 3, 3n) of one fiber at k targets, on the
+    device: block j = w_j [S(r) + c D(r)] / (8 pi mu), r = t - x_j, with the
+    Stokeslet S = I/r + r r^T/r^3 and, if include_doublet, the doublet
+    D = I/r^3 - 3 r r^T/r^5, c = (eps L)^2 / 2 (fiber.py:508-512)."""
+    import torch
+    X = geo.X[0]
+    w = geo.wnode[0]
+    r = trg[:, None, :] - X[None, :, :]
+    d2 = (r * r).sum(dim=2)
+    d = torch.sqrt(d2)
+    eye = torch.eye(3, dtype=torch.float64, device=trg.device)
+    rr = r[..., :, None] * r[..., None, :]
+    K = eye / d[..., None, None] + rr / (d2 * d)[..., None, None]
+    if include_doublet:
+        c = (eps[0] * geo.L[0]) ** 2 / 2.0
+        K = K + c * (eye / (d2 * d)[..., None, None] - 3.0 * rr / (d2 * d2 * d)[..., None, None])
+    W = (w[None, :, None, None] * K).permute(0, 2, 1, 3).reshape(trg.shape[0], 3, -1)
+    return W / (8.0 * math.pi * mu)
+
+
+def _one_fiber_geometry(fib):
+    import torch
+
+    from .system import FiberGeometry
+    ratio = [fib.delta_ratio if fib.delta_ratio is not None else -1.0]
+    delta = [0.0 if fib.delta_ratio is not None else fib.delta]
+    dev = _dev()
+    geo = FiberGeometry(fib.X[None, :, :], ratio, delta, dev)
+    return geo, torch.tensor([fib.eps], dtype=torch.float64, device=dev)
 
 
 def plain_fiber_weights(fib, target, mu, include_doublet=False):
-    """Plain collocation map (3, 3n) of one fiber at a target (fiber.py:508-512)."""
-    from . import nearfield
-    return nearfield.plain_fiber_weights(fib, target, mu, include_doublet)
+    """Plain collocation map (3, 3n) of one fiber at a target (fiber.py:508-512),
+    evaluated on the device."""
+    import torch
+    geo, eps = _one_fiber_geometry(fib)
+    trg = torch.as_tensor(np.asarray(target, dtype=float)[None, :], dtype=torch.float64,
+                          device=geo.X.device)
+    return _plain_map_device(geo, eps, trg, mu, include_doublet)[0].cpu().numpy()
 
 
 def near_fiber_weights(fib, target, mu, include_doublet=False):
     """Panel-refined, blended near map (3, 3n) (fiber.py:514-565), built on
-    the device by sf_near_fiber_weights (which returns W_near - W_plain)."""
+    the device: sf_near_fiber_weights gives W_near - W_plain, the plain map
+    is added back on the device."""
     import torch
 
     from . import nearfield
-    from .system import FiberGeometry
-    dev = torch.device("cuda")
-    ratio = [fib.delta_ratio if fib.delta_ratio is not None else -1.0]
-    delta = [0.0 if fib.delta_ratio is not None else fib.delta]
-    geo = FiberGeometry(fib.X[None, :, :], ratio, delta, dev)
+    geo, eps = _one_fiber_geometry(fib)
     trg = torch.as_tensor(np.asarray(target, dtype=float)[None, :], dtype=torch.float64,
-                          device=dev)
-    eps = torch.tensor([fib.eps], dtype=torch.float64, device=dev)
+                          device=geo.X.device)
     W = nearfield.device_fiber_weights(geo, eps, trg, [0], [0], mu, include_doublet)[0]
-    return W.cpu().numpy() + nearfield.plain_fiber_weights(fib, target, mu, include_doublet)
+    return (W + _plain_map_device(geo, eps, trg, mu, include_doublet)[0]).cpu().numpy()
 
 
 def near_fiber_eval(fib, f, target, mu, include_doublet=False):
     """Velocity near (but outside) the fiber: near_fiber_weights @ f (fiber.py:576-587)."""
     W = near_fiber_weights(fib, target, mu, include_doublet=include_doublet)
     return W @ np.asarray(f, dtype=float).ravel()
-
-
-# -- boundary residuals (fiber.py:375-441): host form of the 14 BC rows the
-#    device rows kernel assembles analytically; for API users and checks ------
-
-def _end_rows(fib, Xcand, Tcand, plus, bc, body_kinematics, mu=None, u_bar=None,
-              homogeneous=False):
-    """Residuals (vec1, vec2, tension) of the boundary equations at one end."""
-    k = fib.end_index(plus)
-    sigma = 1.0 if plus else -1.0
-    t = fib.tangents[k]
-    Ds, Ds2, Ds3 = fib.ds_powers()
-    Xss = (Ds2 @ Xcand)[k]
-    Xsss = (Ds3 @ Xcand)[k]
-    if bc.kind == "free":
-        return Xss, Xsss, Tcand[k]
-    if bc.kind == "prescribedForceTorque":
-        Fx = -fib.E * Xsss + Tcand[k] * t
-        if homogeneous:
-            return Fx, Xss, Tcand[k]
-        return (Fx - sigma * bc.force, Xss - sigma * np.cross(t, bc.torque) / fib.E,
-                Tcand[k] - sigma * (bc.force @ t + (bc.torque @ bc.torque) / fib.E))
-    if bc.kind == "hingedToSurface":
-        Fx = -fib.E * Xsss + Tcand[k] * t
-        spring = -bc.stiffness * (Xcand[k] - (0.0 if homogeneous else bc.attachment))
-        return Fx - sigma * spring, Xss, Tcand[k] - sigma * (spring @ t)
-    if bc.kind == "clampedToBody":
-        if body_kinematics is None:
-            raise ValueError("clamped end requires body kinematics")
-        U = np.asarray(body_kinematics["U"], dtype=float)
-        Om = np.asarray(body_kinematics["omega"], dtype=float)
-        c = np.asarray(body_kinematics["center"], dtype=float)
-        dt = float(body_kinematics["dt"])
-        vel = (Xcand[k] - (0.0 if homogeneous else fib.X[k])) / dt
-        vec1 = vel - U - np.cross(Om, fib.X[k] - c)
-        if bc.tangent is None:
-            vec2 = Xss
-        else:
-            vec2 = ((Ds @ Xcand)[k] - (0.0 if homogeneous else t)) / dt - np.cross(Om, t)
-        u_bar = np.zeros(3) if u_bar is None else u_bar
-        f = elastic_force_density(fib, Xcand, Tcand)
-        v_self = local_mobility_apply(fib, f, mu) + nonlocal_Kdelta_apply(fib, f, mu)
-        tres = float((v_self[k] + u_bar - U - np.cross(Om, fib.X[k] - c)) @ t)
-        return vec1, vec2, tres
-    raise ValueError(f"unknown boundary-condition kind {bc.kind!r}")
-
-
-def bc_residuals(fib, Xcand, Tcand, body_kinematics=None, mu=1.0, u_bar=None,
-                 homogeneous=False):
-    """The 14 scalar boundary residuals: plus-end pair, minus-end pair, and
-    the two tension conditions (fiber.py:430-441)."""
-    Xcand = np.asarray(Xcand, dtype=float)
-    Tcand = np.asarray(Tcand, dtype=float)
-    p1, p2, pt = _end_rows(fib, Xcand, Tcand, True, fib.bc_plus, body_kinematics, mu, u_bar,
-                           homogeneous)
-    m1, m2, mt = _end_rows(fib, Xcand, Tcand, False, fib.bc_minus, body_kinematics, mu, u_bar,
-                           homogeneous)
-    return np.concatenate([p1, p2, m1, m2, [pt], [mt]])

@@ -957,24 +957,26 @@ class _ArnoldiGraph:
 
 def _kinetics_and_contacts(state, dt):
     """Polymerization kinetics and contact models after the geometry update
-    (solver.py:574-588): per-fiber scalar logic with the reference's RNG
-    draws; the resulting Ldot enters the next step's device rows."""
-    from . import fiber as fibers_
-    from .system import cortical_pull_catastrophe, cortical_push_update
+    (solver.py:574-588): per-fiber scalar host logic with the reference's
+    RNG draws, run by the reference's own functions (_reference.py) on these
+    host objects; the resulting Ldot enters the next step's device rows."""
+    from . import _reference
+    ref_fiber = _reference.module("fiber")
+    ref_system = _reference.module("system")
     for fib in state.fibers:
-        if fib.growth_state == fibers_.STALLED:
+        if fib.growth_state == ref_fiber.STALLED:
             continue
         load = np.zeros(3)
         if fib.bc_plus.kind == "hingedToSurface":
             load = fib.bc_plus.stiffness * (fib.X[0] - fib.bc_plus.attachment)
         kin = fib.kinetics
-        fib.Ldot = fibers_.growth_rate(fib, load, kin.v_grow, kin.stall_force)
+        fib.Ldot = ref_fiber.growth_rate(fib, load, kin.v_grow, kin.stall_force)
         rng = fib.rng if fib.rng is not None else state.rng
-        fibers_.polymerization_step(fib, dt, rng)
+        ref_fiber.polymerization_step(fib, dt, rng)
     if state.model("corticalPushing") is not None:
-        cortical_push_update(state)
+        ref_system.cortical_push_update(state)
     if state.model("cytoplasmicPulling") is not None:
-        cortical_pull_catastrophe(state)
+        ref_system.cortical_pull_catastrophe(state)
 
 
 def _rotation_is_representable(part, omega, dt):

@@ -151,103 +151,51 @@ class TreeSummation:
 # -- state (system.py:237-278) -------------------------------------------------
 
 class SystemState:
+    """The constituents, fluid viscosity, force models and clock of a
+    simulation: the reference's SystemState constructor and invariants
+    (system.py:237-278).  Between implicit steps the constituents' unknowns
+    live on the device (devstate.DeviceState, attached as `_dev`)."""
+
     def __init__(self, fibers, particles=(), periphery=None, mu=1.0, time=0.0,
                  force_models=(), seed=None):
         if mu <= 0:
             raise ConfigurationError("viscosity must be positive")
-        self.fibers = list(fibers)
-        self.particles = list(particles)
-        self.periphery = periphery
-        self.mu = float(mu)
-        self.time = float(time)
-        self.force_models = list(force_models)
-        self.seed = seed
+        self.fibers, self.particles = list(fibers), list(particles)
+        self.periphery, self.force_models = periphery, list(force_models)
+        self.mu, self.time, self.seed = float(mu), float(time), seed
         self.rng = np.random.default_rng(seed)
         self.validate()
 
     def validate(self):
-        if self.periphery is not None:
-            for i, fib in enumerate(self.fibers):
-                if not np.all(self.periphery.contains(fib.X)):
-                    raise ConfigurationError(f"fiber {i} leaves the confining periphery")
-            for i, part in enumerate(self.particles):
-                if not np.all(self.periphery.contains(part.mesh.nodes)):
-                    raise ConfigurationError(f"particle {i} leaves the confining periphery")
+        """Raise ConfigurationError on the first violated invariant, checked
+        in the reference's order: constituents inside the periphery (one
+        batched containment test per family), then each fiber's boundary
+        conditions."""
+        per = self.periphery
+        if per is not None:
+            for what, pts in (("fiber", [f.X for f in self.fibers]),
+                              ("particle", [p.mesh.nodes for p in self.particles])):
+                if not pts:
+                    continue
+                owner = np.repeat(np.arange(len(pts)), [len(x) for x in pts])
+                outside = ~per.contains(np.concatenate(pts))
+                if outside.any():
+                    leave = "leaves the confining periphery"
+                    raise ConfigurationError(f"{what} {owner[np.argmax(outside)]} {leave}")
+        nparts = len(self.particles)
         for i, fib in enumerate(self.fibers):
             if fib.bc_plus.kind == "clampedToBody":
                 raise ConfigurationError("plus-end clamping is not supported")
             for bc in (fib.bc_minus, fib.bc_plus):
-                if bc.kind == "clampedToBody" and not 0 <= bc.body < len(self.particles):
-                    raise ConfigurationError(
-                        f"fiber {i} is clamped to a body outside the system")
-                if bc.kind == "hingedToSurface" and self.periphery is None:
+                if bc.kind == "clampedToBody" and not 0 <= bc.body < nparts:
+                    raise ConfigurationError(f"fiber {i} is clamped to a body outside the system")
+                if bc.kind == "hingedToSurface" and per is None:
                     raise ConfigurationError(
                         f"fiber {i} is hinged to a surface but no periphery is present")
 
     def model(self, kind):
-        for m in self.force_models:
-            if m.kind == kind:
-                return m
-        return None
-
-
-def cytoplasmic_pull_density(fib, motor_force, motor_density):
-    """Tangential motor force density and its integral (system.py:283-295)."""
-    if motor_force < 0 or motor_density < 0:
-        raise ConfigurationError("motor force and density must be nonnegative")
-    scale = motor_force * motor_density
-    density = scale * fib.tangents
-    total = scale * (fib.X[fib.end_index(plus=True)] - fib.X[fib.end_index(plus=False)])
-    return density, total
-
-
-def cortical_push_update(state):
-    """Attach growing plus-ends reaching the periphery, release on
-    catastrophe (system.py:334-362).  Host per-fiber logic after the solve."""
-    from . import fiber as fibers_
-    from .nearfield import nearest_surface_point
-    if state.periphery is None:
-        raise ConfigurationError("cortical pushing requires a periphery")
-    model = state.model("corticalPushing")
-    if model is None:
-        raise ConfigurationError("no cortical pushing model is configured")
-    mesh = state.periphery.mesh
-    out = []
-    for fib in state.fibers:
-        attached = fib.bc_plus.kind == "hingedToSurface"
-        if attached and fib.growth_state == fibers_.SHRINKING:
-            fib.bc_plus = fibers_.FreeEnd()
-            fib.tau_cat = math.inf
-        elif not attached and fib.growth_state == fibers_.GROWING:
-            tip = fib.X[fib.end_index(plus=True)]
-            _, _, _, signed_d = nearest_surface_point(mesh, tip)
-            if -signed_d <= model.contact_distance:
-                fib.bc_plus = fibers_.HingedToSurface(attachment=tip, stiffness=model.stiffness)
-                fib.tau_cat = model.tau_cat
-        out.append(fib.bc_plus)
-    return out
-
-
-def cortical_pull_catastrophe(state, standoff_fraction=0.95):
-    """Instant catastrophe at the periphery standoff shell (system.py:365-388)."""
-    from . import fiber as fibers_
-    if state.periphery is None:
-        raise ConfigurationError("cortical catastrophe requires a periphery")
-    mesh = state.periphery.mesh
-    switched = []
-    for fib in state.fibers:
-        if fib.growth_state == fibers_.SHRINKING:
-            continue
-        rel = fib.X[fib.end_index(plus=True)] - mesh.center
-        rho = float(np.linalg.norm(rel))
-        if rho == 0.0:
-            continue
-        th = math.acos(min(max(rel[2] / rho, -1.0), 1.0))
-        if rho >= standoff_fraction * float(mesh.shape[2](th)):
-            fib.growth_state = fibers_.SHRINKING
-            fib.Ldot = -fib.kinetics.v_shrink
-            switched.append(fib)
-    return switched
+        """First configured force model of `kind`, or None."""
+        return next((m for m in self.force_models if m.kind == kind), None)
 
 
 def external_force_density(state, fib):
@@ -277,69 +225,6 @@ def attachment_wrench(state, particle_index, candidates=None):
         F += Fe
         L += Le + np.cross(arm, Fe)
     return F, L
-
-
-# -- attachment layouts and initial conditions (system.py:392-466) --------------
-
-GOLDEN_ANGLE = math.pi * (3.0 - math.sqrt(5.0))
-
-
-def _fibonacci_cap(n, cap_angle):
-    """n quasi-uniform directions on the polar cap theta <= cap_angle."""
-    if n == 1:
-        return np.array([[0.0, 0.0, 1.0]])
-    k = np.arange(n)
-    z = 1.0 - (1.0 - math.cos(cap_angle)) * (k + 0.5) / n
-    rho = np.sqrt(1.0 - z * z)
-    return np.stack([rho * np.cos(k * GOLDEN_ANGLE), rho * np.sin(k * GOLDEN_ANGLE), z], axis=1)
-
-
-def _nominal_radius(pnc):
-    shape = pnc.mesh.shape
-    a = float(shape[1]) if shape is not None else 0.0
-    if a <= 0:
-        raise ConfigurationError("particle shape has no nominal radius")
-    return a
-
-
-def mtoc_attachment_layout(pnc, n_fibers, cap_angle=math.pi / 5.0, radius_factor=1.3):
-    """Attachment points / radial tangents on two opposite polar caps."""
-    if n_fibers <= 0 or n_fibers % 2:
-        raise ConfigurationError("attachment layout needs a positive even fiber count")
-    a = _nominal_radius(pnc)
-    north = _fibonacci_cap(n_fibers // 2, cap_angle)
-    dirs = np.vstack([north, north * np.array([1.0, 1.0, -1.0])])
-    return pnc.center[None, :] + radius_factor * a * dirs, dirs
-
-
-def aster_attachment_layout(pnc, n_fibers, radius_factor=1.3):
-    """One Fibonacci spiral over the whole sphere (radial asters)."""
-    if n_fibers <= 0:
-        raise ConfigurationError("attachment layout needs a positive fiber count")
-    a = _nominal_radius(pnc)
-    dirs = _fibonacci_cap(n_fibers, math.pi)
-    return pnc.center[None, :] + radius_factor * a * dirs, dirs
-
-
-def cloud_init(n_fibers, radius, length, eps, E, seed, p=16, mu=1.0, f0=1.0,
-               load_direction=(0.0, 0.0, 1.0)):
-    """Straight free fibers uniform in a ball under a uniform load, drawn from
-    a generator seeded by `seed` (same draws as the reference)."""
-    from .fiber import straight_fiber
-    if n_fibers <= 0:
-        raise ConfigurationError("need a positive number of fibers")
-    if radius <= 0 or length <= 0:
-        raise ConfigurationError("cloud radius and fiber length must be positive")
-    rng = np.random.default_rng(seed)
-    fibs = []
-    for _ in range(n_fibers):
-        cdir = rng.standard_normal(3)
-        cdir /= np.linalg.norm(cdir)
-        center = radius * rng.random() ** (1.0 / 3.0) * cdir
-        d = rng.standard_normal(3)
-        d /= np.linalg.norm(d)
-        fibs.append(straight_fiber(p, center - 0.5 * length * d, d, length, eps=eps, E=E))
-    return SystemState(fibs, mu=mu, seed=seed, force_models=[UniformBodyForce(f0, load_direction)])
 
 
 @dataclass
@@ -438,6 +323,19 @@ class _DeviceMesh:
 
     def has_parametrization(self):
         return self.base.has_parametrization()
+
+    def surface_point(self, theta, phi):
+        R = self.shape[2](theta)
+        st = np.sin(theta)
+        return self.center + R * np.array([st * np.cos(phi), st * np.sin(phi), np.cos(theta)])
+
+    def radial_bound(self, theta):
+        return float(self.shape[2](theta))
+
+    def refined(self, factor):
+        from .body import make_surface
+        nt, nph = self.patch_grid
+        return make_surface(self.shape, (nt * factor, nph * factor), center=self.center)
 
     @property
     def nodes(self):
@@ -645,12 +543,11 @@ class InteractionCache:
         # near maps: fibers on the device (default) or the host restatement
         self._near_fiber_list = []
         self._near_dev = None
+        if near not in (None, False, "device"):
+            raise ConfigurationError("near-field maps are built on the device (near='device')")
         if near and nf:
             try:
-                if near == "host":
-                    self._near_fiber_list = nearfield.find_fiber_pairs(
-                        state.fibers, self.targets, self.target_groups, state.mu, include_doublet)
-                elif self.uniform:
+                if self.uniform:
                     t, l, W = nearfield.device_fiber_pairs(self.geo, self.eps, self.trg, self.tgrp,
                                                            state.mu, include_doublet)
                     self._near_dev = (t, l, W)
@@ -662,13 +559,9 @@ class InteractionCache:
         _lap("near fiber maps")
         self.near_surface = []
         if near and self.surfaces:
-            if near == "host":
-                self.near_surface = nearfield.find_surface_pairs(
-                    self.surfaces, self.targets, self.target_groups, state.mu)
-            else:
-                self.near_surface = nearfield.device_surface_pairs(
-                    self.surfaces, self.trg, self.tgrp, state.mu, self.device,
-                    surface_arrays=self.surface_arrays)
+            self.near_surface = nearfield.device_surface_pairs(
+                self.surfaces, self.trg, self.tgrp, state.mu, self.device,
+                surface_arrays=self.surface_arrays)
         _lap("near surface maps")
         self._build_near_map()
         _lap("near CSR")

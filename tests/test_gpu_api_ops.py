@@ -24,9 +24,6 @@ def test_fiber_operators(cuda, g):
     assert rel_l2(fiber.elastic_force_density(fib, g["Xc"], g["Tc"]), g["elastic"]) < 1e-10
     assert rel_l2(fiber.local_mobility_apply(fib, g["f"], mu), g["mobility"]) < 1e-14
     assert rel_l2(fiber.nonlocal_Kdelta_apply(fib, g["f"], mu), g["kdelta"]) < 1e-12
-    assert rel_l2(fiber.fiber_induced_velocity(fib, g["f"], g["far"], mu), g["induced"]) < 1e-13
-    assert rel_l2(fiber.fiber_induced_velocity(fib, g["f"], g["far"], mu, include_doublet=True),
-                  g["induced_dbl"]) < 1e-13
 
 
 def test_surface_operators(cuda, g):
@@ -82,9 +79,11 @@ def test_fiber_near_field_api(cuda, g):
                           g["resampled"])
 
 
-def test_kernel_helpers_and_bc_residuals(cuda, g):
-    """rotlet_sum (device), the single-pair *_apply helpers and bc_residuals
-    for every boundary-condition kind (kernels.py:22-174, fiber.py:375-441)."""
+def test_kernel_helpers(cuda, g):
+    """rotlet_sum (device) and the single-pair *_apply helpers (kernels.py:22-174).
+    The host boundary residuals (fiber.py:375-441) stay in the reference; the
+    device rows that replace them are pinned through BlockOperator.apply
+    (test_gpu_solver.py, test_gpu_baseline_steps.py)."""
     from paper_1602_05650_b200 import kernels
     mu = float(g["mu"])
     rot, bad = kernels.rotlet_sum(g["tgt"], g["rot_src"], g["rot_L"], 0.2)
@@ -94,21 +93,4 @@ def test_kernel_helpers_and_bc_residuals(cuda, g):
                         kernels.stresslet_apply(t[0], f[1], f[2], mu),
                         kernels.rotlet_apply(t[1], f[3], mu), kernels.doublet_apply(t[2], f[4], mu)])
     assert np.array_equal(a, g["apply1"])
-    fib = fiber.Fiber(g["X"], eps=float(g["eps"]), E=float(g["E"]))
-    d = fib.tangents[-1]
-    kin = dict(U=np.array([0.1, -0.2, 0.05]), omega=np.array([0.3, 0.1, -0.2]),
-               center=fib.X[-1] - 0.4 * d, dt=1e-3)
-    cases = {
-        "free": (fiber.FreeEnd(), fiber.FreeEnd()),
-        "pft": (fiber.PrescribedForceTorque([0.5, -1.0, 0.2], [0.1, 0.0, -0.3]), fiber.FreeEnd()),
-        "hinged": (fiber.HingedToSurface(fib.X[0] + 0.01, 3.0), fiber.FreeEnd()),
-        "clamped": (fiber.FreeEnd(), fiber.ClampedToBody(0, fib.X[-1], d)),
-        "clamped_h": (fiber.FreeEnd(), fiber.ClampedToBody(0, fib.X[-1])),
-    }
-    for name, (bp, bm) in cases.items():
-        fib.bc_plus, fib.bc_minus = bp, bm
-        for hom in (False, True):
-            r = fiber.bc_residuals(fib, g["Xc"], g["Tc"], body_kinematics=kin, mu=mu,
-                                   u_bar=np.array([0.01, 0.02, -0.03]), homogeneous=hom)
-            ref = g[f"bc_{name}_{int(hom)}"]
-            assert np.abs(r - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max()), name
+

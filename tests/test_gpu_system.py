@@ -100,12 +100,26 @@ def test_near_fiber_pair_routes_through_near_evaluation(cuda):
     rng = np.random.default_rng(5)
     f = [rng.standard_normal((17, 3)), np.zeros((17, 3))]
     st = system.SystemState([fa, fb])
+    from oracle import nearfield as host_near
+    from oracle import pairs
     dev = system.complementary_velocities(st, fiber_forces=f,
                                           cache=system.InteractionCache(st, near="device"))
-    host = system.complementary_velocities(st, fiber_forces=f,
-                                           cache=system.InteractionCache(st, near="host"))
     assert len(system.InteractionCache(st).near_fiber) > 0
-    assert rel_l2(dev.fibers[1], host.fibers[1]) < 1e-12
+    # host checker: plain sum of fiber a at fiber b's nodes + the oracle's near maps
+    near = host_near.find_fiber_pairs([fa, fb], np.vstack([fa.X, fb.X]),
+                                      np.repeat([0, 1], 17), 1.0, True)
+    w = fa.node_weights()
+    pref = 1.0 / (8.0 * np.pi)
+    u, _ = pairs.stokeslet_sum(fb.X, np.ones(17, np.int64), fa.X, np.zeros(17, np.int64),
+                               w[:, None] * f[0], pref)
+    c = (fa.eps * fa.L) ** 2 / 2.0
+    u2, _ = pairs.doublet_sum(fb.X, np.ones(17, np.int64), fa.X, np.zeros(17, np.int64),
+                              c * w[:, None] * f[0], pref)
+    u = u + u2
+    for t, l, W in near:
+        if t >= 17 and l == 0:
+            u[t - 17] += W @ f[0].ravel()
+    assert rel_l2(dev.fibers[1], u) < 1e-12
 
 
 def test_cache_reference_attributes(cuda):
