@@ -175,6 +175,30 @@ int sf_sbt_symmetric_partial(const double *X, const int64_t *grp, int64_t N,
                              const double *dcoef, double pref, int mode, int rank, int world,
                              double *out, int64_t *bad, void *stream);
 
+/* The same sum over an explicit contiguous range [t0, t0 + ntasks) of the
+ * sf_sym_task_count(N, group_size, mode) unit-pair tasks (row-major
+ * {g <= h}): a rank's share when the split is chosen by the caller, e.g. by
+ * modelled cost (sf_sym_task_costs).  Any partition of the tasks into ranges
+ * sums to the full symmetric result. */
+int sf_sbt_symmetric_tasks(const double *X, const int64_t *grp, int64_t N,
+                           int64_t group_size, const double *f, const double *w,
+                           const double *dcoef, double pref, int mode, int64_t t0,
+                           int64_t ntasks, double *out, int64_t *bad, void *stream);
+int64_t sf_sym_task_count(int64_t N, int64_t group_size, int mode);
+/* Points per unit of the symmetric evaluation (units align to fibers). */
+int64_t sf_sym_unit_size(int64_t N, int64_t group_size, int mode);
+/* Modelled cost (device array, one double per task) of every unit-pair task
+ * of the symmetric evaluation of positions X / groups grp: the task kernel's
+ * slab-pair decisions replayed, a check-free cell costing 1, a checked cell
+ * c_checked and a diagonal-task cell c_diag (geometry only; no forces). */
+int sf_sym_task_costs(const double *X, const int64_t *grp, int64_t N, int64_t group_size,
+                      int mode, double c_checked, double c_diag, double *cost, void *stream);
+/* Non-excluded ordered pair interactions and kernel launches of one
+ * sf_sbt_symmetric_tasks call over [t0, t0 + count) (host functions). */
+int64_t sf_sym_range_pairs(int64_t N, int64_t group_size, int mode, int64_t t0, int64_t count);
+int64_t sf_sym_range_launch_count(int64_t N, int64_t group_size, int mode, int64_t t0,
+                                  int64_t count);
+
 /* Source-split factor the pair kernels use for nt targets x ns sources (a
  * pure function of the sizes; each target's sum is split into this many
  * ordered chunks).  Used to count kernel launches. */

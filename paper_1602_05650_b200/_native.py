@@ -60,6 +60,12 @@ _SIGNATURES = {
     "sf_workspace_bytes": [],
     "sf_workspace_release": [],
     "sf_sbt_symmetric_partial": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I, _I, _P, _P, _P],
+    "sf_sbt_symmetric_tasks": [_P, _P, _I64, _I64, _P, _P, _P, _D, _I, _I64, _I64, _P, _P, _P],
+    "sf_sym_task_count": [_I64, _I64, _I],
+    "sf_sym_unit_size": [_I64, _I64, _I],
+    "sf_sym_task_costs": [_P, _P, _I64, _I64, _I, _D, _D, _P, _P],
+    "sf_sym_range_pairs": [_I64, _I64, _I, _I64, _I64],
+    "sf_sym_range_launch_count": [_I64, _I64, _I, _I64, _I64],
     "sf_hi_apply": [_P, _P, _P, _P, _P, _P, _P, _P],
     "sf_fiber_dpow": [_P, _P, _I64, _I64, _P, _P],
     "sf_near_search": [_P, _P, _I64, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P],
@@ -142,6 +148,10 @@ def load(require_device=False):
             fn.restype = _I
         lib.sf_sym_shard_pairs.restype = ctypes.c_int64
         lib.sf_sym_launch_count.restype = ctypes.c_int64
+        lib.sf_sym_task_count.restype = ctypes.c_int64
+        lib.sf_sym_unit_size.restype = ctypes.c_int64
+        lib.sf_sym_range_pairs.restype = ctypes.c_int64
+        lib.sf_sym_range_launch_count.restype = ctypes.c_int64
         lib.sf_workspace_bytes.restype = ctypes.c_int64
         lib.sf_gmres_state_doubles.restype = ctypes.c_int64
         lib.sf_tree_work_doubles.restype = ctypes.c_int64

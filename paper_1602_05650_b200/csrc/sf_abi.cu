@@ -365,12 +365,66 @@ extern "C" int64_t sf_sym_launch_count(int64_t N, int64_t group_size, int mode, 
     return sf::sym_launch_count(N, group_size, mode, rank, world);
 }
 
+static int64_t sym_range_pairs(int64_t N, int64_t group_size, int64_t M, int64_t t0,
+                               int64_t count);
+
 extern "C" int64_t sf_sym_shard_pairs(int64_t N, int64_t group_size, int rank, int world) {
     if (N <= 0 || world < 1 || rank < 0 || rank >= world) return 0;
     const int64_t M = sf::sym_unit_size(N, group_size, SF_MODE_FP64);   // the FP64 task split
     const int64_t G = (N + M - 1) / M;
     int64_t count = 0;
     const int64_t t0 = sf::sym_task_range(G, N, M, rank, world, &count);
+    return sym_range_pairs(N, group_size, M, t0, count);
+}
+
+extern "C" int64_t sf_sym_range_pairs(int64_t N, int64_t group_size, int mode, int64_t t0,
+                                      int64_t count) {
+    if (N <= 0 || t0 < 0 || count <= 0) return 0;
+    return sym_range_pairs(N, group_size, sf::sym_unit_size(N, group_size, mode), t0, count);
+}
+
+extern "C" int64_t sf_sym_unit_size(int64_t N, int64_t group_size, int mode) {
+    if (N <= 0) return 0;
+    return sf::sym_unit_size(N, group_size, mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64);
+}
+
+extern "C" int64_t sf_sym_task_count(int64_t N, int64_t group_size, int mode) {
+    return sf::sym_task_total(N, group_size, mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64);
+}
+
+extern "C" int64_t sf_sym_range_launch_count(int64_t N, int64_t group_size, int mode, int64_t t0,
+                                             int64_t count) {
+    if (N <= 0 || t0 < 0 || count < 0) return 0;
+    return sf::sym_launch_count_range(N, group_size,
+                                      mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64, t0,
+                                      count);
+}
+
+extern "C" int sf_sym_task_costs(const double *X, const int64_t *grp, int64_t N,
+                                 int64_t group_size, int mode, double c_checked, double c_diag,
+                                 double *cost, void *stream) {
+    SF_REQUIRE(N >= 0 && (N == 0 || (X && cost)), "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    return sf::sym_task_costs(X, grp, N, group_size,
+                              mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64, c_checked,
+                              c_diag, cost, st, workspace_for(st));
+}
+
+extern "C" int sf_sbt_symmetric_tasks(const double *X, const int64_t *grp, int64_t N,
+                                      int64_t group_size, const double *f, const double *w,
+                                      const double *dcoef, double pref, int mode, int64_t t0,
+                                      int64_t ntasks, double *out, int64_t *bad, void *stream) {
+    SF_REQUIRE(N >= 0 && t0 >= 0 && ntasks >= 0, "bad sizes");
+    SF_REQUIRE(N == 0 || (X && f && out), "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    return sf::pairs_sbt_symmetric_tasks(X, grp, N, group_size, f, w, dcoef, pref, t0, ntasks, out,
+                                         bad, 0, st, workspace_for(st),
+                                         mode == SF_MODE_FP32C ? SF_MODE_FP32C : SF_MODE_FP64);
+}
+
+static int64_t sym_range_pairs(int64_t N, int64_t group_size, int64_t M, int64_t t0,
+                               int64_t count) {
+    const int64_t G = (N + M - 1) / M;
     auto units = [&](int64_t t, int64_t &g, int64_t &h) {   // row-major {g <= h}
         int64_t r = 0, start = 0;
         while (start + (G - r) <= t) { start += G - r; ++r; }

@@ -88,6 +88,15 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
                               cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
+int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
+                              const double *f, const double *w, const double *dcoef, double pref,
+                              int64_t t0, int64_t ntasks, double *out, int64_t *bad,
+                              int accumulate, cudaStream_t st, Workspace &ws, int mode);
+int64_t sym_task_total(int64_t N, int64_t group_size, int mode);
+int64_t sym_launch_count_range(int64_t N, int64_t group_size, int mode, int64_t t0,
+                               int64_t ntasks);
+int sym_task_costs(const double *x, const int64_t *grp, int64_t N, int64_t group_size, int mode,
+                   double c_checked, double c_diag, double *cost, cudaStream_t st, Workspace &ws);
 int add_counter(int64_t *dst, const int64_t *src, cudaStream_t st);
 int sym_unit_size(int64_t N, int64_t group_size, int mode);
 int64_t sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int world);

@@ -77,6 +77,7 @@ struct SymArgs {
     int64_t Bstride;  // N - ga M
     unsigned long long *bad;
     const double *x;  // (N, 3) FP64 positions: the FP32 variant's coincidence test
+    int nofast;       // SF_SYM_NOFAST=1: every slab pair on the checked path (cost model)
 };
 
 constexpr int kSymThreads = 128;
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             __syncwarp();
             double uj[3] = {0, 0, 0};
             const SlabMeta &mj = a.slab[h0 / 32 + sl];
-            const bool fast = (mj.gmax < gmn || mj.gmin > gmx) &&
+            const bool fast = !a.nofast && (mj.gmax < gmn || mj.gmin > gmx) &&
                               (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
             const int nxt = (lane + 1) & 31;
             // step s: this lane pairs its i's with j = (lane + s) mod 32 and
@@ -437,6 +438,54 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
         nb = warp_sum_int(nb);
         if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
     }
+}
+
+// Modelled cost of every unit-pair task (one thread per task), replaying the
+// task kernel's slab-pair decisions (TBI = 4 i points per lane): a both-ways
+// slab pair on the check-free path costs 1 per (i, j) cell, on the checked
+// path c_checked; a diagonal task's cells cost c_diag (one direction at a
+// time, always checked).  Cells of invalid lanes count too: the kernel
+// evaluates them.  Used to split the tasks over ranks by time, not pairs.
+__global__ void sym_task_cost_kernel(const SlabMeta *__restrict__ meta, int64_t N, int M, int G,
+                                     int64_t ntasks, double c_checked, double c_diag,
+                                     double *__restrict__ cost) {
+    constexpr int TBI = 4, kI = 32 * TBI;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntasks) return;
+    int g, h;
+    task_units(t, G, g, h);
+    const bool both = g != h;
+    const int64_t g0 = (int64_t)g * M, h0 = (int64_t)h * M;
+    const int ng = (int)min((int64_t)M, N - g0), nh = (int)min((int64_t)M, N - h0);
+    const int nslab = (nh + 31) / 32;
+    double c = 0.0;
+    for (int ib = 0; ib < ng; ib += kI) {
+        const SlabMeta *mi = meta + (g0 + ib) / 32;
+        const int kvalid = min(TBI, (ng - ib + 31) / 32);
+        double blo[3], bhi[3];
+        int gmn = mi[0].gmin, gmx = mi[0].gmax;
+        for (int q = 0; q < 3; ++q) { blo[q] = mi[0].lo[q]; bhi[q] = mi[0].hi[q]; }
+        for (int k = 1; k < kvalid; ++k) {
+            for (int q = 0; q < 3; ++q) {
+                blo[q] = fmin(blo[q], mi[k].lo[q]);
+                bhi[q] = fmax(bhi[q], mi[k].hi[q]);
+            }
+            gmn = min(gmn, mi[k].gmin);
+            gmx = max(gmx, mi[k].gmax);
+        }
+        const double cells = (double)kI * 32.0;
+        for (int sl = 0; sl < nslab; ++sl) {
+            const SlabMeta &mj = meta[h0 / 32 + sl];
+            if (!both) {
+                c += c_diag * cells;
+                continue;
+            }
+            const bool fast = (mj.gmax < gmn || mj.gmin > gmx) &&
+                              (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
+            c += (fast ? 1.0 : c_checked) * cells;
+        }
+    }
+    cost[t] = c;
 }
 
 __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
@@ -684,7 +733,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
 #pragma unroll
             for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
             float uj[3] = {0.f, 0.f, 0.f};
-            const bool fast = (mj.gmax < gmn || mj.gmin > gmx) &&
+            const bool fast = !a.nofast && (mj.gmax < gmn || mj.gmin > gmx) &&
                               (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
             const int nxt = (lane + 1) & 31;
             if (fast && both) {
@@ -702,6 +751,254 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
                     uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
                 }
             } else {
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PDataF pj;
+                    const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
+                    pj.x = A0.x; pj.y = A0.y; pj.z = A0.z; pj.fx = A0.w;
+                    pj.fy = B0.x; pj.fz = B0.y; pj.c = B0.z; pj.c3 = B0.w;
+                    pj.g = js_g[warp][k];
+                    int nbi = 0;
+                    if (fast) {
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) sym_pair_f<false, false>(pi[q], pj, uf[q], uj, nbi);
+                    } else {
+                        const double *xj = pj.g != -3 ? a.x + 3 * (h0 + sl * 32 + k) : nullptr;
+#pragma unroll
+                        for (int q = 0; q < TBI; ++q) {
+                            const double *xi = vi[q] ? a.x + 3 * (g0 + ib + 32 * q + lane) : nullptr;
+                            if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                            else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                        }
+                    }
+                    if (pj.g != -3) nb += nbi;
+                    if (both) {
+                        uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                        uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                        uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) {
+                ud[k][0] += (double)uf[k][0];
+                ud[k][1] += (double)uf[k][1];
+                ud[k][2] += (double)uf[k][2];
+            }
+            if (both && jl < nh) {
+                double *dst = jacc_s + 3 * jl;
+                dst[0] += (double)uj[0];
+                dst[1] += (double)uj[1];
+                dst[2] += (double)uj[2];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            ui_s[warp][32 * k + lane][0] = ud[k][0];
+            ui_s[warp][32 * k + lane][1] = ud[k][1];
+            ui_s[warp][32 * k + lane][2] = ud[k][2];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * kI; e += blockDim.x) {
+            const int il = e / 3, c = e - 3 * il;
+            if (ib + il < ng) {
+                const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
+                __stcs(owner_slot(a, g, h, ib + il) + c, sv);
+            }
+        }
+        __syncthreads();
+    }
+    if (both) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
+            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
+    }
+    if (a.bad) {
+        nb = warp_sum_int(nb);
+        if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
+    }
+}
+
+// Packed FP32 variant (sm_100 fma.rn.f32x2 / add / mul .f32x2): the check-free
+// both-ways step evaluates TWO i points per instruction.  The FP32c kernel is
+// issue-bound (19.3 SASS instructions per interaction, FMA pipe 59 % busy,
+// profiles/r01_ncu_sym_f32_notes.md); pairing i points halves the FP32
+// instructions of a pair (33 per two pairs instead of 34 per pair).  The j
+// slab is staged pre-broadcast ({v, v} pairs, positions and c3 negated) so
+// each j operand is one 64-bit register pair loaded by LDS, no moves.  The
+// transposed sum of a j runs in two FP32 halves (the two i of a pair),
+// combined when the slab ends.  Checked and diagonal slab pairs take the
+// scalar path of sym_task_kernel_f32.
+struct JPacked {     // one j, 64 bytes: {-x,-x,-y,-y} {-z,-z,fx,fx} {fy,fy,fz,fz} {c,c,-c3,-c3}
+    float4 a, b, c, d;
+};
+
+template <int TBI>
+__device__ __forceinline__ void sym_step_packed(const float2 (&px)[TBI / 2], const float2 (&py)[TBI / 2],
+                                                const float2 (&pz)[TBI / 2], const float2 (&pfx)[TBI / 2],
+                                                const float2 (&pfy)[TBI / 2], const float2 (&pfz)[TBI / 2],
+                                                const float2 (&pc)[TBI / 2], const float2 (&pnc3)[TBI / 2],
+                                                const JPacked &j, float2 (&ux)[TBI / 2],
+                                                float2 (&uy)[TBI / 2], float2 (&uz)[TBI / 2],
+                                                float2 (&uj)[3]) {
+    const float2 jnx = make_float2(j.a.x, j.a.y), jny = make_float2(j.a.z, j.a.w);
+    const float2 jnz = make_float2(j.b.x, j.b.y), jfx = make_float2(j.b.z, j.b.w);
+    const float2 jfy = make_float2(j.c.x, j.c.y), jfz = make_float2(j.c.z, j.c.w);
+    const float2 jc = make_float2(j.d.x, j.d.y), jnc3 = make_float2(j.d.z, j.d.w);
+#pragma unroll
+    for (int p = 0; p < TBI / 2; ++p) {
+        const float2 rx = __fadd2_rn(px[p], jnx), ry = __fadd2_rn(py[p], jny),
+                     rz = __fadd2_rn(pz[p], jnz);
+        const float2 r2 = __ffma2_rn(rx, rx, __ffma2_rn(ry, ry, __fmul2_rn(rz, rz)));
+        const float2 ir = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+        const float2 ir2 = __fmul2_rn(ir, ir);
+        const float2 ir3 = __fmul2_rn(ir, ir2);
+        const float2 ir5 = __fmul2_rn(ir3, ir2);
+        // j -> i (owner direction)
+        const float2 a = __ffma2_rn(jc, ir3, ir);
+        const float2 b = __fmul2_rn(__ffma2_rn(rz, jfz, __ffma2_rn(ry, jfy, __fmul2_rn(rx, jfx))),
+                                    __ffma2_rn(jnc3, ir5, ir3));
+        ux[p] = __ffma2_rn(a, jfx, __ffma2_rn(b, rx, ux[p]));
+        uy[p] = __ffma2_rn(a, jfy, __ffma2_rn(b, ry, uy[p]));
+        uz[p] = __ffma2_rn(a, jfz, __ffma2_rn(b, rz, uz[p]));
+        // i -> j (transposed direction; (r_ji.f) r_ji = (r_ij.f) r_ij)
+        const float2 ai = __ffma2_rn(pc[p], ir3, ir);
+        const float2 bi = __fmul2_rn(__ffma2_rn(rz, pfz[p], __ffma2_rn(ry, pfy[p], __fmul2_rn(rx, pfx[p]))),
+                                     __ffma2_rn(pnc3[p], ir5, ir3));
+        uj[0] = __ffma2_rn(ai, pfx[p], __ffma2_rn(bi, rx, uj[0]));
+        uj[1] = __ffma2_rn(ai, pfy[p], __ffma2_rn(bi, ry, uj[1]));
+        uj[2] = __ffma2_rn(ai, pfz[p], __ffma2_rn(bi, rz, uj[2]));
+    }
+}
+
+template <int MINB, int TBI>
+__global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArgs a) {
+    static_assert(TBI % 2 == 0, "i points are paired");
+    constexpr int kI = 32 * TBI, P = TBI / 2;
+    extern __shared__ double jacc_s[];
+    __shared__ double ui_s[4][kI][3];
+    __shared__ JPacked js_p[4][32];
+    __shared__ float4 js_a[4][32], js_b[4][32];
+    __shared__ int js_g[4][32];
+    if ((int64_t)blockIdx.x >= a.ntasks) return;
+    const int64_t t = a.task0 + blockIdx.x;
+    int g, h;
+    task_units(t, a.G, g, h);
+    const bool both = g != h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g0 = (int64_t)g * a.M, h0 = (int64_t)h * a.M;
+    const int ng = (int)min((int64_t)a.M, a.N - g0), nh = (int)min((int64_t)a.M, a.N - h0);
+    const int nslab = (nh + 31) / 32;
+    if (both)
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();
+    int nb = 0;
+    for (int ib = 0; ib < ng; ib += kI) {
+        PDataF pi[TBI];
+        float xl[TBI][3];
+        double oi[TBI][3];
+        bool vi[TBI];
+        double ud[TBI][3];
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            vi[k] = ib + 32 * k + lane < ng;
+            pi[k] = load_point_f(a.src, g0 + ib + 32 * k + lane, vi[k]);
+            xl[k][0] = pi[k].x; xl[k][1] = pi[k].y; xl[k][2] = pi[k].z;
+            const int64_t sk = (g0 + ib) / 32 + (vi[k] ? k : 0);
+            slab_origin(a.slab[sk], oi[k]);
+            ud[k][0] = ud[k][1] = ud[k][2] = 0.0;
+        }
+        // i-side packed coefficients (pairs of i points k = 2p, 2p + 1)
+        float2 pfx[P], pfy[P], pfz[P], pc[P], pnc3[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            pfx[p] = make_float2(pi[2 * p].fx, pi[2 * p + 1].fx);
+            pfy[p] = make_float2(pi[2 * p].fy, pi[2 * p + 1].fy);
+            pfz[p] = make_float2(pi[2 * p].fz, pi[2 * p + 1].fz);
+            pc[p] = make_float2(pi[2 * p].c, pi[2 * p + 1].c);
+            pnc3[p] = make_float2(-pi[2 * p].c3, -pi[2 * p + 1].c3);
+        }
+        const SlabMeta *mi = a.slab + (g0 + ib) / 32;
+        const int kvalid = min(TBI, (ng - ib + 31) / 32);
+        double blo[3], bhi[3];
+        int gmn = mi[0].gmin, gmx = mi[0].gmax;
+        for (int c = 0; c < 3; ++c) { blo[c] = mi[0].lo[c]; bhi[c] = mi[0].hi[c]; }
+        for (int k = 1; k < kvalid; ++k) {
+            for (int c = 0; c < 3; ++c) {
+                blo[c] = fmin(blo[c], mi[k].lo[c]);
+                bhi[c] = fmax(bhi[c], mi[k].hi[c]);
+            }
+            gmn = min(gmn, mi[k].gmin);
+            gmx = max(gmx, mi[k].gmax);
+        }
+        for (int sl = warp; sl < nslab; sl += 4) {
+            const int jl = sl * 32 + lane;
+            const SlabMeta &mj = a.slab[h0 / 32 + sl];
+            const bool fast = !a.nofast && (mj.gmax < gmn || mj.gmin > gmx) &&
+                              (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
+            {
+                const PDataF q = load_point_f(a.src, h0 + jl, jl < nh);
+                if (fast && both) {
+                    JPacked jp;
+                    jp.a = make_float4(-q.x, -q.x, -q.y, -q.y);
+                    jp.b = make_float4(-q.z, -q.z, q.fx, q.fx);
+                    jp.c = make_float4(q.fy, q.fy, q.fz, q.fz);
+                    jp.d = make_float4(q.c, q.c, -q.c3, -q.c3);
+                    js_p[warp][lane] = jp;
+                } else {
+                    js_a[warp][lane] = make_float4(q.x, q.y, q.z, q.fx);
+                    js_b[warp][lane] = make_float4(q.fy, q.fz, q.c, q.c3);
+                    js_g[warp][lane] = q.g;
+                }
+            }
+            {
+                double oj[3];
+                slab_origin(mj, oj);
+#pragma unroll
+                for (int k = 0; k < TBI; ++k) {
+                    pi[k].x = vi[k] ? (float)(((double)xl[k][0] + (oi[k][0] - oj[0]))) : 1e18f;
+                    pi[k].y = vi[k] ? (float)(((double)xl[k][1] + (oi[k][1] - oj[1]))) : 1e18f;
+                    pi[k].z = vi[k] ? (float)(((double)xl[k][2] + (oi[k][2] - oj[2]))) : 1e18f;
+                }
+            }
+            __syncwarp();
+            float uf[TBI][3];
+            float uj[3] = {0.f, 0.f, 0.f};
+            const int nxt = (lane + 1) & 31;
+            if (fast && both) {
+                float2 px[P], py[P], pz[P], ux[P], uy[P], uz[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    px[p] = make_float2(pi[2 * p].x, pi[2 * p + 1].x);
+                    py[p] = make_float2(pi[2 * p].y, pi[2 * p + 1].y);
+                    pz[p] = make_float2(pi[2 * p].z, pi[2 * p + 1].z);
+                    ux[p] = uy[p] = uz[p] = make_float2(0.f, 0.f);
+                }
+                float2 uj2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll 4
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    const JPacked jp = js_p[warp][k];
+                    sym_step_packed<TBI>(px, py, pz, pfx, pfy, pfz, pc, pnc3, jp, ux, uy, uz, uj2);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        uj2[c].x = __shfl_sync(0xffffffffu, uj2[c].x, nxt);
+                        uj2[c].y = __shfl_sync(0xffffffffu, uj2[c].y, nxt);
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    uf[2 * p][0] = ux[p].x; uf[2 * p + 1][0] = ux[p].y;
+                    uf[2 * p][1] = uy[p].x; uf[2 * p + 1][1] = uy[p].y;
+                    uf[2 * p][2] = uz[p].x; uf[2 * p + 1][2] = uz[p].y;
+                }
+                uj[0] = uj2[0].x + uj2[0].y;
+                uj[1] = uj2[1].x + uj2[1].y;
+                uj[2] = uj2[2].x + uj2[2].y;
+            } else {
+#pragma unroll
+                for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
                 for (int s = 0; s < 32; ++s) {
                     const int k = (lane + s) & 31;
                     PDataF pj;
@@ -1039,16 +1336,55 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
                               cudaStream_t st, Workspace &ws, int mode) {
+    int64_t ntasks = 0, t0 = 0;
+    if (N > 0) {
+        const int M = sym_unit_size(N, group_size, mode);
+        const int G = (int)((N + M - 1) / M);
+        t0 = sym_task_range(G, N, M, rank, world, &ntasks);
+    }
+    return pairs_sbt_symmetric_tasks(x, grp, N, group_size, f, w, dcoef, pref, t0, ntasks, out, bad,
+                                     accumulate, st, ws, mode);
+}
+
+int64_t sym_task_total(int64_t N, int64_t group_size, int mode) {
+    if (N <= 0) return 0;
+    const int64_t M = sym_unit_size(N, group_size, mode);
+    const int64_t G = (N + M - 1) / M;
+    return G * (G + 1) / 2;
+}
+
+int sym_task_costs(const double *x, const int64_t *grp, int64_t N, int64_t group_size, int mode,
+                   double c_checked, double c_diag, double *cost, cudaStream_t st, Workspace &ws) {
+    if (N == 0) return SF_OK;
+    const int M = sym_unit_size(N, group_size, mode);
+    const int G = (int)((N + M - 1) / M);
+    const int64_t ntasks = (int64_t)G * (G + 1) / 2;
+    const int64_t nslab = (N + 31) / 32;
+    SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)(nslab + 1), st);
+    if (!meta) return SF_ENOMEM;
+    slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, N, meta);
+    sym_task_cost_kernel<<<(unsigned)((ntasks + 127) / 128), 128, 0, st>>>(meta, N, M, G, ntasks,
+                                                                         c_checked, c_diag, cost);
+    return check_launch("sym_task_cost_kernel");
+}
+
+// The unit-pair tasks [t0, t0 + ntasks) (any contiguous range: a rank's
+// share): out receives their contribution to every point.
+int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
+                              const double *f, const double *w, const double *dcoef, double pref,
+                              int64_t t0, int64_t ntasks, double *out, int64_t *bad,
+                              int accumulate, cudaStream_t st, Workspace &ws, int mode) {
     const bool f32 = mode == SF_MODE_FP32C;
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
     const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
+    if (t0 < 0 || ntasks < 0 || t0 + ntasks > (int64_t)G * (G + 1) / 2)
+        return set_error(SF_EINVAL, "task range outside the %lld unit-pair tasks",
+                         (long long)((int64_t)G * (G + 1) / 2));
     const size_t wave_bytes = sym_wave_bytes();
     const int nbuf_env = sym_wave_streams();
-    int64_t ntasks = 0;
-    const int64_t t0 = sym_task_range(G, N, M, rank, world, &ntasks);
     size_t buf_bytes = 0;
     const std::vector<SymWave> waves = sym_waves(G, N, M, t0, t0 + ntasks, wave_bytes, &buf_bytes);
     SidePool *pool = (waves.size() > 1 && nbuf_env > 1) ? side_pool_for(st) : nullptr;
@@ -1083,6 +1419,11 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     a.G = G;
     a.bad = (unsigned long long *)bad;
     a.x = x;
+    static const int nofast = [] {
+        const char *e = getenv("SF_SYM_NOFAST");
+        return e ? atoi(e) : 0;
+    }();
+    a.nofast = nofast;
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
         const char *e = getenv("SF_SYM_VARIANT");
@@ -1102,6 +1443,9 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     auto run = [&](cudaStream_t s) -> int {
         if (f32) {
             switch (fvariant) {
+                case 134: return launch(sym_task_kernel_f32p<3, 4>, s);
+                case 124: return launch(sym_task_kernel_f32p<2, 4>, s);
+                case 136: return launch(sym_task_kernel_f32p<3, 6>, s);
                 case 24: return launch(sym_task_kernel_f32<2, 4>, s);
                 case 33: return launch(sym_task_kernel_f32<3, 3>, s);
                 case 26: return launch(sym_task_kernel_f32<2, 6>, s);
@@ -1162,6 +1506,17 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
     return check_launch("sym_scale_kernel");
 }
 
+// kernels launched by one pairs_sbt_symmetric_tasks call over [t0, t0 + ntasks)
+int64_t sym_launch_count_range(int64_t N, int64_t group_size, int mode, int64_t t0,
+                               int64_t ntasks) {
+    if (N == 0) return 0;
+    const int M = sym_unit_size(N, group_size, mode);
+    const int64_t G = (N + M - 1) / M;
+    size_t mx = 0;
+    const auto w = sym_waves(G, N, M, t0, t0 + ntasks, sym_wave_bytes(), &mx);
+    return 3 + 2 * (int64_t)w.size();   // pack + meta + per wave (tasks + reduce) + scale
+}
+
 // kernels launched by one pairs_sbt_symmetric_shard call (gpu_launches accounting)
 int64_t sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int world) {
     if (N == 0) return 0;
@@ -1169,9 +1524,7 @@ int64_t sym_launch_count(int64_t N, int64_t group_size, int mode, int rank, int 
     const int64_t G = (N + M - 1) / M;
     int64_t ntasks = 0;
     const int64_t t0 = sym_task_range(G, N, M, rank, world, &ntasks);
-    size_t mx = 0;
-    const auto w = sym_waves(G, N, M, t0, t0 + ntasks, sym_wave_bytes(), &mx);
-    return 3 + 2 * (int64_t)w.size();   // pack + meta + per wave (tasks + reduce) + scale
+    return sym_launch_count_range(N, group_size, mode, t0, ntasks);
 }
 
 }  // namespace sf

@@ -10,8 +10,69 @@ at any world size.  The distributed implicit step built on it (sharded block
 rows, gathered or all-reduced GMRES) is dsolver.py.
 """
 
+import os
+
+import numpy as np
 import torch
 import torch.distributed as dist
+
+# modelled cost of a symmetric-kernel cell on the checked path and of a
+# diagonal-task cell, relative to a check-free both-ways cell (measured with
+# SF_SYM_NOFAST, tools/sym_split_balance.py; DESIGN.md §6)
+SYM_CHECKED_COST = float(os.environ.get("SF_SYM_CHECKED_COST", "1.11"))
+SYM_DIAG_COST = float(os.environ.get("SF_SYM_DIAG_COST", "0.75"))
+
+
+def sym_task_costs(X, groups, N, n, mode):
+    """Per-task modelled cost (host array) of the symmetric fiber x fiber
+    evaluation of the positions X (device (N,3)): sf_sym_task_costs replays
+    the task kernel's check-free / checked slab-pair decisions."""
+    import ctypes
+
+    from . import _native
+    lib = _native.load(require_device=True)
+    nt = int(lib.sf_sym_task_count(N, n, mode))
+    cost = torch.empty(nt, dtype=torch.float64, device=X.device)
+    _native.call("sf_sym_task_costs", X.data_ptr(), groups.data_ptr() if groups is not None else None,
+                 N, n, mode, SYM_CHECKED_COST, SYM_DIAG_COST, cost.data_ptr(),
+                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    return cost.cpu().numpy()
+
+
+def cost_split(costs, world):
+    """[(t0, count)] per rank: contiguous task ranges of equal modelled cost
+    (boundaries where the cumulative cost crosses r/world of the total).
+    A pure function of the costs, so every rank computes the same split."""
+    c = np.cumsum(np.asarray(costs, dtype=float))
+    total = c[-1] if c.size else 0.0
+    bounds = [0] + [int(np.searchsorted(c, total * r / world, side="left")) + 1
+                    for r in range(1, world)] + [c.size]
+    bounds = np.maximum.accumulate(np.minimum(bounds, c.size))
+    return [(int(bounds[r]), int(bounds[r + 1] - bounds[r])) for r in range(world)]
+
+
+def pair_costs(N, n, mode):
+    """Per-task pair-geometry count (2 n_g n_h both ways, n_g^2 on the
+    diagonal), tasks row-major {g <= h}: the library's pair-count model."""
+    from . import _native
+    M = int(_native.load().sf_sym_unit_size(N, n, mode))
+    G = -(-N // M)
+    nu = np.minimum(M, N - M * np.arange(G)).astype(float)
+    rows = [np.concatenate([[nu[g] * nu[g]], 2.0 * nu[g] * nu[g + 1:]]) for g in range(G)]
+    return np.concatenate(rows)
+
+
+def pair_split(N, n, mode, world):
+    """[(t0, count)] per rank balanced by pair count (SF_SYM_SPLIT=pairs)."""
+    return cost_split(pair_costs(N, n, mode), world)
+
+
+def task_ranges(X, groups, N, n, mode, world):
+    """The rank task split used by the multi-GPU symmetric evaluation:
+    by modelled cost (default) or by pair count (SF_SYM_SPLIT=pairs)."""
+    if os.environ.get("SF_SYM_SPLIT", "cost") == "pairs":
+        return pair_split(N, n, mode, world)
+    return cost_split(sym_task_costs(X, groups, N, n, mode), world)
 
 
 def shard_range(nf, rank, world):

@@ -312,6 +312,7 @@ class DistBlockOperator:
         self._rs_out = torch.zeros((max(self.per, 1) * n, 3), **f64)
         self._bad = torch.zeros(1, dtype=torch.int64, device=dev)
         self._checked = False
+        self._task_range = None
         self.fiber_blocks = torch.empty((no, 4 * n, 4 * n), **f64)
         if no:
             _native.call("sf_fiber_self_blocks", ctypes.byref(self.sys), _ptr(self.fiber_blocks),
@@ -359,9 +360,14 @@ class DistBlockOperator:
         ub_f = self.cache_fib.apply(f_full, q, wr, check=False) if no else None
         if self.symmetric:
             g = self.geo
-            _native.call("sf_sbt_symmetric_partial", _ptr(g.X), _ptr(self.fgrp), N, n,
+            if self._task_range is None:      # cost-balanced split, once per geometry
+                from .dist import task_ranges
+                self._task_range = task_ranges(g.X.reshape(-1, 3), self.fgrp, N, n, self.mode,
+                                               c.world)[c.rank]
+            t0, cnt = self._task_range
+            _native.call("sf_sbt_symmetric_tasks", _ptr(g.X), _ptr(self.fgrp), N, n,
                          _ptr(f_full), _ptr(g.wnode), _ptr(self.fdcoef),
-                         1.0 / (8.0 * math.pi * self.mu), self.mode, c.rank, c.world,
+                         1.0 / (8.0 * math.pi * self.mu), self.mode, t0, cnt,
                          _ptr(self._part), _ptr(self._bad), st)
             self._rs_in[:N].copy_(self._part)
             c.reduce_scatter_sum(self._rs_out, self._rs_in)

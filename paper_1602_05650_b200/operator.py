@@ -164,15 +164,35 @@ class FiberHIOperator:
         return (self.mode in (SF_MODE_FP64, SF_MODE_FP32C) and self.world > 1 and self.N >= 8192
                 and os.environ.get("SF_SYMMETRIC", "1") != "0")
 
+    def task_ranges(self, world=None):
+        """[(t0, count)] per rank of the symmetric unit-pair tasks, balanced
+        by modelled cost (dist.task_ranges; computed once per geometry and
+        world size, identically on every rank)."""
+        from .dist import task_ranges
+        world = self.world if world is None else world
+        cache = self.__dict__.setdefault("_ranges", {})
+        if world not in cache:
+            cache[world] = task_ranges(self.X.reshape(-1, 3), self.groups, self.N, self.n,
+                                       self.mode, world)
+        return cache[world]
+
+    @property
+    def shard_pairs(self):
+        """Non-excluded ordered pair interactions of this rank's task share."""
+        t0, cnt = self.task_ranges()[self.rank]
+        return int(_native.load().sf_sym_range_pairs(self.N, self.n, self.mode, t0, cnt))
+
     def symmetric_partial(self, f, out=None, rank=None, world=None):
-        """(N,3) contribution of this rank's unit-pair tasks to every point."""
+        """(N,3) contribution of this rank's unit-pair tasks to every point
+        (sf_sbt_symmetric_tasks over the rank's cost-balanced task range)."""
         import torch
         f = torch.as_tensor(f, dtype=torch.float64, device=self.device).contiguous()
         if out is None:
             out = torch.empty((self.N, 3), dtype=torch.float64, device=self.device)
-        _native.call("sf_sbt_symmetric_partial", _ptr(self.X), _ptr(self.groups), self.N, self.n,
-                     _ptr(f), _ptr(self.wnode), _ptr(self.dcoef), self.pref, self.mode,
-                     self.rank if rank is None else rank, self.world if world is None else world,
+        rank = self.rank if rank is None else rank
+        t0, cnt = self.task_ranges(world)[rank]
+        _native.call("sf_sbt_symmetric_tasks", _ptr(self.X), _ptr(self.groups), self.N, self.n,
+                     _ptr(f), _ptr(self.wnode), _ptr(self.dcoef), self.pref, self.mode, t0, cnt,
                      _ptr(out), _ptr(self.bad), _stream())
         return out
 
@@ -201,9 +221,11 @@ class FiberHIOperator:
         task kernel and an ordered reduce per wave, final scale
         (sf_sym_launch_count); direct path = pack, tile meta, pair kernel
         (+ ordered split reduce); then near (if any) and self terms."""
-        if self.symmetric or self.symmetric_shard:
-            rank, world = (self.rank, self.world) if self.symmetric_shard else (0, 1)
-            pair = _native.load().sf_sym_launch_count(self.N, self.n, self.mode, rank, world)
+        if self.symmetric:
+            pair = _native.load().sf_sym_launch_count(self.N, self.n, self.mode, 0, 1)
+        elif self.symmetric_shard:
+            t0, cnt = self.task_ranges()[self.rank]
+            pair = _native.load().sf_sym_range_launch_count(self.N, self.n, self.mode, t0, cnt)
         else:
             split = _native.load().sf_pair_split(self.Nown, self.N)
             pair = 3 + (1 if split > 1 else 0)
