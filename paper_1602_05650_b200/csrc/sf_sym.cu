@@ -57,9 +57,12 @@ struct __align__(16) SymSrc {  // same 80-byte record as the pair engine's Src80
 };
 static_assert(sizeof(SymSrc) == 80, "record must be 80 bytes");
 
-struct __align__(16) SlabMeta {  // bounding box + group range of 32 points
+struct __align__(16) SlabMeta {  // bounding box + group range + capsule of 32 points
     double lo[3], hi[3];
     int gmin, gmax;
+    // capsule: segment from the slab's first to its last point, radius = the
+    // largest point-to-segment distance (a fiber's 32 nodes hug its chord)
+    double p0[3], p1[3], rad;
 };
 
 struct SymArgs {
@@ -254,8 +257,63 @@ __device__ __forceinline__ bool boxes_far(const double *blo, const double *bhi, 
     return d2 > 1e-20;
 }
 
+// Squared distance between the segments [p0, p1] and [q0, q1] (closest
+// points with the parameters clamped to [0, 1]).
+__device__ __forceinline__ double seg_seg_dist2(const double *p0, const double *p1,
+                                                const double *q0, const double *q1) {
+    double d1[3], d2[3], r[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        d1[c] = p1[c] - p0[c];
+        d2[c] = q1[c] - q0[c];
+        r[c] = p0[c] - q0[c];
+    }
+    const double a = d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2];
+    const double e = d2[0] * d2[0] + d2[1] * d2[1] + d2[2] * d2[2];
+    const double f = d2[0] * r[0] + d2[1] * r[1] + d2[2] * r[2];
+    double sp = 0.0, tq = 0.0;
+    if (a > 1e-300 || e > 1e-300) {
+        if (a <= 1e-300) {
+            tq = fmin(fmax(f / e, 0.0), 1.0);
+        } else {
+            const double c = d1[0] * r[0] + d1[1] * r[1] + d1[2] * r[2];
+            if (e <= 1e-300) {
+                sp = fmin(fmax(-c / a, 0.0), 1.0);
+            } else {
+                const double b = d1[0] * d2[0] + d1[1] * d2[1] + d1[2] * d2[2];
+                const double den = a * e - b * b;
+                sp = den > 0.0 ? fmin(fmax((b * f - c * e) / den, 0.0), 1.0) : 0.0;
+                tq = (b * sp + f) / e;
+                if (tq < 0.0) {
+                    tq = 0.0;
+                    sp = fmin(fmax(-c / a, 0.0), 1.0);
+                } else if (tq > 1.0) {
+                    tq = 1.0;
+                    sp = fmin(fmax((b - c) / a, 0.0), 1.0);
+                }
+            }
+        }
+    }
+    double d = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double v = (p0[c] + sp * d1[c]) - (q0[c] + tq * d2[c]);
+        d = fma(v, v, d);
+    }
+    return d;
+}
+
+// Two slabs' capsules more than 1e-10 apart: every point pair of the two
+// slabs is then farther than 1e-10 (the check-free path is exact).  Radial
+// aster fibers have overlapping axis-aligned boxes but separate capsules.
+__device__ __forceinline__ bool capsules_far(const SlabMeta &a, const SlabMeta &b) {
+    if (a.rad < 0.0 || b.rad < 0.0) return false;    // capsules disabled (SF_SYM_CAPSULE=0)
+    const double gap = a.rad + b.rad + 1e-10;
+    return seg_seg_dist2(a.p0, a.p1, b.p0, b.p1) > gap * gap;
+}
+
 // Every i slab of the sub-block (kvalid of them, from global/L1 slab metas)
-// farther than 1e-10 from the j slab's box.  Testing each 32-point slab
+// farther than 1e-10 from the j slab (boxes, then capsules).  Testing each 32-point slab
 // box, rather than the union box of the sub-block, keeps the check-free path
 // for asters: fibers fanning out of a centrosome have overlapping union
 // boxes for most slab pairs (62 % at C2) but separate slab boxes (97 %).
@@ -271,7 +329,7 @@ __device__ __forceinline__ bool islabs_far(const SlabMeta *mi, int kvalid, const
                 const double gap = fmax(0.0, fmax(mj.lo[c] - mi[k].hi[c], mi[k].lo[c] - mj.hi[c]));
                 d2 = fma(gap, gap, d2);
             }
-            far = far && d2 > 1e-20;
+            far = far && (d2 > 1e-20 || capsules_far(mi[k], mj));
         }
     }
     return far;
@@ -488,19 +546,54 @@ __global__ void sym_task_cost_kernel(const SlabMeta *__restrict__ meta, int64_t 
     cost[t] = c;
 }
 
+__constant__ int d_capsules_off;   // SF_SYM_CAPSULE=0 (A/B measurements)
+
+// Read SF_SYM_CAPSULE once per process, before the first slab-meta launch
+// (never inside a stream capture: the first call runs uncaptured).
+static void ensure_capsule_flag() {
+    static const bool done = [] {
+        const char *e = getenv("SF_SYM_CAPSULE");
+        const int off = (e && atoi(e) == 0) ? 1 : 0;
+        cudaMemcpyToSymbol(d_capsules_off, &off, sizeof(int));
+        return true;
+    }();
+    (void)done;
+}
+
+// Capsule of one 32-point slab from every lane's point (valid lanes first):
+// p0 = the slab's first point, p1 = its last valid point, rad = the largest
+// point-to-segment distance (padded up for rounding).
+__device__ __forceinline__ void slab_capsule(const double *pt, bool valid, int nvalid, SlabMeta &m) {
+    const int lane = threadIdx.x & 31;
+    double p0[3], p1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        p0[c] = __shfl_sync(0xffffffffu, pt[c], 0);
+        p1[c] = __shfl_sync(0xffffffffu, pt[c], nvalid - 1);
+    }
+    double d = 0.0;
+    if (valid) d = sqrt(seg_seg_dist2(pt, pt, p0, p1));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if (lane == 0) {
+        for (int c = 0; c < 3; ++c) { m.p0[c] = p0[c]; m.p1[c] = p1[c]; }
+        m.rad = d_capsules_off ? -1.0 : d * (1.0 + 1e-12) + 1e-14;
+    }
+}
+
 __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
                                  SlabMeta *__restrict__ meta) {
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (s * 32 >= N) return;
     const int64_t j = s * 32 + lane;
-    double v[6];
+    double v[6], pt[3] = {0.0, 0.0, 0.0};
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
     if (j < N) {
         const SymSrc &q = src[j];
-        v[0] = v[3] = q.v[0];
-        v[1] = v[4] = q.v[1];
-        v[2] = v[5] = q.v[2];
+        v[0] = v[3] = pt[0] = q.v[0];
+        v[1] = v[4] = pt[1] = q.v[1];
+        v[2] = v[5] = pt[2] = q.v[2];
         if (q.g >= 0) { gmn = q.g; gmx = q.g; }
     } else {
         v[0] = v[1] = v[2] = 1e300;
@@ -516,8 +609,9 @@ __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
         gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
         gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
     }
+    SlabMeta m;
+    slab_capsule(pt, j < N, (int)min((int64_t)32, N - s * 32), m);
     if (lane == 0) {
-        SlabMeta m;
         for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
         m.gmin = gmn;
         m.gmax = gmx;
@@ -820,254 +914,6 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     }
 }
 
-// Packed FP32 variant (sm_100 fma.rn.f32x2 / add / mul .f32x2): the check-free
-// both-ways step evaluates TWO i points per instruction.  The FP32c kernel is
-// issue-bound (19.3 SASS instructions per interaction, FMA pipe 59 % busy,
-// profiles/r01_ncu_sym_f32_notes.md); pairing i points halves the FP32
-// instructions of a pair (33 per two pairs instead of 34 per pair).  The j
-// slab is staged pre-broadcast ({v, v} pairs, positions and c3 negated) so
-// each j operand is one 64-bit register pair loaded by LDS, no moves.  The
-// transposed sum of a j runs in two FP32 halves (the two i of a pair),
-// combined when the slab ends.  Checked and diagonal slab pairs take the
-// scalar path of sym_task_kernel_f32.
-struct JPacked {     // one j, 64 bytes: {-x,-x,-y,-y} {-z,-z,fx,fx} {fy,fy,fz,fz} {c,c,-c3,-c3}
-    float4 a, b, c, d;
-};
-
-template <int TBI>
-__device__ __forceinline__ void sym_step_packed(const float2 (&px)[TBI / 2], const float2 (&py)[TBI / 2],
-                                                const float2 (&pz)[TBI / 2], const float2 (&pfx)[TBI / 2],
-                                                const float2 (&pfy)[TBI / 2], const float2 (&pfz)[TBI / 2],
-                                                const float2 (&pc)[TBI / 2], const float2 (&pnc3)[TBI / 2],
-                                                const JPacked &j, float2 (&ux)[TBI / 2],
-                                                float2 (&uy)[TBI / 2], float2 (&uz)[TBI / 2],
-                                                float2 (&uj)[3]) {
-    const float2 jnx = make_float2(j.a.x, j.a.y), jny = make_float2(j.a.z, j.a.w);
-    const float2 jnz = make_float2(j.b.x, j.b.y), jfx = make_float2(j.b.z, j.b.w);
-    const float2 jfy = make_float2(j.c.x, j.c.y), jfz = make_float2(j.c.z, j.c.w);
-    const float2 jc = make_float2(j.d.x, j.d.y), jnc3 = make_float2(j.d.z, j.d.w);
-#pragma unroll
-    for (int p = 0; p < TBI / 2; ++p) {
-        const float2 rx = __fadd2_rn(px[p], jnx), ry = __fadd2_rn(py[p], jny),
-                     rz = __fadd2_rn(pz[p], jnz);
-        const float2 r2 = __ffma2_rn(rx, rx, __ffma2_rn(ry, ry, __fmul2_rn(rz, rz)));
-        const float2 ir = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
-        const float2 ir2 = __fmul2_rn(ir, ir);
-        const float2 ir3 = __fmul2_rn(ir, ir2);
-        const float2 ir5 = __fmul2_rn(ir3, ir2);
-        // j -> i (owner direction)
-        const float2 a = __ffma2_rn(jc, ir3, ir);
-        const float2 b = __fmul2_rn(__ffma2_rn(rz, jfz, __ffma2_rn(ry, jfy, __fmul2_rn(rx, jfx))),
-                                    __ffma2_rn(jnc3, ir5, ir3));
-        ux[p] = __ffma2_rn(a, jfx, __ffma2_rn(b, rx, ux[p]));
-        uy[p] = __ffma2_rn(a, jfy, __ffma2_rn(b, ry, uy[p]));
-        uz[p] = __ffma2_rn(a, jfz, __ffma2_rn(b, rz, uz[p]));
-        // i -> j (transposed direction; (r_ji.f) r_ji = (r_ij.f) r_ij)
-        const float2 ai = __ffma2_rn(pc[p], ir3, ir);
-        const float2 bi = __fmul2_rn(__ffma2_rn(rz, pfz[p], __ffma2_rn(ry, pfy[p], __fmul2_rn(rx, pfx[p]))),
-                                     __ffma2_rn(pnc3[p], ir5, ir3));
-        uj[0] = __ffma2_rn(ai, pfx[p], __ffma2_rn(bi, rx, uj[0]));
-        uj[1] = __ffma2_rn(ai, pfy[p], __ffma2_rn(bi, ry, uj[1]));
-        uj[2] = __ffma2_rn(ai, pfz[p], __ffma2_rn(bi, rz, uj[2]));
-    }
-}
-
-template <int MINB, int TBI>
-__global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArgs a) {
-    static_assert(TBI % 2 == 0, "i points are paired");
-    constexpr int kI = 32 * TBI, P = TBI / 2;
-    extern __shared__ double jacc_s[];
-    __shared__ double ui_s[4][kI][3];
-    __shared__ JPacked js_p[4][32];
-    __shared__ float4 js_a[4][32], js_b[4][32];
-    __shared__ int js_g[4][32];
-    if ((int64_t)blockIdx.x >= a.ntasks) return;
-    const int64_t t = a.task0 + blockIdx.x;
-    int g, h;
-    task_units(t, a.G, g, h);
-    const bool both = g != h;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t g0 = (int64_t)g * a.M, h0 = (int64_t)h * a.M;
-    const int ng = (int)min((int64_t)a.M, a.N - g0), nh = (int)min((int64_t)a.M, a.N - h0);
-    const int nslab = (nh + 31) / 32;
-    if (both)
-        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
-    __syncthreads();
-    int nb = 0;
-    for (int ib = 0; ib < ng; ib += kI) {
-        PDataF pi[TBI];
-        float xl[TBI][3];
-        double oi[TBI][3];
-        bool vi[TBI];
-        double ud[TBI][3];
-#pragma unroll
-        for (int k = 0; k < TBI; ++k) {
-            vi[k] = ib + 32 * k + lane < ng;
-            pi[k] = load_point_f(a.src, g0 + ib + 32 * k + lane, vi[k]);
-            xl[k][0] = pi[k].x; xl[k][1] = pi[k].y; xl[k][2] = pi[k].z;
-            const int64_t sk = (g0 + ib) / 32 + (vi[k] ? k : 0);
-            slab_origin(a.slab[sk], oi[k]);
-            ud[k][0] = ud[k][1] = ud[k][2] = 0.0;
-        }
-        // i-side packed coefficients (pairs of i points k = 2p, 2p + 1)
-        float2 pfx[P], pfy[P], pfz[P], pc[P], pnc3[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-            pfx[p] = make_float2(pi[2 * p].fx, pi[2 * p + 1].fx);
-            pfy[p] = make_float2(pi[2 * p].fy, pi[2 * p + 1].fy);
-            pfz[p] = make_float2(pi[2 * p].fz, pi[2 * p + 1].fz);
-            pc[p] = make_float2(pi[2 * p].c, pi[2 * p + 1].c);
-            pnc3[p] = make_float2(-pi[2 * p].c3, -pi[2 * p + 1].c3);
-        }
-        const SlabMeta *mi = a.slab + (g0 + ib) / 32;
-        const int kvalid = min(TBI, (ng - ib + 31) / 32);
-        double blo[3], bhi[3];
-        int gmn = mi[0].gmin, gmx = mi[0].gmax;
-        for (int c = 0; c < 3; ++c) { blo[c] = mi[0].lo[c]; bhi[c] = mi[0].hi[c]; }
-        for (int k = 1; k < kvalid; ++k) {
-            for (int c = 0; c < 3; ++c) {
-                blo[c] = fmin(blo[c], mi[k].lo[c]);
-                bhi[c] = fmax(bhi[c], mi[k].hi[c]);
-            }
-            gmn = min(gmn, mi[k].gmin);
-            gmx = max(gmx, mi[k].gmax);
-        }
-        for (int sl = warp; sl < nslab; sl += 4) {
-            const int jl = sl * 32 + lane;
-            const SlabMeta &mj = a.slab[h0 / 32 + sl];
-            const bool fast = !a.nofast && (mj.gmax < gmn || mj.gmin > gmx) &&
-                              (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
-            {
-                const PDataF q = load_point_f(a.src, h0 + jl, jl < nh);
-                if (fast && both) {
-                    JPacked jp;
-                    jp.a = make_float4(-q.x, -q.x, -q.y, -q.y);
-                    jp.b = make_float4(-q.z, -q.z, q.fx, q.fx);
-                    jp.c = make_float4(q.fy, q.fy, q.fz, q.fz);
-                    jp.d = make_float4(q.c, q.c, -q.c3, -q.c3);
-                    js_p[warp][lane] = jp;
-                } else {
-                    js_a[warp][lane] = make_float4(q.x, q.y, q.z, q.fx);
-                    js_b[warp][lane] = make_float4(q.fy, q.fz, q.c, q.c3);
-                    js_g[warp][lane] = q.g;
-                }
-            }
-            {
-                double oj[3];
-                slab_origin(mj, oj);
-#pragma unroll
-                for (int k = 0; k < TBI; ++k) {
-                    pi[k].x = vi[k] ? (float)(((double)xl[k][0] + (oi[k][0] - oj[0]))) : 1e18f;
-                    pi[k].y = vi[k] ? (float)(((double)xl[k][1] + (oi[k][1] - oj[1]))) : 1e18f;
-                    pi[k].z = vi[k] ? (float)(((double)xl[k][2] + (oi[k][2] - oj[2]))) : 1e18f;
-                }
-            }
-            __syncwarp();
-            float uf[TBI][3];
-            float uj[3] = {0.f, 0.f, 0.f};
-            const int nxt = (lane + 1) & 31;
-            if (fast && both) {
-                float2 px[P], py[P], pz[P], ux[P], uy[P], uz[P];
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    px[p] = make_float2(pi[2 * p].x, pi[2 * p + 1].x);
-                    py[p] = make_float2(pi[2 * p].y, pi[2 * p + 1].y);
-                    pz[p] = make_float2(pi[2 * p].z, pi[2 * p + 1].z);
-                    ux[p] = uy[p] = uz[p] = make_float2(0.f, 0.f);
-                }
-                float2 uj2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll 4
-                for (int s = 0; s < 32; ++s) {
-                    const int k = (lane + s) & 31;
-                    const JPacked jp = js_p[warp][k];
-                    sym_step_packed<TBI>(px, py, pz, pfx, pfy, pfz, pc, pnc3, jp, ux, uy, uz, uj2);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        uj2[c].x = __shfl_sync(0xffffffffu, uj2[c].x, nxt);
-                        uj2[c].y = __shfl_sync(0xffffffffu, uj2[c].y, nxt);
-                    }
-                }
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    uf[2 * p][0] = ux[p].x; uf[2 * p + 1][0] = ux[p].y;
-                    uf[2 * p][1] = uy[p].x; uf[2 * p + 1][1] = uy[p].y;
-                    uf[2 * p][2] = uz[p].x; uf[2 * p + 1][2] = uz[p].y;
-                }
-                uj[0] = uj2[0].x + uj2[0].y;
-                uj[1] = uj2[1].x + uj2[1].y;
-                uj[2] = uj2[2].x + uj2[2].y;
-            } else {
-#pragma unroll
-                for (int k = 0; k < TBI; ++k) uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
-                for (int s = 0; s < 32; ++s) {
-                    const int k = (lane + s) & 31;
-                    PDataF pj;
-                    const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
-                    pj.x = A0.x; pj.y = A0.y; pj.z = A0.z; pj.fx = A0.w;
-                    pj.fy = B0.x; pj.fz = B0.y; pj.c = B0.z; pj.c3 = B0.w;
-                    pj.g = js_g[warp][k];
-                    int nbi = 0;
-                    if (fast) {
-#pragma unroll
-                        for (int q = 0; q < TBI; ++q) sym_pair_f<false, false>(pi[q], pj, uf[q], uj, nbi);
-                    } else {
-                        const double *xj = pj.g != -3 ? a.x + 3 * (h0 + sl * 32 + k) : nullptr;
-#pragma unroll
-                        for (int q = 0; q < TBI; ++q) {
-                            const double *xi = vi[q] ? a.x + 3 * (g0 + ib + 32 * q + lane) : nullptr;
-                            if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi, xi, xj);
-                            else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi, xi, xj);
-                        }
-                    }
-                    if (pj.g != -3) nb += nbi;
-                    if (both) {
-                        uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
-                        uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
-                        uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
-                    }
-                }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < TBI; ++k) {
-                ud[k][0] += (double)uf[k][0];
-                ud[k][1] += (double)uf[k][1];
-                ud[k][2] += (double)uf[k][2];
-            }
-            if (both && jl < nh) {
-                double *dst = jacc_s + 3 * jl;
-                dst[0] += (double)uj[0];
-                dst[1] += (double)uj[1];
-                dst[2] += (double)uj[2];
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < TBI; ++k) {
-            ui_s[warp][32 * k + lane][0] = ud[k][0];
-            ui_s[warp][32 * k + lane][1] = ud[k][1];
-            ui_s[warp][32 * k + lane][2] = ud[k][2];
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < 3 * kI; e += blockDim.x) {
-            const int il = e / 3, c = e - 3 * il;
-            if (ib + il < ng) {
-                const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                __stcs(owner_slot(a, g, h, ib + il) + c, sv);
-            }
-        }
-        __syncthreads();
-    }
-    if (both) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
-    }
-    if (a.bad) {
-        nb = warp_sum_int(nb);
-        if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
-    }
-}
-
 // Slab bounds straight from the FP64 positions (the FP32 records are packed
 // relative to these boxes' centres afterwards).
 __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
@@ -1078,8 +924,9 @@ __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *
     const int64_t j = s * 32 + lane;
     double v[6];
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
+    double pt[3] = {0.0, 0.0, 0.0};
     if (j < N) {
-        for (int c = 0; c < 3; ++c) v[c] = v[3 + c] = x[3 * j + c];
+        for (int c = 0; c < 3; ++c) v[c] = v[3 + c] = pt[c] = x[3 * j + c];
         const int gj = grp ? pack_source_group(grp[j]) : -1;
         if (gj >= 0) { gmn = gj; gmx = gj; }
     } else {
@@ -1096,8 +943,9 @@ __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *
         gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
         gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
     }
+    SlabMeta m;
+    slab_capsule(pt, j < N, (int)min((int64_t)32, N - s * 32), m);
     if (lane == 0) {
-        SlabMeta m;
         for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
         m.gmin = gmn;
         m.gmax = gmx;
@@ -1356,6 +1204,7 @@ int64_t sym_task_total(int64_t N, int64_t group_size, int mode) {
 int sym_task_costs(const double *x, const int64_t *grp, int64_t N, int64_t group_size, int mode,
                    double c_checked, double c_diag, double *cost, cudaStream_t st, Workspace &ws) {
     if (N == 0) return SF_OK;
+    ensure_capsule_flag();
     const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
     const int64_t ntasks = (int64_t)G * (G + 1) / 2;
@@ -1378,6 +1227,7 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
     if (N == 0) return SF_OK;
+    ensure_capsule_flag();
     const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
     if (t0 < 0 || ntasks < 0 || t0 + ntasks > (int64_t)G * (G + 1) / 2)
@@ -1443,9 +1293,6 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
     auto run = [&](cudaStream_t s) -> int {
         if (f32) {
             switch (fvariant) {
-                case 134: return launch(sym_task_kernel_f32p<3, 4>, s);
-                case 124: return launch(sym_task_kernel_f32p<2, 4>, s);
-                case 136: return launch(sym_task_kernel_f32p<3, 6>, s);
                 case 24: return launch(sym_task_kernel_f32<2, 4>, s);
                 case 33: return launch(sym_task_kernel_f32<3, 3>, s);
                 case 26: return launch(sym_task_kernel_f32<2, 6>, s);
