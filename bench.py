@@ -327,12 +327,12 @@ def measure_steps(config, count, comm=None, warm=True):
     else:
         from paper_1602_05650_b200 import dsolver
 
-        if body or warm_start:
-            raise ValueError("body coupling and warm start are single-GPU options")
+        if warm_start:
+            raise ValueError("warm start is a single-GPU option")
 
         def one(st):
             return dsolver.dist_backward_euler_step(st, dt, comm, params, return_info=True,
-                                                    precision=precision)
+                                                    precision=precision, body_coupling=body)
 
     def sync():
         torch.cuda.synchronize()
@@ -460,7 +460,7 @@ def run_ours(args, rank, world, local_rank):
 
         def dominant():
             op.symmetric_partial(fs, out=part)
-        rank_pairs = _native.load().sf_sym_shard_pairs(op.N, op.n, rank, world)
+        rank_pairs = op.shard_pairs
     else:
         def dominant():
             op.apply(fs, out_nl=u_nl, self_terms=False)
@@ -546,8 +546,8 @@ def run_ours(args, rank, world, local_rank):
         from paper_1602_05650_b200.dsolver import TorchComm
         comm = TorchComm() if world > 1 else None
         cfgs = [c for c in args.step_config.split(",") if c]
-        if comm is not None:           # the body-coupled preconditioner is single-GPU only
-            cfgs = [c for c in cfgs if not ({"body", "warm"} & set(c.partition(":")[2].split("+")))]
+        if comm is not None:           # the warm start is single-GPU only
+            cfgs = [c for c in cfgs if "warm" not in c.partition(":")[2].split("+")]
         for k, cfg in enumerate(cfgs):
             big = cfg.split(":")[0] in ("c3", "c4", "c5")
             try:

@@ -456,9 +456,22 @@ class DistBlockOperator:
 
 
 class DistPreconditioner:
-    """Own fiber blocks (equilibrated LU) + surface diagonal on rank 0."""
+    """Own fiber blocks (equilibrated LU) + surface diagonal on rank 0.
 
-    def __init__(self, op):
+    body_coupling=True adds the body-coupled correction of
+    solver.Preconditioner (not in the reference): the rigid particles'
+    blocks inverted together with their coupling to the fibers, by the same
+    Schur complement / Woodbury construction.  Distributed: W = D^-1
+    A[f, U omega] for the OWN fibers only (fiber rows are fiber-local); the
+    particle rows' dependence on the fiber unknowns, A[p, f] z, from the own
+    fibers' force densities (all-gathered) and attachment wrenches
+    (all-reduced), evaluated redundantly on every rank at the particle nodes
+    (a target-ranged InteractionCache); S^-1 (pend x pend) redundant on every
+    rank.  Per apply: one all-gather of fiber force densities, one
+    all-reduce of the particle wrenches, one broadcast of the particle rows
+    of v; the gathered GMRES variant only."""
+
+    def __init__(self, op, body_coupling=False):
         import torch
         f64 = dict(dtype=torch.float64, device=op.device)
         self.op = op
@@ -499,6 +512,107 @@ class DistPreconditioner:
             if s["kind"] == 1:
                 d = d + 1.0 / op.mu + (s["nrm"] ** 2) * s["w"][:, None] / (op.mu * s["area"])
             self.diag[s["sl"]] = d.reshape(-1)
+        self.coupled = None
+        if body_coupling and op.np and op.nf:
+            self._setup_body_coupling(op)
+
+    # -- body coupling -----------------------------------------------------------
+    def _setup_body_coupling(self, op):
+        import torch
+
+        from .solver import BlockOperator, _particle_block_inverse
+        lay = op.layout
+        c = op.comm
+        f64 = dict(dtype=torch.float64, device=op.device)
+        n, no, nsize = op.n, op.nown, lay.size
+        pend = lay.q1[-1].stop
+        npn = sum(p.mesh.n_nodes for p in op.state.particles)
+        # particle-node targets against every fiber source (redundant per rank)
+        pc = InteractionCache(op.state, target_range=(0, npn), fiber_geometry=op.geo, mode=op.mode)
+        psurf = []
+        for i, part in enumerate(op.state.particles):
+            m = part.mesh
+            psurf.append(dict(kind=0, pi=i, nodes=torch.as_tensor(m.nodes, **f64),
+                              nrm=torch.as_tensor(m.normals, **f64),
+                              w=torch.as_tensor(m.weights, **f64), n=m.n_nodes, area=m.area,
+                              center=op.pcenter[i], sl=lay.q1[i], uom=lay.U[i].start,
+                              tsl=pc.particle_slices[i]))
+        self._pc, self._psurf, self._pend = pc, psurf, pend
+        self._pq0 = torch.zeros((max(npn, 1), 3), **f64)
+        self._pu0 = torch.zeros(6, **f64)
+        self._pubar = torch.empty((max(npn, 1), 3), **f64)
+        self._prow = torch.empty(pend, **f64)
+        self._pwr = torch.empty((op.np, 6), **f64)
+        self._pwork = torch.empty(16, **f64)
+        lo = lay.fib_off + 4 * n * op.f0          # own fiber block range
+        hi = lo + 4 * n * no
+        self._own = (lo, hi)
+        cols = [k for i in range(op.np) for k in range(lay.U[i].start, lay.U[i].start + 6)]
+        # W = D^-1 A[f, U omega] on the own fibers: clamped ends see U, omega;
+        # U, omega are no flow sources, so the fiber rows take ubar = 0
+        zero_ubar = torch.zeros((max(no * n, 1), 3), **f64)
+        W = torch.zeros((hi - lo, len(cols)), **f64)
+        e = torch.zeros(nsize, **f64)
+        rows = torch.zeros(nsize, **f64)
+        z = torch.zeros(nsize, **f64)
+        st = _stream()
+        for k, j in enumerate(cols):
+            if no:
+                e[j] = 1.0
+                _native.call("sf_fiber_rows", ctypes.byref(op.sys), _ptr(e), _ptr(zero_ubar), 0,
+                             _ptr(rows), st)
+                e[j] = 0.0
+                _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c),
+                             _ptr(self.piv), no, self.m, self.off0, None, 0, _ptr(rows), _ptr(z), st)
+                W[:, k] = z[lo:hi]
+        # Z = A[p, f] W (collectives inside, every rank in the same order)
+        Z = torch.empty((pend, len(cols)), **f64)
+        t = torch.zeros(nsize, **f64)
+        for k in range(len(cols)):
+            t[lo:hi] = W[:, k]
+            Z[:, k] = self._particle_rows(t)
+        adapter = _ParticleBlocks(psurf, lay, op.device, op.mu, BlockOperator)
+        Ainv = _particle_block_inverse(adapter)
+        colt = torch.as_tensor(cols, device=op.device)
+        AZ = Ainv @ Z
+        C = torch.eye(len(cols), **f64) - AZ[colt]
+        Cinv, info = torch.linalg.inv_ex(C)
+        ok = torch.tensor([float(int(info.item()) == 0 and bool(torch.isfinite(Cinv).all()))],
+                          **f64)
+        c.all_reduce_sum(ok)                      # every rank raises together
+        if float(ok.item()) < c.world:
+            raise FactorizationError("particle Schur complement is singular")
+        Sinv = torch.addmm(Ainv, AZ, Cinv @ Ainv[colt])
+        self.coupled = dict(W=W, Sinv=Sinv, cols=colt)
+
+    def _particle_rows(self, u):
+        """A[particle rows, fiber columns] u from the fiber entries of u this
+        rank owns (solver.BlockOperator.particle_rows_device, distributed)."""
+        op, c = self.op, self.op.comm
+        st = _stream()
+        no = op.nown
+        sysp = ctypes.byref(op.sys)
+        op._f_pad.zero_()
+        self._pwr.zero_()
+        if no:
+            _native.call("sf_fiber_forces", sysp, _ptr(u), 0, _ptr(op._f_pad), st)
+            _native.call("sf_particle_wrenches", sysp, _ptr(u), None, 0, _ptr(op._wf),
+                         _ptr(self._pwr), st)
+        c.all_gather(op._f_full, op._f_pad)
+        c.all_reduce_sum(self._pwr)
+        f_full = op._f_full[:op.nf * op.n].contiguous()
+        ubar = self._pc.apply(f_full, self._pq0, self._pwr, out=self._pubar, check=False)
+        out = self._prow
+        out.zero_()
+        for s in self._psurf:
+            rows = out[s["sl"]]
+            _native.call("sf_wrench_flow", _ptr(s["nodes"]), s["n"], _ptr(s["center"]),
+                         _ptr(self._pwr[s["pi"]]), op.mu, _ptr(rows), st)
+            _native.call("sf_surface_rows", 0, _ptr(s["nodes"]), _ptr(s["nrm"]), _ptr(s["w"]),
+                         s["n"], _ptr(s["center"]), s["area"], _ptr(self._pq0[:s["n"]]),
+                         _ptr(ubar[s["tsl"]]), _ptr(self._pu0), op.mu, _ptr(self._pwork),
+                         _ptr(rows), _ptr(out[s["uom"]:s["uom"] + 6]), st)
+        return out
 
     def apply_device(self, v, out=None):
         import torch
@@ -507,7 +621,31 @@ class DistPreconditioner:
         _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c), _ptr(self.piv),
                      self.op.nown, self.m, self.off0, _ptr(self.diag), self.ndiag, _ptr(v),
                      _ptr(out), _stream())
+        cp = self.coupled
+        if cp is not None:
+            pend = self._pend
+            vp = v[:pend].clone()
+            self.op.comm.broadcast(vp, src=0)          # particle rows live on rank 0
+            r = vp - self._particle_rows(out)
+            zb = torch.mv(cp["Sinv"], r)
+            out[:pend] = zb
+            lo, hi = self._own
+            if hi > lo:
+                out[lo:hi].addmv_(cp["W"], zb[cp["cols"]], alpha=-1.0)
         return out
+
+
+class _ParticleBlocks:
+    """What solver._particle_block_inverse needs of an operator: the particle
+    surface records, the layout, device and viscosity, and the dense own-
+    particle block A[p, p] (BlockOperator.particle_block_matrix)."""
+
+    def __init__(self, surf, layout, device, mu, block_operator_cls):
+        self.surf, self.layout, self.device, self.mu = surf, layout, device, mu
+        self._cls = block_operator_cls
+
+    def particle_block_matrix(self):
+        return self._cls.particle_block_matrix(self)
 
 
 # ----------------------------------------------------------------- GMRES ----
@@ -663,12 +801,14 @@ def _dist_gmres_reduced(op, prec, rhs, params=None):
 
 
 def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, symmetric=None,
-                             precision="fp64", dt_min=None):
+                             precision="fp64", dt_min=None, body_coupling=False):
     """backward_euler_step (solver.py:528-592) over `comm`'s ranks: the same
     dt halving on NonconvergenceError down to dt_min (every rank takes the
     same GMRES decisions, so every rank retries together) and the same
     rotation check for non-spherical particles before any state changes.
-    The host state is replicated; every rank ends with the same state."""
+    body_coupling=True selects the body-coupled preconditioner
+    (DistPreconditioner; not in the reference).  The host state is
+    replicated; every rank ends with the same state."""
     import torch
     if dt <= 0:
         raise ConfigurationError("time step must be positive")
@@ -679,7 +819,9 @@ def dist_backward_euler_step(state, dt, comm, params=None, return_info=False, sy
     while True:
         op = DistBlockOperator(state, attempt, comm, symmetric=symmetric, precision=precision)
         rhs = op.rhs_device()
-        prec = DistPreconditioner(op)
+        if body_coupling and variant != "gathered":
+            raise ConfigurationError("the body-coupled preconditioner needs SF_DIST_GMRES=gathered")
+        prec = DistPreconditioner(op, body_coupling=body_coupling)
         try:
             x, iters, history = dist_gmres_solve(op, prec, rhs, params, variant=variant)
             break

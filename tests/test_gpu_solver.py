@@ -197,3 +197,27 @@ def test_error_paths_match_reference(cuda):
         solver.backward_euler_step(st, 0.0)
     with pytest.raises(system.ConfigurationError):
         solver.backward_euler_step(st, 1e-3, precision="fp16")
+
+
+@pytest.mark.parametrize("name", ["step_aster.npz", "step_confined.npz"])
+def test_graph_replayed_arnoldi_steps_equal_eager_launches(cuda, name, monkeypatch):
+    """gmres_solve replays one captured CUDA graph per Arnoldi step (matvec
+    with its side-stream pair sums, preconditioner, fused MGS, device Givens);
+    the solution, iteration count and residual history equal those of the
+    kernel-by-kernel launches bit for bit, with or without the lagged status
+    read."""
+    import torch
+    g = golden(name)
+    st = CASES[name](g)
+    op, rhs = solver.assemble_step_operator(st, float(g["dt"]))
+    prec = solver.Preconditioner(op)
+    params = solver.GmresParams(tolerance=float(g["tol"]))
+    res = {}
+    for graph, lag in (("0", 0), ("1", 0), ("1", 1), ("0", 1)):
+        monkeypatch.setenv("SF_GMRES_GRAPH", graph)
+        x, it, hist = solver.gmres_solve(op, prec, rhs, params, lag=lag)
+        res[(graph, lag)] = (x.clone(), it, list(hist))
+    x0, it0, h0 = res[("0", 0)]
+    for key, (x, it, h) in res.items():
+        assert it == it0 and h == h0, key
+        assert torch.equal(x, x0), key
