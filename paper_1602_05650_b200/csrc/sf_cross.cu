@@ -295,6 +295,7 @@ int round_to(int64_t v, int64_t m) { return (int)((v + m - 1) / m * m); }
 bool use_cross(int64_t NA, int64_t NB) {
     const char *e = getenv("SF_CROSS");
     if (e && atoi(e) == 0) return false;
+    if (e && atoi(e) == 2) return NA > 0 && NB > 0;   // forced on (A/B measurements)
     // small surfaces (a C2 particle, 1,024 nodes) give tasks too short to
     // beat the two tiled sweeps; the C4 periphery (40,960 nodes) gains 7 %
     return NA >= 4096 && NB >= 4096;

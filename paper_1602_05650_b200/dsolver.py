@@ -189,12 +189,22 @@ class DistBlockOperator:
         self.cache_fib = (InteractionCache(state, target_range=(lo_f, hi_f), fiber_geometry=geo,
                                            fiber_pairs=not self.symmetric, mode=self.mode)
                           if self.nown else None)
-        # surface targets: rank 0 evaluates the surface/particle sources and the
-        # near maps; the fiber-source sums are split by fiber over the ranks
-        # (each rank: surface targets <- its own fibers) and all-reduced
-        self.cache_surf = (InteractionCache(state, target_range=(0, n_surf_t), fiber_geometry=geo,
+        # surface targets: the fiber-source sums are split by fiber over the
+        # ranks (each rank: surface targets <- its own fibers); the surface-
+        # source sums, completion flows and near maps are split by target
+        # (each rank: its slice of the surface targets); both land in one
+        # (n_surf_t, 3) buffer and ONE all-reduce sums them for rank 0's rows.
+        # Without fibers rank 0 evaluates every surface target itself.
+        if n_surf_t and nf:
+            per_t = -(-n_surf_t // world)
+            a_t = min(n_surf_t, rank * per_t)
+            self._surf_t_slice = (a_t, min(n_surf_t, a_t + per_t))
+        else:
+            self._surf_t_slice = (0, n_surf_t) if rank == 0 else (0, 0)
+        a_t, b_t = self._surf_t_slice
+        self.cache_surf = (InteractionCache(state, target_range=(a_t, b_t), fiber_geometry=geo,
                                             mode=self.mode, fiber_pairs=False)
-                           if rank == 0 and n_surf_t else None)
+                           if b_t > a_t else None)
         self._surf_part = None
         if n_surf_t and nf:
             tgt = np.vstack([p.mesh.nodes for p in state.particles]
@@ -278,6 +288,11 @@ class DistBlockOperator:
                         nrm=torch.as_tensor(m.normals, **f64), w=torch.as_tensor(m.weights, **f64),
                         out=torch.empty((m.n_nodes, 3), **f64))
         self.surf = []
+        # each surface's range in the surface-target list [particles | periphery]
+        counts = [p.mesh.n_nodes for p in state.particles] + (
+            [state.periphery.mesh.n_nodes] if state.periphery is not None else [])
+        edges = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+        surf_slices = [slice(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
         if rank == 0:
             for i, part in enumerate(state.particles):
                 m = part.mesh
@@ -286,14 +301,14 @@ class DistBlockOperator:
                                       w=torch.as_tensor(m.weights, **f64), n=m.n_nodes,
                                       area=m.area, center=self.pcenter[i], sl=lay.q1[i],
                                       uom=lay.U[i].start,
-                                      tsl=self.cache_surf.particle_slices[i]))
+                                      tsl=surf_slices[i]))
             if state.periphery is not None:
                 m = state.periphery.mesh
                 self.surf.append(dict(kind=1, nodes=torch.as_tensor(m.nodes, **f64),
                                       nrm=torch.as_tensor(m.normals, **f64),
                                       w=torch.as_tensor(m.weights, **f64), n=m.n_nodes,
                                       area=m.area, center=None, sl=lay.q0, uom=None,
-                                      tsl=self.cache_surf.periphery_slice))
+                                      tsl=surf_slices[-1]))
         # surface densities in cache order: (slice in u) for every surface, every rank
         self.dens_sl = list(lay.q1) + ([lay.q0] if lay.q0 is not None else [])
         # owned entries of the unknown vector: one contiguous range per rank
@@ -387,6 +402,9 @@ class DistBlockOperator:
                              _ptr(self._surf_bad), st)
             else:
                 self._surf_part.zero_()
+            if self.cache_surf is not None:       # this rank's slice of the surface targets
+                a_t, b_t = self._surf_t_slice
+                self._surf_part[a_t:b_t] += self.cache_surf.apply(f_full, q, wr, check=False)
             c.all_reduce_sum(self._surf_part)
         pref_dl = -3.0 / (4.0 * math.pi * self.mu)
         for d in self.dl_split.values():
@@ -396,7 +414,8 @@ class DistBlockOperator:
             c.all_reduce_sum(d["out"])
         # surfaces (rank 0)
         if self.surf:
-            ub_s = self.cache_surf.apply(f_full, q, wr, check=False) + self._surf_part
+            ub_s = (self._surf_part if self._surf_part is not None
+                    else self.cache_surf.apply(f_full, q, wr, check=False))
             for s in self.surf:
                 qs = u[s["sl"]]
                 rows = out[s["sl"]]
@@ -437,7 +456,7 @@ class DistBlockOperator:
             flags[3] = self._bad.to(torch.float64)[0]
         if self._surf_part is not None and self.nown:
             flags[4] = self._surf_bad.to(torch.float64)[0]
-        if self.surf:
+        if self.cache_surf is not None:
             flags[5] = self.cache_surf.bad.to(torch.float64).sum()
         self.comm.all_reduce_sum(flags)
         self._checked = True

@@ -30,5 +30,7 @@ def test_bench_two_ranks_gloo(cuda):
     assert d["config"]["parallelism"] == "target-shard2"
     assert d["variant_fp32c"]["rel_l2_vs_fp64"] < 1e-5
     steps = d["implicit_steps"]
-    assert len(steps) == 1 and steps[0]["ranks"] == 2          # ':body' is single-GPU only
+    assert len(steps) == 2 and all(s["ranks"] == 2 for s in steps)
+    assert steps[1]["preconditioner"].startswith("body-coupled")   # distributed body coupling
+    assert steps[1]["gmres_iterations"][0] < steps[0]["gmres_iterations"][0]
     assert "error" not in steps[0] and steps[0]["gmres_iterations"][0] > 0

@@ -150,3 +150,22 @@ def test_aster_full_size_rows_match_oracle(cuda, name):
             W = W.cpu().numpy() if torch.is_tensor(W) else np.asarray(W)
             ref[pos[t]] += W.reshape(3, -1) @ qs[si].ravel()
     assert rel(u[rows], ref) < 1e-12
+
+
+def test_full_size_self_terms_match_oracle(cuda, big):
+    """u_self = M f + K_delta f (fiber.py:244-258), the local part of the bench
+    step, at full C5 / C3 size: 48 sampled fibers against the oracle's
+    per-fiber local mobility and K_delta matrix (oracle/ops.py)."""
+    import torch
+
+    from oracle import ops
+    name, cl, F = big
+    op = FiberHIOperator(cl.X, cl.eps)
+    _, u_self = op.apply(torch.as_tensor(F, device=cuda), self_terms=True)
+    u_self = u_self.cpu().numpy().reshape(cl.n_fibers, cl.n_nodes, 3)
+    fibs = np.random.default_rng(9).choice(cl.n_fibers, 48, replace=False)
+    for m in fibs:
+        geo = ops.geometry(cl.X[m])
+        ref = ops.local_mobility_apply(geo["tangents"], cl.eps, F[m], 1.0) + \
+            (ops.kdelta_matrix(cl.X[m], geo, 1.0) @ F[m].ravel()).reshape(-1, 3)
+        assert rel(u_self[m], ref) < 1e-12, m
