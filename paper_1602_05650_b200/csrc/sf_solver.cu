@@ -1400,7 +1400,7 @@ int sf_surface_rows(int kind, const double *nodes, const double *nrm, const doub
                                                         out_uom);
         return check_launch("particle_rows_kernel");
     }
-    flux_kernel<<<1, 256, 0, st>>>(nrm, w, q, n, work);
+    flux_kernel<<<1, 1024, 0, st>>>(nrm, w, q, n, work);   // one block: a fixed summation order
     int rc = check_launch("flux_kernel");
     if (rc) return rc;
     periphery_rows_kernel<<<grid1d(n), 256, 0, st>>>(nrm, n, q, work, 1.0 / (mu * area), ubar, mu,

@@ -164,8 +164,11 @@ def test_full_size_self_terms_match_oracle(cuda, big):
     _, u_self = op.apply(torch.as_tensor(F, device=cuda), self_terms=True)
     u_self = u_self.cpu().numpy().reshape(cl.n_fibers, cl.n_nodes, 3)
     fibs = np.random.default_rng(9).choice(cl.n_fibers, 48, replace=False)
+    errs = []
     for m in fibs:
         geo = ops.geometry(cl.X[m])
         ref = ops.local_mobility_apply(geo["tangents"], cl.eps, F[m], 1.0) + \
             (ops.kdelta_matrix(cl.X[m], geo, 1.0) @ F[m].ravel()).reshape(-1, 3)
-        assert rel(u_self[m], ref) < 1e-12, m
+        errs.append(rel(u_self[m], ref))
+    print(f"{name} u_self per-fiber rel L2: max {max(errs):.2e}, median {np.median(errs):.2e}")
+    assert max(errs) < 1e-10          # north_star operator tolerance

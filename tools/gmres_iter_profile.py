@@ -19,6 +19,7 @@ st = {"c2": lambda: configs.aster(n_fibers=1024), "c4": lambda: configs.confined
     cfg, lambda: configs.cloud_state(cfg))()
 dt = 1e-3 if cfg in ("c2", "c4") else 5e-3
 params = solver.GmresParams(tolerance=1e-8 if cfg == "c4" else 1e-10)
+os.environ["SF_GMRES_GRAPH"] = "0"      # launch by launch: the profiler window counts matvec calls
 st, info = solver.backward_euler_step(st, dt, params, return_info=True)      # warm-up step
 orig = solver.BlockOperator.rows_device
 calls = [0]
