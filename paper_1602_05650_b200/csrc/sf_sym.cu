@@ -1056,6 +1056,10 @@ int sym_unit_size(int64_t N, int64_t group_size, int mode) {
         const int64_t fill = N / 128;
         if (fill < target) target = fill;
         if (target < 256) target = 256;
+        // r02 sweep (tools/gpu_r02_unit.sh): at N = 32,768 (C2) 384-point
+        // units beat 256 by 2.2 % (1.653 vs 1.690 ms) and still give 7 waves
+        // of tasks; at N = 65,536 (C4 fibers) N/128 = 512 stays best
+        if (N >= 24576 && target < 384) target = 384;
     }
     // multiple of the 128-point i-sub-block (4 per lane x 32 lanes) so no
     // sub-block runs part-empty, and of the fiber size when possible
