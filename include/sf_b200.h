@@ -328,9 +328,14 @@ int sf_fiber_forces(const sf_fiber_sys *S, const double *u, int constants, doubl
 int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *ext,
                          int constants, double *work, double *wout, void *stream);
 /* Fiber residual rows into out (solver.py:137-184, fiber.py:375-441); ubar
- * (nf*n,3) complementary velocity at the fiber nodes or NULL. */
-int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *ubar, int constants,
-                  double *out, void *stream);
+ * (nf*n,3) complementary velocity at the fiber nodes or NULL.  fpre
+ * (optional, point order): the force densities sf_fiber_forces already
+ * computed from the same u and constants; the rows then read them instead
+ * of re-applying D_s^4 and D_s (bit-identical: same arithmetic).  Ignored
+ * when constants are on and S has external forces (the clamped-end rows
+ * need the elastic part alone). */
+int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *fpre, const double *ubar,
+                  int constants, double *out, void *stream);
 /* Dense 4n x 4n self blocks (solver.py:250-294) into A (nf,4n,4n). */
 int sf_fiber_self_blocks(const sf_fiber_sys *S, double *A, void *stream);
 /* In-place equilibrated LU with partial pivoting of nb m x m blocks

@@ -75,7 +75,7 @@ _SIGNATURES = {
                               _P, _P, _P],
     "sf_fiber_forces": [_P, _P, _I, _P, _P],
     "sf_particle_wrenches": [_P, _P, _P, _I, _P, _P, _P],
-    "sf_fiber_rows": [_P, _P, _P, _I, _P, _P],
+    "sf_fiber_rows": [_P, _P, _P, _P, _I, _P, _P],
     "sf_fiber_self_blocks": [_P, _P, _P],
     "sf_block_lu": [_P, _I64, _I64, _P, _P, _P, _P, _P],
     "sf_block_solve": [_P, _P, _P, _P, _I64, _I64, _P, _P, _P, _P],

@@ -228,6 +228,7 @@ __global__ void wrench_reduce_kernel(sf_fiber_sys S, const double *__restrict__ 
 // fiber.py:375-441): velocity rows, inextensibility rows, and the 14
 // boundary residuals in their replacement slots.
 __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
+                                  const double *__restrict__ fpre,
                                   const double *__restrict__ ubar, int constants,
                                   double *__restrict__ out) {
     extern __shared__ double sm[];
@@ -246,10 +247,17 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
     __syncthreads();
     FiberCtx c = fiber_ctx(S, m);
     const double E = S.E[m];
-    elastic_force(c, E, X, T, t, fel);
-    __syncthreads();
-    for (int e = threadIdx.x; e < n3; e += blockDim.x)
-        f[e] = (constants && S.f_ext) ? fel[e] + S.f_ext[o3 + e] : fel[e];
+    const bool ext = constants && S.f_ext;
+    if (fpre && !ext) {
+        // the forces of this u were computed for the HI sum (sf_fiber_forces,
+        // the same elastic_force arithmetic): read them, skip D_s^4 / D_s
+        for (int e = threadIdx.x; e < n3; e += blockDim.x) fel[e] = f[e] = fpre[p3 + e];
+    } else {
+        elastic_force(c, E, X, T, t, fel);
+        __syncthreads();
+        for (int e = threadIdx.x; e < n3; e += blockDim.x)
+            f[e] = ext ? fel[e] + S.f_ext[o3 + e] : fel[e];
+    }
     __syncthreads();
     // flow = M f + K f + u_bar ; warp per row
     const double *K = S.K + (int64_t)n3 * n3 * m;
@@ -1296,15 +1304,15 @@ int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *e
     return check_launch("wrench_reduce_kernel");
 }
 
-int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *ubar, int constants,
-                  double *out, void *stream) {
+int sf_fiber_rows(const sf_fiber_sys *S, const double *u, const double *fpre, const double *ubar,
+                  int constants, double *out, void *stream) {
     SF_CHECK_SYS(S);
     if (S->nf == 0) return SF_OK;
     const size_t smem = sizeof(double) * (8 * 3 * S->n + 2 * S->n + 16);
     int rc = set_smem((const void *)fiber_rows_kernel, smem);
     if (rc) return rc;
-    fiber_rows_kernel<<<(unsigned)S->nf, 128, smem, (cudaStream_t)stream>>>(*S, u, ubar, constants,
-                                                                           out);
+    fiber_rows_kernel<<<(unsigned)S->nf, 128, smem, (cudaStream_t)stream>>>(*S, u, fpre, ubar,
+                                                                           constants, out);
     return check_launch("fiber_rows_kernel");
 }
 

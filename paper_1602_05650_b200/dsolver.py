@@ -389,7 +389,8 @@ class DistBlockOperator:
             if no:
                 ub_f = ub_f + self._rs_out[:no * n]
         if no:
-            _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(ub_f), int(constants), _ptr(out), st)
+            _native.call("sf_fiber_rows", sysp, _ptr(u), _ptr(self._f_pad), _ptr(ub_f),
+                         int(constants), _ptr(out), st)
         # surface targets <- own fibers, summed over ranks
         if self._surf_part is not None:
             if no:
@@ -578,8 +579,8 @@ class DistPreconditioner:
         for k, j in enumerate(cols):
             if no:
                 e[j] = 1.0
-                _native.call("sf_fiber_rows", ctypes.byref(op.sys), _ptr(e), _ptr(zero_ubar), 0,
-                             _ptr(rows), st)
+                _native.call("sf_fiber_rows", ctypes.byref(op.sys), _ptr(e), None, _ptr(zero_ubar),
+                             0, _ptr(rows), st)
                 e[j] = 0.0
                 _native.call("sf_precond_apply", _ptr(self.LU), _ptr(self.r), _ptr(self.c),
                              _ptr(self.piv), no, self.m, self.off0, None, 0, _ptr(rows), _ptr(z), st)

@@ -324,8 +324,8 @@ class BlockOperator:
                              s["n"], None, s["area"], _ptr(qs), _ptr(ub), None, self.mu,
                              _ptr(self._work), _ptr(rows), None, st)
         for b in self.batches:
-            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), _ptr(ubar[c.fiber_slice]),
-                         int(constants), _ptr(out), st)
+            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), _ptr(self._f),
+                         _ptr(ubar[c.fiber_slice]), int(constants), _ptr(out), st)
         self.matvecs += 1
         return out
 
@@ -341,8 +341,8 @@ class BlockOperator:
             self._zero_ubar = torch.zeros((max(npts, 1), 3), dtype=torch.float64,
                                           device=self.device)
         for b in self.batches:
-            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), _ptr(self._zero_ubar), 0,
-                         _ptr(out), _stream())
+            _native.call("sf_fiber_rows", ctypes.byref(b.sys), _ptr(u), None, _ptr(self._zero_ubar),
+                         0, _ptr(out), _stream())
         return out
 
     def particle_rows_device(self, u, out=None):
