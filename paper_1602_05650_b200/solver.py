@@ -16,6 +16,7 @@ import ctypes
 import logging
 import math
 import os
+import threading
 
 import numpy as np
 
@@ -485,6 +486,7 @@ def assemble_step_operator(state, dt, mu=None, backend=None, cache=None, implici
 
 
 _PARTICLE_INV_CACHE = []      # [(key arrays, mu, device, inverse)], most recent first
+_PARTICLE_INV_LOCK = threading.Lock()   # emulated ranks (dsolver.ThreadComm) share it
 
 
 def _particle_block_inverse(op):
@@ -509,20 +511,22 @@ def _particle_block_inverse(op):
             flags.append(((r1 - r2).abs().max() <= 1e-13 * scale) & ((n1 - n2).abs().max() <= 1e-13)
                          & ((w1 - w2).abs().max() <= 1e-13 * w1.abs().max()))
         return bool(torch.stack(flags).all())
-    for idx, entry in enumerate(_PARTICLE_INV_CACHE):
-        k, mu, dev, inv = entry
-        if mu == op.mu and dev == op.device and same(k, key):
-            del _PARTICLE_INV_CACHE[idx]          # by position: entries hold tensors
-            _PARTICLE_INV_CACHE.insert(0, entry)
-            return inv
+    with _PARTICLE_INV_LOCK:
+        for idx, entry in enumerate(_PARTICLE_INV_CACHE):
+            k, mu, dev, inv = entry
+            if mu == op.mu and dev == op.device and same(k, key):
+                del _PARTICLE_INV_CACHE[idx]          # by position: entries hold tensors
+                _PARTICLE_INV_CACHE.insert(0, entry)
+                return inv
     A = op.particle_block_matrix()
     if not bool(torch.isfinite(A).all()):
         raise FactorizationError("particle block is not finite")
     inv, info = torch.linalg.inv_ex(A)
     if int(info.item()) != 0 or not bool(torch.isfinite(inv).all()):
         raise FactorizationError("particle block is singular")
-    _PARTICLE_INV_CACHE.insert(0, (key, op.mu, op.device, inv))
-    del _PARTICLE_INV_CACHE[4:]
+    with _PARTICLE_INV_LOCK:
+        _PARTICLE_INV_CACHE.insert(0, (key, op.mu, op.device, inv))
+        del _PARTICLE_INV_CACHE[4:]
     return inv
 
 
@@ -795,11 +799,13 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
     _native.call("sf_gmres_reset", _ptr(gs), R, maxit, beta0, params.tolerance, st)
     history = []
     iters = 0
-    # One Arnoldi step (matvec, preconditioner, fused MGS, Givens) captured
-    # once as a CUDA graph and replayed for every later step: the step index
-    # is read from the device state, so the same graph serves every k; only
-    # the copy V[k] -> vin and the status copy run outside it.  Device-native
-    # operators only (rows_device / apply_device); SF_GMRES_GRAPH=0 disables.
+    # SF_GMRES_GRAPH=1: one Arnoldi step (matvec, preconditioner, fused MGS,
+    # Givens) captured once as a CUDA graph and replayed for every later
+    # step; the step index is read from the device state, so the same graph
+    # serves every k.  Off by default: with the lagged status read the host
+    # already stays ahead of the GPU, so replaying measured no faster at C2
+    # (410 vs 410 ms per step) and the per-solve capture costs ~1 ms at C1
+    # (6.0 vs 5.3 ms per step).  Device-native operators only.
     graph = _ArnoldiGraph.create(operator, preconditioner, V, hcol, gs, hist_off - 8, R, vec,
                                  fused) if n else None
     while True:
@@ -874,7 +880,7 @@ class _ArnoldiGraph:
 
     @classmethod
     def create(cls, operator, preconditioner, V, hcol, gs, sc_off, R, vec, fused):
-        if not fused or os.environ.get("SF_GMRES_GRAPH", "1") == "0":
+        if not fused or os.environ.get("SF_GMRES_GRAPH", "0") != "1":
             return None
         if not hasattr(operator, "rows_device"):
             return None

@@ -201,11 +201,11 @@ def test_error_paths_match_reference(cuda):
 
 @pytest.mark.parametrize("name", ["step_aster.npz", "step_confined.npz"])
 def test_graph_replayed_arnoldi_steps_equal_eager_launches(cuda, name, monkeypatch):
-    """gmres_solve replays one captured CUDA graph per Arnoldi step (matvec
-    with its side-stream pair sums, preconditioner, fused MGS, device Givens);
-    the solution, iteration count and residual history equal those of the
-    kernel-by-kernel launches bit for bit, with or without the lagged status
-    read."""
+    """With SF_GMRES_GRAPH=1 gmres_solve replays one captured CUDA graph per
+    Arnoldi step (matvec with its side-stream pair sums, preconditioner,
+    fused MGS, device Givens); the solution, iteration count and residual
+    history equal those of the kernel-by-kernel launches bit for bit, with
+    or without the lagged status read."""
     import torch
     g = golden(name)
     st = CASES[name](g)

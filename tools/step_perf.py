@@ -18,7 +18,12 @@ ap.add_argument("--tol", type=float, default=1e-10)
 a = ap.parse_args()
 if not a.fibers:
     a.fibers = 2048 if a.config == "c4" else 1024
-if a.config == "c2":
+if a.config == "c1":
+    import bench
+    from paper_1602_05650_b200 import body, fiber, system
+    st = bench.c1_step_state({"fiber": fiber, "body": body, "system": system})
+    dt = 5e-3
+elif a.config == "c2":
     st = configs.aster(n_fibers=a.fibers)
     dt = 1e-3
 elif a.config == "c4":
