@@ -39,10 +39,17 @@ CASES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "bste
 SENS = json.load(open(os.path.join(GOLDEN, "tension_sensitivity.json")))
 
 
+# full-size trajectory fixtures use the sensitivity measured on their
+# reduced-size analogue (same physics; re-running the reference twice more
+# at full size would take hours): the 256-fiber aster for the 10-step C2,
+# the 128-fiber confined aster for C4
+SENS_PROXY = {"bstep_c2_10": "bstep_aster256", "bstep_c4": "bstep_confined"}
+
+
 def sens_tol(name, step, key, base):
     """max(base, 20x the reference's own change of `key` after `step` under
     a 1e-15 relative input perturbation)."""
-    rec = SENS.get(name[:-4])
+    rec = SENS.get(SENS_PROXY.get(name[:-4], name[:-4]))
     if rec is None:
         return base
     steps = rec.get("steps", [])
@@ -50,6 +57,10 @@ def sens_tol(name, step, key, base):
         return max(base, 20.0 * steps[step][key])
     vals = [s[key] for s in steps if key in s] or ([rec["d" + key]] if "d" + key in rec else [])
     return max(base, 20.0 * max(vals)) if vals else base
+
+
+def _light(g):
+    return "light" in g.files
 
 
 def op_tol(name, key, base):
@@ -92,6 +103,8 @@ def test_fixtures_present():
 @pytest.mark.parametrize("name", CASES)
 def test_operator_rhs_preconditioner_at_baseline_orders(cuda, name):
     g = golden(name)
+    if _light(g):
+        pytest.skip("trajectory-only fixture (operator records live in its reduced analogue)")
     st = state_from(g)
     op, rhs = solver.assemble_step_operator(st, float(g["dt"]))
     n = op.layout.size
@@ -118,8 +131,9 @@ def test_trajectory_matches_reference_every_step(cuda, name):
         assert err <= sens_tol(name, s, "X", 1e-8), (s, err)
         assert abs(info["iterations"] - int(g[f"iters_{s}"])) <= 1, (s, info["iterations"])
         assert abs(st.time - float(g[f"time_{s}"])) <= 1e-15
-        T = np.stack([f.T for f in st.fibers])
-        assert rel_l2(T, g[f"step{s}_T"]) < sens_tol(name, s, "T", 1e-6), s
+        if f"step{s}_T" in g.files:
+            T = np.stack([f.T for f in st.fibers])
+            assert rel_l2(T, g[f"step{s}_T"]) < sens_tol(name, s, "T", 1e-6), s
         if st.particles:
             U = np.stack([p.U for p in st.particles])
             assert rel_l2(U, g[f"step{s}_U"]) < sens_tol(name, s, "U", 1e-6), s
