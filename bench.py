@@ -53,9 +53,9 @@ def parse():
     ap.add_argument("--no-variant", action="store_true", help="skip the FP32c variant line")
     ap.add_argument("--launch-check", action="store_true",
                     help="start the ranks (gloo), print one JSON line per rank, do no work")
-    ap.add_argument("--step-config", default="c1,c2,c2:body,c3,c4,c4:body,c5,c5:fp32c",
+    ap.add_argument("--step-config", default="c1,c2,c2:body,c3,c4,c4:body,c4:body+ico,c5,c5:fp32c",
                     help="implicit-step workloads, comma separated, each with optional "
-                         "':fp32c' / ':body' / ':warm' ('+'-joined) options ('' to skip)")
+                         "':fp32c' / ':body' / ':warm' / ':ico' ('+'-joined) options ('' to skip)")
     ap.add_argument("--step-count", type=int, default=3, help="timed steps per small config")
     ap.add_argument("--big-step-count", type=int, default=1,
                     help="timed steps of c3/c4/c5 (2 s / 8 s / 38 s each on one GPU)")
@@ -310,10 +310,13 @@ def measure_steps(config, count, comm=None, warm=True):
         dt, tol = 1e-3, 1e-10
         desc = "c2: 1024 fibers x 32 nodes clamped to a sphere (8x8 patches), plus-end force 1"
     elif config == "c4":
-        st = configs.confined_aster()
+        ico = "ico" in opts
+        st = configs.confined_aster(periphery_mesh="ico" if ico else "patch")
         dt, tol = 1e-3, 1e-8
-        desc = ("c4: 2048 fibers x 32 nodes clamped to a centrosome in a 40,960-node periphery, "
-                "fiber<->boundary and boundary<->boundary double layers")
+        desc = ("c4: 2048 fibers x 32 nodes clamped to a centrosome in a "
+                + ("40,962-vertex icosphere periphery (BASELINE's literal mesh; beyond the "
+                   "reference)" if ico else "40,960-node periphery")
+                + ", fiber<->boundary and boundary<->boundary double layers")
     else:
         st = configs.cloud_state(config)
         dt, tol = 5e-3, 1e-10

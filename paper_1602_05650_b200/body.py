@@ -154,6 +154,54 @@ def make_surface(shape, resolution, center=(0.0, 0.0, 0.0)):
                        phis=ph, patch_grid=(nt, nph), shape=(kind, param, R, Rp), center=center)
 
 
+def make_icosphere(radius, subdivisions, center=(0.0, 0.0, 0.0)):
+    """Icosphere triangle mesh of a sphere (BASELINE config 4 asks for a
+    40,962-vertex icosphere: subdivisions = 6 gives 10 * 4^6 + 2 vertices;
+    the reference supports only patch meshes, make_surface).  Nodes are the
+    vertices projected onto the sphere, normals radial, weights the vertex
+    share (1/3) of the adjacent flat triangles' areas, scaled so they sum to
+    the sphere's area (vertex quadrature, second order).  The mesh carries
+    the sphere's shape (containment and overlap tests) but no patch grid, so
+    targets in its near shell cannot get near-surface maps (GeometryError)."""
+    if radius <= 0 or subdivisions < 0:
+        raise GeometryError("icosphere needs a positive radius and subdivisions >= 0")
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    verts = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t),
+             (0, 1, -t), (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4),
+             (11, 10, 2), (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8),
+             (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    V = np.array(verts, dtype=float)
+    V /= np.linalg.norm(V, axis=1)[:, None]
+    F = np.array(faces, dtype=np.int64)
+    for _ in range(subdivisions):
+        # one midpoint per edge, shared by its two faces
+        e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+        e.sort(axis=1)
+        uniq, inv = np.unique(e, axis=0, return_inverse=True)
+        mid = V[uniq[:, 0]] + V[uniq[:, 1]]
+        mid /= np.linalg.norm(mid, axis=1)[:, None]
+        m = inv.reshape(3, -1) + V.shape[0]          # midpoints of edges 01, 12, 20
+        V = np.vstack([V, mid])
+        a, b, c = F[:, 0], F[:, 1], F[:, 2]
+        F = np.concatenate([np.stack([a, m[0], m[2]], 1), np.stack([b, m[1], m[0]], 1),
+                            np.stack([c, m[2], m[1]], 1), np.stack([m[0], m[1], m[2]], 1)])
+    r = float(radius)
+    P = V * r
+    tri = np.cross(P[F[:, 1]] - P[F[:, 0]], P[F[:, 2]] - P[F[:, 0]])
+    area = 0.5 * np.linalg.norm(tri, axis=1)
+    w = np.zeros(V.shape[0])
+    for k in range(3):
+        np.add.at(w, F[:, k], area / 3.0)
+    w *= 4.0 * math.pi * r * r / w.sum()
+    th = np.arccos(np.clip(V[:, 2], -1.0, 1.0))
+    ph = np.arctan2(V[:, 1], V[:, 0]) % (2.0 * math.pi)
+    mesh = SurfaceMesh(P + np.asarray(center, dtype=float), V.copy(), w, thetas=th, phis=ph,
+                       patch_grid=None, shape=sphere_shape(r), center=center)
+    mesh.triangles = F
+    return mesh
+
+
 class RigidParticle:
     """Closed rigid surface with its double-layer density and wrenches (body.py:197-215)."""
 
@@ -203,7 +251,12 @@ class Periphery:
     """Confining outer surface; fluid on its interior side (body.py:218-234)."""
 
     def __init__(self, mesh):
-        if not mesh.has_parametrization():
+        # the reference needs a patch-parametrized mesh; a star-shaped mesh
+        # without patches (make_icosphere) is accepted for BASELINE config
+        # 4's icosphere -- containment uses its shape, and only near-surface
+        # maps need the patches
+        if not (mesh.has_parametrization() or (mesh.shape is not None and
+                                               getattr(mesh, "triangles", None) is not None)):
             raise GeometryError("periphery requires a parametrized mesh")
         self._dev = None        # devstate.DeviceState holding the density
         self.mesh = mesh

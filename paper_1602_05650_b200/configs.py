@@ -326,15 +326,21 @@ def cloud_state(name="c3_scaled", seed=0, f0=1.0, direction=(0.0, 0.0, -1.0), **
 
 def confined_aster(n_fibers=2048, p=31, centrosome_radius=0.3, centrosome_center=(0.5, 0.0, 0.0),
                    centrosome_res=(8, 8), periphery_radius=2.0, periphery_res=(40, 64),
-                   standoff=1.3, eps=1e-2, E=1.0, motor_force=1.0):
+                   standoff=1.3, eps=1e-2, E=1.0, motor_force=1.0, periphery_mesh="patch"):
     """BASELINE config 4: fibers clamped radially (reference Fibonacci layout,
     system.py:428-443) to a centrosome sphere inside a confining sphere.  The
     icosphere of the baseline is not expressible in the reference; the
-    (40,64)-patch sphere has 40,960 nodes."""
+    (40,64)-patch sphere has 40,960 nodes and is the default.
+    periphery_mesh="ico" uses the literal 40,962-vertex icosphere instead
+    (body.make_icosphere, 6 subdivisions; beyond the reference)."""
     from . import body
     st = aster(n_fibers=n_fibers, p=p, radius=centrosome_radius, standoff=standoff,
                center=centrosome_center, eps=eps, E=E, mesh_res=centrosome_res,
                motor_force=motor_force, layout="fibonacci")
-    per = body.Periphery(body.make_surface(body.sphere_shape(periphery_radius), periphery_res))
+    if periphery_mesh == "ico":
+        per = body.Periphery(body.make_icosphere(periphery_radius, 6))
+    else:
+        per = body.Periphery(body.make_surface(body.sphere_shape(periphery_radius),
+                                               periphery_res))
     from .system import SystemState
     return SystemState(st.fibers, st.particles, per)

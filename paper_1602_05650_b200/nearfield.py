@@ -201,6 +201,10 @@ def device_surface_weights(mesh, targets, mu, device, interior_jump=True, upsamp
 
     def ptr(x):
         return x.data_ptr() if x is not None and x.numel() else None
+    if getattr(mesh, "patch_grid", None) is None:
+        from .body import GeometryError
+        raise GeometryError("a target lies in the near shell of a surface without patches "
+                            "(icosphere); near-surface maps need a make_surface mesh")
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     f64 = dict(dtype=torch.float64, device=device)
     targets = np.atleast_2d(np.asarray(targets, dtype=float))

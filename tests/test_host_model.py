@@ -152,3 +152,19 @@ def test_warm_start_vector_round_trips_through_the_layout():
     assert np.array_equal(parts.q1[0], part.q)
     for m, f in enumerate(st.fibers):
         assert np.array_equal(parts.X[m], f.X) and np.array_equal(parts.T[m], f.T)
+
+
+def test_icosphere_mesh():
+    """make_icosphere (BASELINE config 4's literal 40,962-vertex mesh): vertex
+    count 10 * 4^k + 2, nodes on the sphere, radial unit normals, weights
+    summing to the sphere's area, accepted as a periphery."""
+    import math
+    m = body.make_icosphere(2.0, 6)
+    assert m.n_nodes == 40962 and m.triangles.shape == (20 * 4 ** 6, 3)
+    assert np.allclose(np.linalg.norm(m.nodes, axis=1), 2.0, atol=1e-14)
+    assert np.allclose(m.normals, m.nodes / 2.0, atol=1e-15)
+    assert abs(m.weights.sum() - 16.0 * math.pi) < 1e-11 and m.weights.min() > 0
+    assert m.weights.max() / m.weights.min() < 2.0
+    per = body.Periphery(m)
+    assert per.contains(np.array([[0.0, 0.0, 1.9]]))[0] and not per.contains(
+        np.array([[0.0, 0.0, 2.1]]))[0]
