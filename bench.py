@@ -107,11 +107,36 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- reference (CPU) ----
-def cpu_pair_rate(X, forces, eps, sample_rows, seed=0):
-    """Reference algorithm on the host cores (oracle C port of the numba
-    kernels, OpenMP over all threads): the Stokeslet pass plus the doublet
-    pass of complementary_velocities (system.py:656-671) for a row sample of
-    targets against all sources.  Returns (pairs/s, seconds, pairs, threads)."""
+_REF_KERNELS = None
+
+
+def reference_kernels(threads):
+    """slenderflow.kernels -- the reference's own numba kernels (staged in
+    baseline/_ref by build()) with numba's prange over `threads` threads, or
+    None when the reference is not staged."""
+    global _REF_KERNELS
+    if _REF_KERNELS is None:
+        if not os.path.isdir(os.path.join(REF_PKG, "slenderflow")):
+            _REF_KERNELS = False
+        else:
+            os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+            os.environ["NUMBA_NUM_THREADS"] = str(threads)
+            import importlib
+            sys.path.insert(0, REF_PKG)
+            try:
+                _REF_KERNELS = importlib.import_module("slenderflow.kernels")
+            finally:
+                sys.path.remove(REF_PKG)
+    return _REF_KERNELS or None
+
+
+def cpu_pair_rate(X, forces, eps, sample_rows, seed=0, use_reference=True):
+    """The reference's pair sums on the host cores: the Stokeslet pass plus
+    the doublet pass of complementary_velocities (system.py:656-671) for a
+    row sample of targets against all sources, by slenderflow's OWN numba
+    kernels (kernels.py:72-145, prange over every host thread; JIT compiled
+    before timing) when the reference is staged, else by the oracle's C port
+    of them (OpenMP).  Returns (pairs/s, seconds, pairs, threads, kind)."""
     from oracle import ops, pairs
     nf, n, _ = X.shape
     src = X.reshape(-1, 3)
@@ -124,12 +149,26 @@ def cpu_pair_rate(X, forces, eps, sample_rows, seed=0):
     rng = np.random.default_rng(seed)
     rows = np.sort(rng.choice(src.shape[0], size=sample_rows, replace=False))
     pref = 1.0 / (8.0 * np.pi)
-    t0 = time.perf_counter()
-    u1, _ = pairs.stokeslet_sum(src[rows], grp[rows], src, grp, strengths, pref)
-    u2, _ = pairs.doublet_sum(src[rows], grp[rows], src, grp, dbl, pref)
-    dt = time.perf_counter() - t0
+    threads = host_threads()
+    K = reference_kernels(threads) if use_reference else None
+    if K is not None:
+        t_src, t_grp = np.ascontiguousarray(src[rows]), np.ascontiguousarray(grp[rows])
+        K.stokeslet_sum(t_src[:8], t_grp[:8], src[:64], grp[:64], strengths[:64], pref)   # JIT
+        K.doublet_sum(t_src[:8], t_grp[:8], src[:64], grp[:64], dbl[:64], pref)
+        t0 = time.perf_counter()
+        u1, _ = K.stokeslet_sum(t_src, t_grp, src, grp, strengths, pref)
+        u2, _ = K.doublet_sum(t_src, t_grp, src, grp, dbl, pref)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+    else:
+        t0 = time.perf_counter()
+        u1, _ = pairs.stokeslet_sum(src[rows], grp[rows], src, grp, strengths, pref)
+        u2, _ = pairs.doublet_sum(src[rows], grp[rows], src, grp, dbl, pref)
+        dt = time.perf_counter() - t0
+        threads = pairs.num_threads()
+        kind = "port"
     npairs = sample_rows * (src.shape[0] - n)
-    return npairs / dt, dt, npairs, pairs.num_threads()
+    return npairs / dt, dt, npairs, threads, kind
 
 
 def workload_config(args, cloud, world):
@@ -242,11 +281,13 @@ def reference_implicit_steps(threads, c2_iterations=None):
 
 
 def run_reference(args, rank, world):
-    """The reference's pair sums on the host cores: the oracle C port of the
-    numba kernels (kernels.py:72-145), OpenMP over every host thread.  A step
-    is a bounded row sample of the config's matvec (each target row costs the
-    same Ns pairs), timed as it runs: ms_per_step is that
-    sample's wall time, value its pair-interactions/s."""
+    """The reference's pair sums on the host cores: slenderflow's own numba
+    kernels (kernels.py:72-145, staged in baseline/_ref; the oracle C port if
+    it is not staged), over every host thread.  A step is a bounded row
+    sample of the config's matvec (each target row costs the same Ns pairs,
+    SURVEY §8c), timed as it runs: ms_per_step is that sample's wall time,
+    value its pair-interactions/s.  Plus slenderflow's own implicit steps
+    (reference_implicit_steps)."""
     if rank != 0:
         return
     from oracle import pairs
@@ -261,7 +302,7 @@ def run_reference(args, rank, world):
         cpu_pair_rate(cloud.X, f, cloud.eps, min(rows, 256), seed=1)
     rates, times = [], []
     for k in range(args.steps):
-        r, dt, npairs, threads = cpu_pair_rate(cloud.X, f, cloud.eps, rows, seed=100 + k)
+        r, dt, npairs, threads, kind = cpu_pair_rate(cloud.X, f, cloud.eps, rows, seed=100 + k)
         rates.append(r)
         times.append(dt)
     value = statistics.median(rates)
@@ -273,11 +314,14 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded rejection-sampled perturbed fiber cloud, N(0,1) forces)",
         "config": workload_config(args, cloud, world),
         "cpu_baseline": {"value": value, "unit": "pair-interactions/s", "cores": threads,
-                         "kind": "port",
+                         "kind": kind,
                          "sample": f"each step: {rows} target rows x {N} sources, Stokeslet + "
-                                   f"doublet passes (oracle/oracle_pairs.c, OpenMP on {threads} "
-                                   f"host threads); ms_per_step is the sample's own wall time "
-                                   f"(a full matvec is {N / rows:.0f}x the sample)"},
+                                   f"doublet passes ("
+                                   + ("slenderflow.kernels, the reference's own numba kernels, "
+                                      "prange" if kind == "reference" else
+                                      "oracle/oracle_pairs.c, the C port, OpenMP")
+                                   + f" on {threads} host threads); ms_per_step is the sample's "
+                                   f"own wall time (a full matvec is {N / rows:.0f}x the sample)"},
         "e2e": {"value": value, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "implicit_steps": (reference_implicit_steps(threads)
@@ -567,10 +611,12 @@ def run_ours(args, rank, world, local_rank):
             from oracle import pairs as _pairs
             _pairs.set_num_threads(pairs_mod_threads)
             rows = max(64, int(round(2e10 / cloud.n_points)))     # ~13 s on 16 host cores
-            rate, dt, npairs, threads = cpu_pair_rate(cloud.X, f_all, cloud.eps, rows)
-            cpu = {"value": rate, "unit": "pair-interactions/s", "cores": threads, "kind": "port",
+            rate, dt, npairs, threads, kind = cpu_pair_rate(cloud.X, f_all, cloud.eps, rows)
+            cpu = {"value": rate, "unit": "pair-interactions/s", "cores": threads, "kind": kind,
                    "sample": f"{rows} target rows x {cloud.n_points} sources, Stokeslet + doublet "
-                             f"passes of the oracle C port (OpenMP), {dt:.1f} s"}
+                             f"passes of "
+                             + ("slenderflow's own numba kernels" if kind == "reference"
+                                else "the oracle C port (OpenMP)") + f", {dt:.1f} s"}
         clocks = clk.summary()
         lines = {
             "metric": "stokes_pair_interactions_per_s", "value": value,
