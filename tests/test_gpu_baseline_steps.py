@@ -60,7 +60,7 @@ def sens_tol(name, step, key, base):
 
 
 def _light(g):
-    return "light" in g.files
+    return "light" in g
 
 
 def op_tol(name, key, base):
@@ -131,7 +131,7 @@ def test_trajectory_matches_reference_every_step(cuda, name):
         assert err <= sens_tol(name, s, "X", 1e-8), (s, err)
         assert abs(info["iterations"] - int(g[f"iters_{s}"])) <= 1, (s, info["iterations"])
         assert abs(st.time - float(g[f"time_{s}"])) <= 1e-15
-        if f"step{s}_T" in g.files:
+        if f"step{s}_T" in g:
             T = np.stack([f.T for f in st.fibers])
             assert rel_l2(T, g[f"step{s}_T"]) < sens_tol(name, s, "T", 1e-6), s
         if st.particles:
