@@ -863,8 +863,12 @@ constexpr int kTargetsPerCta = kNT * kTB;
 int choose_split(int64_t nt, int64_t ns) {
     const int64_t blocks = (nt + kTargetsPerCta - 1) / kTargetsPerCta;
     static const int min_tiles = [] {   // source tiles per split (tuning knob)
+        // 2 (r02 A/B): finer source splits for few-target launches, such as
+        // the C2 particle targets x fiber sources sum on the side stream,
+        // fill the symmetric kernel's gaps better (C2 matvec + precond
+        // 2.02 -> 1.98 ms, C1 step 5.67 -> 5.53 ms, C4 unchanged)
         const char *e = getenv("SF_SPLIT_TILES");
-        return e ? atoi(e) : 4;
+        return e ? atoi(e) : 2;
     }();
     int64_t s = (16384 + blocks - 1) / blocks;
     int64_t max_s = ns / (min_tiles * kTS);
