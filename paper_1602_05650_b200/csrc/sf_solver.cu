@@ -1089,7 +1089,10 @@ __global__ void wrench_flow_kernel(const double *__restrict__ trg, int64_t nt,
 // ---------------------------------------------------------- vector kernels
 // Deterministic dot product: fixed grid, fixed per-thread stride order,
 // block tree, then one block sums the block partials in order.
-constexpr int kDotBlocks = 296, kDotThreads = 256;
+// 296 blocks x 512 threads: the fused MGS is latency-bound at mid sizes
+// (C2: ~3 us per inner product); 512-thread blocks cut it 99 -> 83 us per
+// Arnoldi step (148 blocks x 256: 111 us)
+constexpr int kDotBlocks = 296, kDotThreads = 512;
 __global__ void dot_partial_kernel(const double *__restrict__ x, const double *__restrict__ y,
                                    int64_t n, double *__restrict__ part) {
     __shared__ double red[kDotThreads / 32];
