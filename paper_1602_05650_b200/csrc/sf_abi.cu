@@ -127,8 +127,20 @@ SidePool *side_pool_for(cudaStream_t st) {
     SidePool *p = new SidePool();
     bool ok = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&p->done[0], cudaEventDisableTiming) == cudaSuccess;
+    // SF_SIDE_FIRST=1 (A/B, see sf_operator.cu) also puts the last stream,
+    // which carries the operator's overlapping sums, at the highest priority
+    static const bool prio = [] {
+        const char *e = getenv("SF_SIDE_FIRST");
+        return e && atoi(e) == 1;
+    }();
+    int least = 0, greatest = 0;
+    if (prio && cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+        cudaGetLastError();
+        greatest = 0;
+    }
     for (int k = 0; ok && k < SidePool::kStreams; ++k) {
-        ok = cudaStreamCreateWithFlags(&p->s[k], cudaStreamNonBlocking) == cudaSuccess &&
+        const int pr = (prio && k == SidePool::kStreams - 1) ? greatest : 0;
+        ok = cudaStreamCreateWithPriority(&p->s[k], cudaStreamNonBlocking, pr) == cudaSuccess &&
              cudaEventCreateWithFlags(&p->done[k + 1], cudaEventDisableTiming) == cudaSuccess;
     }
     if (!ok) {

@@ -1,6 +1,7 @@
 // sf_internal.h — library-internal declarations shared by the .cu files.
 #pragma once
 #include <cuda_runtime.h>
+#include <functional>
 #include <stddef.h>
 #include <stdint.h>
 
@@ -82,16 +83,19 @@ int pair_split(int64_t nt, int64_t ns);
 int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                         const double *f, const double *w, const double *dcoef, double pref,
                         double *out, int64_t *bad, int accumulate, cudaStream_t st,
-                        Workspace &ws, int mode = SF_MODE_FP64);
+                        Workspace &ws, int mode = SF_MODE_FP64,
+                        const std::function<int()> *after_pack = nullptr);
 bool use_symmetric(int mode, int64_t N);
 int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
-                              cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64);
+                              cudaStream_t st, Workspace &ws, int mode = SF_MODE_FP64,
+                              const std::function<int()> *after_pack = nullptr);
 int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int64_t t0, int64_t ntasks, double *out, int64_t *bad,
-                              int accumulate, cudaStream_t st, Workspace &ws, int mode);
+                              int accumulate, cudaStream_t st, Workspace &ws, int mode,
+                              const std::function<int()> *after_pack = nullptr);
 int64_t sym_task_total(int64_t N, int64_t group_size, int mode);
 int64_t sym_launch_count_range(int64_t N, int64_t group_size, int mode, int64_t t0,
                                int64_t ntasks);

@@ -7,6 +7,7 @@
 //   4. near-field correction maps (block-sparse, CSR by target)
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <mutex>
 #include <unordered_map>
 
@@ -164,41 +165,60 @@ extern "C" int sf_hi_apply(const sf_hi_layout *L, const double *f, const double 
         }
         // non-fiber targets against fiber sources and every target against
         // the surface sources (on the side stream when there is one),
-        // concurrently with the fiber block done symmetrically
+        // concurrently with the fiber block done symmetrically.  The side
+        // work is queued BEFORE the symmetric sum: its first kernel runs
+        // beside the task kernel's first blocks and the rest fills the task
+        // kernel's last-wave tail.  Forking it after the packing kernels at
+        // the highest stream priority (SF_SIDE_FIRST=1) overlaps all of it
+        // with the task kernel instead, which measured slower at C2 (2.34 vs
+        // 2.28 ms per Arnoldi step): both are FP64-bound, so the task kernel
+        // stretches by the side work, and the small side kernels wait ~100 us
+        // each for a slot as the long task blocks retire.
         SideStream side_s;
         SideStream *side = ((off > 0 || L->nss > 0) && side_for(st, &side_s)) ? &side_s : nullptr;
-        if (off > 0 || side) {
+        bool forked = false;
+        std::function<int()> side_work = [&]() -> int {
             cudaStream_t rs = st;
             if (side) {
                 if (cudaEventRecord(side->fork, st) != cudaSuccess ||
                     cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
                     return check_launch("side stream fork");
+                forked = true;
                 rs = side->s;
             }
             Workspace &rws = side ? workspace_for(rs) : ws;
-            rc = off > 0 ? pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f,
-                                              L->fw, L->fdcoef, pref, SF_MODE_FP64, u, bad_f, rs,
-                                              rws, 0)
-                         : SF_OK;
-            if (!rc && side && L->nss > 0) {
+            int r = off > 0 ? pairs_sbt_weighted(L->trg, L->tgrp, off, L->fsrc, L->fgrp, L->nfs, f,
+                                                 L->fw, L->fdcoef, pref, SF_MODE_FP64, u, bad_f, rs,
+                                                 rws, 0)
+                            : SF_OK;
+            if (!r && side && L->nss > 0) {
                 // the stresslet sum unscaled into a side buffer, added after the join
                 stress_tmp = (double *)rws.get(11, sizeof(double) * 3 * (size_t)L->nt, rs);
-                rc = stress_tmp ? pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss,
-                                                  L->snrm, q, 1.0, stress_tmp, bad_s, rs, rws,
-                                                  L->sw, 0)
-                                : SF_ENOMEM;
+                r = stress_tmp ? pairs_stresslet(L->trg, L->tgrp, L->nt, L->ssrc, L->sgrp, L->nss,
+                                                 L->snrm, q, 1.0, stress_tmp, bad_s, rs, rws,
+                                                 L->sw, 0)
+                               : SF_ENOMEM;
             }
-            if (side && cudaEventRecord(side->join, side->s) != cudaSuccess && !rc)
-                rc = check_launch("side stream join");
-            if (rc) {
-                if (side) cudaStreamWaitEvent(st, side->join, 0);
-                return rc;
-            }
+            if (side && cudaEventRecord(side->join, side->s) != cudaSuccess && !r)
+                r = check_launch("side stream join");
+            return r;
+        };
+        static const bool side_first = [] {
+            const char *e = getenv("SF_SIDE_FIRST");
+            return e && atoi(e) == 1;
+        }();
+        if (side && side_first) {
+            rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
+                                     L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws, L->mode,
+                                     &side_work);
+        } else {
+            rc = (off > 0 || side) ? side_work() : SF_OK;
+            if (!rc)
+                rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
+                                         L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws, L->mode);
         }
-        rc = pairs_sbt_symmetric(L->fsrc, L->fgrp, L->nfs, L->fiber_group_size, f, L->fw,
-                                 L->fdcoef, pref, u + 3 * off, bad_sym, 0, st, ws, L->mode);
         // join before anything else touches rows [0, off) or the counters
-        if (side && cudaStreamWaitEvent(st, side->join, 0) != cudaSuccess && !rc)
+        if (forked && cudaStreamWaitEvent(st, side->join, 0) != cudaSuccess && !rc)
             rc = check_launch("side stream wait");
         if (rc) return rc;
         if (bad) {

@@ -751,12 +751,50 @@ __global__ void reduce_partials(const double *__restrict__ partial, int nsplit, 
     double u[P::NACC];
 #pragma unroll
     for (int c = 0; c < P::NACC; ++c) u[c] = 0.0;
-    for (int s = 0; s < nsplit; ++s) {
-        const double *p = partial + ((int64_t)s * nt + i) * P::NACC;
+    // chunk order as before; the loads of 4 chunks are issued together (the
+    // one-load-per-add loop ran latency-bound with only nt threads: 21-45 us
+    // for the 1,024 C2 particle targets over 128 chunks)
+    const int64_t stride = nt * P::NACC;
+    const double *p = partial + i * P::NACC;
+    int s = 0;
+    for (; s + 4 <= nsplit; s += 4) {
+        double v[4][P::NACC];
 #pragma unroll
-        for (int c = 0; c < P::NACC; ++c) u[c] += p[c];
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int c = 0; c < P::NACC; ++c) v[k][c] = __ldcs(p + (s + k) * stride + c);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int c = 0; c < P::NACC; ++c) u[c] += v[k][c];
     }
+    for (; s < nsplit; ++s)
+#pragma unroll
+        for (int c = 0; c < P::NACC; ++c) u[c] += __ldcs(p + s * stride + c);
     write_out<P>(out + (int64_t)P::NOUT * i, u, pref, accumulate);
+}
+
+// The same chunk-order sums with one thread per output element (NOUT == NACC
+// == 3): 3x the threads, and the loads of 8 chunks issued together; few-target
+// launches (1,024 C2 particle nodes x 128 chunks) ran latency-bound at one
+// load per add per target (21-45 us).  Bit-identical to reduce_partials.
+__global__ void reduce_partials3(const double *__restrict__ partial, int nsplit, int64_t nt,
+                                 double pref, double *__restrict__ out, int accumulate) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= 3 * nt) return;
+    const int64_t stride = 3 * nt;
+    const double *p = partial + e;
+    double u = 0.0;
+    int s = 0;
+    for (; s + 8 <= nsplit; s += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldcs(p + (s + k) * stride);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) u += v[k];
+    }
+    for (; s < nsplit; ++s) u += __ldcs(p + s * stride);
+    out[e] = accumulate ? out[e] + pref * u : pref * u;
 }
 
 // ---------------------------------------------------------------- packing ----
@@ -937,7 +975,11 @@ static int launch_pairs(PairArgs a, cudaStream_t st, Workspace &ws) {
                 <<<dim3(nb(kTargetsPerCta), ny), kNT, 0, st>>>(a, meta);
     }
     if (a.nsplit > 1) {
-        reduce_partials<P><<<(unsigned)((a.nt + 255) / 256), 256, 0, st>>>(a.partial, a.nsplit,
+        if (P::NOUT == 3 && P::NACC == 3)
+            reduce_partials3<<<(unsigned)((3 * a.nt + 127) / 128), 128, 0, st>>>(
+                a.partial, a.nsplit, a.nt, a.pref, a.out, a.accumulate);
+        else
+            reduce_partials<P><<<(unsigned)((a.nt + 255) / 256), 256, 0, st>>>(a.partial, a.nsplit,
                                                                           a.nt, a.pref, a.out,
                                                                           a.accumulate);
     }

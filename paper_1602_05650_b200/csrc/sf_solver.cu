@@ -155,26 +155,41 @@ __global__ void fiber_forces_kernel(sf_fiber_sys S, const double *__restrict__ u
 // (fiber.py:361-372), plus the moment arm of the stored attachment point
 // (system.py:308-329).  wf (nf,6) holds F and Le + arm x F (zeros if the fiber
 // is not clamped).
+// A warp per fiber: the lanes stage row n-1 of D_s^2, D_s^3 and the
+// candidate X in shared memory (coalesced), then lane 0 runs the node sums in
+// node order from there -- the arithmetic of the former thread-per-fiber
+// kernel, whose 2n dependent global loads per thread made it latency-bound
+// (16 us at C2).
 __global__ void end_wrench_kernel(sf_fiber_sys S, const double *__restrict__ u,
                                   double *__restrict__ wf) {
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    extern __shared__ double ew_sm[];
+    const int lane = threadIdx.x & 31;
+    const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (m >= S.nf) return;
     const int n = (int)S.n;
-    double *o = wf + 6 * (int64_t)m;
+    double *o = wf + 6 * m;
     const int body = S.bc_body[m];
     if (S.bc_kind[2 * m + 1] != BC_CLAMPED || body < 0) {
-        for (int c = 0; c < 6; ++c) o[c] = 0.0;
+        if (lane < 6) o[lane] = 0.0;
         return;
     }
-    FiberCtx c = fiber_ctx(S, m);
-    const double *blk = u + ublock(S, m);
+    FiberCtx c = fiber_ctx(S, (int)m);
+    const double *blk = u + ublock(S, (int)m);
     const int k = n - 1;
+    double *d2s = ew_sm + (int64_t)(threadIdx.x >> 5) * 5 * n, *d3s = d2s + n, *xs = d3s + n;
+    for (int j = lane; j < n; j += 32) {
+        d2s[j] = c.Ds2[k * n + j];
+        d3s[j] = c.Ds3[k * n + j];
+    }
+    for (int e = lane; e < 3 * n; e += 32) xs[e] = blk[e];
+    __syncwarp();
+    if (lane != 0) return;
     double xss[3] = {0, 0, 0}, xsss[3] = {0, 0, 0};
     for (int j = 0; j < n; ++j) {
-        const double d2 = c.Ds2[k * n + j], d3 = c.Ds3[k * n + j];
+        const double d2 = d2s[j], d3 = d3s[j];
         for (int a = 0; a < 3; ++a) {
-            xss[a] = fma(d2, blk[3 * j + a], xss[a]);
-            xsss[a] = fma(d3, blk[3 * j + a], xsss[a]);
+            xss[a] = fma(d2, xs[3 * j + a], xss[a]);
+            xsss[a] = fma(d3, xs[3 * j + a], xsss[a]);
         }
     }
     const double *t = S.tang + (int64_t)3 * n * m + 3 * k;
@@ -227,7 +242,10 @@ __global__ void wrench_reduce_kernel(sf_fiber_sys S, const double *__restrict__ 
 // One fiber's 4n residual rows (solver.py:137-184 with bc_residuals,
 // fiber.py:375-441): velocity rows, inextensibility rows, and the 14
 // boundary residuals in their replacement slots.
-__global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
+// 128 threads, <= 64 registers: 8 CTAs per SM keep all 1,024 C2 fibers in
+// one wave (94 registers gave 5 per SM and 1.4 waves)
+__global__ void __launch_bounds__(128, 8) fiber_rows_kernel(sf_fiber_sys S,
+                                                            const double *__restrict__ u,
                                   const double *__restrict__ fpre,
                                   const double *__restrict__ ubar, int constants,
                                   double *__restrict__ out) {
@@ -321,9 +339,12 @@ __global__ void fiber_rows_kernel(sf_fiber_sys S, const double *__restrict__ u,
         if (constants) v -= (1.0 / dt + Ldot / Lm) * (x0 * x0 + x1 * x1 + x2 * x2);
         o[n3 + i] = v;
     }
-    // boundary residuals (warp 0)
-    if (warp == 0) {
+    // boundary residuals: the two ends on the last two warps, concurrently
+    // with the inextensibility rows on the first ones (warp 0 for both ends
+    // when the block has fewer than 4 warps)
+    {
         for (int end = 0; end < 2; ++end) {  // 0 = plus (node 0), 1 = minus (node n-1)
+            if (warp != (nw >= 4 ? nw - 2 + end : 0)) continue;
             const int k = end == 0 ? 0 : n - 1;
             const double sig = end == 0 ? 1.0 : -1.0;
             const int kind = S.bc_kind[2 * m + end];
@@ -1299,7 +1320,8 @@ int sf_particle_wrenches(const sf_fiber_sys *S, const double *u, const double *e
     if (S->np == 0) return SF_OK;
     cudaStream_t st = (cudaStream_t)stream;
     if (S->nf > 0) {
-        end_wrench_kernel<<<grid1d(S->nf, 128), 128, 0, st>>>(*S, u, work);
+        end_wrench_kernel<<<(unsigned)((32 * S->nf + 127) / 128), 128,
+                            sizeof(double) * 4 * 5 * S->n, st>>>(*S, u, work);
         int rc = check_launch("end_wrench_kernel");
         if (rc) return rc;
     }

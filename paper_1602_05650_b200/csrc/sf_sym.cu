@@ -81,7 +81,18 @@ struct SymArgs {
     unsigned long long *bad;
     const double *x;  // (N, 3) FP64 positions: the FP32 variant's coincidence test
     int nofast;       // SF_SYM_NOFAST=1: every slab pair on the checked path (cost model)
+    int cs;           // partials stored evict-first (waves larger than L2 can keep)
 };
+
+// Partial stores: evict-first when the wave's partials would not stay in L2
+// anyway (they must not push out the source records, C5), plain write-back
+// when they fit and the ordered reduce can read them from L2 (C2: 67 MB).
+__device__ __forceinline__ void part_store(const SymArgs &a, double *p, double v) {
+    if (a.cs)
+        __stcs(p, v);
+    else
+        *p = v;
+}
 
 constexpr int kSymThreads = 128;
 
@@ -481,7 +492,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double s = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                __stcs(owner_slot(a, g, h, ib + il) + c, s);
+                part_store(a, owner_slot(a, g, h, ib + il) + c, s);
             }
         }
         __syncthreads();
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel(SymArgs a) 
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
+            part_store(a, trans_slot(a, g, h0) + e, jacc_s[e]);
     }
     // invalid i lanes never count (their g is -3 and they sit at 1e30)
     if (a.bad) {
@@ -898,7 +909,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
             const int il = e / 3, c = e - 3 * il;
             if (ib + il < ng) {
                 const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
-                __stcs(owner_slot(a, g, h, ib + il) + c, sv);
+                part_store(a, owner_slot(a, g, h, ib + il) + c, sv);
             }
         }
         __syncthreads();
@@ -906,7 +917,7 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     if (both) {
         __syncthreads();
         for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
-            __stcs(trans_slot(a, g, h0) + e, jacc_s[e]);
+            part_store(a, trans_slot(a, g, h0) + e, jacc_s[e]);
     }
     if (a.bad) {
         nb = warp_sum_int(nb);
@@ -988,6 +999,24 @@ __device__ __forceinline__ int64_t task_index(int64_t g, int64_t h, int64_t G) {
 // slots k in [ga, min(gl, u - 1)] (tasks {k, u}), then, when u is one of the
 // wave's rows, the owner slots h >= u (tasks {u, h}); only tasks inside the
 // wave's range [tb, te) (a partial first or last row, a rank's share) count.
+// The task index grows along both slot runs, so the counted slots are one
+// contiguous run each; their loads are issued 8 at a time (independent) and
+// added in slot order, so the sum is the same as one load per add (the
+// serial form ran latency-bound: 51 us at C2 for 67 MB).
+__device__ __forceinline__ double strided_sum(double s, const double *__restrict__ q,
+                                              int64_t stride, int64_t n) {
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcs(q + (i + j) * stride);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; i < n; ++i) s += __ldcs(q + i * stride);
+    return s;
+}
+
 __global__ void sym_wave_reduce_kernel(const double *__restrict__ A, const double *__restrict__ B,
                                        int G, int64_t N, int M, int64_t ga, int64_t gl,
                                        int64_t tb, int64_t te, int64_t Acols, int64_t Bstride,
@@ -997,19 +1026,19 @@ __global__ void sym_wave_reduce_kernel(const double *__restrict__ A, const doubl
     const int64_t p = e / 3, c = e - 3 * p;
     const int64_t u = p / M;
     double s = acc[e];
-    const int64_t kmax = min(gl, u - 1);
-    for (int64_t k = ga; k <= kmax; ++k) {
-        const int64_t t = task_index(k, u, G);
-        if (t >= te) break;
-        if (t >= tb) s += B[((k - ga) * Bstride + (p - ga * M)) * 3 + c];
-    }
+    int64_t k0 = ga, k1 = min(gl, u - 1);
+    while (k0 <= k1 && task_index(k0, u, G) < tb) ++k0;
+    while (k1 >= k0 && task_index(k1, u, G) >= te) --k1;
+    if (k1 >= k0)
+        s = strided_sum(s, B + ((k0 - ga) * Bstride + (p - ga * M)) * 3 + c, Bstride * 3, k1 - k0 + 1);
     if (u >= ga && u <= gl) {
         const int64_t loc = p - u * M;
-        for (int64_t h = u; h < G; ++h) {
-            const int64_t t = task_index(u, h, G);
-            if (t >= te) break;
-            if (t >= tb) s += A[(((u - ga) * Acols + (h - ga)) * M + loc) * 3 + c];
-        }
+        int64_t h0 = u, h1 = G - 1;
+        while (h0 <= h1 && task_index(u, h0, G) < tb) ++h0;
+        while (h1 >= h0 && task_index(u, h1, G) >= te) --h1;
+        if (h1 >= h0)
+            s = strided_sum(s, A + (((u - ga) * Acols + (h0 - ga)) * M + loc) * 3 + c,
+                            (int64_t)M * 3, h1 - h0 + 1);
     }
     acc[e] = s;
 }
@@ -1086,9 +1115,9 @@ bool use_symmetric(int mode, int64_t N) {
 int pairs_sbt_symmetric(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                         const double *f, const double *w, const double *dcoef, double pref,
                         double *out, int64_t *bad, int accumulate, cudaStream_t st,
-                        Workspace &ws, int mode) {
+                        Workspace &ws, int mode, const std::function<int()> *after_pack) {
     return pairs_sbt_symmetric_shard(x, grp, N, group_size, f, w, dcoef, pref, 0, 1, out, bad,
-                                     accumulate, st, ws, mode);
+                                     accumulate, st, ws, mode, after_pack);
 }
 
 // The unit-pair tasks of rank `rank` of `world`: out receives this rank's
@@ -1187,7 +1216,8 @@ static std::vector<SymWave> sym_waves(int64_t G, int64_t N, int64_t M, int64_t t
 int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int rank, int world, double *out, int64_t *bad, int accumulate,
-                              cudaStream_t st, Workspace &ws, int mode) {
+                              cudaStream_t st, Workspace &ws, int mode,
+                              const std::function<int()> *after_pack) {
     int64_t ntasks = 0, t0 = 0;
     if (N > 0) {
         const int M = sym_unit_size(N, group_size, mode);
@@ -1195,7 +1225,7 @@ int pairs_sbt_symmetric_shard(const double *x, const int64_t *grp, int64_t N, in
         t0 = sym_task_range(G, N, M, rank, world, &ntasks);
     }
     return pairs_sbt_symmetric_tasks(x, grp, N, group_size, f, w, dcoef, pref, t0, ntasks, out, bad,
-                                     accumulate, st, ws, mode);
+                                     accumulate, st, ws, mode, after_pack);
 }
 
 int64_t sym_task_total(int64_t N, int64_t group_size, int mode) {
@@ -1222,15 +1252,19 @@ int sym_task_costs(const double *x, const int64_t *grp, int64_t N, int64_t group
 }
 
 // The unit-pair tasks [t0, t0 + ntasks) (any contiguous range: a rank's
-// share): out receives their contribution to every point.
+// share): out receives their contribution to every point.  `after_pack`
+// (optional) runs once the packing kernels are queued and before the task
+// kernel: the operator forks its overlapping side-stream work there, so the
+// short packing kernels are not held up behind it.
 int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, int64_t group_size,
                               const double *f, const double *w, const double *dcoef, double pref,
                               int64_t t0, int64_t ntasks, double *out, int64_t *bad,
-                              int accumulate, cudaStream_t st, Workspace &ws, int mode) {
+                              int accumulate, cudaStream_t st, Workspace &ws, int mode,
+                              const std::function<int()> *after_pack) {
     const bool f32 = mode == SF_MODE_FP32C;
     if (bad && cudaMemsetAsync(bad, 0, sizeof(int64_t), st) != cudaSuccess)
         return check_launch("memset");
-    if (N == 0) return SF_OK;
+    if (N == 0) return (after_pack && *after_pack) ? (*after_pack)() : SF_OK;
     ensure_capsule_flag();
     const int M = sym_unit_size(N, group_size, mode);
     const int G = (int)((N + M - 1) / M);
@@ -1265,6 +1299,7 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
     }
     int rc = check_launch("sym_pack");
     if (rc) return rc;
+    if (after_pack && *after_pack && (rc = (*after_pack)())) return rc;
     SymArgs a;
     a.src = packed;
     a.slab = meta;
@@ -1278,6 +1313,11 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
         return e ? atoi(e) : 0;
     }();
     a.nofast = nofast;
+    static const double l2_keep_mb = [] {   // SF_SYM_L2_MB: largest wave kept in L2
+        const char *e = getenv("SF_SYM_L2_MB");
+        return e ? atof(e) : 80.0;
+    }();
+    const double l2_keep = l2_keep_mb * (double)(1 << 20);
     const size_t smem = sizeof(double) * 3 * M;
     static const int variant = [] {  // tuning knob: MINB*10 + i-per-lane
         const char *e = getenv("SF_SYM_VARIANT");
@@ -1337,6 +1377,8 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
         a.Bstride = N - W.ga * M;
         a.partA = A;
         a.partB = A + (size_t)rows * a.Acols * M * 3;
+        // bytes of partials the wave writes (two M-point slices per task)
+        a.cs = (double)a.ntasks * 2.0 * M * 3 * sizeof(double) > l2_keep ? 1 : 0;
         if ((rc = run(s))) return rc;
         // the running sums are added to in wave order
         if (prev >= 0 && prev != b && cudaStreamWaitEvent(s, pool->done[prev], 0) != cudaSuccess)

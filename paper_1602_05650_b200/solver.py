@@ -802,10 +802,7 @@ def gmres_solve(operator, preconditioner, rhs, params=None, x0=None, lag=None):
     # SF_GMRES_GRAPH=1: one Arnoldi step (matvec, preconditioner, fused MGS,
     # Givens) captured once as a CUDA graph and replayed for every later
     # step; the step index is read from the device state, so the same graph
-    # serves every k.  Off by default: with the lagged status read the host
-    # already stays ahead of the GPU, so replaying measured no faster at C2
-    # (410 vs 410 ms per step) and the per-solve capture costs ~1 ms at C1
-    # (6.0 vs 5.3 ms per step).  Device-native operators only.
+    # serves every k (_graph_wanted).  Device-native operators only.
     graph = _ArnoldiGraph.create(operator, preconditioner, V, hcol, gs, hist_off - 8, R, vec,
                                  fused) if n else None
     while True:
@@ -868,6 +865,16 @@ def _eager_arnoldi_step(apply_a, apply_m, V, k, hcol, gs, R, vec, fused, n, stat
     _native.call("sf_gmres_givens", _ptr(hcol), _ptr(gs), R, k, _ptr(status), st)
 
 
+# Replaying the captured Arnoldi step removes the launch bubbles between the
+# ~40 kernels of a step: at C2 the steady step period drops from 2.03 to
+# 1.99 ms (tools/step_timeline.py), but whole C2 steps measured 377-400 ms
+# against 381 ms eager (tools/c2_step_ab.py: per-solve capture and replay
+# variance), and at C1 the ~1-2 ms capture per solve outweighs it (6.5-7.2
+# vs 5.5 ms per step).  Opt-in: SF_GMRES_GRAPH=1.
+def _graph_wanted(operator):
+    return os.environ.get("SF_GMRES_GRAPH", "0") == "1"
+
+
 class _ArnoldiGraph:
     """The Arnoldi step of gmres_solve as one CUDA graph: A vin -> tmp,
     M tmp -> w (both into fixed buffers), the fused MGS and the Givens
@@ -880,7 +887,7 @@ class _ArnoldiGraph:
 
     @classmethod
     def create(cls, operator, preconditioner, V, hcol, gs, sc_off, R, vec, fused):
-        if not fused or os.environ.get("SF_GMRES_GRAPH", "0") != "1":
+        if not fused or not _graph_wanted(operator):
             return None
         if not hasattr(operator, "rows_device"):
             return None
@@ -945,13 +952,15 @@ class _ArnoldiGraph:
                 # +140 ms per C2 step in a process holding a C5 state)
                 self.stream.wait_stream(cur)
                 with torch.cuda.stream(self.stream):
-                    g.capture_begin(capture_error_mode="thread_local")
+                    g.capture_begin(capture_error_mode=os.environ.get(
+                        "SF_GMRES_CAPTURE_MODE", "thread_local"))
                     try:
                         self._body()
                     finally:
                         g.capture_end()
             except Exception as err:      # noqa: BLE001 - capture unsupported: stay eager
-                LOG.warning("GMRES step graph capture failed (%s); running eagerly", err)
+                LOG.warning("GMRES step graph capture failed (%s); running eagerly", err,
+                            exc_info=os.environ.get("SF_GMRES_CAPTURE_TRACE") == "1")
                 self.failed = True
                 torch.cuda.synchronize()
                 if matvecs is not None:
