@@ -523,12 +523,17 @@ def run_ours(args, rank, world, local_rank):
     peak_flops, _ = kernels.dfma_peak(1 << 15)
     achieved = rank_pairs * FLOPS_PER_PAIR / (pair_ms * 1e-3)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_sym_c5_metrics.json")
+    traffic_wave = None
+    prof = os.path.join(ROOT, "profiles", "r02_ncu_sym_c5_wave_metrics.json")
     if args.config == "c5" and world == 1 and op.symmetric and os.path.exists(prof):
+        # ncu --set full of one wave launch of the task kernel; scaled to the
+        # matvec by the number of wave launches (all but the last are full)
         m = json.load(open(prof))
-        gb = {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1.0}
-        traffic = sum(float(m[k][1].replace(",", "")) * gb.get(m[k][0], 1.0)
-                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+        gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        traffic_wave = sum(float(m[k][1].replace(",", "")) * gb.get(m[k][0], 1.0)
+                           for k in ("dram__bytes_read.sum", "dram__bytes_write.sum") if k in m)
+        n_waves = (_native.load().sf_sym_launch_count(op.N, op.n, op.mode, 0, 1) - 3) // 2
+        traffic = traffic_wave * n_waves
 
     # ---- the FP32-compute / FP64-accumulate variant on the same workload
     variant = None
@@ -638,12 +643,16 @@ def run_ours(args, rank, world, local_rank):
                                       "symmetric kernel's own minimal work; frac_hw: FP64 "
                                       "hardware flops executed per interaction (ncu "
                                       "instruction counts)",
-                         "traffic_note": "DRAM bytes per launch of the symmetric kernel "
-                                         "(profiles/r01_ncu_sym_c5_metrics.json, ncu): mostly "
-                                         "the deterministic unit-pair partial buffer, written "
-                                         "once with streaming stores and read once by the "
-                                         "ordered reduce; algorithmic inputs are 80 MB; the "
-                                         "kernel is FP64-pipe bound, not HBM bound",
+                         "traffic_wave": traffic_wave,
+                         "traffic_note": "DRAM bytes of the task kernel per matvec, like "
+                                         "achieved: ncu bytes of one wave launch "
+                                         "(traffic_wave, profiles/r02_ncu_sym_c5_wave_metrics"
+                                         ".json) x the wave launches of one matvec; mostly "
+                                         "the wave's partial sums (written once, read once by "
+                                         "the ordered reduce) and source re-reads after they "
+                                         "evict the 80 MB of packed sources from L2; the "
+                                         "kernel is FP64-pipe bound (7 GB/s of DRAM), not "
+                                         "HBM bound",
                          "kernel": "pack + slab meta + sym_task_kernel (symmetric fiber-fiber "
                                    "pairs) + ordered partial reduce",
                          "flops_per_pair": FLOPS_PER_PAIR,

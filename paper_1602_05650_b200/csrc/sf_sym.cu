@@ -925,6 +925,311 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
     }
 }
 
+// ---------------------------------------------------------------------------
+// Packed FP32c variant: the check-free both-direction slab pairs run on
+// packed FP32 (FFMA2 / FADD2 / FMUL2, two lanes of arithmetic per issue slot).
+// The FP32c kernel above is issue-bound (19.3 SASS instructions per pair
+// interaction, FP32 pipe ~59 % busy); here the packing is over TWO j points
+// against one i point, so nothing is broadcast inside the loop: a j slab of
+// 32 points is staged in shared memory as 16 pairs {j, j + 16} (positions
+// negated, so r = x_i + (-y_j) is the same FP32 subtraction as above), each
+// half-warp rotates the 16 pairs among its 16 lanes, and a pair's transposed
+// accumulator is one float2 per component -- 6 shuffles per step for 2 j
+// points, the same shuffle count per interaction as the scalar kernel.  The
+// i operands are duplicated into both halves of a register pair once per
+// slab.  After the 16 steps the two half-warps' transposed partials are
+// added with one xor-16 shuffle, and each i point's two packed halves once.
+// Per step and i point: 33 packed FP32 instructions + 2 MUFU for 4 pair
+// interactions.  Checked and diagonal slab pairs use the scalar path.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
+
+template <int TBI, bool GROUPED>
+__device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[4], int lane,
+                                                const float2 (&ix)[TBI], const float2 (&iy)[TBI],
+                                                const float2 (&iz)[TBI], const float2 (&ifx)[TBI],
+                                                const float2 (&ify)[TBI], const float2 (&ifz)[TBI],
+                                                const float2 (&ic)[TBI], const float2 (&inc3)[TBI],
+                                                float (&uf)[TBI][3], float (&ujo)[3]) {
+    float2 ua[TBI][3], uj[3];
+#pragma unroll
+    for (int q = 0; q < TBI; ++q) ua[q][0] = ua[q][1] = ua[q][2] = f2(0.f, 0.f);
+    uj[0] = uj[1] = uj[2] = f2(0.f, 0.f);
+    const int half = lane & 16, l = lane & 15;
+    const int nxt = half | ((l + 1) & 15);
+#pragma unroll 2
+    for (int s = 0; s < 16; ++s) {
+        const int p = (l + s) & 15;
+        const float4 A = jp[p][0], B = jp[p][1], C = jp[p][2], D = jp[p][3];
+        const float2 nxj = f2(A.x, A.y), nyj = f2(A.z, A.w), nzj = f2(B.x, B.y);
+        const float2 fxj = f2(B.z, B.w), fyj = f2(C.x, C.y), fzj = f2(C.z, C.w);
+        const float2 cj = f2(D.x, D.y), nc3j = f2(D.z, D.w);
+        if (GROUPED) {   // phase by phase over the i points: independent work between
+                         // each MUFU / FFMA2 and its first use
+            float2 rx[TBI], ry[TBI], rz[TBI], ir[TBI], ir3[TBI], ir5[TBI];
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {
+                rx[q] = __fadd2_rn(ix[q], nxj);
+                ry[q] = __fadd2_rn(iy[q], nyj);
+                rz[q] = __fadd2_rn(iz[q], nzj);
+            }
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {
+                const float2 r2 =
+                    __ffma2_rn(rx[q], rx[q], __ffma2_rn(ry[q], ry[q], __fmul2_rn(rz[q], rz[q])));
+                ir[q] = f2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+            }
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {
+                const float2 ir2 = __fmul2_rn(ir[q], ir[q]);
+                ir3[q] = __fmul2_rn(ir[q], ir2);
+                ir5[q] = __fmul2_rn(ir3[q], ir2);
+            }
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {   // the two j sources onto i
+                const float2 a = __ffma2_rn(cj, ir3[q], ir[q]);
+                const float2 rf =
+                    __ffma2_rn(rz[q], fzj, __ffma2_rn(ry[q], fyj, __fmul2_rn(rx[q], fxj)));
+                const float2 b = __fmul2_rn(rf, __ffma2_rn(nc3j, ir5[q], ir3[q]));
+                ua[q][0] = __ffma2_rn(a, fxj, __ffma2_rn(b, rx[q], ua[q][0]));
+                ua[q][1] = __ffma2_rn(a, fyj, __ffma2_rn(b, ry[q], ua[q][1]));
+                ua[q][2] = __ffma2_rn(a, fzj, __ffma2_rn(b, rz[q], ua[q][2]));
+            }
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {   // i onto the two j targets
+                const float2 a = __ffma2_rn(ic[q], ir3[q], ir[q]);
+                const float2 rf = __ffma2_rn(rz[q], ifz[q],
+                                             __ffma2_rn(ry[q], ify[q], __fmul2_rn(rx[q], ifx[q])));
+                const float2 b = __fmul2_rn(rf, __ffma2_rn(inc3[q], ir5[q], ir3[q]));
+                uj[0] = __ffma2_rn(a, ifx[q], __ffma2_rn(b, rx[q], uj[0]));
+                uj[1] = __ffma2_rn(a, ify[q], __ffma2_rn(b, ry[q], uj[1]));
+                uj[2] = __ffma2_rn(a, ifz[q], __ffma2_rn(b, rz[q], uj[2]));
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < TBI; ++q) {
+                const float2 rx = __fadd2_rn(ix[q], nxj);
+                const float2 ry = __fadd2_rn(iy[q], nyj);
+                const float2 rz = __fadd2_rn(iz[q], nzj);
+                const float2 r2 = __ffma2_rn(rx, rx, __ffma2_rn(ry, ry, __fmul2_rn(rz, rz)));
+                const float2 ir = f2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+                const float2 ir2 = __fmul2_rn(ir, ir);
+                const float2 ir3 = __fmul2_rn(ir, ir2);
+                const float2 ir5 = __fmul2_rn(ir3, ir2);
+                {   // the two j sources onto i
+                    const float2 a = __ffma2_rn(cj, ir3, ir);
+                    const float2 rf = __ffma2_rn(rz, fzj, __ffma2_rn(ry, fyj, __fmul2_rn(rx, fxj)));
+                    const float2 b = __fmul2_rn(rf, __ffma2_rn(nc3j, ir5, ir3));
+                    ua[q][0] = __ffma2_rn(a, fxj, __ffma2_rn(b, rx, ua[q][0]));
+                    ua[q][1] = __ffma2_rn(a, fyj, __ffma2_rn(b, ry, ua[q][1]));
+                    ua[q][2] = __ffma2_rn(a, fzj, __ffma2_rn(b, rz, ua[q][2]));
+                }
+                {   // i onto the two j targets
+                    const float2 a = __ffma2_rn(ic[q], ir3, ir);
+                    const float2 rf =
+                        __ffma2_rn(rz, ifz[q], __ffma2_rn(ry, ify[q], __fmul2_rn(rx, ifx[q])));
+                    const float2 b = __fmul2_rn(rf, __ffma2_rn(inc3[q], ir5, ir3));
+                    uj[0] = __ffma2_rn(a, ifx[q], __ffma2_rn(b, rx, uj[0]));
+                    uj[1] = __ffma2_rn(a, ify[q], __ffma2_rn(b, ry, uj[1]));
+                    uj[2] = __ffma2_rn(a, ifz[q], __ffma2_rn(b, rz, uj[2]));
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            uj[c].x = __shfl_sync(0xffffffffu, uj[c].x, nxt);
+            uj[c].y = __shfl_sync(0xffffffffu, uj[c].y, nxt);
+        }
+    }
+    // lane l of each half now holds pair l = {j = l, j = l + 16}, summed over
+    // its half's i points; the sum of both halves is the same in both (a + b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float ox = __shfl_xor_sync(0xffffffffu, uj[c].x, 16);
+        const float oy = __shfl_xor_sync(0xffffffffu, uj[c].y, 16);
+        ujo[c] = half ? uj[c].y + oy : uj[c].x + ox;
+    }
+#pragma unroll
+    for (int q = 0; q < TBI; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) uf[q][c] = ua[q][c].x + ua[q][c].y;
+}
+
+template <int MINB, int TBI, bool GROUPED = false, bool UDS = false>
+__global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArgs a) {
+    constexpr int kI = 32 * TBI;
+    extern __shared__ double jacc_s[];
+    __shared__ double ui_s[4][kI][3];
+    __shared__ float4 js_a[4][32], js_b[4][32];
+    __shared__ int js_g[4][32];
+    __shared__ float4 jp_s[4][16][4];
+    if ((int64_t)blockIdx.x >= a.ntasks) return;
+    const int64_t t = a.task0 + blockIdx.x;
+    int g, h;
+    task_units(t, a.G, g, h);
+    const bool both = g != h;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g0 = (int64_t)g * a.M, h0 = (int64_t)h * a.M;
+    const int ng = (int)min((int64_t)a.M, a.N - g0), nh = (int)min((int64_t)a.M, a.N - h0);
+    const int nslab = (nh + 31) / 32;
+    if (both)
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x) jacc_s[e] = 0.0;
+    __syncthreads();   // zero-fill (any warp) before the owning warp's first +=
+    int nb = 0;
+    for (int ib = 0; ib < ng; ib += kI) {
+        // i strengths, duplicated into both halves of a register pair
+        float2 ifx[TBI], ify[TBI], ifz[TBI], ic[TBI], inc3[TBI];
+        bool vi[TBI];
+        double ud[TBI][3];
+#pragma unroll
+        for (int k = 0; k < TBI; ++k) {
+            vi[k] = ib + 32 * k + lane < ng;
+            const PDataF p = load_point_f(a.src, g0 + ib + 32 * k + lane, vi[k]);
+            ifx[k] = dup2(p.fx); ify[k] = dup2(p.fy); ifz[k] = dup2(p.fz);
+            ic[k] = dup2(p.c); inc3[k] = dup2(-p.c3);
+            if constexpr (UDS) {   // FP64 owner sums in this warp's shared rows (registers
+                                   // for the packed loop)
+                ui_s[warp][32 * k + lane][0] = ui_s[warp][32 * k + lane][1] =
+                    ui_s[warp][32 * k + lane][2] = 0.0;
+            } else {
+                ud[k][0] = ud[k][1] = ud[k][2] = 0.0;
+            }
+        }
+        const SlabMeta *mi = a.slab + (g0 + ib) / 32;
+        const int kvalid = min(TBI, (ng - ib + 31) / 32);
+        double blo[3], bhi[3];
+        int gmn = mi[0].gmin, gmx = mi[0].gmax;
+        for (int c = 0; c < 3; ++c) { blo[c] = mi[0].lo[c]; bhi[c] = mi[0].hi[c]; }
+        for (int k = 1; k < kvalid; ++k) {
+            for (int c = 0; c < 3; ++c) {
+                blo[c] = fmin(blo[c], mi[k].lo[c]);
+                bhi[c] = fmax(bhi[c], mi[k].hi[c]);
+            }
+            gmn = min(gmn, mi[k].gmin);
+            gmx = max(gmx, mi[k].gmax);
+        }
+        for (int sl = warp; sl < nslab; sl += 4) {
+            const int jl = sl * 32 + lane;
+            const PDataF qj = load_point_f(a.src, h0 + jl, jl < nh);
+            const SlabMeta &mj = a.slab[h0 / 32 + sl];
+            const bool fast = !a.nofast && both && (mj.gmax < gmn || mj.gmin > gmx) &&
+                              (boxes_far(blo, bhi, mj) || islabs_far<TBI>(mi, kvalid, mj));
+            // i points relative to this j slab's origin (FP64 positions, once
+            // per slab); padding i lanes sit 1e18 away and carry no strength
+            double oj[3];
+            slab_origin(mj, oj);
+            float px[TBI], py[TBI], pz[TBI];
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) {
+                const double *xi = a.x + 3 * (g0 + ib + 32 * k + (vi[k] ? lane : 0));
+                px[k] = vi[k] ? (float)(xi[0] - oj[0]) : 1e18f;
+                py[k] = vi[k] ? (float)(xi[1] - oj[1]) : 1e18f;
+                pz[k] = vi[k] ? (float)(xi[2] - oj[2]) : 1e18f;
+            }
+            float uf[TBI][3];
+            float uj[3] = {0.f, 0.f, 0.f};
+            if (fast) {
+                {   // stage the slab as 16 pairs {p, p + 16}
+                    float *d = reinterpret_cast<float *>(jp_s[warp][lane & 15]);
+                    const int hh = lane >> 4;
+                    d[0 + hh] = -qj.x; d[2 + hh] = -qj.y; d[4 + hh] = -qj.z;
+                    d[6 + hh] = qj.fx; d[8 + hh] = qj.fy; d[10 + hh] = qj.fz;
+                    d[12 + hh] = qj.c; d[14 + hh] = -qj.c3;
+                }
+                __syncwarp();
+                float2 ix[TBI], iy[TBI], iz[TBI];
+#pragma unroll
+                for (int k = 0; k < TBI; ++k) { ix[k] = dup2(px[k]); iy[k] = dup2(py[k]); iz[k] = dup2(pz[k]); }
+                sym_slab_packed<TBI, GROUPED>(jp_s[warp], lane, ix, iy, iz, ifx, ify, ifz, ic, inc3, uf, uj);
+            } else {
+                js_a[warp][lane] = make_float4(qj.x, qj.y, qj.z, qj.fx);
+                js_b[warp][lane] = make_float4(qj.fy, qj.fz, qj.c, qj.c3);
+                js_g[warp][lane] = qj.g;
+                __syncwarp();
+                PDataF pi[TBI];
+#pragma unroll
+                for (int k = 0; k < TBI; ++k) {
+                    pi[k].x = px[k]; pi[k].y = py[k]; pi[k].z = pz[k];
+                    pi[k].fx = ifx[k].x; pi[k].fy = ify[k].x; pi[k].fz = ifz[k].x;
+                    pi[k].c = ic[k].x; pi[k].c3 = -inc3[k].x;
+                    pi[k].g = vi[k] ? a.src[g0 + ib + 32 * k + lane].g : -3;
+                    uf[k][0] = uf[k][1] = uf[k][2] = 0.f;
+                }
+                const int nxt = (lane + 1) & 31;
+                for (int s = 0; s < 32; ++s) {
+                    const int k = (lane + s) & 31;
+                    PDataF pj;
+                    const float4 A0 = js_a[warp][k], B0 = js_b[warp][k];
+                    pj.x = A0.x; pj.y = A0.y; pj.z = A0.z; pj.fx = A0.w;
+                    pj.fy = B0.x; pj.fz = B0.y; pj.c = B0.z; pj.c3 = B0.w;
+                    pj.g = js_g[warp][k];
+                    int nbi = 0;
+                    const double *xj = pj.g != -3 ? a.x + 3 * (h0 + sl * 32 + k) : nullptr;
+#pragma unroll
+                    for (int q = 0; q < TBI; ++q) {
+                        const double *xi = vi[q] ? a.x + 3 * (g0 + ib + 32 * q + lane) : nullptr;
+                        if (both) sym_pair_f<true, true>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                        else sym_pair_f<true, false>(pi[q], pj, uf[q], uj, nbi, xi, xj);
+                    }
+                    if (pj.g != -3) nb += nbi;
+                    if (both) {
+                        uj[0] = __shfl_sync(0xffffffffu, uj[0], nxt);
+                        uj[1] = __shfl_sync(0xffffffffu, uj[1], nxt);
+                        uj[2] = __shfl_sync(0xffffffffu, uj[2], nxt);
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) {
+                if constexpr (UDS) {
+                    double *d = ui_s[warp][32 * k + lane];
+                    d[0] += (double)uf[k][0];
+                    d[1] += (double)uf[k][1];
+                    d[2] += (double)uf[k][2];
+                } else {
+                    ud[k][0] += (double)uf[k][0];
+                    ud[k][1] += (double)uf[k][1];
+                    ud[k][2] += (double)uf[k][2];
+                }
+            }
+            if (both && jl < nh) {
+                double *dst = jacc_s + 3 * jl;
+                dst[0] += (double)uj[0];
+                dst[1] += (double)uj[1];
+                dst[2] += (double)uj[2];
+            }
+        }
+        if constexpr (!UDS) {
+#pragma unroll
+            for (int k = 0; k < TBI; ++k) {
+                ui_s[warp][32 * k + lane][0] = ud[k][0];
+                ui_s[warp][32 * k + lane][1] = ud[k][1];
+                ui_s[warp][32 * k + lane][2] = ud[k][2];
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * kI; e += blockDim.x) {
+            const int il = e / 3, c = e - 3 * il;
+            if (ib + il < ng) {
+                const double sv = ((ui_s[0][il][c] + ui_s[1][il][c]) + ui_s[2][il][c]) + ui_s[3][il][c];
+                part_store(a, owner_slot(a, g, h, ib + il) + c, sv);
+            }
+        }
+        __syncthreads();
+    }
+    if (both) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 3 * nh; e += blockDim.x)
+            part_store(a, trans_slot(a, g, h0) + e, jacc_s[e]);
+    }
+    if (a.bad) {
+        nb = warp_sum_int(nb);
+        if (lane == 0 && nb) atomicAdd(a.bad, (unsigned long long)nb);
+    }
+}
+
 // Slab bounds straight from the FP64 positions (the FP32 records are packed
 // relative to these boxes' centres afterwards).
 __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
@@ -1073,14 +1378,15 @@ __global__ void sym_pack_kernel(const double *__restrict__ x, const int64_t *__r
 int sym_unit_size(int64_t N, int64_t group_size, int mode) {
     // units: a multiple of the 32-point slab (and of the fiber size when that
     // keeps them near the target, so units align to fibers), at most 3072
-    // points in FP64 (2048 for FP32c, whose 3 CTAs/SM need the smaller
-    // M x 3 shared accumulator), and small enough that the G(G+1)/2 unit-pair
+    // points in FP64 (1408 for FP32c, whose 4 CTAs/SM need the smaller
+    // M x 3 shared accumulator: 1.478e12 pair/s at C5 against 1.420e12 with
+    // 1536 points, where shared memory allows only 3), and small enough that the G(G+1)/2 unit-pair
     // tasks fill the GPU many times over (G >= 128 -> >= 8256 tasks) for
     // mid-size systems; the sweeps (tools/gpu_unit_sweep.sh) peak at
     // N/128..N/85 for N = 32k-64k, and at C5 M = 3072 matches 2048 (750 vs
     // 748 G/s) with a third fewer partial slots (8.6 instead of 12.9 GB)
     const char *e = getenv("SF_SYM_UNIT");
-    int64_t target = e ? atoi(e) : (mode == SF_MODE_FP32C ? 2048 : 3072);
+    int64_t target = e ? atoi(e) : (mode == SF_MODE_FP32C ? 1408 : 3072);
     if (!e) {
         const int64_t fill = N / 128;
         if (fill < target) target = fill;
@@ -1325,7 +1631,7 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
     }();
     static const int fvariant = [] {
         const char *e = getenv("SF_SYM_F32_VARIANT");
-        return e ? atoi(e) : 34;
+        return e ? atoi(e) : 344;   // packed, grouped, owner sums in shared memory, 4 CTAs/SM
     }();
     auto launch = [&](auto kern, cudaStream_t s) -> int {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -1341,6 +1647,17 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
                 case 33: return launch(sym_task_kernel_f32<3, 3>, s);
                 case 26: return launch(sym_task_kernel_f32<2, 6>, s);
                 case 44: return launch(sym_task_kernel_f32<4, 4>, s);
+                case 134: return launch(sym_task_kernel_f32p<3, 4>, s);
+                case 124: return launch(sym_task_kernel_f32p<2, 4>, s);
+                case 133: return launch(sym_task_kernel_f32p<3, 3>, s);
+                case 142: return launch(sym_task_kernel_f32p<4, 2>, s);
+                case 234: return launch(sym_task_kernel_f32p<3, 4, true>, s);
+                case 224: return launch(sym_task_kernel_f32p<2, 4, true>, s);
+                case 233: return launch(sym_task_kernel_f32p<3, 3, true>, s);
+                case 334: return launch(sym_task_kernel_f32p<3, 4, true, true>, s);
+                case 344: return launch(sym_task_kernel_f32p<4, 4, true, true>, s);
+                case 343: return launch(sym_task_kernel_f32p<4, 3, true, true>, s);
+                case 444: return launch(sym_task_kernel_f32p<4, 4, false, true>, s);
                 default: return launch(sym_task_kernel_f32<3, 4>, s);
             }
         }
