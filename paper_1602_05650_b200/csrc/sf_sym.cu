@@ -946,7 +946,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 __device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
 
 template <int TBI, bool GROUPED>
-__device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[4], int lane,
+__device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[16], int lane,
                                                 const float2 (&ix)[TBI], const float2 (&iy)[TBI],
                                                 const float2 (&iz)[TBI], const float2 (&ifx)[TBI],
                                                 const float2 (&ify)[TBI], const float2 (&ifz)[TBI],
@@ -961,7 +961,7 @@ __device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[
 #pragma unroll 2
     for (int s = 0; s < 16; ++s) {
         const int p = (l + s) & 15;
-        const float4 A = jp[p][0], B = jp[p][1], C = jp[p][2], D = jp[p][3];
+        const float4 A = jp[0][p], B = jp[1][p], C = jp[2][p], D = jp[3][p];
         const float2 nxj = f2(A.x, A.y), nyj = f2(A.z, A.w), nzj = f2(B.x, B.y);
         const float2 fxj = f2(B.z, B.w), fyj = f2(C.x, C.y), fzj = f2(C.z, C.w);
         const float2 cj = f2(D.x, D.y), nc3j = f2(D.z, D.w);
@@ -1063,7 +1063,9 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArg
     __shared__ double ui_s[4][kI][3];
     __shared__ float4 js_a[4][32], js_b[4][32];
     __shared__ int js_g[4][32];
-    __shared__ float4 jp_s[4][16][4];
+    __shared__ float4 jp_s[4][4][16];   // [warp][record quarter][pair]: a half-warp's LDS.128 of
+                                        // one quarter reads 16 consecutive float4 (no bank
+                                        // conflicts; [pair][quarter] cost 4 wavefronts per load)
     if ((int64_t)blockIdx.x >= a.ntasks) return;
     const int64_t t = a.task0 + blockIdx.x;
     int g, h;
@@ -1131,11 +1133,9 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArg
             float uj[3] = {0.f, 0.f, 0.f};
             if (fast) {
                 {   // stage the slab as 16 pairs {p, p + 16}
-                    float *d = reinterpret_cast<float *>(jp_s[warp][lane & 15]);
-                    const int hh = lane >> 4;
-                    d[0 + hh] = -qj.x; d[2 + hh] = -qj.y; d[4 + hh] = -qj.z;
-                    d[6 + hh] = qj.fx; d[8 + hh] = qj.fy; d[10 + hh] = qj.fz;
-                    d[12 + hh] = qj.c; d[14 + hh] = -qj.c3;
+                    float *d = reinterpret_cast<float *>(&jp_s[warp][0][lane & 15]) + (lane >> 4);
+                    d[0] = -qj.x; d[2] = -qj.y; d[64] = -qj.z; d[66] = qj.fx;
+                    d[128] = qj.fy; d[130] = qj.fz; d[192] = qj.c; d[194] = -qj.c3;
                 }
                 __syncwarp();
                 float2 ix[TBI], iy[TBI], iz[TBI];
