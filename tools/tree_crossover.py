@@ -43,7 +43,9 @@ for nfib in sizes:
     rec = {"n_fibers": nfib, "points": N, "direct_ms": t_dir,
            "direct_pairs_per_s": (N * N - nfib * cl.n_nodes ** 2) / (t_dir * 1e-3)}
     for name, kw in (("reference_gates", {}), ("theta0.5_tol1e-4", dict(cell_tolerance=1e-4)),
-                     ("theta0.7_tol1e-3", dict(theta=0.7, cell_tolerance=1e-3))):
+                     ("theta0.7_tol1e-3", dict(theta=0.7, cell_tolerance=1e-3)),
+                     ("theta0.5_tol1e-1", dict(theta=0.5, cell_tolerance=1e-1)),
+                     ("theta0.5_tol1", dict(theta=0.5, cell_tolerance=1.0))):
         tb = system.TreeSummation(**kw)
         t_tree, u_tree = timed(lambda: tb.stokeslet(X, grp, f, X, grp, 1.0))
         rec[name] = {"ms": t_tree, "speedup": t_dir / t_tree,
