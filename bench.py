@@ -564,7 +564,15 @@ def run_ours(args, rank, world, local_rank):
         variant = {"dtype": "f32-compute/f64-accumulate", "value": total_pairs / (vms * 1e-3),
                    "unit": "pair-interactions/s", "ms_per_step": vms,
                    "rel_l2_vs_fp64": float((err[0] / err[1]).sqrt().item()),
-                   "tolerance": 1e-5}
+                   "tolerance": 1e-5,
+                   # whole matvec (self terms included), against the NOMINAL FP32 peak
+                   # of 148 SMs x 128 lanes x 2 x 1.965 GHz: there is no measured FP32
+                   # figure in MEASURED_PEAKS.json (profiles/r02_ffma2_probe2.txt
+                   # measures 73.3 TFLOP/s with packed FFMA2)
+                   "roofline": {"bound": "fp32", "unit": "TFLOP/s", "flops_per_pair": 35,
+                                "achieved": 35.0 * total_pairs / (vms * 1e-3) / 1e12 / world,
+                                "peak": 74.4, "peak_source": "nominal",
+                                "frac": 35.0 * total_pairs / (vms * 1e-3) / 1e12 / world / 74.4}}
         del op32, sop32, u32
 
     # ---- e2e through the reference's own operator signature (world 1):
