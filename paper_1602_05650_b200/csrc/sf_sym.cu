@@ -63,6 +63,10 @@ struct __align__(16) SlabMeta {  // bounding box + group range + capsule of 32 p
     // capsule: segment from the slab's first to its last point, radius = the
     // largest point-to-segment distance (a fiber's 32 nodes hug its chord)
     double p0[3], p1[3], rad;
+    // the doublet coefficient c shared by the slab's points, NaN when they differ
+    // (a fiber-aligned slab has one c: the packed FP32c kernel then takes c_j as
+    // a 32-bit broadcast operand instead of a register pair)
+    double cuni;
 };
 
 struct SymArgs {
@@ -592,19 +596,28 @@ __device__ __forceinline__ void slab_capsule(const double *pt, bool valid, int n
     }
 }
 
+// The slab's common doublet coefficient (lane 0 is always a real point), NaN
+// when its real points differ.
+__device__ __forceinline__ double slab_common_c(double c, bool valid) {
+    const double c0 = __shfl_sync(0xffffffffu, c, 0);
+    const bool same = __all_sync(0xffffffffu, !valid || c == c0);
+    return same ? c0 : __longlong_as_double(0x7ff8000000000000ll);
+}
+
 __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
                                  SlabMeta *__restrict__ meta) {
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (s * 32 >= N) return;
     const int64_t j = s * 32 + lane;
-    double v[6], pt[3] = {0.0, 0.0, 0.0};
+    double v[6], pt[3] = {0.0, 0.0, 0.0}, cj = 0.0;
     int gmn = 0x7fffffff, gmx = (int)0x80000000;
     if (j < N) {
         const SymSrc &q = src[j];
         v[0] = v[3] = pt[0] = q.v[0];
         v[1] = v[4] = pt[1] = q.v[1];
         v[2] = v[5] = pt[2] = q.v[2];
+        cj = q.v[6];
         if (q.g >= 0) { gmn = q.g; gmx = q.g; }
     } else {
         v[0] = v[1] = v[2] = 1e300;
@@ -622,10 +635,12 @@ __global__ void slab_meta_kernel(const SymSrc *__restrict__ src, int64_t N,
     }
     SlabMeta m;
     slab_capsule(pt, j < N, (int)min((int64_t)32, N - s * 32), m);
+    const double cu = slab_common_c(cj, j < N);
     if (lane == 0) {
         for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
         m.gmin = gmn;
         m.gmax = gmx;
+        m.cuni = cu;
         meta[s] = m;
     }
 }
@@ -945,8 +960,9 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32(SymArgs
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
 
-template <int TBI, bool GROUPED>
+template <int TBI, bool GROUPED, bool JUNI>
 __device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[16], int lane,
+                                                float cjf, float nc3jf,
                                                 const float2 (&ix)[TBI], const float2 (&iy)[TBI],
                                                 const float2 (&iz)[TBI], const float2 (&ifx)[TBI],
                                                 const float2 (&ify)[TBI], const float2 (&ifz)[TBI],
@@ -961,10 +977,16 @@ __device__ __forceinline__ void sym_slab_packed(const float4 (*__restrict__ jp)[
 #pragma unroll 2
     for (int s = 0; s < 16; ++s) {
         const int p = (l + s) & 15;
-        const float4 A = jp[0][p], B = jp[1][p], C = jp[2][p], D = jp[3][p];
+        const float4 A = jp[0][p], B = jp[1][p], C = jp[2][p];
         const float2 nxj = f2(A.x, A.y), nyj = f2(A.z, A.w), nzj = f2(B.x, B.y);
         const float2 fxj = f2(B.z, B.w), fyj = f2(C.x, C.y), fzj = f2(C.z, C.w);
-        const float2 cj = f2(D.x, D.y), nc3j = f2(D.z, D.w);
+        float2 cj, nc3j;
+        if (JUNI) {   // one c for the whole j slab: a 32-bit broadcast operand
+            cj = dup2(cjf); nc3j = dup2(nc3jf);
+        } else {
+            const float4 D = jp[3][p];
+            cj = f2(D.x, D.y); nc3j = f2(D.z, D.w);
+        }
         if (GROUPED) {   // phase by phase over the i points: independent work between
                          // each MUFU / FFMA2 and its first use
             float2 rx[TBI], ry[TBI], rz[TBI], ir[TBI], ir3[TBI], ir5[TBI];
@@ -1141,7 +1163,15 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArg
                 float2 ix[TBI], iy[TBI], iz[TBI];
 #pragma unroll
                 for (int k = 0; k < TBI; ++k) { ix[k] = dup2(px[k]); iy[k] = dup2(py[k]); iz[k] = dup2(pz[k]); }
-                sym_slab_packed<TBI, GROUPED>(jp_s[warp], lane, ix, iy, iz, ifx, ify, ifz, ic, inc3, uf, uj);
+                // records hold float(c), float(3c): the same roundings here
+                const float cjf = __double2float_rn(mj.cuni);
+                const float nc3jf = -__double2float_rn(3.0 * mj.cuni);
+                if (mj.cuni == mj.cuni)   // not NaN: the slab's points share c
+                    sym_slab_packed<TBI, GROUPED, true>(jp_s[warp], lane, cjf, nc3jf, ix, iy, iz, ifx,
+                                                        ify, ifz, ic, inc3, uf, uj);
+                else
+                    sym_slab_packed<TBI, GROUPED, false>(jp_s[warp], lane, cjf, nc3jf, ix, iy, iz,
+                                                         ifx, ify, ifz, ic, inc3, uf, uj);
             } else {
                 js_a[warp][lane] = make_float4(qj.x, qj.y, qj.z, qj.fx);
                 js_b[warp][lane] = make_float4(qj.fy, qj.fz, qj.c, qj.c3);
@@ -1233,7 +1263,8 @@ __global__ void __launch_bounds__(kSymThreads, MINB) sym_task_kernel_f32p(SymArg
 // Slab bounds straight from the FP64 positions (the FP32 records are packed
 // relative to these boxes' centres afterwards).
 __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *__restrict__ grp,
-                                   int64_t N, SlabMeta *__restrict__ meta) {
+                                   const double *__restrict__ dcoef, int64_t N,
+                                   SlabMeta *__restrict__ meta) {
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (s * 32 >= N) return;
@@ -1261,10 +1292,12 @@ __global__ void slab_meta_x_kernel(const double *__restrict__ x, const int64_t *
     }
     SlabMeta m;
     slab_capsule(pt, j < N, (int)min((int64_t)32, N - s * 32), m);
+    const double cu = slab_common_c((dcoef && j < N) ? dcoef[j] : 0.0, j < N);
     if (lane == 0) {
         for (int c = 0; c < 3; ++c) { m.lo[c] = v[c]; m.hi[c] = v[3 + c]; }
         m.gmin = gmn;
         m.gmax = gmx;
+        m.cuni = cu;
         meta[s] = m;
     }
 }
@@ -1551,7 +1584,7 @@ int sym_task_costs(const double *x, const int64_t *grp, int64_t N, int64_t group
     const int64_t nslab = (N + 31) / 32;
     SlabMeta *meta = (SlabMeta *)ws.get(4, sizeof(SlabMeta) * (size_t)(nslab + 1), st);
     if (!meta) return SF_ENOMEM;
-    slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, N, meta);
+    slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, nullptr, N, meta);
     sym_task_cost_kernel<<<(unsigned)((ntasks + 127) / 128), 128, 0, st>>>(meta, N, M, G, ntasks,
                                                                          c_checked, c_diag, cost);
     return check_launch("sym_task_cost_kernel");
@@ -1595,7 +1628,7 @@ int pairs_sbt_symmetric_tasks(const double *x, const int64_t *grp, int64_t N, in
     int64_t pg = (N + 255) / 256;
     const int64_t nslab = (N + 31) / 32;
     if (f32) {
-        slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, N, meta);
+        slab_meta_x_kernel<<<(unsigned)((nslab + 7) / 8), 256, 0, st>>>(x, grp, dcoef, N, meta);
         sym_pack_f32_kernel<<<(unsigned)(pg > 4096 ? 4096 : pg), 256, 0, st>>>(x, grp, f, w, dcoef,
                                                                              N, meta, packed);
     } else {
